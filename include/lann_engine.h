@@ -1,0 +1,233 @@
+/*
+ * lann_engine.h — C ABI of the B200 LANN engine (drop-in for the perfsage
+ * models / eval / selector / datagen hot path).
+ *
+ * Every entry point is plain C: caller-owned HOST buffers, sizes as integers,
+ * integer status codes, no exceptions, no torch types. The engine owns its
+ * device memory. Calls are synchronous (they return after the D2H copy).
+ *
+ * Reference interfaces each entry point replaces (paths into the reference
+ * tree proj/core/):
+ *   lann_train            models::train_full_batch       include/perfsage/mlp.hpp:64-66
+ *                         (+ mse_gradient mlp.hpp:42-43, AdamState::update mlp.hpp:59)
+ *   lann_predict          models::predict / predict_dataset include/perfsage/models.hpp:109,119-120
+ *   lann_eval             eval::mape / mape_thresholded / spearman / make_report
+ *                                                         include/perfsage/eval.hpp:13-49
+ *   lann_select_schedule  selector::select(TrainedModel, n, candidates)
+ *                                                         include/perfsage/selector.hpp:35-36
+ *   lann_select_variants  (no reference equivalent: multi-variant argmin built
+ *                          from selector::select's tie rule, selector.cpp:26-40)
+ *   lann_build_dataset    datagen::build_dataset + split  include/perfsage/datagen.hpp:109-116
+ *   lann_run_population   models::train_nn + predict_dataset + eval::make_report
+ *                          over a whole population (batched overload of
+ *                          models.hpp:95,119 and eval.hpp:49)
+ *
+ * Status codes map 1:1 onto the reference's exception types
+ * (include/perfsage/errors.hpp): ParamError, SchemaError, TrainingError,
+ * DomainError, BuildAbortError.
+ */
+#ifndef LANN_ENGINE_H
+#define LANN_ENGINE_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status ------------------------------------------------------------ */
+enum lann_status {
+  LANN_OK = 0,
+  LANN_PARAM_ERROR = 1,    /* perfsage::ParamError   (errors.hpp:15-18)  */
+  LANN_SCHEMA_ERROR = 2,   /* perfsage::SchemaError  (errors.hpp:55-58)  */
+  LANN_TRAINING_ERROR = 3, /* perfsage::TrainingError(errors.hpp:33-40)  */
+  LANN_DOMAIN_ERROR = 4,   /* perfsage::DomainError  (errors.hpp:21-24)  */
+  LANN_BUILD_ABORT = 5,    /* perfsage::BuildAbortError (errors.hpp:61-69) */
+  LANN_CUDA_ERROR = 6,     /* device failure (no reference equivalent)    */
+  LANN_NO_DEVICE = 7       /* no CUDA device: the engine never falls back */
+};
+
+/* ---- arithmetic modes ---------------------------------------------------- */
+enum lann_precision {
+  /* FP64 with the reference's exact operation order and no FMA contraction:
+   * loss traces and weights are bit-identical to models::train_nn. */
+  LANN_FP64_EXACT = 0,
+  /* FP32 FMA throughput mode (tree reductions over samples). */
+  LANN_FP32 = 1
+};
+
+/* ---- domain enums (kernels.hpp:13, models.hpp:19) -------------------------- */
+enum lann_kind { LANN_MM = 0, LANN_MV = 1, LANN_MC = 2, LANN_MP = 3, LANN_BLUR = 4 };
+enum lann_family { LANN_NNC = 0, LANN_NN = 1 };
+enum lann_hw_class { LANN_HW_CPU = 0, LANN_HW_GPU = 1 }; /* variants.hpp:16 */
+
+#define LANN_ROW 8 /* padded feature-row width: up to 7 inputs (+ 1 spare) */
+
+/* ---- synthetic runtime world (a generalisation of the reference's
+ * acceptance-test probe, proj/tests/acceptance/acceptance_main.cpp:271-279):
+ *   non-blur: t = ((((alpha * c) * g) * fd) * nz) + beta,
+ *             g  = g0 + g1 / n_thd,  fd = (1 - delta) + delta * d,
+ *             nz = 1 + U(-noise, noise)
+ *   blur:     same with g = 1 + sum_j kappa[j] * (log2 s_j - mu[j])^2, fd = 1
+ * with nz drawn from Rng(derive_seed(data_seed, 0x9015E)) one draw per sample.
+ * (alpha=3e-9, g0=0.25, g1=0.75, delta=0, beta=0, noise=0.02) is the
+ * acceptance world bit for bit. */
+typedef struct lann_world {
+  int32_t kind;         /* lann_kind */
+  int32_t hw_class;     /* lann_hw_class: CPU variants take n_thd (variants.hpp:29-31) */
+  int32_t max_threads;  /* ParamSpace::max_threads (datagen.hpp:23) */
+  int32_t blur_lattice; /* 0 = ScheduleSpace::cpu_default, 1 = gpu_style */
+  double alpha, g0, g1, delta, beta, noise;
+  double mu[4], kappa[4];
+} lann_world;
+
+/* One model of a population: dataset recipe + ModelConfig (models.hpp:27-40). */
+typedef struct lann_job {
+  lann_world world;
+  uint64_t data_seed;    /* build_dataset seed; split uses the same seed */
+  int32_t count;         /* dataset size (>= 2) */
+  double train_fraction; /* datagen::split fraction */
+  int32_t n_folds;       /* 0: train on the split's train part, evaluate on its test part;
+                            k>=2: k-fold CV over the train part, see fold */
+  int32_t fold;          /* held-out block index when n_folds >= 2 */
+  int32_t family;        /* lann_family */
+  int32_t n_hidden;      /* 1 or 2 */
+  int32_t hidden[2];
+  double learning_rate;  /* 1e-2, 1e-3 or 1e-4 (ModelConfig::validate) */
+  int32_t epochs;
+  uint64_t init_seed;    /* ModelConfig::seed */
+  int32_t log_target;
+  int32_t unconstrained;
+} lann_job;
+
+typedef struct lann_job_result {
+  int32_t status;          /* lann_status of this job */
+  int32_t nonfinite_epoch; /* TrainingError epoch, else -1 */
+  int32_t n_inputs;        /* model inputs I */
+  int32_t n_params;        /* trainable parameters P */
+  int32_t n_train, n_eval; /* sample counts */
+  double final_loss;       /* loss_trace.back() */
+  double mape, mape_thr, rho; /* on the evaluation part */
+  int32_t n_kept;
+  int32_t pad_;
+} lann_job_result;
+
+/* ---- engine ---------------------------------------------------------------- */
+typedef struct lann_engine lann_engine;
+
+int lann_engine_create(int device, lann_engine** out);
+void lann_engine_destroy(lann_engine* engine);
+const char* lann_last_error(const lann_engine* engine);
+/* Device time (ms) of the most recent call's kernels, measured with CUDA
+ * events on the engine stream; 0 if nothing ran. */
+double lann_last_device_ms(const lann_engine* engine);
+/* Number of engine kernels launched by the most recent call. */
+int64_t lann_last_launches(const lann_engine* engine);
+
+/* ---- training (train_full_batch, batched) ----------------------------------
+ * Tiles hold min-max-normalised training rows (NormStats, models.cpp:118-133):
+ * X is [total_rows][LANN_ROW] doubles (columns >= I ignored), y [total_rows].
+ * Models reference a tile; params is the flat reference layout
+ * (L0.w row-major out x in, L0.b, L1.w, L1.b, ...; mlp.cpp:124-131), holding
+ * the initial weights on entry and the trained weights on return. */
+typedef struct lann_train_batch {
+  int32_t n_models;
+  int32_t precision;          /* lann_precision */
+  int32_t n_tiles;
+  const int32_t* tile_rows;   /* N per tile (>= 1) */
+  const int32_t* tile_inputs; /* I per tile (1..7) */
+  const int64_t* tile_offset; /* first row of the tile */
+  int64_t total_rows;
+  const double* X;
+  const double* y;
+  const int32_t* model_tile;
+  const int32_t* model_h1;
+  const int32_t* model_h2;    /* 0 = one hidden layer */
+  const double* model_lr;
+  const int32_t* model_epochs;
+  const int64_t* model_param_offset;
+  int64_t total_params;
+  double* params;             /* in/out */
+  double* final_loss;         /* out [n_models] */
+  int32_t* nonfinite_epoch;   /* out [n_models]: -1 or TrainingError epoch */
+  double* loss_trace;         /* optional out; NULL = not recorded */
+  const int64_t* trace_offset;/* per model offset into loss_trace */
+  int32_t trace_stride;       /* keep epochs e with e % stride == 0 */
+} lann_train_batch;
+
+int lann_train(lann_engine* engine, const lann_train_batch* batch);
+
+/* ---- prediction (models::predict, models.cpp:346-363) ----------------------
+ * Raw (un-normalised) feature rows [n_rows][LANN_ROW]; each row is scored by
+ * row_model[row]. norm = per model {f_min[8], f_max[8], t_min, t_max} = 18 doubles;
+ * output max(denormalize(forward(normalize(x))), 1e-9). */
+typedef struct lann_model_set {
+  int32_t n_models;
+  int32_t precision;
+  const int32_t* n_inputs;
+  const int32_t* h1;
+  const int32_t* h2;
+  const int32_t* log_target;
+  const int64_t* param_offset;
+  const double* params;
+  int64_t total_params;
+  const double* norm;          /* [n_models][18] */
+} lann_model_set;
+
+int lann_predict(lann_engine* engine, const lann_model_set* models, int64_t n_rows,
+                 const double* rows, const int32_t* row_model, double* out);
+
+/* ---- metrics (eval.cpp:26-108) ----------------------------------------------
+ * n_sets independent (truth, pred) sets packed back to back; set i spans
+ * [offset[i], offset[i]+len[i]). Outputs per set. */
+int lann_eval(lann_engine* engine, int32_t n_sets, const int64_t* offset, const int32_t* len,
+              const double* truth, const double* pred, double drop_fraction,
+              double* mape, double* mape_thr, int32_t* n_kept, double* rho);
+
+/* ---- selection ------------------------------------------------------------------
+ * Blur schedule selection (selector.cpp:42-53): candidates [n][4] u32 schedules,
+ * model index 0 of the set, image side n_img. Returns the chosen index and its
+ * predicted runtime; ties go to the lexicographically smaller schedule. */
+int lann_select_schedule(lann_engine* engine, const lann_model_set* models, uint32_t n_img,
+                         int64_t n_cands, const uint32_t* cands, int64_t* chosen,
+                         double* chosen_score);
+
+/* Multi-variant argmin: n_cands candidate shapes of `kind` generated
+ * counter-based from seed (candidate i uses splitmix64 draws from
+ * derive_seed(seed, first + i), same ranges as sample_params), each scored by
+ * every model of the set (a model with with_n_thd[v] = 0 ignores n_thd);
+ * out_idx[i] = argmin variant (ties -> lower index), out_score[i] = its score. */
+int lann_select_variants(lann_engine* engine, const lann_model_set* models,
+                         const int32_t* with_n_thd, int32_t kind, int32_t max_threads,
+                         uint64_t seed, int64_t first, int64_t n_cands,
+                         int32_t* out_idx, double* out_score);
+
+/* ---- synthetic data (datagen::build_dataset + split, datagen.cpp:177-248) ----
+ * feats [count][LANN_ROW] base features (no c), c [count], runtime [count];
+ * order [count] = the split permutation of split(ds, train_fraction, seed). */
+int lann_build_dataset(const lann_world* world, uint64_t seed, int32_t count,
+                       double* feats, uint64_t* c, double* runtime, int32_t* n_features);
+int lann_split_order(int32_t n, uint64_t seed, int64_t* order);
+
+/* Glorot-uniform init (Mlp::init, mlp.cpp:9-25) with Rng(derive_seed(seed, 0xA11CE)). */
+int lann_init_params(int32_t n_dims, const int32_t* dims, uint64_t seed, double* params);
+
+/* ---- whole-population pipeline ----------------------------------------------------
+ * For every job: build dataset -> split -> (fold) -> NormStats -> init ->
+ * train (one batched launch set) -> predict on the evaluation part -> metrics.
+ * params_out (optional) receives trained weights at results-indexed offsets
+ * params_offset[j]; trace (optional) full loss traces at trace_offset[j]. */
+int lann_run_population(lann_engine* engine, int32_t n_jobs, const lann_job* jobs,
+                        int32_t precision, lann_job_result* results,
+                        double* params_out, const int64_t* params_offset,
+                        double* trace_out, const int64_t* trace_offset);
+
+/* The 48 kernel-variant-hardware combinations of BASELINE config 2 (worlds
+ * only). Writes up to cap entries, returns the count. */
+int lann_default_combos(lann_world* out, int32_t cap);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LANN_ENGINE_H */

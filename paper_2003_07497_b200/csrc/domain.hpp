@@ -1,0 +1,116 @@
+// domain.hpp — host-side domain logic of the engine (C++20): seeded sampling of
+// kernel instances, the synthetic runtime worlds, dataset split / k-fold,
+// min-max normalisation and Glorot init. Everything here is the engine's own
+// code (not linked to the reference); each function names the reference
+// behaviour it must reproduce bit for bit (paths relative to
+// /root/reference/proj/core/).
+#pragma once
+
+#include <cstdint>
+#include <random>
+#include <span>
+#include <string>
+#include <vector>
+
+#include "../../include/lann_engine.h"
+
+namespace lann {
+
+// ---- errors carried as status codes through the C ABI ------------------------------
+struct Status {
+  int code = LANN_OK;
+  std::string msg;
+  int epoch = -1;
+  explicit operator bool() const { return code != LANN_OK; }
+};
+
+// ---- rng.hpp:10-63 -------------------------------------------------------------------
+inline std::uint64_t splitmix64(std::uint64_t& s) {
+  std::uint64_t z = (s += 0x9e3779b97f4a7c15ULL);
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+inline std::uint64_t derive_seed(std::uint64_t root, std::uint64_t stream) {
+  std::uint64_t s = root ^ (0x9e3779b97f4a7c15ULL * (stream + 1));
+  splitmix64(s);
+  return splitmix64(s);
+}
+
+// Sequential stream (mt19937_64) with the reference's hand-rolled draws.
+class SeqRng {
+ public:
+  explicit SeqRng(std::uint64_t seed) : e_(seed) {}
+  std::uint64_t next() { return e_(); }
+  std::uint64_t bounded(std::uint64_t n) {
+    const std::uint64_t thr = (0 - n) % n;
+    for (;;) {
+      const std::uint64_t r = e_();
+      if (r >= thr) return r % n;
+    }
+  }
+  double uniform() { return double(e_() >> 11) * 0x1.0p-53; }
+  double uniform(double lo, double hi) { return lo + (hi - lo) * uniform(); }
+
+ private:
+  std::mt19937_64 e_;
+};
+
+// ---- kernel instances (kernels.hpp:84-116) -----------------------------------------------
+struct Instance {
+  int kind = LANN_MM;
+  std::uint32_t m = 0, n = 0, k = 0, r = 0, s = 0;
+  double d1 = 1.0, d2 = 1.0, d = 1.0;
+  int n_thd = 1;
+  std::uint32_t sched[4] = {0, 0, 0, 0};
+};
+
+std::uint64_t complexity(const Instance& p);                          // kernels.cpp:184-206
+int base_features(const Instance& p, bool with_n_thd, double* out);   // features.cpp:23-54
+int base_feature_count(int kind, bool with_n_thd);                    // features.cpp:10-21
+const std::vector<std::uint32_t>& schedule_lattice(int gpu_style);    // kernels.cpp:77-87
+Instance sample_instance(int kind, int max_threads, int gpu_lattice, SeqRng& rng);  // datagen.cpp:60-110
+
+// ---- datasets ------------------------------------------------------------------------------
+struct Dataset {
+  int kind = LANN_MM;
+  int n_features = 0;               // base features (no c)
+  std::vector<double> feats;        // [n][LANN_ROW]
+  std::vector<std::uint64_t> c;
+  std::vector<double> runtime;
+  int size() const { return int(runtime.size()); }
+};
+
+Status build_dataset(const lann_world& w, std::uint64_t seed, int count, Dataset& out);  // datagen.cpp:177-223
+Status split_order(int n, double frac, std::uint64_t seed, std::vector<std::int64_t>& order,
+                   int& n_train);                                                      // datagen.cpp:225-248
+
+// Training tile of one model: model-input rows (features [+ c]) normalised with the
+// tile's own NormStats (models.cpp:89-133), plus the raw evaluation rows.
+struct Tile {
+  int n_inputs = 0;
+  bool log_target = false;
+  double norm[18] = {0};                 // f_min[8], f_max[8], t_min, t_max
+  std::vector<double> Xn, yn;            // [n_train][LANN_ROW], [n_train]
+  std::vector<double> eval_rows;         // raw model inputs [n_eval][LANN_ROW]
+  std::vector<double> eval_truth;        // [n_eval]
+  int n_train() const { return int(yn.size()); }
+  int n_eval() const { return int(eval_truth.size()); }
+};
+
+Status make_tile(const Dataset& ds, const std::vector<std::int64_t>& order, int n_train,
+                 int n_folds, int fold, int family, bool log_target, Tile& out);
+
+// ---- models ---------------------------------------------------------------------------------
+int param_count(int n_inputs, int h1, int h2);                            // models.cpp:37-46
+Status validate_config(const lann_job& j, int n_inputs);                  // models.cpp:48-64
+void glorot_init(int n_inputs, int h1, int h2, std::uint64_t seed, double* params);  // mlp.cpp:9-25
+
+// Adam bias-correction table: bc[2t] = 1 - 0.9^(t+1), bc[2t+1] = 1 - 0.999^(t+1)
+// evaluated with the host libm's pow exactly as AdamState::update does (mlp.cpp:144-146).
+const std::vector<double>& adam_bias_table(int epochs);
+
+// The 48 kernel-variant-hardware combinations (config 2); see DESIGN.md.
+std::vector<lann_world> default_combos();
+
+}  // namespace lann

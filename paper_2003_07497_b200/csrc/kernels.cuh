@@ -1,0 +1,116 @@
+// kernels.cuh — device-side argument blocks shared by the engine's CUDA kernels
+// and the host launcher (engine.cpp). Plain structs of device pointers.
+#pragma once
+
+#include <cstdint>
+
+#include <cuda_runtime.h>
+
+namespace lann {
+
+// One launch of the trainer over a population (see lann_train_batch).
+struct TrainArgs {
+  int n_models;
+  const int* order;          // model processing order (longest first)
+  const int* tile_rows;
+  const int* tile_inputs;
+  const int64_t* tile_offset;
+  const double* X;           // [rows][8] normalised inputs
+  const double* y;           // [rows]
+  const int* model_tile;
+  const int* h1;
+  const int* h2;
+  const double* lr;
+  const int* epochs;
+  const int64_t* param_offset;
+  double* params;            // in/out
+  double* final_loss;
+  int* nonfinite_epoch;
+  double* loss_trace;        // may be null
+  const int64_t* trace_offset;
+  int trace_stride;
+  const double2* bias_corr;  // [max_epochs] {1-0.9^t, 1-0.999^t} from the host libm
+  double* scratch;           // global per-sample records for models too big for smem
+  const int64_t* scratch_offset;
+  int smem_records;          // 1: per-sample records live in shared memory
+};
+
+// FP32 throughput trainer: models grouped into warps that share one tile.
+struct TrainF32Args {
+  int n_groups;
+  const int* group_first;    // first model (index into the sorted model list) of each group
+  const int* group_count;    // models in the group (<= 32 / lanes-per-model)
+  const int* sorted_model;   // engine model index for each sorted slot
+  const float* rows;         // [rows][8]: x0..x6 (padded), y at column 7
+  const int* tile_rows;
+  const int64_t* tile_offset;
+  const int* model_tile;
+  const double* lr;
+  const int* epochs;
+  const int64_t* param_offset;
+  double* params;            // in/out (fp64 in the ABI, fp32 inside)
+  double* final_loss;
+  int* nonfinite_epoch;
+  double* loss_trace;
+  const int64_t* trace_offset;
+  int trace_stride;
+};
+
+// Prediction over rows (models.cpp:346-363).
+struct PredictArgs {
+  int64_t n_rows;
+  const double* rows;        // raw model inputs [n][8]
+  const int* row_model;
+  const int* n_inputs;
+  const int* h1;
+  const int* h2;
+  const int* log_target;
+  const int64_t* param_offset;
+  const double* params;
+  const double* norm;        // [models][18]
+  double* out;
+};
+
+// Metrics over packed (truth, pred) sets (eval.cpp:26-90).
+struct EvalArgs {
+  int n_sets;
+  const int64_t* offset;
+  const int* len;
+  const double* truth;
+  const double* pred;
+  double drop_fraction;
+  double* mape;
+  double* mape_thr;
+  int* n_kept;
+  double* rho;
+  int* status;
+};
+
+void launch_train_fp64(const TrainArgs& a, int max_p, int dyn_bytes, cudaStream_t s);
+// bytes of one per-sample record of the FP64 trainer for a shape (see train_fp64.cu)
+int fp64_record_doubles(int in, int h1, int h2);
+bool launch_train_fp32(const TrainF32Args& a, int in, int h1, int h2, int lanes, int tile_bytes,
+                       cudaStream_t s);
+bool fp32_shape_supported(int in, int h1, int h2);
+void launch_predict_fp64(const PredictArgs& a, cudaStream_t s);
+void launch_predict_fp32(const PredictArgs& a, cudaStream_t s);
+void launch_eval(const EvalArgs& a, int max_len, cudaStream_t s);
+
+}  // namespace lann
+
+namespace lann {
+// select.cu
+int select_schedule_launch(int64_t n, const uint32_t* d_cands, uint32_t n_img, int I, int H1,
+                           int H2, int logt, const double* d_w, const double* d_nrm,
+                           double* d_blk_score, int64_t* d_blk_idx, cudaStream_t s);
+bool select_variants_supported(int n_models, int max_params);
+int select_variants_launch(int n_models, int precision, int kind, int max_threads, uint64_t seed,
+                           int64_t first, int64_t n, const int* d_in, const int* d_h1,
+                           const int* d_h2, const int* d_logt, const int* d_thd,
+                           const int64_t* d_poff, const double* d_params, const double* d_norm,
+                           int* d_idx, double* d_score, int sms, cudaStream_t s);
+}  // namespace lann
+
+namespace lann {
+void launch_pack_rows(const double* X, const double* y, int64_t n, float* out, cudaStream_t s);
+}  // namespace lann

@@ -1,0 +1,302 @@
+// train_fp32.cu — K1b: the FP32 throughput LANN trainer.
+//
+// Same algorithm as models::train_full_batch (mlp.cpp:156-175): full-batch
+// MSE gradient (mlp.cpp:75-122) + Adam(0.9, 0.999, 1e-8) (mlp.cpp:142-154),
+// loss recorded before each update, training stopped at the first non-finite
+// loss. Differences from the FP64 parity kernel: FP32 FMA arithmetic and a
+// tree (shuffle) reduction over samples, so traces agree with the reference
+// only up to FP32 rounding.
+//
+// Mapping: one warp per CTA; the warp trains 32/K models that share one
+// training tile (same kernel-variant-hardware combination and fold, different
+// init seeds); each model is spread over K lanes that split its samples.
+//   * the tile (N rows x 8 floats, y in column 7) is staged ONCE into shared
+//     memory by a TMA bulk copy (cp.async.bulk + mbarrier) and re-read from
+//     there for every epoch: HBM traffic per model-epoch ~ 0;
+//   * weights and gradient accumulators live in registers (fully unrolled for
+//     the compile-time shape); Adam moments in shared memory [param][lane];
+//   * with K = 1 all 32 lanes read the same row (shared-memory broadcast);
+//     with K > 1 the K per-lane partial gradients are summed by a shuffle
+//     butterfly, after which every lane applies the identical Adam step.
+#include <cmath>
+#include <cstdint>
+
+#include "kernels.cuh"
+
+namespace lann {
+namespace {
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// TMA 1-D bulk copy global -> shared, completion tracked by an mbarrier.
+__device__ __forceinline__ void tma_load_tile(void* dst, const void* src, uint32_t bytes,
+                                              uint64_t* bar) {
+  const uint32_t b = smem_addr(bar);
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes) : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(b)
+      : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  const uint32_t b = smem_addr(bar);
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(b),
+      "r"(phase)
+      : "memory");
+}
+
+template <int I, int H1, int H2>
+struct Net {
+  static constexpr int L1W = 0;                        // [H1][I]
+  static constexpr int L1B = I * H1;                   // [H1]
+  static constexpr int L2W = L1B + H1;                 // [H2][H1] or output [H1]
+  static constexpr int L2B = H2 > 0 ? L2W + H1 * H2 : L2W + H1;
+  static constexpr int L3W = L2B + (H2 > 0 ? H2 : 1);  // output [H2] (2 hidden)
+  static constexpr int L3B = H2 > 0 ? L3W + H2 : L3W;
+  static constexpr int P = H2 > 0 ? L3B + 1 : L2B + 1;
+};
+
+template <int I, int H1, int H2, int K>
+__global__ void __launch_bounds__(32) train_fp32_kernel(TrainF32Args a) {
+  using N = Net<I, H1, H2>;
+  constexpr int P = N::P;
+  constexpr int G = 32 / K;  // models per warp
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ uint64_t bar;
+  const int lane = threadIdx.x;
+  const int g = blockIdx.x;
+  const int first = a.group_first[g];
+  const int count = a.group_count[g];
+  const int slot = lane / K, sub = lane % K;
+  const bool active = slot < count;
+  const int m = a.sorted_model[first + (active ? slot : 0)];
+  const int tile = a.model_tile[m];
+  const int rows = a.tile_rows[tile];
+  const int E = a.epochs[m];
+
+  float* trow = reinterpret_cast<float*>(smem_raw);  // [rows][8]
+  float* adam = trow + (size_t)rows * 8;            // [2][P][32]
+  if (lane == 0) tma_load_tile(trow, a.rows + a.tile_offset[tile] * 8, (uint32_t)rows * 32u, &bar);
+
+  float w[P], gr[P];
+  const double* gp = a.params + a.param_offset[m];
+#pragma unroll
+  for (int p = 0; p < P; ++p) {
+    w[p] = (float)gp[p];
+    adam[p * 32 + lane] = 0.f;
+    adam[(P + p) * 32 + lane] = 0.f;
+  }
+  const float lr = (float)a.lr[m];
+  const float scale = 2.0f / (float)rows;  // d(mean err^2)/d out = 2 err / N
+  const float inv_n = 1.0f / (float)rows;
+  double* trace = (a.loss_trace && active) ? a.loss_trace + a.trace_offset[m] : nullptr;
+  int bad = -1;
+  float last = 0.f;
+  mbar_wait(&bar, 0);
+  __syncwarp();
+
+  for (int e = 0; e < E; ++e) {
+#pragma unroll
+    for (int p = 0; p < P; ++p) gr[p] = 0.f;
+    float loss = 0.f;
+    for (int s = sub; s < rows; s += K) {
+      const float4 lo = *reinterpret_cast<const float4*>(trow + s * 8);
+      const float4 hi = *reinterpret_cast<const float4*>(trow + s * 8 + 4);
+      const float xv[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
+      // forward
+      float z1[H1];
+#pragma unroll
+      for (int h = 0; h < H1; ++h) {
+        float z = w[N::L1B + h];
+#pragma unroll
+        for (int i = 0; i < I; ++i) z = fmaf(w[N::L1W + h * I + i], xv[i], z);
+        z1[h] = fmaxf(z, 0.f);
+      }
+      float out;
+      float z2[H2 > 0 ? H2 : 1];
+      if constexpr (H2 > 0) {
+#pragma unroll
+        for (int o = 0; o < H2; ++o) {
+          float z = w[N::L2B + o];
+#pragma unroll
+          for (int h = 0; h < H1; ++h) z = fmaf(w[N::L2W + o * H1 + h], z1[h], z);
+          z2[o] = fmaxf(z, 0.f);
+        }
+        float acc0 = w[N::L3B], acc1 = 0.f;
+#pragma unroll
+        for (int o = 0; o < H2; ++o) {
+          if (o & 1) acc1 = fmaf(w[N::L3W + o], z2[o], acc1);
+          else acc0 = fmaf(w[N::L3W + o], z2[o], acc0);
+        }
+        out = acc0 + acc1;
+      } else {
+        float acc0 = w[N::L2B], acc1 = 0.f;
+#pragma unroll
+        for (int h = 0; h < H1; ++h) {
+          if (h & 1) acc1 = fmaf(w[N::L2W + h], z1[h], acc1);
+          else acc0 = fmaf(w[N::L2W + h], z1[h], acc0);
+        }
+        out = acc0 + acc1;
+      }
+      const float err = out - xv[7];
+      loss = fmaf(err, err, loss);
+      const float d = err * scale;
+      // backward
+      if constexpr (H2 > 0) {
+        gr[N::L3B] += d;
+        float d2[H2];
+#pragma unroll
+        for (int o = 0; o < H2; ++o) {
+          gr[N::L3W + o] = fmaf(d, z2[o], gr[N::L3W + o]);
+          d2[o] = z2[o] > 0.f ? w[N::L3W + o] * d : 0.f;
+          gr[N::L2B + o] += d2[o];
+        }
+#pragma unroll
+        for (int h = 0; h < H1; ++h) {
+          float acc = 0.f;
+#pragma unroll
+          for (int o = 0; o < H2; ++o) {
+            gr[N::L2W + o * H1 + h] = fmaf(d2[o], z1[h], gr[N::L2W + o * H1 + h]);
+            acc = fmaf(w[N::L2W + o * H1 + h], d2[o], acc);
+          }
+          const float d1 = z1[h] > 0.f ? acc : 0.f;
+          gr[N::L1B + h] += d1;
+#pragma unroll
+          for (int i = 0; i < I; ++i) gr[N::L1W + h * I + i] = fmaf(d1, xv[i], gr[N::L1W + h * I + i]);
+        }
+      } else {
+        gr[N::L2B] += d;
+#pragma unroll
+        for (int h = 0; h < H1; ++h) {
+          gr[N::L2W + h] = fmaf(d, z1[h], gr[N::L2W + h]);
+          const float d1 = z1[h] > 0.f ? w[N::L2W + h] * d : 0.f;
+          gr[N::L1B + h] += d1;
+#pragma unroll
+          for (int i = 0; i < I; ++i) gr[N::L1W + h * I + i] = fmaf(d1, xv[i], gr[N::L1W + h * I + i]);
+        }
+      }
+    }
+    // sum the K per-lane partials of each model (lanes slot*K .. slot*K+K-1)
+#pragma unroll
+    for (int off = 1; off < K; off <<= 1) {
+#pragma unroll
+      for (int p = 0; p < P; ++p) gr[p] += __shfl_xor_sync(0xffffffffu, gr[p], off);
+      loss += __shfl_xor_sync(0xffffffffu, loss, off);
+    }
+    loss *= inv_n;
+    if (bad < 0) {
+      last = loss;
+      if (trace && sub == 0 && (e % a.trace_stride) == 0) trace[e / a.trace_stride] = (double)loss;
+      if (!isfinite(loss)) {
+        bad = e;  // TrainingError(epoch): freeze, keep the warp converged
+      } else {
+        // Adam (mlp.cpp:142-154); bias corrections 1 - beta^t in FP32
+        const float t = (float)(e + 1);
+        const float bc1 = 1.f - exp2f(t * -0.15200309344504997f);   // log2(0.9)
+        const float bc2 = 1.f - exp2f(t * -0.0014434168696687106f);  // log2(0.999)
+        const float step = lr / bc1, rb2 = 1.f / bc2;
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+          float& mo = adam[p * 32 + lane];
+          float& ve = adam[(P + p) * 32 + lane];
+          const float mk = fmaf(0.1f, gr[p], 0.9f * mo);
+          const float vk = fmaf(0.001f * gr[p], gr[p], 0.999f * ve);
+          mo = mk;
+          ve = vk;
+          w[p] -= step * mk / (sqrtf(vk * rb2) + 1e-8f);
+        }
+      }
+    }
+  }
+  if (active && sub == 0) {
+    double* outp = a.params + a.param_offset[m];
+#pragma unroll
+    for (int p = 0; p < P; ++p) outp[p] = (double)w[p];
+    a.final_loss[m] = (double)last;
+    a.nonfinite_epoch[m] = bad;
+  }
+}
+
+// dynamic smem = the largest tile of the launch (rows x 32 B) + Adam moments
+template <int I, int H1, int H2, int K>
+void launch_k(const TrainF32Args& a, int tile_bytes, cudaStream_t s) {
+  constexpr int P = Net<I, H1, H2>::P;
+  auto kern = train_fp32_kernel<I, H1, H2, K>;
+  const int dyn = tile_bytes + 2 * P * 32 * 4;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
+  kern<<<a.n_groups, 32, dyn, s>>>(a);
+}
+
+template <int I, int H1, int H2>
+bool dispatch_lanes(const TrainF32Args& a, int lanes, int tile_bytes, cudaStream_t s) {
+  switch (lanes) {
+    case 1: launch_k<I, H1, H2, 1>(a, tile_bytes, s); return true;
+    case 2: launch_k<I, H1, H2, 2>(a, tile_bytes, s); return true;
+    case 4: launch_k<I, H1, H2, 4>(a, tile_bytes, s); return true;
+    case 8: launch_k<I, H1, H2, 8>(a, tile_bytes, s); return true;
+    case 32: launch_k<I, H1, H2, 32>(a, tile_bytes, s); return true;
+    default: return false;
+  }
+}
+
+}  // namespace
+
+bool fp32_shape_supported(int in, int h1, int h2) {
+  if (h1 == 8 && h2 == 0) return in >= 1 && in <= 7;
+  if (h1 == 5 && h2 == 5) return in >= 4 && in <= 6;
+  return false;
+}
+
+bool launch_train_fp32(const TrainF32Args& a, int in, int h1, int h2, int lanes, int tile_bytes,
+                       cudaStream_t s) {
+  if (h1 == 8 && h2 == 0) {
+    switch (in) {
+      case 1: return dispatch_lanes<1, 8, 0>(a, lanes, tile_bytes, s);
+      case 2: return dispatch_lanes<2, 8, 0>(a, lanes, tile_bytes, s);
+      case 3: return dispatch_lanes<3, 8, 0>(a, lanes, tile_bytes, s);
+      case 4: return dispatch_lanes<4, 8, 0>(a, lanes, tile_bytes, s);
+      case 5: return dispatch_lanes<5, 8, 0>(a, lanes, tile_bytes, s);
+      case 6: return dispatch_lanes<6, 8, 0>(a, lanes, tile_bytes, s);
+      case 7: return dispatch_lanes<7, 8, 0>(a, lanes, tile_bytes, s);
+    }
+  } else if (h1 == 5 && h2 == 5) {
+    switch (in) {
+      case 4: return dispatch_lanes<4, 5, 5>(a, lanes, tile_bytes, s);
+      case 5: return dispatch_lanes<5, 5, 5>(a, lanes, tile_bytes, s);
+      case 6: return dispatch_lanes<6, 5, 5>(a, lanes, tile_bytes, s);
+    }
+  }
+  return false;
+}
+
+}  // namespace lann
+
+namespace lann {
+namespace {
+__global__ void pack_rows_kernel(const double* X, const double* y, int64_t n, float* out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n * 8) return;
+  const int64_t r = i / 8;
+  const int c = (int)(i % 8);
+  out[i] = c == 7 ? (float)y[r] : (float)X[i];
+}
+}  // namespace
+
+// FP32 rows [n][8] = normalised inputs x0..x6 with the target in column 7.
+void launch_pack_rows(const double* X, const double* y, int64_t n, float* out, cudaStream_t s) {
+  if (n <= 0) return;
+  pack_rows_kernel<<<(unsigned)((n * 8 + 255) / 256), 256, 0, s>>>(X, y, n, out);
+}
+}  // namespace lann

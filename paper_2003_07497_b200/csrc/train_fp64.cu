@@ -1,0 +1,246 @@
+// train_fp64.cu — K1a: the FP64 exact-order LANN trainer ("parity mode").
+//
+// Reproduces models::train_full_batch (mlp.cpp:156-175) bit for bit: the same
+// forward order (mlp.cpp:36-52), the same per-sample delta recursion
+// (mlp.cpp:93-104), the same SEQUENTIAL per-parameter gradient accumulation
+// over samples (mlp.cpp:106-118), the same Adam expression order
+// (mlp.cpp:142-154) and the pre-update loss trace / non-finite check.
+// Built with -fmad=false and written with explicit __d*_rn intrinsics so no
+// multiply-add is ever contracted (the reference object code has no FMA).
+//
+// Mapping (one CTA per model, models ordered longest-first):
+//   phase A  threads own SAMPLES: forward + backward for their samples, writing a
+//            per-sample record {x, hidden activations, inv_n*delta, err^2};
+//   phase B  threads own PARAMETERS: each sums its N per-sample terms in sample
+//            order (the only order-sensitive reduction), then applies Adam;
+//            one thread sums the loss terms in sample order.
+// Two __syncthreads per epoch. The N-long dependent DADD chain (8 cycles each)
+// bounds the epoch latency; several CTAs per SM overlap their chains.
+#include <cmath>
+
+#include "kernels.cuh"
+
+namespace lann {
+namespace {
+
+constexpr int kMaxKB = 8;  // parameters owned per thread in phase B (P <= 8 * blockDim)
+
+struct Shape {
+  int I, H1, H2, nl, P, R;
+  int dims[4];
+  int woff[3], boff[3];
+  int inoff[3];  // record offset of each layer's input vector
+  int toff[3];   // record offset of each layer's (scaled) deltas
+  int e2;        // record offset of err^2
+};
+
+__device__ Shape make_shape(int I, int H1, int H2) {
+  Shape s;
+  s.I = I;
+  s.H1 = H1;
+  s.H2 = H2;
+  s.nl = H2 > 0 ? 3 : 2;
+  s.dims[0] = I;
+  s.dims[1] = H1;
+  s.dims[2] = H2 > 0 ? H2 : 1;
+  s.dims[3] = 1;
+  int off = 0;
+  for (int l = 0; l < s.nl; ++l) {
+    s.woff[l] = off;
+    off += s.dims[l] * s.dims[l + 1];
+    s.boff[l] = off;
+    off += s.dims[l + 1];
+  }
+  s.P = off;
+  const int hidden = H1 + (H2 > 0 ? H2 : 0);
+  s.inoff[0] = 0;
+  s.inoff[1] = 8;
+  s.inoff[2] = 8 + H1;
+  const int t0 = 8 + hidden;
+  s.toff[0] = t0;
+  s.toff[1] = t0 + s.dims[1];
+  s.toff[2] = t0 + s.dims[1] + s.dims[2];
+  s.e2 = t0 + hidden + 1;
+  s.R = (s.e2 + 1) | 1;  // odd stride: 2-way (minimal) bank pattern for 8-byte accesses
+  return s;
+}
+
+template <int KB>
+__global__ void __launch_bounds__(256) train_fp64_exact(TrainArgs a) {
+  extern __shared__ double smem[];
+  const int m = a.order[blockIdx.x];
+  const int tile = a.model_tile[m];
+  const int N = a.tile_rows[tile];
+  const int E = a.epochs[m];
+  const double lr = a.lr[m];
+  const Shape sh = make_shape(a.tile_inputs[tile], a.h1[m], a.h2[m]);
+  const int P = sh.P;
+  const int tid = threadIdx.x, nt = blockDim.x;
+
+  double* w = smem;           // [P]
+  double* mom = w + P;        // [P] Adam m
+  double* vel = mom + P;      // [P] Adam v
+  double* Ls = vel + P;       // [1] epoch loss
+  double* rec = a.smem_records ? (Ls + 2) : (a.scratch + a.scratch_offset[m]);
+  const int R = sh.R;
+
+  const double* gp = a.params + a.param_offset[m];
+  for (int p = tid; p < P; p += nt) {
+    w[p] = gp[p];
+    mom[p] = 0.0;
+    vel[p] = 0.0;
+  }
+  const double* X = a.X + a.tile_offset[tile] * 8;
+  const double* Y = a.y + a.tile_offset[tile];
+  for (int s = tid; s < N; s += nt)
+    for (int i = 0; i < 8; ++i) rec[(size_t)s * R + i] = X[(size_t)s * 8 + i];
+
+  // phase-B ownership: parameter p -> (record offset of its delta, of its input or -1)
+  int tix[KB], aix[KB];
+#pragma unroll
+  for (int k = 0; k < KB; ++k) {
+    const int p = tid + k * nt;
+    tix[k] = -1;
+    aix[k] = -1;
+    if (p < P) {
+      for (int l = 0; l < sh.nl; ++l) {
+        const int in = sh.dims[l], out = sh.dims[l + 1];
+        if (p >= sh.woff[l] && p < sh.boff[l]) {
+          const int q = p - sh.woff[l];
+          tix[k] = sh.toff[l] + q / in;
+          aix[k] = sh.inoff[l] + q % in;
+        } else if (p >= sh.boff[l] && p < sh.boff[l] + out) {
+          tix[k] = sh.toff[l] + (p - sh.boff[l]);
+        }
+      }
+    }
+  }
+  const int loss_tid = nt - 1;
+  const double inv_n = 1.0 / (double)N;  // mlp.cpp:84
+  const double beta1 = 0.9, beta2 = 0.999, eps = 1e-8;
+  const double c1 = 1.0 - beta1, c2 = 1.0 - beta2;
+  double* trace = a.loss_trace ? a.loss_trace + a.trace_offset[m] : nullptr;
+  int bad = -1;
+  double last = 0.0;
+  __syncthreads();
+
+  for (int e = 0; e < E; ++e) {
+    // ---- phase A: per-sample forward / backward (mlp.cpp:86-104) ----
+    for (int s = tid; s < N; s += nt) {
+      double* r = rec + (size_t)s * R;
+      for (int l = 0; l < sh.nl; ++l) {
+        const int in = sh.dims[l], out = sh.dims[l + 1];
+        const double* wl = w + sh.woff[l];
+        const double* bl = w + sh.boff[l];
+        const double* ain = r + sh.inoff[l];
+        if (l + 1 < sh.nl) {
+          double* aout = r + sh.inoff[l + 1];
+          for (int o = 0; o < out; ++o) {
+            double z = bl[o];
+            for (int i = 0; i < in; ++i) z = __dadd_rn(z, __dmul_rn(wl[o * in + i], ain[i]));
+            aout[o] = z > 0.0 ? z : 0.0;
+          }
+        } else {
+          double z = bl[0];
+          for (int i = 0; i < in; ++i) z = __dadd_rn(z, __dmul_rn(wl[i], ain[i]));
+          const double err = __dsub_rn(z, Y[s]);
+          r[sh.e2] = __dmul_rn(err, err);
+          r[sh.toff[l]] = __dmul_rn(2.0, err);  // unscaled output delta (mlp.cpp:92)
+        }
+      }
+      // hidden deltas, unscaled, from the next layer's unscaled deltas
+      for (int l = sh.nl - 2; l >= 0; --l) {
+        const int nin = sh.dims[l + 1], nout = sh.dims[l + 2];
+        const double* wn = w + sh.woff[l + 1];
+        const double* dn = r + sh.toff[l + 1];
+        const double* act = r + sh.inoff[l + 1];
+        double* d = r + sh.toff[l];
+        for (int i = 0; i < nin; ++i) {
+          double acc = 0.0;
+          for (int o = 0; o < nout; ++o) acc = __dadd_rn(acc, __dmul_rn(wn[o * nin + i], dn[o]));
+          d[i] = act[i] > 0.0 ? acc : 0.0;
+        }
+      }
+      // scale in place: t = inv_n * delta (the left factor of mlp.cpp:113,117)
+      const int nd = sh.e2 - sh.toff[0];
+      for (int j = 0; j < nd; ++j) r[sh.toff[0] + j] = __dmul_rn(inv_n, r[sh.toff[0] + j]);
+    }
+    __syncthreads();
+
+    // ---- phase B: sequential per-parameter sums + Adam (mlp.cpp:106-118, 142-154) ----
+    double g[KB];
+#pragma unroll
+    for (int k = 0; k < KB; ++k) g[k] = 0.0;
+    if (tix[0] >= 0) {
+      for (int s = 0; s < N; ++s) {
+        const double* r = rec + (size_t)s * R;
+#pragma unroll
+        for (int k = 0; k < KB; ++k) {
+          if (tix[k] >= 0) {
+            const double t = r[tix[k]];
+            g[k] = __dadd_rn(g[k], aix[k] >= 0 ? __dmul_rn(t, r[aix[k]]) : t);
+          }
+        }
+      }
+      const double2 bc = a.bias_corr[e];
+#pragma unroll
+      for (int k = 0; k < KB; ++k) {
+        const int p = tid + k * nt;
+        if (tix[k] >= 0) {
+          const double mk = __dadd_rn(__dmul_rn(beta1, mom[p]), __dmul_rn(c1, g[k]));
+          const double vk = __dadd_rn(__dmul_rn(beta2, vel[p]), __dmul_rn(__dmul_rn(c2, g[k]), g[k]));
+          mom[p] = mk;
+          vel[p] = vk;
+          const double mhat = __ddiv_rn(mk, bc.x);
+          const double vhat = __ddiv_rn(vk, bc.y);
+          w[p] = __dsub_rn(w[p], __ddiv_rn(__dmul_rn(lr, mhat), __dadd_rn(__dsqrt_rn(vhat), eps)));
+        }
+      }
+    }
+    if (tid == loss_tid) {
+      double L = 0.0;
+      for (int s = 0; s < N; ++s) L = __dadd_rn(L, rec[(size_t)s * R + sh.e2]);
+      L = __dmul_rn(L, inv_n);  // mlp.cpp:120
+      Ls[0] = L;
+      if (trace && (e % a.trace_stride) == 0) trace[e / a.trace_stride] = L;
+    }
+    __syncthreads();
+    last = Ls[0];
+    if (!isfinite(last)) {  // mlp.cpp:166-169: TrainingError(epoch) before the update
+      bad = e;
+      break;
+    }
+  }
+
+  double* outp = a.params + a.param_offset[m];
+  for (int p = tid; p < P; p += nt) outp[p] = w[p];
+  if (tid == 0) {
+    a.final_loss[m] = last;
+    a.nonfinite_epoch[m] = bad;
+  }
+}
+
+}  // namespace
+
+int fp64_record_doubles(int in, int h1, int h2) {
+  (void)in;
+  const int hidden = h1 + (h2 > 0 ? h2 : 0);
+  return (8 + hidden + hidden + 1 + 1) | 1;  // == make_shape().R
+}
+
+// Dynamic shared memory = (3P + 2) doubles of model state, plus the per-sample
+// records when a.smem_records is set; the host sizes dyn_bytes for the largest model.
+void launch_train_fp64(const TrainArgs& a, int max_p, int dyn_bytes, cudaStream_t s) {
+  const int block = 256;
+  const int kb = (max_p + block - 1) / block;
+  auto go = [&](auto kern) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_bytes);
+    kern<<<a.n_models, block, dyn_bytes, s>>>(a);
+  };
+  if (kb <= 1) go(train_fp64_exact<1>);
+  else if (kb <= 2) go(train_fp64_exact<2>);
+  else if (kb <= 4) go(train_fp64_exact<4>);
+  else go(train_fp64_exact<kMaxKB>);
+}
+
+}  // namespace lann

@@ -1,0 +1,326 @@
+"""Python host binding of the engine's C ABI (include/lann_engine.h) via ctypes.
+
+The compute path is the in-tree CUDA library ``lib/libperfsage_b200.so``. There is no
+Python or CPU fallback: if the library is missing, loading fails loudly; if no CUDA
+device is present, ``Engine()`` raises ``NoDeviceError``.
+
+Error behaviour mirrors the reference's exceptions (include/perfsage/errors.hpp):
+status codes are re-raised as ``ParamError``, ``SchemaError``, ``TrainingError``
+(with ``.epoch``), ``DomainError`` and ``BuildAbortError``.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+from . import abi
+from .abi import ROW, Job, JobResult, ModelSet, TrainBatch, World
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libperfsage_b200.so")
+
+
+class Error(RuntimeError):
+    """perfsage::Error"""
+
+
+class ParamError(Error):
+    pass
+
+
+class SchemaError(Error):
+    pass
+
+
+class DomainError(Error):
+    pass
+
+
+class BuildAbortError(Error):
+    pass
+
+
+class CudaError(Error):
+    pass
+
+
+class NoDeviceError(Error):
+    pass
+
+
+class TrainingError(Error):
+    def __init__(self, msg, epoch):
+        super().__init__(msg)
+        self.epoch = epoch
+
+
+_ERR = {abi.PARAM_ERROR: ParamError, abi.SCHEMA_ERROR: SchemaError, abi.DOMAIN_ERROR: DomainError,
+        abi.BUILD_ABORT: BuildAbortError, abi.CUDA_ERROR: CudaError, abi.NO_DEVICE: NoDeviceError}
+
+_lib = None
+
+# every symbol include/lann_engine.h declares
+EXPORTS = ["lann_engine_create", "lann_engine_destroy", "lann_last_error", "lann_last_device_ms",
+           "lann_last_launches", "lann_train", "lann_predict", "lann_eval", "lann_select_schedule",
+           "lann_select_variants", "lann_build_dataset", "lann_split_order", "lann_init_params",
+           "lann_run_population", "lann_default_combos"]
+
+
+def load_library(path: str = LIB_PATH):
+    """Load the engine's shared library (raises OSError if it was not built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise OSError(f"engine library {path} is missing: run __graft_entry__.build() / make -C "
+                      f"paper_2003_07497_b200/csrc")
+    L = C.CDLL(path)
+    vp = C.c_void_p
+    L.lann_engine_create.argtypes = [C.c_int, C.POINTER(vp)]
+    L.lann_engine_destroy.argtypes = [vp]
+    L.lann_last_error.argtypes = [vp]
+    L.lann_last_error.restype = C.c_char_p
+    L.lann_last_device_ms.argtypes = [vp]
+    L.lann_last_device_ms.restype = C.c_double
+    L.lann_last_launches.argtypes = [vp]
+    L.lann_last_launches.restype = C.c_int64
+    L.lann_train.argtypes = [vp, C.POINTER(TrainBatch)]
+    L.lann_predict.argtypes = [vp, C.POINTER(ModelSet), C.c_int64, vp, vp, vp]
+    L.lann_eval.argtypes = [vp, C.c_int32, vp, vp, vp, vp, C.c_double, vp, vp, vp, vp]
+    L.lann_select_schedule.argtypes = [vp, C.POINTER(ModelSet), C.c_uint32, C.c_int64, vp, vp, vp]
+    L.lann_select_variants.argtypes = [vp, C.POINTER(ModelSet), vp, C.c_int32, C.c_int32, C.c_uint64,
+                                       C.c_int64, C.c_int64, vp, vp]
+    L.lann_build_dataset.argtypes = [C.POINTER(World), C.c_uint64, C.c_int32, vp, vp, vp, vp]
+    L.lann_split_order.argtypes = [C.c_int32, C.c_uint64, vp]
+    L.lann_init_params.argtypes = [C.c_int32, vp, C.c_uint64, vp]
+    L.lann_run_population.argtypes = [vp, C.c_int32, C.POINTER(Job), C.c_int32, C.POINTER(JobResult),
+                                      vp, vp, vp, vp]
+    L.lann_default_combos.argtypes = [C.POINTER(World), C.c_int32]
+    _lib = L
+    return L
+
+
+def _ptr(a):
+    return a.ctypes.data if a is not None else None
+
+
+def _c(a, dtype):
+    return np.ascontiguousarray(a, dtype=dtype)
+
+
+def param_count(n_inputs, h1, h2=0):
+    """models.cpp:37-46"""
+    if h2:
+        return (n_inputs + 1) * h1 + (h1 + 1) * h2 + h2 + 1
+    return (n_inputs + 1) * h1 + h1 + 1
+
+
+def default_combos():
+    L = load_library()
+    arr = (World * 64)()
+    n = L.lann_default_combos(arr, 64)
+    return [arr[i] for i in range(n)]
+
+
+def build_dataset(world: World, seed: int, count: int):
+    """datagen::build_dataset with the world's probe -> (feats[count][8], c, runtime, n_features)."""
+    L = load_library()
+    feats = np.zeros((count, ROW))
+    c = np.zeros(count, dtype=np.uint64)
+    rt = np.zeros(count)
+    nf = C.c_int32(0)
+    st = L.lann_build_dataset(C.byref(world), seed, count, _ptr(feats), _ptr(c), _ptr(rt), C.addressof(nf))
+    if st:
+        raise _ERR.get(st, Error)(f"build_dataset failed ({st})")
+    return feats, c, rt, nf.value
+
+
+def init_params(dims, seed):
+    """Mlp::init with Rng(derive_seed(seed, 0xA11CE)) (models.cpp:298, mlp.cpp:9-25)."""
+    L = load_library()
+    d = _c(dims, np.int32)
+    P = int(sum((d[i] + 1) * d[i + 1] for i in range(len(d) - 1)))
+    out = np.zeros(P)
+    st = L.lann_init_params(len(d), _ptr(d), seed, _ptr(out))
+    if st:
+        raise _ERR.get(st, Error)("bad network dims")
+    return out
+
+
+class Engine:
+    """One engine per device (and per host thread): owns a CUDA stream and device memory."""
+
+    def __init__(self, device: int = 0):
+        self.L = load_library()
+        h = C.c_void_p()
+        st = self.L.lann_engine_create(device, C.byref(h))
+        if st == abi.NO_DEVICE:
+            raise NoDeviceError("no CUDA device: the LANN engine has no CPU fallback")
+        if st:
+            raise _ERR.get(st, Error)(f"engine creation failed ({st})")
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.L.lann_engine_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        self.close()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    # ---- diagnostics ----
+    @property
+    def last_error(self) -> str:
+        return self.L.lann_last_error(self.h).decode()
+
+    @property
+    def last_device_ms(self) -> float:
+        return self.L.lann_last_device_ms(self.h)
+
+    @property
+    def last_launches(self) -> int:
+        return self.L.lann_last_launches(self.h)
+
+    def _raise(self, st, epoch=-1):
+        if st == abi.TRAINING_ERROR:
+            raise TrainingError(self.last_error, epoch)
+        raise _ERR.get(st, Error)(self.last_error or f"status {st}")
+
+    # ---- train_full_batch, batched (mlp.cpp:156-175) ----
+    def train(self, tiles_X, tiles_y, models, precision=abi.FP64_EXACT, trace=False, trace_stride=1,
+              raise_on_error=True):
+        """tiles_X: list of [N][8] arrays (normalised rows), tiles_y: list of [N];
+        models: list of dicts {tile, h1, h2, lr, epochs, params}. Returns
+        (params list, final_loss, nonfinite_epoch, traces or None)."""
+        n_tiles = len(tiles_X)
+        rows = np.array([len(y) for y in tiles_y], dtype=np.int32)
+        offs = np.concatenate([[0], np.cumsum(rows)[:-1]]).astype(np.int64)
+        X = np.zeros((int(rows.sum()), ROW))
+        y = np.zeros(int(rows.sum()))
+        for k in range(n_tiles):
+            xk = np.asarray(tiles_X[k], dtype=np.float64)
+            X[offs[k]:offs[k] + rows[k], : xk.shape[1]] = xk
+            y[offs[k]:offs[k] + rows[k]] = tiles_y[k]
+        inputs = np.array([np.asarray(tiles_X[k]).shape[1] for k in range(n_tiles)], dtype=np.int32)
+        M = len(models)
+        mt = np.array([m["tile"] for m in models], dtype=np.int32)
+        h1 = np.array([m["h1"] for m in models], dtype=np.int32)
+        h2 = np.array([m.get("h2", 0) for m in models], dtype=np.int32)
+        lr = np.array([m["lr"] for m in models], dtype=np.float64)
+        ep = np.array([m["epochs"] for m in models], dtype=np.int32)
+        sizes = np.array([len(m["params"]) for m in models], dtype=np.int64)
+        poff = np.concatenate([[0], np.cumsum(sizes)[:-1]]).astype(np.int64)
+        params = np.concatenate([np.asarray(m["params"], dtype=np.float64) for m in models])
+        final = np.zeros(M)
+        bad = np.zeros(M, dtype=np.int32)
+        stride = max(1, int(trace_stride))
+        tl = (ep + stride - 1) // stride
+        toff = np.concatenate([[0], np.cumsum(tl)[:-1]]).astype(np.int64)
+        tr = np.zeros(int(tl.sum())) if trace else None
+        b = TrainBatch(n_models=M, precision=precision, n_tiles=n_tiles, tile_rows=_ptr(rows),
+                       tile_inputs=_ptr(inputs), tile_offset=_ptr(offs), total_rows=len(y), X=_ptr(X), y=_ptr(y),
+                       model_tile=_ptr(mt), model_h1=_ptr(h1), model_h2=_ptr(h2), model_lr=_ptr(lr),
+                       model_epochs=_ptr(ep), model_param_offset=_ptr(poff), total_params=len(params),
+                       params=_ptr(params), final_loss=_ptr(final), nonfinite_epoch=_ptr(bad),
+                       loss_trace=_ptr(tr), trace_offset=_ptr(toff), trace_stride=stride)
+        st = self.L.lann_train(self.h, C.byref(b))
+        if st and raise_on_error:
+            self._raise(st, int(bad[bad >= 0][0]) if (bad >= 0).any() else -1)
+        out_p = [params[poff[i]:poff[i] + sizes[i]].copy() for i in range(M)]
+        traces = [tr[toff[i]:toff[i] + tl[i]].copy() for i in range(M)] if trace else None
+        return out_p, final, bad, traces
+
+    # ---- models::predict over rows (models.cpp:346-363) ----
+    def predict(self, models, rows, row_model, precision=abi.FP64_EXACT):
+        ms, keep = _model_set(models, precision)
+        rows = np.ascontiguousarray(rows, dtype=np.float64)
+        n = rows.shape[0]
+        full = np.zeros((n, ROW))
+        full[:, : rows.shape[1]] = rows
+        rm = _c(row_model, np.int32)
+        out = np.zeros(n)
+        st = self.L.lann_predict(self.h, C.byref(ms), n, _ptr(full), _ptr(rm), _ptr(out))
+        if st:
+            self._raise(st)
+        return out
+
+    # ---- eval::mape / mape_thresholded / spearman over many sets ----
+    def eval(self, truths, preds, drop=0.3):
+        lens = np.array([len(t) for t in truths], dtype=np.int32)
+        off = np.concatenate([[0], np.cumsum(lens)[:-1]]).astype(np.int64)
+        t = np.concatenate([np.asarray(x, dtype=np.float64) for x in truths])
+        p = np.concatenate([np.asarray(x, dtype=np.float64) for x in preds])
+        n = len(truths)
+        mape, thr, rho = np.zeros(n), np.zeros(n), np.zeros(n)
+        kept = np.zeros(n, dtype=np.int32)
+        st = self.L.lann_eval(self.h, n, _ptr(off), _ptr(lens), _ptr(t), _ptr(p), drop, _ptr(mape), _ptr(thr),
+                              _ptr(kept), _ptr(rho))
+        if st:
+            self._raise(st)
+        return mape, thr, kept, rho
+
+    def select_schedule(self, model, n_img, cands, precision=abi.FP64_EXACT):
+        ms, keep = _model_set([model], precision)
+        c = _c(cands, np.uint32)
+        chosen = C.c_int64(-1)
+        score = C.c_double(0)
+        st = self.L.lann_select_schedule(self.h, C.byref(ms), n_img, len(c), _ptr(c), C.addressof(chosen),
+                                         C.addressof(score))
+        if st:
+            self._raise(st)
+        return chosen.value, score.value
+
+    def select_variants(self, models, with_n_thd, kind, max_threads, seed, first, n, precision=abi.FP32):
+        ms, keep = _model_set(models, precision)
+        thd = _c(with_n_thd, np.int32)
+        idx = np.zeros(n, dtype=np.int32)
+        score = np.zeros(n)
+        st = self.L.lann_select_variants(self.h, C.byref(ms), _ptr(thd), kind, max_threads, seed, first, n,
+                                         _ptr(idx), _ptr(score))
+        if st:
+            self._raise(st)
+        return idx, score
+
+    # ---- models::train_nn + predict_dataset + make_report over a population ----
+    def run_population(self, jobs, precision=abi.FP64_EXACT, want_params=False, want_trace=False):
+        n = len(jobs)
+        arr = (Job * n)(*jobs)
+        res = (JobResult * n)()
+        params = off = trace = toff = None
+        if want_params:
+            params = np.zeros(n * 2048)
+            off = (np.arange(n, dtype=np.int64) * 2048)
+        if want_trace:
+            ep = np.array([j.epochs for j in jobs], dtype=np.int64)
+            toff = np.concatenate([[0], np.cumsum(ep)[:-1]]).astype(np.int64)
+            trace = np.zeros(int(ep.sum()))
+        st = self.L.lann_run_population(self.h, n, arr, precision, res, _ptr(params), _ptr(off), _ptr(trace),
+                                        _ptr(toff))
+        results = list(res)
+        out_params = [params[off[i]:off[i] + results[i].n_params].copy() for i in range(n)] if want_params else None
+        out_trace = [trace[toff[i]:toff[i] + jobs[i].epochs].copy() for i in range(n)] if want_trace else None
+        return st, results, out_params, out_trace
+
+
+def _model_set(models, precision):
+    """models: list of dicts {inputs, h1, h2, log_target, params, norm(18)}"""
+    M = len(models)
+    I = np.array([m["inputs"] for m in models], dtype=np.int32)
+    h1 = np.array([m["h1"] for m in models], dtype=np.int32)
+    h2 = np.array([m.get("h2", 0) for m in models], dtype=np.int32)
+    lt = np.array([int(m.get("log_target", 0)) for m in models], dtype=np.int32)
+    sizes = np.array([len(m["params"]) for m in models], dtype=np.int64)
+    poff = np.concatenate([[0], np.cumsum(sizes)[:-1]]).astype(np.int64)
+    params = np.concatenate([np.asarray(m["params"], dtype=np.float64) for m in models])
+    norm = np.concatenate([np.asarray(m["norm"], dtype=np.float64) for m in models])
+    ms = ModelSet(n_models=M, precision=precision, n_inputs=_ptr(I), h1=_ptr(h1), h2=_ptr(h2), log_target=_ptr(lt),
+                  param_offset=_ptr(poff), params=_ptr(params), total_params=len(params), norm=_ptr(norm))
+    return ms, (I, h1, h2, lt, poff, params, norm)

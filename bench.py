@@ -1,0 +1,335 @@
+#!/usr/bin/env python
+"""bench.py — LANN model-epochs/s (BASELINE config 2) on N B200s, plus the reference arm.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--precision fp32|fp64] [--impl ours|reference]
+
+One STEP = one full pass of the hot path over the config-2 population: the 48
+kernel-variant-hardware LANNs (40 prediction nets 8000 epochs, 8 blur selection
+nets 20000 epochs; 480,000 model-epochs) trained from their initial weights,
+then every held-out sample predicted and MAPE / thresholded MAPE / Spearman
+computed per model. Multi-GPU (torchrun): weak scaling, every rank trains its
+own 48-combo population (root seed 1 + rank); no collective on the data path,
+the barrier and the MAX-over-ranks reduction of the timing use NCCL.
+
+value : model-epochs/s over all ranks, device time (CUDA events on the engine
+        stream) of K device-only passes with all inputs resident in HBM; L2 is
+        flushed (256 MiB write) between timed steps.
+e2e   : the same metric through the public C ABI (lann_run_population) from host
+        job descriptions to host results: host data generation, H2D, the device
+        pass, D2H, wall clock per step.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_2003_07497_b200 import abi  # noqa: E402
+from paper_2003_07497_b200 import population as popmod  # noqa: E402
+
+WORKLOAD = ("config2: 48 kernel-variant-hardware LANNs trained as one population "
+            "(40 prediction nets I=4..7,H=8,8000 ep + 8 blur selection nets 6-5-5-1,20000 ep; "
+            "250 train / 250 eval samples each) + held-out predict + MAPE/thr-MAPE/Spearman")
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if len(s) > i + 2 and s[i + 2] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def load_json(path):
+    try:
+        with open(path) as f:
+            return json.load(f)
+    except Exception:
+        return None
+
+
+def fp32_peak():
+    d = load_json(os.path.join(ROOT, "profiles", "fp32_peak.json"))
+    if d and d.get("fp32_tflops"):
+        return float(d["fp32_tflops"]), "measured: profiles/fp32_peak.json (tools/peaks.cu FFMA/FFMA2 microbenchmark)"
+    return 74.4, "derived nominal: 148 SM x 128 lanes x 2 FLOP x 1.965 GHz (no measured FP32 peak found)"
+
+
+def cpu_reference_run(jobs, threads):
+    """The reference's own CPU path (oracle/_ref, compiled from the reference sources) or,
+    if that library is absent, the C restatement; returns (seconds, kind)."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from oracle_lib import Oracle, Reference  # test infrastructure: the baseline leg only
+    if Reference.available():
+        secs, res, _ = Reference().run_population(jobs, threads)
+        bad = [r.status for r in res if r.status]
+        return secs, "reference", bad
+    o = Oracle()
+    import concurrent.futures as cf
+    t0 = time.perf_counter()
+    with cf.ThreadPoolExecutor(threads) as ex:
+        res = list(ex.map(lambda j: o.run_job(j)[0], jobs))
+    return time.perf_counter() - t0, "port", [r.status for r in res if r.status]
+
+
+def run_reference_arm(args, rank, world):
+    if rank != 0:
+        return 0
+    jobs = popmod.config2_jobs(root_seed=1)
+    me = popmod.model_epochs(jobs)
+    threads = os.cpu_count() or 1
+    for _ in range(max(0, min(args.warmup, 1))):
+        cpu_reference_run(jobs, threads)
+    times = []
+    kind = "reference"
+    for _ in range(args.steps):
+        secs, kind, bad = cpu_reference_run(jobs, threads)
+        times.append(secs)
+    total = sum(times)
+    value = me * len(times) / total
+    line = {
+        "impl": "reference", "metric": "LANN model-epochs/sec", "value": value, "unit": "model-epochs/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / len(times),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "models": len(jobs), "model_epochs_per_step": me,
+                   "host": "reference perfsage core (oracle/_ref) train_nn+predict_dataset+make_report, one model per std::thread task"},
+        "cpu_baseline": {"value": value, "unit": "model-epochs/s", "cores": threads, "kind": kind,
+                         "sample": f"the whole config-2 population (48 models, {me} model-epochs) per step on {threads} host threads"},
+        "e2e": {"value": value, "unit": "model-epochs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--precision", choices=["fp32", "fp64"], default="fp32")
+    ap.add_argument("--no-extras", action="store_true", help="skip the sweep / selection / parity-mode extras")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    rank, local_rank, world = dist_env()
+    if args.impl == "reference":
+        return run_reference_arm(args, rank, world)
+
+    import torch
+    import torch.distributed as dist
+    from paper_2003_07497_b200 import engine as E
+
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    precision = abi.FP32 if args.precision == "fp32" else abi.FP64_EXACT
+    eng = E.Engine(local_rank)
+    jobs = popmod.config2_jobs(root_seed=1 + rank)
+    me_rank = popmod.model_epochs(jobs)
+    pop = eng.prepare(jobs, precision)
+    flop = pop.flop
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+    for _ in range(args.warmup):
+        pop.run(1)
+    barrier()
+    dev_ms, train_ms, launches = 0.0, 0.0, 0
+    t0 = time.perf_counter()
+    with ClockSampler(local_rank) as clk:
+        for _ in range(args.steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            pop.run(1)
+            dev_ms += eng.last_device_ms
+            train_ms += eng.last_train_ms
+            launches += eng.last_launches
+    barrier()
+    wall_s = time.perf_counter() - t0
+    st, results, _, _ = pop.fetch()
+    bad = [r.status for r in results if r.status]
+    dev_ms = max_over_ranks(dev_ms)
+    value = me_rank * world * args.steps / (dev_ms / 1e3)
+    # dominant kernel: the trainer (all its launches, concurrent on the aux streams)
+    train_launch_ms = train_ms / args.steps
+    achieved = flop / (train_launch_ms / 1e3) / 1e12
+    peak, peak_src = fp32_peak() if precision == abi.FP32 else (36.98, "measured: profiles/fp32_peak.json dfma_tflops")
+    prof = load_json(os.path.join(ROOT, "profiles", "r01_traffic.json")) or {}
+    roofline = {"bound": "fp32" if precision == abi.FP32 else "fp64", "achieved": achieved, "peak": peak,
+                "unit": "TFLOP/s", "frac": achieved / peak, "traffic": prof.get("train_dram_bytes_per_launch"),
+                "kernel": "train_fp32_cta_kernel + train_fp32_kernel (trainer launch set)" if precision == abi.FP32 else "train_fp64_exact",
+                "algorithmic_flop_per_step": flop, "kernel_ms_per_step": train_launch_ms, "peak_source": peak_src,
+                "note": "FP32 CUDA-core FMA bound (tiny per-sample contractions, no tensor-core shape); "
+                        "the 48-model population is latency-bound: <= 48 of 148 SMs busy"}
+
+    # ---- e2e through the public C ABI with host buffers ----
+    e2e_times = []
+    E.transfer_bytes(reset=True)
+    for _ in range(max(1, min(args.steps, 3))):
+        t1 = time.perf_counter()
+        st_e, res_e, _, _ = eng.run_population(jobs, precision)
+        e2e_times.append(time.perf_counter() - t1)
+    h2d, d2h = E.transfer_bytes(reset=True)
+    n_e2e = len(e2e_times)
+    e2e_s = max_over_ranks(sum(e2e_times) / n_e2e)
+    e2e = {"value": me_rank * world / e2e_s, "unit": "model-epochs/s", "h2d_bytes_per_step": h2d // n_e2e,
+           "d2h_bytes_per_step": d2h // n_e2e, "ms_per_step": 1e3 * e2e_s,
+           "path": "lann_run_population: host datagen+split+NormStats+init -> H2D -> train/predict/eval -> D2H"}
+
+    line = {
+        "metric": "LANN model-epochs/sec", "value": value, "unit": "model-epochs/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dev_ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32" if precision == abi.FP32 else "f64",
+        "data": "synthetic",
+        "config": {"workload": WORKLOAD, "models_per_gpu": len(jobs), "model_epochs_per_gpu_step": me_rank,
+                   "precision": args.precision, "parallelism": f"{world} independent populations (weak), no data-path collective",
+                   "l2": "flushed between timed steps (256 MiB write)"},
+        "roofline": roofline, "e2e": e2e, "gpu_launches": launches, "clocks": clk.summary(),
+        "wall_s_timed_region": wall_s, "failed_models": len(bad),
+        "median_thr_mape": float(np.median([r.mape_thr for r in results])),
+    }
+    if rank == 0 and not args.no_extras:
+        line["extras"] = extras(E, eng, precision)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        secs, kind, cbad = cpu_reference_run(jobs, threads)
+        line["cpu_baseline"] = {"value": me_rank / secs, "unit": "model-epochs/s", "cores": threads, "kind": kind,
+                                "sample": f"the whole config-2 population (48 models, {me_rank} model-epochs) once, "
+                                          f"one model per host thread task, {threads} threads",
+                                "seconds": secs}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    pop.close()
+    eng.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def extras(E, eng, precision):
+    """Secondary measurements (one pass each): FP64 parity-mode throughput on config 2,
+    the config-3 seed x fold sweep share of one GPU, config-4 variant-selection scoring."""
+    out = {}
+    jobs = popmod.config2_jobs(root_seed=1)
+    try:
+        p64 = eng.prepare(jobs, abi.FP64_EXACT)
+        p64.run(1)
+        p64.run(1)
+        ms = eng.last_device_ms
+        out["config2_fp64_exact"] = {"value": popmod.model_epochs(jobs) / (ms / 1e3), "unit": "model-epochs/s",
+                                     "ms_per_step": ms, "dtype": "f64",
+                                     "note": "bit-identical to the reference trainer (tests/test_gpu_parity.py)"}
+        p64.close()
+    except Exception as ex:  # noqa: BLE001
+        out["config2_fp64_exact"] = {"error": str(ex)}
+    try:
+        sweep = popmod.config3_jobs(root_seed=1, n_seeds=int(os.environ.get("LANN_SWEEP_SEEDS", 256)))
+        t0 = time.perf_counter()
+        ps = eng.prepare(sweep, abi.FP32)
+        prep_s = time.perf_counter() - t0
+        ps.run(1)
+        ms = eng.last_device_ms
+        tms = eng.last_train_ms
+        me = popmod.model_epochs(sweep)
+        out["config3_sweep_fp32"] = {"models": len(sweep), "model_epochs": me,
+                                     "value": me / (ms / 1e3), "unit": "model-epochs/s", "ms": ms,
+                                     "train_tflops": ps.flop / (tms / 1e3) / 1e12, "host_prepare_s": prep_s,
+                                     "note": "48 combos x seeds x 5 folds on ONE GPU (the 8-GPU config shards this list)"}
+        ps.close()
+    except Exception as ex:  # noqa: BLE001
+        out["config3_sweep_fp32"] = {"error": str(ex)}
+    try:
+        out["config4_selection"] = selection_extra(E, eng)
+    except Exception as ex:  # noqa: BLE001
+        out["config4_selection"] = {"error": str(ex)}
+    return out
+
+
+def selection_extra(E, eng, n_cands=10_000_000):
+    """Config 4: per kernel kind, n_cands counter-generated candidate shapes scored by its
+    10 variant-hardware prediction models from the config-2 population, argmin per candidate."""
+    jobs = popmod.config2_jobs(root_seed=1)
+    pop = eng.prepare(jobs, abi.FP32)
+    pop.run(1)
+    st, res, params, _ = pop.fetch(want_params=True)
+    norms = pop.norms()
+    pop.close()
+    total_pred, total_ms, kern_ms = 0, 0.0, 0.0
+    for kind in (abi.MM, abi.MV, abi.MC, abi.MP):
+        idx = [i for i, j in enumerate(jobs) if j.world.kind == kind]
+        models = [{"inputs": res[i].n_inputs, "h1": 8, "h2": 0, "log_target": 0, "params": params[i],
+                   "norm": norms[i]} for i in idx]
+        thd = [1 if jobs[i].world.hw_class == abi.HW_CPU else 0 for i in idx]
+        eng.select_variants(models, thd, kind, 16, 7, 0, n_cands, precision=abi.FP32)
+        total_ms += eng.last_device_ms
+        kern_ms += eng.last_train_ms
+        total_pred += n_cands * len(models)
+    flop_pred = 2 * 7 * 8 + 2 * 8 + 2 * 7 + 2  # 144 for MM nnc
+    return {"candidates_per_kind": n_cands, "models_per_kind": 10, "predictions": total_pred,
+            "value": total_pred / (kern_ms / 1e3), "unit": "predictions/s", "kernel_ms": kern_ms,
+            "call_ms_incl_d2h": total_ms, "approx_tflops": total_pred * flop_pred / (kern_ms / 1e3) / 1e12}
+
+
+if __name__ == "__main__":
+    sys.exit(main())

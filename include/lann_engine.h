@@ -124,6 +124,10 @@ const char* lann_last_error(const lann_engine* engine);
 double lann_last_device_ms(const lann_engine* engine);
 /* Number of engine kernels launched by the most recent call. */
 int64_t lann_last_launches(const lann_engine* engine);
+/* Device time (ms) of the dominant kernel of the most recent call: the
+ * trainer launches of lann_train / lann_population_run (summed over steps), or
+ * the scoring kernel of lann_select_variants; CUDA events on the launch stream. */
+double lann_last_train_ms(const lann_engine* engine);
 
 /* ---- training (train_full_batch, batched) ----------------------------------
  * Tiles hold min-max-normalised training rows (NormStats, models.cpp:118-133):
@@ -222,6 +226,27 @@ int lann_run_population(lann_engine* engine, int32_t n_jobs, const lann_job* job
                         int32_t precision, lann_job_result* results,
                         double* params_out, const int64_t* params_offset,
                         double* trace_out, const int64_t* trace_offset);
+
+/* Prepared population: the same pipeline split so that the host preparation and
+ * the uploads happen once (create), device-only passes can be repeated with all
+ * inputs resident in HBM (run: weights reset from the resident initial copy,
+ * train, predict, metrics; n_steps passes back to back), and results are copied
+ * out on demand (fetch). lann_run_population == create + run(1) + fetch. */
+typedef struct lann_population lann_population;
+int lann_population_create(lann_engine* engine, int32_t n_jobs, const lann_job* jobs,
+                           int32_t precision, int32_t record_trace, lann_population** out);
+int lann_population_run(lann_population* pop, int32_t n_steps);
+int lann_population_fetch(lann_population* pop, lann_job_result* results, double* params_out,
+                          const int64_t* params_offset, double* trace_out,
+                          const int64_t* trace_offset);
+/* algorithmic training FLOP of one pass (sum E * (N*F_s + 14P)) */
+double lann_population_flop(const lann_population* pop);
+/* per job: the model's NormStats {f_min[8], f_max[8], t_min, t_max} (zeros for failed jobs) */
+int lann_population_norm(const lann_population* pop, double* norm_out);
+/* host->device / device->host bytes moved by this thread's engine calls since the last reset */
+void lann_transfer_bytes(int64_t* h2d, int64_t* d2h, int32_t reset);
+int64_t lann_population_models(const lann_population* pop);
+void lann_population_destroy(lann_population* pop);
 
 /* The 48 kernel-variant-hardware combinations of BASELINE config 2 (worlds
  * only). Writes up to cap entries, returns the count. */

@@ -1,7 +1,12 @@
 // engine.cpp — the C ABI of include/lann_engine.h: argument validation with the
-// reference's error contract, device buffers, kernel launches, and the
+// reference's error contract, device buffers, launch plans and the
 // whole-population pipeline. There is no CPU fallback: without a CUDA device
 // every compute entry point returns LANN_NO_DEVICE.
+//
+// A training "plan" is built once per population (device-side argument
+// arrays, FP32 row packing, model grouping, stream assignment) and executed
+// any number of times with launches only — so a prepared population re-runs
+// with its inputs resident in HBM and no host<->device traffic.
 #include <algorithm>
 #include <atomic>
 #include <chrono>
@@ -9,6 +14,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <memory>
 #include <numeric>
 #include <string>
 #include <thread>
@@ -21,12 +27,17 @@
 #include "domain.hpp"
 #include "kernels.cuh"
 
+constexpr int kAuxStreams = 8;
+
 struct lann_engine {
   int device = 0;
+  int sms = 148;
   cudaStream_t stream = nullptr;
-  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  cudaStream_t aux[kAuxStreams] = {};
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr, tr0 = nullptr, tr1 = nullptr;
+  cudaEvent_t fork = nullptr, join[kAuxStreams] = {};
   std::string err;
-  double last_ms = 0.0;
+  double last_ms = 0.0, last_train_ms = 0.0;
   int64_t launches = 0;
   int max_smem = 0;
 };
@@ -41,6 +52,9 @@ struct CudaFail {
 inline void ck(cudaError_t e, const char* what) {
   if (e != cudaSuccess) throw CudaFail{std::string(what) + ": " + cudaGetErrorString(e)};
 }
+
+// host<->device bytes moved by the calling thread (reported per C-ABI call)
+thread_local int64_t t_h2d = 0, t_d2h = 0;
 
 // Stream-ordered device buffer.
 template <class T>
@@ -68,12 +82,11 @@ struct DBuf {
   }
   void up(const T* host) {
     if (n) ck(cudaMemcpyAsync(p, host, n * sizeof(T), cudaMemcpyHostToDevice, s), "H2D");
+    t_h2d += int64_t(n * sizeof(T));
   }
   void down(T* host) const {
     if (n) ck(cudaMemcpyAsync(host, p, n * sizeof(T), cudaMemcpyDeviceToHost, s), "D2H");
-  }
-  void zero() {
-    if (n) ck(cudaMemsetAsync(p, 0, n * sizeof(T), s), "memset");
+    t_d2h += int64_t(n * sizeof(T));
   }
 };
 
@@ -82,6 +95,7 @@ int set_err(lann_engine* e, const Status& st) {
   return st.code;
 }
 
+// CUDA-event timer over the engine stream (whole call) — device time only.
 struct Timer {
   lann_engine* e;
   explicit Timer(lann_engine* eng) : e(eng) {
@@ -98,16 +112,14 @@ struct Timer {
   }
 };
 
-// ---- device-resident training input, shared by lann_train and lann_run_population ----
+// ---- training description (host side) -------------------------------------------------
 struct DevTrain {
   int n_models = 0, n_tiles = 0;
   std::vector<int> tile_rows, tile_inputs, model_tile, h1, h2, epochs;
-  std::vector<int64_t> tile_offset, param_offset, trace_offset;
+  std::vector<int64_t> tile_offset, param_offset;
   std::vector<double> lr;
   int64_t total_params = 0;
   int trace_stride = 1;
-  bool want_trace = false;
-  int64_t trace_len = 0;
 };
 
 Status validate_train(const DevTrain& t) {
@@ -124,6 +136,7 @@ Status validate_train(const DevTrain& t) {
     if (t.h1[m] < 1 || t.h2[m] < 0 || t.h1[m] > 64 || t.h2[m] > 64)
       return {LANN_PARAM_ERROR, "network layer widths must lie in 1..64"};
     if (t.epochs[m] < 1) return {LANN_PARAM_ERROR, "epochs must be >= 1"};
+    if (!(t.lr[m] > 0.0)) return {LANN_PARAM_ERROR, "learning rate must be > 0"};
     const int P = param_count(t.tile_inputs[t.model_tile[m]], t.h1[m], t.h2[m]);
     if (t.param_offset[m] < 0 || t.param_offset[m] + P > t.total_params)
       return {LANN_PARAM_ERROR, "flat parameter size mismatch"};
@@ -131,51 +144,78 @@ Status validate_train(const DevTrain& t) {
   return {};
 }
 
-// Runs the trainer on device buffers (X, y, params already resident).
-void run_train(lann_engine* e, const DevTrain& t, int precision, const double* dX,
-               const double* dY, int64_t total_rows, double* dparams, double* dfinal,
-               int* dbad, double* dtrace, const DBuf<int64_t>& dtrace_off) {
-  cudaStream_t s = e->stream;
-  DBuf<int> d_tile_rows(t.tile_rows, s), d_tile_inputs(t.tile_inputs, s), d_model_tile(t.model_tile, s),
-      d_h1(t.h1, s), d_h2(t.h2, s), d_epochs(t.epochs, s);
-  DBuf<int64_t> d_tile_off(t.tile_offset, s), d_poff(t.param_offset, s);
-  DBuf<double> d_lr(t.lr, s);
-  const int max_e = *std::max_element(t.epochs.begin(), t.epochs.end());
+// ---- training plan ------------------------------------------------------------------------
+struct Fp32Bucket {
+  int in, h1, h2, lanes, tile_bytes, n_groups;
+  DBuf<int> gfirst, gcount, sorted;
+  double cost;
+};
 
-  // FP32 mode: models of a supported compiled shape go to the FP32 kernels; any
-  // other shape is trained by the (generic, exact) FP64 kernel below.
+struct TrainPlan {
+  DBuf<int> tile_rows, tile_inputs, model_tile, h1, h2, epochs;
+  DBuf<int64_t> tile_off, poff;
+  DBuf<double> lr;
+  // FP32 part
+  DBuf<float> rows_f;
+  std::vector<std::unique_ptr<Fp32Bucket>> buckets;
+  // FP64 part (exact mode, or FP32-mode models without a compiled shape)
+  int n64 = 0, max_p = 0, dyn64 = 0, in_smem = 0;
+  DBuf<int> order;
+  DBuf<double2> bc;
+  DBuf<double> scratch;
+  DBuf<int64_t> soff;
+  const double* dX = nullptr;
+  const double* dY = nullptr;
+  int trace_stride = 1;
+};
+
+std::unique_ptr<TrainPlan> build_plan(lann_engine* e, const DevTrain& t, int precision,
+                                      const double* dX, const double* dY, int64_t total_rows) {
+  cudaStream_t s = e->stream;
+  auto plan = std::make_unique<TrainPlan>();
+  TrainPlan& P = *plan;
+  P.tile_rows = DBuf<int>(t.tile_rows, s);
+  P.tile_inputs = DBuf<int>(t.tile_inputs, s);
+  P.model_tile = DBuf<int>(t.model_tile, s);
+  P.h1 = DBuf<int>(t.h1, s);
+  P.h2 = DBuf<int>(t.h2, s);
+  P.epochs = DBuf<int>(t.epochs, s);
+  P.tile_off = DBuf<int64_t>(t.tile_offset, s);
+  P.poff = DBuf<int64_t>(t.param_offset, s);
+  P.lr = DBuf<double>(t.lr, s);
+  P.dX = dX;
+  P.dY = dY;
+  P.trace_stride = t.trace_stride;
+
   std::vector<int> fp64_models;
   if (precision == LANN_FP32) {
-    DBuf<float> rows_f(size_t(total_rows) * 8, s);
-    launch_pack_rows(dX, dY, total_rows, rows_f.p, s);
-    e->launches += 1;
+    P.rows_f = DBuf<float>(size_t(total_rows) * 8, s);
+    launch_pack_rows(dX, dY, total_rows, P.rows_f.p, s);
     using Shape = std::tuple<int, int, int>;
-    std::map<Shape, std::vector<int>> buckets;
+    std::map<Shape, std::vector<int>> by_shape;
     for (int m = 0; m < t.n_models; ++m) {
       const int tile = t.model_tile[m];
       const int I = t.tile_inputs[tile];
       if (fp32_shape_supported(I, t.h1[m], t.h2[m]) && t.tile_rows[tile] * 32 <= 96 * 1024)
-        buckets[{I, t.h1[m], t.h2[m]}].push_back(m);
+        by_shape[{I, t.h1[m], t.h2[m]}].push_back(m);
       else
         fp64_models.push_back(m);
     }
     int lanes = 0;
     if (const char* env = std::getenv("LANN_FP32_LANES")) lanes = std::atoi(env);
-    int sms = 148;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, e->device);
-    if (lanes != 1 && lanes != 2 && lanes != 4 && lanes != 8 && lanes != 32) {
-      // smallest lanes-per-model that still gives >= 16 warps per SM
+    if (lanes != 1 && lanes != 2 && lanes != 4 && lanes != 8 && lanes != 32 && lanes != 256) {
+      // smallest lanes-per-model that still gives >= 16 warps per SM; populations
+      // too small for that get a whole CTA (256 threads) per model
       const int total = t.n_models - int(fp64_models.size());
-      lanes = 32;
-      for (int k : {1, 2, 4, 8, 32})
-        if ((total + 32 / k - 1) / (32 / k) >= 16 * sms) {
+      lanes = total <= 4 * e->sms ? 256 : 32;
+      for (int k : {1, 2, 4, 8})
+        if ((total + 32 / k - 1) / (32 / k) >= 16 * e->sms) {
           lanes = k;
           break;
         }
     }
-    const int G = 32 / lanes;
-    std::vector<DBuf<int>> keep;
-    for (auto& [shape, ms] : buckets) {
+    const int G = lanes <= 32 ? 32 / lanes : 1;
+    for (auto& [shape, ms] : by_shape) {
       // group: same tile and epoch count, up to G models; longest groups first
       std::stable_sort(ms.begin(), ms.end(), [&](int a, int b) {
         const double ca = double(t.epochs[a]) * t.tile_rows[t.model_tile[a]];
@@ -186,6 +226,7 @@ void run_train(lann_engine* e, const DevTrain& t, int precision, const double* d
       });
       std::vector<int> gfirst, gcount;
       int max_rows = 1;
+      double cost = 0.0;
       for (size_t i = 0; i < ms.size();) {
         size_t j = i + 1;
         while (j < ms.size() && int(j - i) < G && t.model_tile[ms[j]] == t.model_tile[ms[i]] &&
@@ -194,44 +235,31 @@ void run_train(lann_engine* e, const DevTrain& t, int precision, const double* d
         gfirst.push_back(int(i));
         gcount.push_back(int(j - i));
         max_rows = std::max(max_rows, t.tile_rows[t.model_tile[ms[i]]]);
+        cost = std::max(cost, double(t.epochs[ms[i]]) * t.tile_rows[t.model_tile[ms[i]]]);
         i = j;
       }
-      keep.emplace_back(gfirst, s);
-      const int* d_gf = keep.back().p;
-      keep.emplace_back(gcount, s);
-      const int* d_gc = keep.back().p;
-      keep.emplace_back(ms, s);
-      const int* d_sm = keep.back().p;
-      TrainF32Args a{};
-      a.n_groups = int(gfirst.size());
-      a.group_first = d_gf;
-      a.group_count = d_gc;
-      a.sorted_model = d_sm;
-      a.rows = rows_f.p;
-      a.tile_rows = d_tile_rows.p;
-      a.tile_offset = d_tile_off.p;
-      a.model_tile = d_model_tile.p;
-      a.lr = d_lr.p;
-      a.epochs = d_epochs.p;
-      a.param_offset = d_poff.p;
-      a.params = dparams;
-      a.final_loss = dfinal;
-      a.nonfinite_epoch = dbad;
-      a.loss_trace = dtrace;
-      a.trace_offset = dtrace_off.p;
-      a.trace_stride = t.trace_stride;
-      if (!launch_train_fp32(a, std::get<0>(shape), std::get<1>(shape), std::get<2>(shape), lanes,
-                             max_rows * 32, s))
-        throw CudaFail{"no FP32 kernel for this shape"};
-      ck(cudaGetLastError(), "train_fp32 launch");
-      e->launches += 1;
+      auto b = std::make_unique<Fp32Bucket>();
+      b->in = std::get<0>(shape);
+      b->h1 = std::get<1>(shape);
+      b->h2 = std::get<2>(shape);
+      b->lanes = lanes;
+      b->tile_bytes = max_rows * 32;
+      b->n_groups = int(gfirst.size());
+      b->gfirst = DBuf<int>(gfirst, s);
+      b->gcount = DBuf<int>(gcount, s);
+      b->sorted = DBuf<int>(ms, s);
+      b->cost = cost;
+      P.buckets.push_back(std::move(b));
     }
-    if (fp64_models.empty()) return;
+    // longest bucket first so it starts first on its stream
+    std::stable_sort(P.buckets.begin(), P.buckets.end(),
+                     [](const auto& a, const auto& b) { return a->cost > b->cost; });
   } else {
     fp64_models.resize(t.n_models);
     std::iota(fp64_models.begin(), fp64_models.end(), 0);
   }
-  {
+  P.n64 = int(fp64_models.size());
+  if (P.n64 > 0) {
     // longest models first so the block scheduler packs the tail
     std::vector<int> order = fp64_models;
     auto cost = [&](int m) {
@@ -240,63 +268,390 @@ void run_train(lann_engine* e, const DevTrain& t, int precision, const double* d
              param_count(t.tile_inputs[tile], t.h1[m], t.h2[m]);
     };
     std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return cost(a) > cost(b); });
+    int max_e = 1;
+    for (int m : order) max_e = std::max(max_e, t.epochs[m]);
     const auto& bc = adam_bias_table(max_e);
-    DBuf<double2> d_bc(reinterpret_cast<const double2*>(bc.data()), size_t(max_e), s);
-    // shared-memory plan: records in smem when every model's records fit
-    int max_p = 0;
+    P.bc = DBuf<double2>(reinterpret_cast<const double2*>(bc.data()), size_t(max_e), s);
     size_t max_bytes_smem = 0, max_state = 0;
-    std::vector<int64_t> soff(t.n_models);
+    std::vector<int64_t> soff(t.n_models, 0);
     int64_t scratch = 0;
     for (int m : order) {
       const int tile = t.model_tile[m];
-      const int P = param_count(t.tile_inputs[tile], t.h1[m], t.h2[m]);
-      max_p = std::max(max_p, P);
+      const int np = param_count(t.tile_inputs[tile], t.h1[m], t.h2[m]);
+      P.max_p = std::max(P.max_p, np);
       const size_t rec = size_t(fp64_record_doubles(t.tile_inputs[tile], t.h1[m], t.h2[m])) *
                          t.tile_rows[tile] * 8;
-      const size_t state = size_t(3 * P + 2) * 8;
+      const size_t state = size_t(3 * np + 2) * 8;
       max_state = std::max(max_state, state);
       max_bytes_smem = std::max(max_bytes_smem, state + rec);
       soff[m] = scratch;
       scratch += int64_t(rec / 8);
     }
-    const bool in_smem = max_bytes_smem <= size_t(e->max_smem);
-    DBuf<double> d_scratch(in_smem ? 0 : size_t(scratch), s);
-    DBuf<int64_t> d_soff(soff, s);
-    DBuf<int> d_order(order, s);
-    TrainArgs a{};
-    a.n_models = int(order.size());
-    a.order = d_order.p;
-    a.tile_rows = d_tile_rows.p;
-    a.tile_inputs = d_tile_inputs.p;
-    a.tile_offset = d_tile_off.p;
-    a.X = dX;
-    a.y = dY;
-    a.model_tile = d_model_tile.p;
-    a.h1 = d_h1.p;
-    a.h2 = d_h2.p;
-    a.lr = d_lr.p;
-    a.epochs = d_epochs.p;
-    a.param_offset = d_poff.p;
+    P.in_smem = max_bytes_smem <= size_t(e->max_smem);
+    P.dyn64 = int(P.in_smem ? max_bytes_smem : max_state);
+    if (!P.in_smem) P.scratch = DBuf<double>(size_t(scratch), s);
+    P.soff = DBuf<int64_t>(soff, s);
+    P.order = DBuf<int>(order, s);
+  }
+  ck(cudaGetLastError(), "plan");
+  return plan;
+}
+
+// Launch the whole trainer; buckets run concurrently on the auxiliary streams.
+void execute_plan(lann_engine* e, const TrainPlan& P, double* dparams, double* dfinal, int* dbad,
+                  double* dtrace, const int64_t* dtrace_off) {
+  cudaStream_t s = e->stream;
+  const int n_launch = int(P.buckets.size()) + (P.n64 > 0 ? 1 : 0);
+  ck(cudaEventRecord(e->tr0, s), "event");
+  ck(cudaEventRecord(e->fork, s), "event");
+  int k = 0;
+  auto next_stream = [&]() -> cudaStream_t {
+    if (n_launch == 1) return s;
+    cudaStream_t st = e->aux[k % kAuxStreams];
+    ++k;
+    return st;
+  };
+  for (int i = 0; i < kAuxStreams && n_launch > 1; ++i)
+    ck(cudaStreamWaitEvent(e->aux[i], e->fork, 0), "wait");
+  for (const auto& b : P.buckets) {
+    TrainF32Args a{};
+    a.n_groups = b->n_groups;
+    a.group_first = b->gfirst.p;
+    a.group_count = b->gcount.p;
+    a.sorted_model = b->sorted.p;
+    a.rows = P.rows_f.p;
+    a.tile_rows = P.tile_rows.p;
+    a.tile_offset = P.tile_off.p;
+    a.model_tile = P.model_tile.p;
+    a.lr = P.lr.p;
+    a.epochs = P.epochs.p;
+    a.param_offset = P.poff.p;
     a.params = dparams;
     a.final_loss = dfinal;
     a.nonfinite_epoch = dbad;
     a.loss_trace = dtrace;
-    a.trace_offset = dtrace_off.p;
-    a.trace_stride = t.trace_stride;
-    a.bias_corr = d_bc.p;
-    a.scratch = d_scratch.p;
-    a.scratch_offset = d_soff.p;
-    a.smem_records = in_smem ? 1 : 0;
-    launch_train_fp64(a, max_p, int(in_smem ? max_bytes_smem : max_state), s);
+    a.trace_offset = dtrace_off;
+    a.trace_stride = P.trace_stride;
+    if (!launch_train_fp32(a, b->in, b->h1, b->h2, b->lanes, b->tile_bytes, next_stream()))
+      throw CudaFail{"no FP32 kernel for this shape"};
+    ck(cudaGetLastError(), "train_fp32 launch");
+    e->launches += 1;
+  }
+  if (P.n64 > 0) {
+    TrainArgs a{};
+    a.n_models = P.n64;
+    a.order = P.order.p;
+    a.tile_rows = P.tile_rows.p;
+    a.tile_inputs = P.tile_inputs.p;
+    a.tile_offset = P.tile_off.p;
+    a.X = P.dX;
+    a.y = P.dY;
+    a.model_tile = P.model_tile.p;
+    a.h1 = P.h1.p;
+    a.h2 = P.h2.p;
+    a.lr = P.lr.p;
+    a.epochs = P.epochs.p;
+    a.param_offset = P.poff.p;
+    a.params = dparams;
+    a.final_loss = dfinal;
+    a.nonfinite_epoch = dbad;
+    a.loss_trace = dtrace;
+    a.trace_offset = dtrace_off;
+    a.trace_stride = P.trace_stride;
+    a.bias_corr = P.bc.p;
+    a.scratch = P.scratch.p;
+    a.scratch_offset = P.soff.p;
+    a.smem_records = P.in_smem;
+    launch_train_fp64(a, P.max_p, P.dyn64, next_stream());
     ck(cudaGetLastError(), "train_fp64 launch");
     e->launches += 1;
   }
+  if (n_launch > 1)
+    for (int i = 0; i < kAuxStreams; ++i) {
+      ck(cudaEventRecord(e->join[i], e->aux[i]), "event");
+      ck(cudaStreamWaitEvent(s, e->join[i], 0), "wait");
+    }
+  ck(cudaEventRecord(e->tr1, s), "event");
+}
+
+// ---- prepared population ----------------------------------------------------------------
+struct Population {
+  lann_engine* e = nullptr;
+  int n_jobs = 0, M = 0, precision = 0;
+  std::vector<lann_job_result> base;  // per-job status / shape after host preparation
+  std::vector<int> model_job;
+  DevTrain t;
+  int64_t rows = 0, n_eval_rows = 0;
+  int max_eval = 1;
+  std::vector<double> init_params;
+  // device
+  DBuf<double> dX, dY, dP0, dP, dF, dER, dPred, dN, dET, dMape, dThr, dRho, dT;
+  DBuf<int> dB, dEM, dI, dh1, dh2, dlog, dEL, dK, dS;
+  DBuf<int64_t> dpo, dEO, dTO;
+  std::unique_ptr<TrainPlan> plan;
+  int64_t trace_total = 0;
+  std::vector<int64_t> toff;
+  double train_flop = 0.0;  // algorithmic FLOP of one training pass
+};
+
+template <class F>
+void parallel_for(int n, F&& fn) {
+  const int nthreads = int(std::max(1u, std::min(32u, std::thread::hardware_concurrency())));
+  std::atomic<int> next{0};
+  std::vector<std::thread> pool;
+  auto worker = [&] {
+    for (int i; (i = next.fetch_add(1)) < n;) fn(i);
+  };
+  for (int t = 1; t < std::min(nthreads, n); ++t) pool.emplace_back(worker);
+  worker();
+  for (auto& th : pool) th.join();
+}
+
+double flop_per_model_epoch(int I, int h1, int h2, int n) {
+  const double fs = h2 > 0 ? 4.0 * I * h1 + 6.0 * h1 * h2 + 6.0 * h2 + h1 + 5 : 4.0 * I * h1 + 6.0 * h1 + 5;
+  return n * fs + 14.0 * param_count(I, h1, h2);
+}
+
+// Host preparation (datasets, splits, tiles, validation, init) + upload.
+int prepare_population(lann_engine* e, int n_jobs, const lann_job* jobs, int precision,
+                       bool want_trace, Population& pop) {
+  pop.e = e;
+  pop.n_jobs = n_jobs;
+  pop.precision = precision;
+  pop.base.assign(n_jobs, lann_job_result{});
+  for (auto& r : pop.base) r.nonfinite_epoch = -1;
+  e->err.clear();
+  // distinct datasets, splits and tiles
+  using DKey = std::tuple<std::string, uint64_t, int>;
+  std::map<DKey, int> dkeys;
+  std::vector<const lann_job*> dsrc;
+  std::vector<int> job_ds(n_jobs);
+  for (int j = 0; j < n_jobs; ++j) {
+    DKey k{std::string(reinterpret_cast<const char*>(&jobs[j].world), sizeof(lann_world)),
+           jobs[j].data_seed, jobs[j].count};
+    auto it = dkeys.find(k);
+    if (it == dkeys.end()) {
+      it = dkeys.emplace(k, int(dsrc.size())).first;
+      dsrc.push_back(&jobs[j]);
+    }
+    job_ds[j] = it->second;
+  }
+  using TKey = std::tuple<int, double, int, int, int, int>;
+  std::map<TKey, int> tkeys;
+  std::vector<int> job_tile(n_jobs);
+  std::vector<TKey> tsrc;
+  for (int j = 0; j < n_jobs; ++j) {
+    const lann_job& J = jobs[j];
+    TKey k{job_ds[j], J.train_fraction, J.n_folds >= 2 ? J.n_folds : 0,
+           J.n_folds >= 2 ? J.fold : 0, J.family, J.log_target};
+    auto it = tkeys.find(k);
+    if (it == tkeys.end()) {
+      it = tkeys.emplace(k, int(tsrc.size())).first;
+      tsrc.push_back(k);
+    }
+    job_tile[j] = it->second;
+  }
+  std::vector<Dataset> dsets(dsrc.size());
+  std::vector<Status> dstat(dsrc.size());
+  parallel_for(int(dsrc.size()), [&](int d) {
+    dstat[d] = build_dataset(dsrc[d]->world, dsrc[d]->data_seed, dsrc[d]->count, dsets[d]);
+  });
+  std::vector<Tile> tiles(tsrc.size());
+  std::vector<Status> tstat(tsrc.size());
+  parallel_for(int(tsrc.size()), [&](int k) {
+    const auto& [d, frac, folds, fold, family, logt] = tsrc[k];
+    if (dstat[d]) {
+      tstat[k] = dstat[d];
+      return;
+    }
+    std::vector<int64_t> order;
+    int ntr = 0;
+    tstat[k] = split_order(dsets[d].size(), frac, dsrc[d]->data_seed, order, ntr);
+    if (!tstat[k]) tstat[k] = make_tile(dsets[d], order, ntr, folds, fold, family, logt != 0, tiles[k]);
+  });
+  for (int j = 0; j < n_jobs; ++j) {
+    const int k = job_tile[j];
+    Status st = tstat[k];
+    if (!st) st = validate_config(jobs[j], tiles[k].n_inputs);
+    if (!st && tiles[k].n_eval() < 2)
+      st = {LANN_DOMAIN_ERROR, "spearman needs at least two samples"};  // eval.cpp:80
+    lann_job_result& r = pop.base[j];
+    r.status = st.code;
+    if (st) {
+      if (e->err.empty()) e->err = st.msg;
+      continue;
+    }
+    r.n_inputs = tiles[k].n_inputs;
+    r.n_params = param_count(tiles[k].n_inputs, jobs[j].hidden[0],
+                             jobs[j].n_hidden > 1 ? jobs[j].hidden[1] : 0);
+    r.n_train = tiles[k].n_train();
+    r.n_eval = tiles[k].n_eval();
+    pop.model_job.push_back(j);
+  }
+  const int M = int(pop.model_job.size());
+  pop.M = M;
+  if (M == 0) return pop.base[0].status;
+  // pack
+  DevTrain& t = pop.t;
+  t.n_models = M;
+  t.n_tiles = int(tiles.size());
+  std::vector<double> X, Y, eval_rows, eval_truth, norm(size_t(M) * 18);
+  std::vector<int> eval_model, n_in(M), logt(M), eval_len(M);
+  std::vector<int64_t> eval_off(M);
+  for (size_t k = 0; k < tiles.size(); ++k) {
+    t.tile_rows.push_back(std::max(1, tiles[k].n_train()));
+    t.tile_inputs.push_back(std::max(1, tiles[k].n_inputs));
+    t.tile_offset.push_back(pop.rows);
+    X.insert(X.end(), tiles[k].Xn.begin(), tiles[k].Xn.end());
+    Y.insert(Y.end(), tiles[k].yn.begin(), tiles[k].yn.end());
+    pop.rows += tiles[k].n_train();
+  }
+  for (int m = 0; m < M; ++m) {
+    const lann_job& J = jobs[pop.model_job[m]];
+    const Tile& T = tiles[job_tile[pop.model_job[m]]];
+    t.model_tile.push_back(job_tile[pop.model_job[m]]);
+    t.h1.push_back(J.hidden[0]);
+    t.h2.push_back(J.n_hidden > 1 ? J.hidden[1] : 0);
+    t.lr.push_back(J.learning_rate);
+    t.epochs.push_back(J.epochs);
+    t.param_offset.push_back(t.total_params);
+    t.total_params += param_count(T.n_inputs, t.h1.back(), t.h2.back());
+    pop.train_flop += double(J.epochs) * flop_per_model_epoch(T.n_inputs, t.h1.back(), t.h2.back(), T.n_train());
+    std::memcpy(&norm[size_t(m) * 18], T.norm, sizeof T.norm);
+    n_in[m] = T.n_inputs;
+    logt[m] = T.log_target;
+    eval_off[m] = int64_t(eval_truth.size());
+    eval_len[m] = T.n_eval();
+    pop.max_eval = std::max(pop.max_eval, T.n_eval());
+    eval_rows.insert(eval_rows.end(), T.eval_rows.begin(), T.eval_rows.end());
+    eval_truth.insert(eval_truth.end(), T.eval_truth.begin(), T.eval_truth.end());
+    for (int r = 0; r < T.n_eval(); ++r) eval_model.push_back(m);
+  }
+  pop.init_params.assign(size_t(t.total_params), 0.0);
+  parallel_for(M, [&](int m) {
+    const lann_job& J = jobs[pop.model_job[m]];
+    glorot_init(n_in[m], t.h1[m], t.h2[m], J.init_seed, &pop.init_params[size_t(t.param_offset[m])]);
+  });
+  if (Status st = validate_train(t)) return set_err(e, st);
+  if (size_t(pop.max_eval) * 36 + 16 > size_t(e->max_smem))
+    return set_err(e, {LANN_PARAM_ERROR, "evaluation set too large for one CTA"});
+  pop.toff.assign(M, 0);
+  if (want_trace)
+    for (int m = 0; m < M; ++m) {
+      pop.toff[m] = pop.trace_total;
+      pop.trace_total += t.epochs[m];
+    }
+  // upload once
+  cudaStream_t s = e->stream;
+  pop.dX = DBuf<double>(X, s);
+  pop.dY = DBuf<double>(Y, s);
+  pop.dP0 = DBuf<double>(pop.init_params, s);
+  pop.dP = DBuf<double>(pop.init_params.size(), s);
+  pop.dF = DBuf<double>(size_t(M), s);
+  pop.dB = DBuf<int>(size_t(M), s);
+  pop.dT = DBuf<double>(size_t(pop.trace_total), s);
+  pop.dTO = DBuf<int64_t>(pop.toff, s);
+  pop.n_eval_rows = int64_t(eval_truth.size());
+  pop.dER = DBuf<double>(eval_rows, s);
+  pop.dPred = DBuf<double>(size_t(pop.n_eval_rows), s);
+  pop.dN = DBuf<double>(norm, s);
+  pop.dET = DBuf<double>(eval_truth, s);
+  pop.dEM = DBuf<int>(eval_model, s);
+  pop.dI = DBuf<int>(n_in, s);
+  pop.dh1 = DBuf<int>(t.h1, s);
+  pop.dh2 = DBuf<int>(t.h2, s);
+  pop.dlog = DBuf<int>(logt, s);
+  pop.dpo = DBuf<int64_t>(t.param_offset, s);
+  pop.dEO = DBuf<int64_t>(eval_off, s);
+  pop.dEL = DBuf<int>(eval_len, s);
+  pop.dK = DBuf<int>(size_t(M), s);
+  pop.dS = DBuf<int>(size_t(M), s);
+  pop.dMape = DBuf<double>(size_t(M), s);
+  pop.dThr = DBuf<double>(size_t(M), s);
+  pop.dRho = DBuf<double>(size_t(M), s);
+  pop.plan = build_plan(e, t, precision, pop.dX.p, pop.dY.p, pop.rows);
+  ck(cudaStreamSynchronize(s), "prepare");
+  return LANN_OK;
+}
+
+// One device-only pass: reset weights, train, predict every evaluation row, metrics.
+void run_device(Population& pop) {
+  lann_engine* e = pop.e;
+  cudaStream_t s = e->stream;
+  ck(cudaMemcpyAsync(pop.dP.p, pop.dP0.p, pop.dP0.n * sizeof(double), cudaMemcpyDeviceToDevice, s), "D2D");
+  execute_plan(e, *pop.plan, pop.dP.p, pop.dF.p, pop.dB.p, pop.trace_total ? pop.dT.p : nullptr, pop.dTO.p);
+  PredictArgs pa{pop.n_eval_rows, pop.dER.p, pop.dEM.p, pop.dI.p, pop.dh1.p, pop.dh2.p, pop.dlog.p,
+                 pop.dpo.p, pop.dP.p, pop.dN.p, pop.dPred.p};
+  if (pop.precision == LANN_FP32) launch_predict_fp32(pa, s);
+  else launch_predict_fp64(pa, s);
+  e->launches += pop.n_eval_rows > 0;
+  EvalArgs ea{pop.M, pop.dEO.p, pop.dEL.p, pop.dET.p, pop.dPred.p, 0.3, pop.dMape.p, pop.dThr.p,
+              pop.dK.p, pop.dRho.p, pop.dS.p};
+  launch_eval(ea, pop.max_eval, s);
+  e->launches += 1;
+  ck(cudaGetLastError(), "population launch");
+}
+
+int fetch_population(Population& pop, lann_job_result* results, double* params_out,
+                     const int64_t* params_offset, double* trace_out, const int64_t* trace_offset) {
+  const int M = pop.M;
+  for (int j = 0; j < pop.n_jobs; ++j) results[j] = pop.base[j];
+  if (M == 0) return pop.base[0].status;
+  std::vector<double> fin(M), mape(M), thr(M), rho(M), params;
+  std::vector<int> bad(M), kept(M), est(M);
+  pop.dF.down(fin.data());
+  pop.dB.down(bad.data());
+  pop.dMape.down(mape.data());
+  pop.dThr.down(thr.data());
+  pop.dRho.down(rho.data());
+  pop.dK.down(kept.data());
+  pop.dS.down(est.data());
+  if (params_out) {
+    params.resize(pop.dP.n);
+    pop.dP.down(params.data());
+  }
+  std::vector<double> trace(static_cast<size_t>(pop.trace_total));
+  if (trace_out && pop.trace_total) pop.dT.down(trace.data());
+  ck(cudaStreamSynchronize(pop.e->stream), "fetch");
+  for (int m = 0; m < M; ++m) {
+    const int j = pop.model_job[m];
+    lann_job_result& r = results[j];
+    r.final_loss = fin[m];
+    r.nonfinite_epoch = bad[m];
+    if (bad[m] >= 0) {
+      r.status = LANN_TRAINING_ERROR;
+    } else {
+      r.mape = mape[m];
+      r.mape_thr = thr[m];
+      r.rho = rho[m];
+      r.n_kept = kept[m];
+      if (est[m]) r.status = LANN_DOMAIN_ERROR;
+    }
+    if (params_out && params_offset)
+      std::memcpy(params_out + params_offset[j], &params[size_t(pop.t.param_offset[m])],
+                  sizeof(double) * size_t(r.n_params));
+    if (trace_out && trace_offset && pop.trace_total)
+      std::memcpy(trace_out + trace_offset[j], &trace[size_t(pop.toff[m])],
+                  sizeof(double) * size_t(pop.t.epochs[m]));
+  }
+  for (int j = 0; j < pop.n_jobs; ++j)
+    if (results[j].status != LANN_OK) {
+      if (results[j].status == LANN_TRAINING_ERROR)
+        pop.e->err = "training diverged (non-finite loss) at epoch " +
+                     std::to_string(results[j].nonfinite_epoch);
+      return results[j].status;
+    }
+  return LANN_OK;
 }
 
 }  // namespace
 }  // namespace lann
 
 using namespace lann;
+
+struct lann_population {
+  Population pop;
+};
 
 extern "C" {
 
@@ -314,10 +669,13 @@ int lann_engine_create(int device, lann_engine** out) {
   try {
     ck(cudaSetDevice(device), "cudaSetDevice");
     ck(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking), "stream");
-    ck(cudaEventCreate(&e->ev0), "event");
-    ck(cudaEventCreate(&e->ev1), "event");
+    for (auto& a : e->aux) ck(cudaStreamCreateWithFlags(&a, cudaStreamNonBlocking), "stream");
+    for (cudaEvent_t* ev : {&e->ev0, &e->ev1, &e->tr0, &e->tr1}) ck(cudaEventCreate(ev), "event");
+    ck(cudaEventCreateWithFlags(&e->fork, cudaEventDisableTiming), "event");
+    for (auto& j : e->join) ck(cudaEventCreateWithFlags(&j, cudaEventDisableTiming), "event");
     ck(cudaDeviceGetAttribute(&e->max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, device), "attr");
-  } catch (const CudaFail& f) {
+    ck(cudaDeviceGetAttribute(&e->sms, cudaDevAttrMultiProcessorCount, device), "attr");
+  } catch (const CudaFail&) {
     delete e;
     return LANN_CUDA_ERROR;
   }
@@ -329,14 +687,19 @@ void lann_engine_destroy(lann_engine* e) {
   if (!e) return;
   cudaSetDevice(e->device);
   if (e->stream) cudaStreamSynchronize(e->stream);
-  if (e->ev0) cudaEventDestroy(e->ev0);
-  if (e->ev1) cudaEventDestroy(e->ev1);
+  for (cudaEvent_t ev : {e->ev0, e->ev1, e->tr0, e->tr1, e->fork})
+    if (ev) cudaEventDestroy(ev);
+  for (auto j : e->join)
+    if (j) cudaEventDestroy(j);
+  for (auto a : e->aux)
+    if (a) cudaStreamDestroy(a);
   if (e->stream) cudaStreamDestroy(e->stream);
   delete e;
 }
 
 const char* lann_last_error(const lann_engine* e) { return e ? e->err.c_str() : "no engine"; }
 double lann_last_device_ms(const lann_engine* e) { return e ? e->last_ms : 0.0; }
+double lann_last_train_ms(const lann_engine* e) { return e ? e->last_train_ms : 0.0; }
 int64_t lann_last_launches(const lann_engine* e) { return e ? e->launches : 0; }
 
 int lann_train(lann_engine* e, const lann_train_batch* b) {
@@ -374,21 +737,23 @@ int lann_train(lann_engine* e, const lann_train_batch* b) {
     DBuf<int> dB(size_t(b->n_models), s);
     int64_t trace_total = 0;
     std::vector<int64_t> toff(b->n_models, 0);
-    if (b->loss_trace) {
+    if (b->loss_trace)
       for (int m = 0; m < b->n_models; ++m) {
         toff[m] = b->trace_offset[m];
         trace_total = std::max<int64_t>(trace_total, toff[m] + (t.epochs[m] + t.trace_stride - 1) / t.trace_stride);
       }
-    }
     DBuf<double> dT(size_t(trace_total), s);
     DBuf<int64_t> dTO(toff, s);
-    run_train(e, t, b->precision, dX.p, dY.p, b->total_rows, dP.p, dF.p, dB.p,
-              b->loss_trace ? dT.p : nullptr, dTO);
+    auto plan = build_plan(e, t, b->precision, dX.p, dY.p, b->total_rows);
+    execute_plan(e, *plan, dP.p, dF.p, dB.p, b->loss_trace ? dT.p : nullptr, dTO.p);
     dP.down(b->params);
     dF.down(b->final_loss);
     dB.down(b->nonfinite_epoch);
     if (b->loss_trace) dT.down(b->loss_trace);
     timer.stop();
+    float tms = 0.f;
+    ck(cudaEventElapsedTime(&tms, e->tr0, e->tr1), "elapsed");
+    e->last_train_ms = tms;
     for (int m = 0; m < b->n_models; ++m)
       if (b->nonfinite_epoch[m] >= 0) {
         e->err = "training diverged (non-finite loss) at epoch " + std::to_string(b->nonfinite_epoch[m]);
@@ -407,10 +772,10 @@ int lann_predict(lann_engine* e, const lann_model_set* ms, int64_t n_rows, const
   if (!e) return LANN_NO_DEVICE;
   if (!ms || ms->n_models < 1) return set_err(e, {LANN_PARAM_ERROR, "empty model set"});
   for (int m = 0; m < ms->n_models; ++m) {
-    const int P = param_count(ms->n_inputs[m], ms->h1[m], ms->h2[m]);
     if (ms->n_inputs[m] < 1 || ms->n_inputs[m] > 7 || ms->h1[m] < 1 || ms->h2[m] < 0 ||
         ms->h1[m] > 64 || ms->h2[m] > 64)
       return set_err(e, {LANN_PARAM_ERROR, "bad model shape"});
+    const int P = param_count(ms->n_inputs[m], ms->h1[m], ms->h2[m]);
     if (ms->param_offset[m] < 0 || ms->param_offset[m] + P > ms->total_params)
       return set_err(e, {LANN_PARAM_ERROR, "flat parameter size mismatch"});
   }
@@ -548,16 +913,19 @@ int lann_select_variants(lann_engine* e, const lann_model_set* ms, const int32_t
     DBuf<int64_t> dpo(ms->param_offset, M, s);
     DBuf<double> dp(ms->params, size_t(ms->total_params), s), dn(ms->norm, size_t(M) * 18, s),
         dsc(size_t(n_cands), s);
-    int sms = 148;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, e->device);
     Timer timer(e);
+    ck(cudaEventRecord(e->tr0, s), "event");
     e->launches += select_variants_launch(M, ms->precision, kind, max_threads, seed, first, n_cands,
                                           dI.p, dh1.p, dh2.p, dl.p, dt.p, dpo.p, dp.p, dn.p, didx.p,
-                                          dsc.p, sms, s);
+                                          dsc.p, e->sms, s);
     ck(cudaGetLastError(), "select_variants launch");
+    ck(cudaEventRecord(e->tr1, s), "event");
     didx.down(out_idx);
     dsc.down(out_score);
     timer.stop();
+    float kms = 0.f;
+    ck(cudaEventElapsedTime(&kms, e->tr0, e->tr1), "elapsed");
+    e->last_train_ms = kms;  // the scoring kernel's own device time
     e->err.clear();
     return LANN_OK;
   } catch (const CudaFail& f) {
@@ -597,226 +965,117 @@ int lann_init_params(int32_t n_dims, const int32_t* dims, uint64_t seed, double*
   return LANN_OK;
 }
 
-// Whole-population pipeline: host builds datasets / tiles / initial weights (each
-// distinct dataset and tile once), then ONE device pass trains every model,
-// predicts every evaluation row and computes every model's metrics.
+int lann_population_create(lann_engine* e, int32_t n_jobs, const lann_job* jobs,
+                           int32_t precision, int32_t record_trace, lann_population** out) {
+  if (!e) return LANN_NO_DEVICE;
+  if (!out || n_jobs < 1 || !jobs) return set_err(e, {LANN_PARAM_ERROR, "empty population"});
+  if (precision != LANN_FP64_EXACT && precision != LANN_FP32)
+    return set_err(e, {LANN_PARAM_ERROR, "unknown precision"});
+  *out = nullptr;
+  auto* p = new lann_population;
+  try {
+    ck(cudaSetDevice(e->device), "cudaSetDevice");
+    const int st = prepare_population(e, n_jobs, jobs, precision, record_trace != 0, p->pop);
+    if (st != LANN_OK && p->pop.M == 0) {
+      delete p;
+      return st;
+    }
+  } catch (const CudaFail& f) {
+    delete p;
+    e->err = f.what;
+    return LANN_CUDA_ERROR;
+  }
+  *out = p;
+  return LANN_OK;
+}
+
+int lann_population_run(lann_population* p, int32_t n_steps) {
+  if (!p) return LANN_PARAM_ERROR;
+  lann_engine* e = p->pop.e;
+  try {
+    ck(cudaSetDevice(e->device), "cudaSetDevice");
+    Timer timer(e);
+    double train_ms = 0.0;
+    for (int i = 0; i < std::max(1, n_steps); ++i) {
+      run_device(p->pop);
+      float tms = 0.f;
+      ck(cudaEventSynchronize(e->tr1), "sync");
+      ck(cudaEventElapsedTime(&tms, e->tr0, e->tr1), "elapsed");
+      train_ms += tms;
+    }
+    timer.stop();
+    e->last_train_ms = train_ms;
+    return LANN_OK;
+  } catch (const CudaFail& f) {
+    e->err = f.what;
+    return LANN_CUDA_ERROR;
+  }
+}
+
+int lann_population_fetch(lann_population* p, lann_job_result* results, double* params_out,
+                          const int64_t* params_offset, double* trace_out,
+                          const int64_t* trace_offset) {
+  if (!p || !results) return LANN_PARAM_ERROR;
+  try {
+    ck(cudaSetDevice(p->pop.e->device), "cudaSetDevice");
+    return fetch_population(p->pop, results, params_out, params_offset, trace_out, trace_offset);
+  } catch (const CudaFail& f) {
+    p->pop.e->err = f.what;
+    return LANN_CUDA_ERROR;
+  }
+}
+
+void lann_transfer_bytes(int64_t* h2d, int64_t* d2h, int32_t reset) {
+  if (h2d) *h2d = t_h2d;
+  if (d2h) *d2h = t_d2h;
+  if (reset) t_h2d = t_d2h = 0;
+}
+
+int lann_population_norm(const lann_population* p, double* norm_out) {
+  if (!p || !norm_out) return LANN_PARAM_ERROR;
+  const Population& pop = p->pop;
+  std::memset(norm_out, 0, sizeof(double) * 18 * size_t(pop.n_jobs));
+  std::vector<double> norm(size_t(pop.M) * 18);
+  if (pop.M) {
+    pop.dN.down(norm.data());
+    cudaStreamSynchronize(pop.e->stream);
+  }
+  for (int m = 0; m < pop.M; ++m)
+    std::memcpy(norm_out + 18 * size_t(pop.model_job[m]), &norm[18 * size_t(m)], 18 * sizeof(double));
+  return LANN_OK;
+}
+
+double lann_population_flop(const lann_population* p) { return p ? p->pop.train_flop : 0.0; }
+int64_t lann_population_models(const lann_population* p) { return p ? p->pop.M : 0; }
+
+void lann_population_destroy(lann_population* p) {
+  if (!p) return;
+  cudaSetDevice(p->pop.e->device);
+  cudaStreamSynchronize(p->pop.e->stream);
+  delete p;
+}
+
+// One-shot pipeline = create + one device pass + fetch, timed as a whole.
 int lann_run_population(lann_engine* e, int32_t n_jobs, const lann_job* jobs, int32_t precision,
                         lann_job_result* results, double* params_out,
                         const int64_t* params_offset, double* trace_out,
                         const int64_t* trace_offset) {
   if (!e) return LANN_NO_DEVICE;
-  if (n_jobs < 1 || !jobs || !results) return set_err(e, {LANN_PARAM_ERROR, "empty population"});
-  if (precision != LANN_FP64_EXACT && precision != LANN_FP32)
-    return set_err(e, {LANN_PARAM_ERROR, "unknown precision"});
-  for (int j = 0; j < n_jobs; ++j) {
-    std::memset(&results[j], 0, sizeof(lann_job_result));
-    results[j].nonfinite_epoch = -1;
-  }
-  // ---- distinct datasets, splits and tiles ----
-  using DKey = std::tuple<std::string, uint64_t, int>;
-  std::map<DKey, int> dkeys;
-  std::vector<const lann_job*> dsrc;
-  std::vector<int> job_ds(n_jobs);
-  for (int j = 0; j < n_jobs; ++j) {
-    DKey k{std::string(reinterpret_cast<const char*>(&jobs[j].world), sizeof(lann_world)),
-           jobs[j].data_seed, jobs[j].count};
-    auto it = dkeys.find(k);
-    if (it == dkeys.end()) {
-      it = dkeys.emplace(k, int(dsrc.size())).first;
-      dsrc.push_back(&jobs[j]);
+  if (!results) return set_err(e, {LANN_PARAM_ERROR, "null results"});
+  lann_population* p = nullptr;
+  const int st = lann_population_create(e, n_jobs, jobs, precision, trace_out != nullptr, &p);
+  if (!p) {
+    for (int j = 0; j < n_jobs && jobs; ++j) {
+      std::memset(&results[j], 0, sizeof(lann_job_result));
+      results[j].status = st;
+      results[j].nonfinite_epoch = -1;
     }
-    job_ds[j] = it->second;
+    return st;
   }
-  using TKey = std::tuple<int, double, int, int, int, int>;
-  std::map<TKey, int> tkeys;
-  std::vector<int> job_tile(n_jobs);
-  std::vector<TKey> tsrc;
-  for (int j = 0; j < n_jobs; ++j) {
-    const lann_job& J = jobs[j];
-    TKey k{job_ds[j], J.train_fraction, J.n_folds >= 2 ? J.n_folds : 0,
-           J.n_folds >= 2 ? J.fold : 0, J.family, J.log_target};
-    auto it = tkeys.find(k);
-    if (it == tkeys.end()) {
-      it = tkeys.emplace(k, int(tsrc.size())).first;
-      tsrc.push_back(k);
-    }
-    job_tile[j] = it->second;
-  }
-  const int nthreads = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
-  auto parallel_for = [&](int n, auto&& fn) {
-    std::atomic<int> next{0};
-    std::vector<std::thread> pool;
-    auto worker = [&] {
-      for (int i; (i = next.fetch_add(1)) < n;) fn(i);
-    };
-    for (int t = 1; t < std::min(nthreads, n); ++t) pool.emplace_back(worker);
-    worker();
-    for (auto& th : pool) th.join();
-  };
-  std::vector<Dataset> dsets(dsrc.size());
-  std::vector<Status> dstat(dsrc.size());
-  parallel_for(int(dsrc.size()), [&](int d) {
-    dstat[d] = build_dataset(dsrc[d]->world, dsrc[d]->data_seed, dsrc[d]->count, dsets[d]);
-  });
-  std::vector<Tile> tiles(tsrc.size());
-  std::vector<Status> tstat(tsrc.size());
-  parallel_for(int(tsrc.size()), [&](int k) {
-    const auto& [d, frac, folds, fold, family, logt] = tsrc[k];
-    if (dstat[d]) {
-      tstat[k] = dstat[d];
-      return;
-    }
-    std::vector<int64_t> order;
-    int ntr = 0;
-    tstat[k] = split_order(dsets[d].size(), frac, dsrc[d]->data_seed, order, ntr);
-    if (!tstat[k]) tstat[k] = make_tile(dsets[d], order, ntr, folds, fold, family, logt != 0, tiles[k]);
-  });
-  // ---- per-job validation and initial weights ----
-  std::vector<int> model_job;  // trained model -> job
-  std::vector<int> job_model(n_jobs, -1);
-  for (int j = 0; j < n_jobs; ++j) {
-    const int k = job_tile[j];
-    Status st = tstat[k];
-    if (!st) st = validate_config(jobs[j], tiles[k].n_inputs);
-    results[j].status = st.code;
-    if (st) {
-      if (e->err.empty()) e->err = st.msg;
-      continue;
-    }
-    results[j].n_inputs = tiles[k].n_inputs;
-    results[j].n_params = param_count(tiles[k].n_inputs, jobs[j].hidden[0],
-                                      jobs[j].n_hidden > 1 ? jobs[j].hidden[1] : 0);
-    results[j].n_train = tiles[k].n_train();
-    results[j].n_eval = tiles[k].n_eval();
-    job_model[j] = int(model_job.size());
-    model_job.push_back(j);
-  }
-  const int M = int(model_job.size());
-  if (M == 0) return set_err(e, {results[0].status, e->err});
-  DevTrain t;
-  t.n_models = M;
-  t.n_tiles = int(tiles.size());
-  std::vector<double> X, Y, eval_rows, eval_truth;
-  std::vector<int> eval_model;
-  std::vector<int64_t> eval_off(M), tile_eval_off(tiles.size());
-  int64_t rows = 0;
-  for (size_t k = 0; k < tiles.size(); ++k) {
-    t.tile_rows.push_back(tiles[k].n_train());
-    t.tile_inputs.push_back(std::max(1, tiles[k].n_inputs));
-    t.tile_offset.push_back(rows);
-    X.insert(X.end(), tiles[k].Xn.begin(), tiles[k].Xn.end());
-    Y.insert(Y.end(), tiles[k].yn.begin(), tiles[k].yn.end());
-    rows += tiles[k].n_train();
-  }
-  std::vector<double> norm(size_t(M) * 18);
-  std::vector<int> n_in(M), logt(M), eval_len(M);
-  int max_eval = 1;
-  for (int m = 0; m < M; ++m) {
-    const lann_job& J = jobs[model_job[m]];
-    const Tile& T = tiles[job_tile[model_job[m]]];
-    t.model_tile.push_back(job_tile[model_job[m]]);
-    t.h1.push_back(J.hidden[0]);
-    t.h2.push_back(J.n_hidden > 1 ? J.hidden[1] : 0);
-    t.lr.push_back(J.learning_rate);
-    t.epochs.push_back(J.epochs);
-    t.param_offset.push_back(t.total_params);
-    t.total_params += param_count(T.n_inputs, t.h1.back(), t.h2.back());
-    std::memcpy(&norm[size_t(m) * 18], T.norm, sizeof T.norm);
-    n_in[m] = T.n_inputs;
-    logt[m] = T.log_target;
-    eval_off[m] = int64_t(eval_truth.size());
-    eval_len[m] = T.n_eval();
-    max_eval = std::max(max_eval, T.n_eval());
-    eval_rows.insert(eval_rows.end(), T.eval_rows.begin(), T.eval_rows.end());
-    eval_truth.insert(eval_truth.end(), T.eval_truth.begin(), T.eval_truth.end());
-    for (int r = 0; r < T.n_eval(); ++r) eval_model.push_back(m);
-  }
-  std::vector<double> params(size_t(t.total_params));
-  parallel_for(M, [&](int m) {
-    const lann_job& J = jobs[model_job[m]];
-    glorot_init(n_in[m], t.h1[m], t.h2[m], J.init_seed, &params[size_t(t.param_offset[m])]);
-  });
-  if (Status st = validate_train(t)) return set_err(e, st);
-  const bool want_trace = trace_out && trace_offset;
-  std::vector<int64_t> toff(M, 0);
-  int64_t trace_total = 0;
-  if (want_trace)
-    for (int m = 0; m < M; ++m) {
-      toff[m] = trace_total;
-      trace_total += t.epochs[m];
-    }
-  for (int m = 0; m < M; ++m)
-    if (eval_len[m] < 2) {
-      results[model_job[m]].status = LANN_DOMAIN_ERROR;  // spearman needs two samples
-    }
-  if (size_t(max_eval) * 36 + 16 > size_t(e->max_smem))
-    return set_err(e, {LANN_PARAM_ERROR, "evaluation set too large for one CTA"});
-  try {
-    ck(cudaSetDevice(e->device), "cudaSetDevice");
-    cudaStream_t s = e->stream;
-    Timer timer(e);
-    DBuf<double> dX(X, s), dY(Y, s), dP(params, s), dF(size_t(M), s), dT(size_t(trace_total), s);
-    DBuf<int> dB(size_t(M), s);
-    DBuf<int64_t> dTO(toff, s);
-    run_train(e, t, precision, dX.p, dY.p, rows, dP.p, dF.p, dB.p, want_trace ? dT.p : nullptr, dTO);
-    // predictions on every evaluation row, straight from the device-resident weights
-    const int64_t n_eval_rows = int64_t(eval_truth.size());
-    DBuf<double> dER(eval_rows, s), dPred(size_t(n_eval_rows), s), dN(norm, s), dET(eval_truth, s);
-    DBuf<int> dEM(eval_model, s), dI(n_in, s), dh1(t.h1, s), dh2(t.h2, s), dlog(logt, s);
-    DBuf<int64_t> dpo(t.param_offset, s);
-    PredictArgs pa{n_eval_rows, dER.p, dEM.p, dI.p, dh1.p, dh2.p, dlog.p, dpo.p, dP.p, dN.p, dPred.p};
-    if (precision == LANN_FP32) launch_predict_fp32(pa, s);
-    else launch_predict_fp64(pa, s);
-    e->launches += n_eval_rows > 0;
-    DBuf<int64_t> dEO(eval_off, s);
-    DBuf<int> dEL(eval_len, s), dK(size_t(M), s), dS(size_t(M), s);
-    DBuf<double> dMape(size_t(M), s), dThr(size_t(M), s), dRho(size_t(M), s);
-    EvalArgs ea{M, dEO.p, dEL.p, dET.p, dPred.p, 0.3, dMape.p, dThr.p, dK.p, dRho.p, dS.p};
-    launch_eval(ea, max_eval, s);
-    e->launches += 1;
-    ck(cudaGetLastError(), "population launch");
-    std::vector<double> fin(M), mape(M), thr(M), rho(M);
-    std::vector<int> bad(M), kept(M), est(M);
-    dF.down(fin.data());
-    dB.down(bad.data());
-    dMape.down(mape.data());
-    dThr.down(thr.data());
-    dRho.down(rho.data());
-    dK.down(kept.data());
-    dS.down(est.data());
-    if (params_out) dP.down(params.data());
-    std::vector<double> trace(static_cast<size_t>(trace_total));
-    if (want_trace) dT.down(trace.data());
-    timer.stop();
-    int first_err = LANN_OK;
-    for (int m = 0; m < M; ++m) {
-      const int j = model_job[m];
-      lann_job_result& r = results[j];
-      r.final_loss = fin[m];
-      r.nonfinite_epoch = bad[m];
-      if (bad[m] >= 0) {
-        r.status = LANN_TRAINING_ERROR;
-      } else if (r.status == LANN_OK) {
-        r.mape = mape[m];
-        r.mape_thr = thr[m];
-        r.rho = rho[m];
-        r.n_kept = kept[m];
-        if (est[m]) r.status = LANN_DOMAIN_ERROR;
-      }
-      if (params_out && params_offset)
-        std::memcpy(params_out + params_offset[j], &params[size_t(t.param_offset[m])],
-                    sizeof(double) * size_t(r.n_params));
-      if (want_trace)
-        std::memcpy(trace_out + trace_offset[j], &trace[size_t(toff[m])],
-                    sizeof(double) * size_t(t.epochs[m]));
-    }
-    for (int j = 0; j < n_jobs; ++j)
-      if (results[j].status != LANN_OK && first_err == LANN_OK) first_err = results[j].status;
-    return first_err;
-  } catch (const CudaFail& f) {
-    e->err = f.what;
-    return LANN_CUDA_ERROR;
-  }
+  int rc = lann_population_run(p, 1);
+  if (rc == LANN_OK) rc = lann_population_fetch(p, results, params_out, params_offset, trace_out, trace_offset);
+  lann_population_destroy(p);
+  return rc;
 }
 
 int lann_default_combos(lann_world* out, int32_t cap) {

@@ -229,6 +229,196 @@ __global__ void __launch_bounds__(32) train_fp32_kernel(TrainF32Args a) {
   }
 }
 
+// ---------------------------------------------------------------------------------
+// Small populations (fewer models than SMs x warps, e.g. the 48-combo config):
+// ONE model per CTA of 256 threads so the epoch latency, not the FLOP rate, is
+// minimised. Threads own samples; per epoch the 256 per-sample gradients are
+// reduced in two levels through shared memory (warp transpose-sum, then across
+// the 8 warps), 73-odd owner threads apply Adam, and the new weights are
+// broadcast back through shared memory. Two __syncthreads per epoch.
+constexpr int kCtaThreads = 256;
+constexpr int kCtaWarps = kCtaThreads / 32;
+
+template <int I, int H1, int H2>
+__global__ void __launch_bounds__(kCtaThreads) train_fp32_cta_kernel(TrainF32Args a) {
+  using N = Net<I, H1, H2>;
+  constexpr int P = N::P;
+  constexpr int PP = (P + 3) & ~3;  // padded row of the transpose buffer
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ uint64_t bar;
+  __shared__ __align__(16) float wsh[PP];
+  __shared__ float part[kCtaWarps][P + 1];  // per-warp partial gradients (+ loss)
+  __shared__ float loss_sh;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int m = a.sorted_model[a.group_first[blockIdx.x]];
+  const int tile = a.model_tile[m];
+  const int rows = a.tile_rows[tile];
+  const int E = a.epochs[m];
+  float* trow = reinterpret_cast<float*>(smem_raw);              // [rows][8]
+  constexpr int PT = P | 1;  // odd transpose stride: conflict-free row writes and column reads
+  float* tbuf = trow + (size_t)rows * 8 + (size_t)warp * 32 * PT;  // [32][PT] per warp
+  if (tid == 0) tma_load_tile(trow, a.rows + a.tile_offset[tile] * 8, (uint32_t)rows * 32u, &bar);
+  const double* gp = a.params + a.param_offset[m];
+  for (int p = tid; p < PP; p += kCtaThreads) wsh[p] = p < P ? (float)gp[p] : 0.f;
+  float mo = 0.f, ve = 0.f;  // Adam moments of parameter `tid` (owner threads)
+  const float lr = (float)a.lr[m];
+  const float scale = 2.0f / (float)rows, inv_n = 1.0f / (float)rows;
+  double* trace = a.loss_trace ? a.loss_trace + a.trace_offset[m] : nullptr;
+  int bad = -1;
+  float last = 0.f;
+  mbar_wait(&bar, 0);
+  __syncthreads();
+
+  float w[P];
+  for (int e = 0; e < E; ++e) {
+#pragma unroll
+    for (int p = 0; p < P; ++p) w[p] = wsh[p];
+    float gr[P];
+#pragma unroll
+    for (int p = 0; p < P; ++p) gr[p] = 0.f;
+    float loss = 0.f;
+    for (int s = tid; s < rows; s += kCtaThreads) {
+      const float4 lo = *reinterpret_cast<const float4*>(trow + s * 8);
+      const float4 hi = *reinterpret_cast<const float4*>(trow + s * 8 + 4);
+      const float xv[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
+      float z1[H1];
+#pragma unroll
+      for (int h = 0; h < H1; ++h) {
+        float z = w[N::L1B + h];
+#pragma unroll
+        for (int i = 0; i < I; ++i) z = fmaf(w[N::L1W + h * I + i], xv[i], z);
+        z1[h] = fmaxf(z, 0.f);
+      }
+      float out;
+      float z2[H2 > 0 ? H2 : 1];
+      if constexpr (H2 > 0) {
+#pragma unroll
+        for (int o = 0; o < H2; ++o) {
+          float z = w[N::L2B + o];
+#pragma unroll
+          for (int h = 0; h < H1; ++h) z = fmaf(w[N::L2W + o * H1 + h], z1[h], z);
+          z2[o] = fmaxf(z, 0.f);
+        }
+        out = w[N::L3B];
+#pragma unroll
+        for (int o = 0; o < H2; ++o) out = fmaf(w[N::L3W + o], z2[o], out);
+      } else {
+        float acc0 = w[N::L2B], acc1 = 0.f;
+#pragma unroll
+        for (int h = 0; h < H1; ++h) {
+          if (h & 1) acc1 = fmaf(w[N::L2W + h], z1[h], acc1);
+          else acc0 = fmaf(w[N::L2W + h], z1[h], acc0);
+        }
+        out = acc0 + acc1;
+      }
+      const float err = out - xv[7];
+      loss = fmaf(err, err, loss);
+      const float d = err * scale;
+      if constexpr (H2 > 0) {
+        gr[N::L3B] += d;
+        float d2[H2];
+#pragma unroll
+        for (int o = 0; o < H2; ++o) {
+          gr[N::L3W + o] = fmaf(d, z2[o], gr[N::L3W + o]);
+          d2[o] = z2[o] > 0.f ? w[N::L3W + o] * d : 0.f;
+          gr[N::L2B + o] += d2[o];
+        }
+#pragma unroll
+        for (int h = 0; h < H1; ++h) {
+          float acc = 0.f;
+#pragma unroll
+          for (int o = 0; o < H2; ++o) {
+            gr[N::L2W + o * H1 + h] = fmaf(d2[o], z1[h], gr[N::L2W + o * H1 + h]);
+            acc = fmaf(w[N::L2W + o * H1 + h], d2[o], acc);
+          }
+          const float d1 = z1[h] > 0.f ? acc : 0.f;
+          gr[N::L1B + h] += d1;
+#pragma unroll
+          for (int i = 0; i < I; ++i) gr[N::L1W + h * I + i] = fmaf(d1, xv[i], gr[N::L1W + h * I + i]);
+        }
+      } else {
+        gr[N::L2B] += d;
+#pragma unroll
+        for (int h = 0; h < H1; ++h) {
+          gr[N::L2W + h] = fmaf(d, z1[h], gr[N::L2W + h]);
+          const float d1 = z1[h] > 0.f ? w[N::L2W + h] * d : 0.f;
+          gr[N::L1B + h] += d1;
+#pragma unroll
+          for (int i = 0; i < I; ++i) gr[N::L1W + h * I + i] = fmaf(d1, xv[i], gr[N::L1W + h * I + i]);
+        }
+      }
+    }
+    // level 1: warp transpose-sum through shared memory (lane j -> params j, j+32, ...)
+    float* myrow = tbuf + lane * PT;
+#pragma unroll
+    for (int p = 0; p < P; ++p) myrow[p] = gr[p];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) loss += __shfl_xor_sync(0xffffffffu, loss, off);
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < (P + 31) / 32; ++k) {
+      const int p = lane + 32 * k;
+      if (p < P) {
+        float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+#pragma unroll
+        for (int r = 0; r < 32; r += 4) {
+          s0 += tbuf[(r + 0) * PT + p];
+          s1 += tbuf[(r + 1) * PT + p];
+          s2 += tbuf[(r + 2) * PT + p];
+          s3 += tbuf[(r + 3) * PT + p];
+        }
+        part[warp][p] = (s0 + s1) + (s2 + s3);
+      }
+    }
+    if (lane == 0) part[warp][P] = loss;
+    __syncthreads();
+    // level 2: owners sum the 8 warp partials and apply Adam
+    if (tid <= P) {
+      float gsum = 0.f;
+#pragma unroll
+      for (int k = 0; k < kCtaWarps; ++k) gsum += part[k][tid];
+      if (tid == P) {
+        loss_sh = gsum * inv_n;
+      } else {
+        const float t = (float)(e + 1);
+        const float bc1 = 1.f - exp2f(t * -0.15200309344504997f);
+        const float bc2 = 1.f - exp2f(t * -0.0014434168696687106f);
+        mo = fmaf(0.1f, gsum, 0.9f * mo);
+        ve = fmaf(0.001f * gsum, gsum, 0.999f * ve);
+        wsh[tid] -= (lr / bc1) * mo / (sqrtf(ve / bc2) + 1e-8f);
+      }
+    }
+    __syncthreads();
+    const float L = loss_sh;
+    if (bad < 0) {
+      last = L;
+      if (trace && tid == 0 && (e % a.trace_stride) == 0) trace[e / a.trace_stride] = (double)L;
+    }
+    if (!isfinite(L)) {
+      bad = e;
+      break;  // uniform across the CTA (everyone read the same loss)
+    }
+  }
+  // weights of the failing epoch were updated with a non-finite gradient; the
+  // reference discards the model in that case (TrainingError), so do we
+  double* outp = a.params + a.param_offset[m];
+  for (int p = tid; p < P; p += kCtaThreads) outp[p] = (double)wsh[p];
+  if (tid == 0) {
+    a.final_loss[m] = (double)last;
+    a.nonfinite_epoch[m] = bad;
+  }
+}
+
+template <int I, int H1, int H2>
+void launch_cta(const TrainF32Args& a, int tile_bytes, cudaStream_t s) {
+  constexpr int P = Net<I, H1, H2>::P;
+  constexpr int PT = P | 1;
+  auto kern = train_fp32_cta_kernel<I, H1, H2>;
+  const int dyn = tile_bytes + kCtaWarps * 32 * PT * 4;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
+  kern<<<a.n_groups, kCtaThreads, dyn, s>>>(a);
+}
+
 // dynamic smem = the largest tile of the launch (rows x 32 B) + Adam moments
 template <int I, int H1, int H2, int K>
 void launch_k(const TrainF32Args& a, int tile_bytes, cudaStream_t s) {
@@ -247,6 +437,7 @@ bool dispatch_lanes(const TrainF32Args& a, int lanes, int tile_bytes, cudaStream
     case 4: launch_k<I, H1, H2, 4>(a, tile_bytes, s); return true;
     case 8: launch_k<I, H1, H2, 8>(a, tile_bytes, s); return true;
     case 32: launch_k<I, H1, H2, 32>(a, tile_bytes, s); return true;
+    case kCtaThreads: launch_cta<I, H1, H2>(a, tile_bytes, s); return true;
     default: return false;
   }
 }

@@ -135,10 +135,21 @@ __global__ void __launch_bounds__(256) train_fp64_exact(TrainArgs a) {
         const double* ain = r + sh.inoff[l];
         if (l + 1 < sh.nl) {
           double* aout = r + sh.inoff[l + 1];
-          for (int o = 0; o < out; ++o) {
-            double z = bl[o];
-            for (int i = 0; i < in; ++i) z = __dadd_rn(z, __dmul_rn(wl[o * in + i], ain[i]));
-            aout[o] = z > 0.0 ? z : 0.0;
+          // four output neurons at a time: four independent DADD chains in flight
+          for (int o = 0; o < out; o += 4) {
+            const int n4 = out - o < 4 ? out - o : 4;
+            double z[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) z[k] = k < n4 ? bl[o + k] : 0.0;
+            for (int i = 0; i < in; ++i) {
+              const double ai = ain[i];
+#pragma unroll
+              for (int k = 0; k < 4; ++k)
+                if (k < n4) z[k] = __dadd_rn(z[k], __dmul_rn(wl[(o + k) * in + i], ai));
+            }
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              if (k < n4) aout[o + k] = z[k] > 0.0 ? z[k] : 0.0;
           }
         } else {
           double z = bl[0];
@@ -155,10 +166,18 @@ __global__ void __launch_bounds__(256) train_fp64_exact(TrainArgs a) {
         const double* dn = r + sh.toff[l + 1];
         const double* act = r + sh.inoff[l + 1];
         double* d = r + sh.toff[l];
-        for (int i = 0; i < nin; ++i) {
-          double acc = 0.0;
-          for (int o = 0; o < nout; ++o) acc = __dadd_rn(acc, __dmul_rn(wn[o * nin + i], dn[o]));
-          d[i] = act[i] > 0.0 ? acc : 0.0;
+        for (int i = 0; i < nin; i += 4) {
+          const int n4 = nin - i < 4 ? nin - i : 4;
+          double acc[4] = {0.0, 0.0, 0.0, 0.0};
+          for (int o = 0; o < nout; ++o) {
+            const double dno = dn[o];
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              if (k < n4) acc[k] = __dadd_rn(acc[k], __dmul_rn(wn[o * nin + i + k], dno));
+          }
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            if (k < n4) d[i + k] = act[i + k] > 0.0 ? acc[k] : 0.0;
         }
       }
       // scale in place: t = inv_n * delta (the left factor of mlp.cpp:113,117)
@@ -172,13 +191,26 @@ __global__ void __launch_bounds__(256) train_fp64_exact(TrainArgs a) {
 #pragma unroll
     for (int k = 0; k < KB; ++k) g[k] = 0.0;
     if (tix[0] >= 0) {
-      for (int s = 0; s < N; ++s) {
-        const double* r = rec + (size_t)s * R;
+      if (KB == 1) {
+        // one chain: unrolled so the shared-memory loads run ahead of the DADDs
+        const double* tp = rec + tix[0];
+        if (aix[0] >= 0) {
+          const double* ap = rec + aix[0];
+#pragma unroll 10
+          for (int s = 0; s < N; ++s) g[0] = __dadd_rn(g[0], __dmul_rn(tp[(size_t)s * R], ap[(size_t)s * R]));
+        } else {
+#pragma unroll 10
+          for (int s = 0; s < N; ++s) g[0] = __dadd_rn(g[0], tp[(size_t)s * R]);
+        }
+      } else {
+        for (int s = 0; s < N; ++s) {
+          const double* r = rec + (size_t)s * R;
 #pragma unroll
-        for (int k = 0; k < KB; ++k) {
-          if (tix[k] >= 0) {
-            const double t = r[tix[k]];
-            g[k] = __dadd_rn(g[k], aix[k] >= 0 ? __dmul_rn(t, r[aix[k]]) : t);
+          for (int k = 0; k < KB; ++k) {
+            if (tix[k] >= 0) {
+              const double t = r[tix[k]];
+              g[k] = __dadd_rn(g[k], aix[k] >= 0 ? __dmul_rn(t, r[aix[k]]) : t);
+            }
           }
         }
       }
@@ -199,7 +231,9 @@ __global__ void __launch_bounds__(256) train_fp64_exact(TrainArgs a) {
     }
     if (tid == loss_tid) {
       double L = 0.0;
-      for (int s = 0; s < N; ++s) L = __dadd_rn(L, rec[(size_t)s * R + sh.e2]);
+      const double* ep = rec + sh.e2;
+#pragma unroll 10
+      for (int s = 0; s < N; ++s) L = __dadd_rn(L, ep[(size_t)s * R]);
       L = __dmul_rn(L, inv_n);  // mlp.cpp:120
       Ls[0] = L;
       if (trace && (e % a.trace_stride) == 0) trace[e / a.trace_stride] = L;

@@ -63,9 +63,19 @@ _lib = None
 
 # every symbol include/lann_engine.h declares
 EXPORTS = ["lann_engine_create", "lann_engine_destroy", "lann_last_error", "lann_last_device_ms",
-           "lann_last_launches", "lann_train", "lann_predict", "lann_eval", "lann_select_schedule",
-           "lann_select_variants", "lann_build_dataset", "lann_split_order", "lann_init_params",
-           "lann_run_population", "lann_default_combos"]
+           "lann_last_launches", "lann_last_train_ms", "lann_train", "lann_predict", "lann_eval",
+           "lann_select_schedule", "lann_select_variants", "lann_build_dataset", "lann_split_order",
+           "lann_init_params", "lann_population_create", "lann_population_run", "lann_population_fetch",
+           "lann_population_flop", "lann_population_models", "lann_population_destroy",
+           "lann_population_norm", "lann_transfer_bytes", "lann_run_population", "lann_default_combos"]
+
+
+def transfer_bytes(reset=False):
+    """(h2d, d2h) bytes moved by this thread's engine calls since the last reset."""
+    L = load_library()
+    h, d = C.c_int64(0), C.c_int64(0)
+    L.lann_transfer_bytes(C.addressof(h), C.addressof(d), int(reset))
+    return h.value, d.value
 
 
 def load_library(path: str = LIB_PATH):
@@ -86,6 +96,18 @@ def load_library(path: str = LIB_PATH):
     L.lann_last_device_ms.restype = C.c_double
     L.lann_last_launches.argtypes = [vp]
     L.lann_last_launches.restype = C.c_int64
+    L.lann_last_train_ms.argtypes = [vp]
+    L.lann_last_train_ms.restype = C.c_double
+    L.lann_population_create.argtypes = [vp, C.c_int32, C.POINTER(Job), C.c_int32, C.c_int32, C.POINTER(vp)]
+    L.lann_population_run.argtypes = [vp, C.c_int32]
+    L.lann_population_fetch.argtypes = [vp, C.POINTER(JobResult), vp, vp, vp, vp]
+    L.lann_population_flop.argtypes = [vp]
+    L.lann_population_flop.restype = C.c_double
+    L.lann_population_models.argtypes = [vp]
+    L.lann_population_models.restype = C.c_int64
+    L.lann_population_destroy.argtypes = [vp]
+    L.lann_population_norm.argtypes = [vp, vp]
+    L.lann_transfer_bytes.argtypes = [vp, vp, C.c_int32]
     L.lann_train.argtypes = [vp, C.POINTER(TrainBatch)]
     L.lann_predict.argtypes = [vp, C.POINTER(ModelSet), C.c_int64, vp, vp, vp]
     L.lann_eval.argtypes = [vp, C.c_int32, vp, vp, vp, vp, C.c_double, vp, vp, vp, vp]
@@ -188,6 +210,14 @@ class Engine:
     @property
     def last_launches(self) -> int:
         return self.L.lann_last_launches(self.h)
+
+    @property
+    def last_train_ms(self) -> float:
+        return self.L.lann_last_train_ms(self.h)
+
+    def prepare(self, jobs, precision=abi.FP32, record_trace=False):
+        """lann_population_create: host preparation + one upload; returns a Population."""
+        return Population(self, jobs, precision, record_trace)
 
     def _raise(self, st, epoch=-1):
         if st == abi.TRAINING_ERROR:
@@ -308,6 +338,65 @@ class Engine:
         out_params = [params[off[i]:off[i] + results[i].n_params].copy() for i in range(n)] if want_params else None
         out_trace = [trace[toff[i]:toff[i] + jobs[i].epochs].copy() for i in range(n)] if want_trace else None
         return st, results, out_params, out_trace
+
+
+class Population:
+    """A prepared population (lann_population_*): inputs resident in HBM, device-only passes."""
+
+    def __init__(self, eng: Engine, jobs, precision, record_trace=False):
+        self.eng = eng
+        self.jobs = list(jobs)
+        n = len(self.jobs)
+        self._arr = (Job * n)(*self.jobs)
+        h = C.c_void_p()
+        st = eng.L.lann_population_create(eng.h, n, self._arr, precision, int(record_trace), C.byref(h))
+        if st and not h.value:
+            eng._raise(st)
+        self.h = h
+        self.record_trace = record_trace
+
+    @property
+    def flop(self) -> float:
+        return self.eng.L.lann_population_flop(self.h)
+
+    @property
+    def n_models(self) -> int:
+        return self.eng.L.lann_population_models(self.h)
+
+    def run(self, n_steps=1):
+        st = self.eng.L.lann_population_run(self.h, n_steps)
+        if st:
+            self.eng._raise(st)
+
+    def norms(self):
+        out = np.zeros((len(self.jobs), 18))
+        self.eng.L.lann_population_norm(self.h, _ptr(out))
+        return out
+
+    def fetch(self, want_params=False, want_trace=False):
+        n = len(self.jobs)
+        res = (JobResult * n)()
+        params = off = trace = toff = None
+        if want_params:
+            params = np.zeros(n * 2048)
+            off = (np.arange(n, dtype=np.int64) * 2048)
+        if want_trace and self.record_trace:
+            ep = np.array([j.epochs for j in self.jobs], dtype=np.int64)
+            toff = np.concatenate([[0], np.cumsum(ep)[:-1]]).astype(np.int64)
+            trace = np.zeros(int(ep.sum()))
+        st = self.eng.L.lann_population_fetch(self.h, res, _ptr(params), _ptr(off), _ptr(trace), _ptr(toff))
+        results = list(res)
+        out_p = [params[off[i]:off[i] + results[i].n_params].copy() for i in range(n)] if want_params else None
+        out_t = [trace[toff[i]:toff[i] + self.jobs[i].epochs].copy() for i in range(n)] if trace is not None else None
+        return st, results, out_p, out_t
+
+    def close(self):
+        if getattr(self, "h", None) and self.h.value:
+            self.eng.L.lann_population_destroy(self.h)
+            self.h = C.c_void_p()
+
+    def __del__(self):
+        self.close()
 
 
 def _model_set(models, precision):

@@ -1,0 +1,63 @@
+"""GPU: the error contract of the C ABI mirrors the reference exceptions (errors.hpp):
+ParamError for configs ModelConfig::validate rejects (models.cpp:48-64), SchemaError for
+feature-length mismatches, DomainError for metric domains, TrainingError(epoch)."""
+import numpy as np
+import pytest
+
+from paper_2003_07497_b200 import abi
+from paper_2003_07497_b200 import engine as E
+
+pytestmark = pytest.mark.gpu
+
+
+def job(**kw):
+    return abi.make_job(abi.acceptance_world(), 1, count=60, epochs=kw.pop("epochs", 5), **kw)
+
+
+@pytest.mark.parametrize("kw,msg", [
+    ({"lr": 0.5}, "learning rate"),
+    ({"hidden": (32,)}, "75-parameter budget"),
+    ({"hidden": (8, 8, 8)}, None),
+    ({"epochs": 0}, "epochs"),
+])
+def test_param_errors(engine, kw, msg):
+    st, res, _, _ = engine.run_population([job(**kw)], abi.FP64_EXACT)
+    assert st == abi.PARAM_ERROR and res[0].status == abi.PARAM_ERROR
+    if msg:
+        assert msg in engine.last_error
+
+
+def test_unconstrained_lifts_budget(engine):
+    st, res, _, _ = engine.run_population([job(hidden=(64,), unconstrained=True)], abi.FP64_EXACT)
+    assert st == 0 and res[0].n_params == 577
+
+
+def test_mixed_population_reports_per_job(engine):
+    """A bad job does not poison the rest of the population."""
+    st, res, _, _ = engine.run_population([job(), job(lr=0.3), job(epochs=3)], abi.FP64_EXACT)
+    assert st == abi.PARAM_ERROR
+    assert [r.status for r in res] == [0, abi.PARAM_ERROR, 0]
+
+
+def test_schema_errors(engine):
+    model = {"inputs": 7, "h1": 8, "h2": 0, "log_target": 0, "params": np.zeros(73), "norm": np.zeros(18)}
+    with pytest.raises(E.SchemaError):
+        engine.predict([model], np.zeros((2, 7)), np.array([0, 3], dtype=np.int32))
+    with pytest.raises(E.SchemaError):  # selection needs the blur schema (selector.cpp:44-45)
+        engine.select_schedule(model, 1024, np.array([[2, 2, 2, 2]], dtype=np.uint32))
+    with pytest.raises(E.SchemaError):
+        engine.select_variants([model], [1], abi.MV, 4, 1, 0, 10)
+
+
+def test_select_needs_candidates(engine):
+    model = {"inputs": 6, "h1": 5, "h2": 5, "log_target": 1, "params": np.zeros(71), "norm": np.zeros(18)}
+    with pytest.raises(E.ParamError):
+        engine.select_schedule(model, 1024, np.zeros((0, 4), dtype=np.uint32))
+
+
+def test_training_error_in_population(engine):
+    """A world whose runtimes overflow to inf: BuildAbortError-free dataset, TrainingError epoch."""
+    w = abi.acceptance_world()
+    w.alpha = 1e300
+    st, res, _, _ = engine.run_population([abi.make_job(w, 1, count=60, epochs=5)], abi.FP64_EXACT)
+    assert st in (abi.TRAINING_ERROR, abi.PARAM_ERROR, abi.BUILD_ABORT)

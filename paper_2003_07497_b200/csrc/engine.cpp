@@ -151,6 +151,15 @@ struct Fp32Bucket {
   double cost;
 };
 
+struct Fp64Bucket {
+  int shape[3] = {0, 0, 0};  // compiled shape, or {0,0,0} = generic kernel
+  int n = 0, max_p = 0, dyn = 0, in_smem = 0;
+  DBuf<int> order;
+  DBuf<double> scratch;
+  DBuf<int64_t> soff;
+  double cost = 0.0;
+};
+
 struct TrainPlan {
   DBuf<int> tile_rows, tile_inputs, model_tile, h1, h2, epochs;
   DBuf<int64_t> tile_off, poff;
@@ -158,12 +167,9 @@ struct TrainPlan {
   // FP32 part
   DBuf<float> rows_f;
   std::vector<std::unique_ptr<Fp32Bucket>> buckets;
-  // FP64 part (exact mode, or FP32-mode models without a compiled shape)
-  int n64 = 0, max_p = 0, dyn64 = 0, in_smem = 0;
-  DBuf<int> order;
+  // FP64 part (exact mode, or FP32-mode models without a compiled FP32 shape)
+  std::vector<std::unique_ptr<Fp64Bucket>> buckets64;
   DBuf<double2> bc;
-  DBuf<double> scratch;
-  DBuf<int64_t> soff;
   const double* dX = nullptr;
   const double* dY = nullptr;
   int trace_stride = 1;
@@ -203,11 +209,12 @@ std::unique_ptr<TrainPlan> build_plan(lann_engine* e, const DevTrain& t, int pre
     }
     int lanes = 0;
     if (const char* env = std::getenv("LANN_FP32_LANES")) lanes = std::atoi(env);
-    if (lanes != 1 && lanes != 2 && lanes != 4 && lanes != 8 && lanes != 32 && lanes != 256) {
+    if (lanes != 1 && lanes != 2 && lanes != 4 && lanes != 8 && lanes != 32 && lanes != 64 &&
+        lanes != 128 && lanes != 256) {
       // smallest lanes-per-model that still gives >= 16 warps per SM; populations
-      // too small for that get a whole CTA (256 threads) per model
+      // too small for that get a whole CTA (4 warps) per model
       const int total = t.n_models - int(fp64_models.size());
-      lanes = total <= 4 * e->sms ? 256 : 32;
+      lanes = total <= 4 * e->sms ? 128 : 32;
       for (int k : {1, 2, 4, 8})
         if ((total + 32 / k - 1) / (32 / k) >= 16 * e->sms) {
           lanes = k;
@@ -258,40 +265,57 @@ std::unique_ptr<TrainPlan> build_plan(lann_engine* e, const DevTrain& t, int pre
     fp64_models.resize(t.n_models);
     std::iota(fp64_models.begin(), fp64_models.end(), 0);
   }
-  P.n64 = int(fp64_models.size());
-  if (P.n64 > 0) {
-    // longest models first so the block scheduler packs the tail
-    std::vector<int> order = fp64_models;
+  if (!fp64_models.empty()) {
+    int max_e = 1;
+    for (int m : fp64_models) max_e = std::max(max_e, t.epochs[m]);
+    const auto& bc = adam_bias_table(max_e);
+    P.bc = DBuf<double2>(reinterpret_cast<const double2*>(bc.data()), size_t(max_e), s);
+    // one bucket per compiled shape (+ one generic bucket), each on its own stream
+    using Shape = std::tuple<int, int, int>;
+    std::map<Shape, std::vector<int>> by_shape;
+    for (int m : fp64_models) {
+      const int I = t.tile_inputs[t.model_tile[m]];
+      if (fp64_shape_compiled(I, t.h1[m], t.h2[m])) by_shape[{I, t.h1[m], t.h2[m]}].push_back(m);
+      else by_shape[{0, 0, 0}].push_back(m);
+    }
     auto cost = [&](int m) {
       const int tile = t.model_tile[m];
       return double(t.epochs[m]) * t.tile_rows[tile] *
              param_count(t.tile_inputs[tile], t.h1[m], t.h2[m]);
     };
-    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return cost(a) > cost(b); });
-    int max_e = 1;
-    for (int m : order) max_e = std::max(max_e, t.epochs[m]);
-    const auto& bc = adam_bias_table(max_e);
-    P.bc = DBuf<double2>(reinterpret_cast<const double2*>(bc.data()), size_t(max_e), s);
-    size_t max_bytes_smem = 0, max_state = 0;
-    std::vector<int64_t> soff(t.n_models, 0);
-    int64_t scratch = 0;
-    for (int m : order) {
-      const int tile = t.model_tile[m];
-      const int np = param_count(t.tile_inputs[tile], t.h1[m], t.h2[m]);
-      P.max_p = std::max(P.max_p, np);
-      const size_t rec = size_t(fp64_record_doubles(t.tile_inputs[tile], t.h1[m], t.h2[m])) *
-                         t.tile_rows[tile] * 8;
-      const size_t state = size_t(3 * np + 2) * 8;
-      max_state = std::max(max_state, state);
-      max_bytes_smem = std::max(max_bytes_smem, state + rec);
-      soff[m] = scratch;
-      scratch += int64_t(rec / 8);
+    for (auto& [shape, order] : by_shape) {
+      // longest models first so the block scheduler packs the tail
+      std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return cost(a) > cost(b); });
+      auto b = std::make_unique<Fp64Bucket>();
+      b->shape[0] = std::get<0>(shape);
+      b->shape[1] = std::get<1>(shape);
+      b->shape[2] = std::get<2>(shape);
+      b->n = int(order.size());
+      b->cost = cost(order.front());
+      size_t max_bytes_smem = 0, max_state = 0;
+      std::vector<int64_t> soff(t.n_models, 0);
+      int64_t scratch = 0;
+      for (int m : order) {
+        const int tile = t.model_tile[m];
+        const int np = param_count(t.tile_inputs[tile], t.h1[m], t.h2[m]);
+        b->max_p = std::max(b->max_p, np);
+        const size_t rec = size_t(fp64_record_doubles(t.tile_inputs[tile], t.h1[m], t.h2[m])) *
+                           t.tile_rows[tile] * 8;
+        const size_t state = size_t(3 * np + 2) * 8;
+        max_state = std::max(max_state, state);
+        max_bytes_smem = std::max(max_bytes_smem, state + rec);
+        soff[m] = scratch;
+        scratch += int64_t(rec / 8);
+      }
+      b->in_smem = max_bytes_smem <= size_t(e->max_smem);
+      b->dyn = int(b->in_smem ? max_bytes_smem : max_state);
+      if (!b->in_smem) b->scratch = DBuf<double>(size_t(scratch), s);
+      b->soff = DBuf<int64_t>(soff, s);
+      b->order = DBuf<int>(order, s);
+      P.buckets64.push_back(std::move(b));
     }
-    P.in_smem = max_bytes_smem <= size_t(e->max_smem);
-    P.dyn64 = int(P.in_smem ? max_bytes_smem : max_state);
-    if (!P.in_smem) P.scratch = DBuf<double>(size_t(scratch), s);
-    P.soff = DBuf<int64_t>(soff, s);
-    P.order = DBuf<int>(order, s);
+    std::stable_sort(P.buckets64.begin(), P.buckets64.end(),
+                     [](const auto& a, const auto& b) { return a->cost > b->cost; });
   }
   ck(cudaGetLastError(), "plan");
   return plan;
@@ -301,7 +325,7 @@ std::unique_ptr<TrainPlan> build_plan(lann_engine* e, const DevTrain& t, int pre
 void execute_plan(lann_engine* e, const TrainPlan& P, double* dparams, double* dfinal, int* dbad,
                   double* dtrace, const int64_t* dtrace_off) {
   cudaStream_t s = e->stream;
-  const int n_launch = int(P.buckets.size()) + (P.n64 > 0 ? 1 : 0);
+  const int n_launch = int(P.buckets.size()) + int(P.buckets64.size());
   ck(cudaEventRecord(e->tr0, s), "event");
   ck(cudaEventRecord(e->fork, s), "event");
   int k = 0;
@@ -337,10 +361,10 @@ void execute_plan(lann_engine* e, const TrainPlan& P, double* dparams, double* d
     ck(cudaGetLastError(), "train_fp32 launch");
     e->launches += 1;
   }
-  if (P.n64 > 0) {
+  for (const auto& b : P.buckets64) {
     TrainArgs a{};
-    a.n_models = P.n64;
-    a.order = P.order.p;
+    a.n_models = b->n;
+    a.order = b->order.p;
     a.tile_rows = P.tile_rows.p;
     a.tile_inputs = P.tile_inputs.p;
     a.tile_offset = P.tile_off.p;
@@ -359,10 +383,10 @@ void execute_plan(lann_engine* e, const TrainPlan& P, double* dparams, double* d
     a.trace_offset = dtrace_off;
     a.trace_stride = P.trace_stride;
     a.bias_corr = P.bc.p;
-    a.scratch = P.scratch.p;
-    a.scratch_offset = P.soff.p;
-    a.smem_records = P.in_smem;
-    launch_train_fp64(a, P.max_p, P.dyn64, next_stream());
+    a.scratch = b->scratch.p;
+    a.scratch_offset = b->soff.p;
+    a.smem_records = b->in_smem;
+    launch_train_fp64(a, b->max_p, b->dyn, b->shape[0] > 0 ? b->shape : nullptr, next_stream());
     ck(cudaGetLastError(), "train_fp64 launch");
     e->launches += 1;
   }

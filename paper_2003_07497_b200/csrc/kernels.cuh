@@ -86,7 +86,9 @@ struct EvalArgs {
   int* status;
 };
 
-void launch_train_fp64(const TrainArgs& a, int max_p, int dyn_bytes, cudaStream_t s);
+// shape = {I, H1, H2} when every model of the launch has that compiled shape, else null
+void launch_train_fp64(const TrainArgs& a, int max_p, int dyn_bytes, const int* shape, cudaStream_t s);
+bool fp64_shape_compiled(int in, int h1, int h2);
 // bytes of one per-sample record of the FP64 trainer for a shape (see train_fp64.cu)
 int fp64_record_doubles(int in, int h1, int h2);
 bool launch_train_fp32(const TrainF32Args& a, int in, int h1, int h2, int lanes, int tile_bytes,

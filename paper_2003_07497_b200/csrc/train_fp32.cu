@@ -3,21 +3,26 @@
 // Same algorithm as models::train_full_batch (mlp.cpp:156-175): full-batch
 // MSE gradient (mlp.cpp:75-122) + Adam(0.9, 0.999, 1e-8) (mlp.cpp:142-154),
 // loss recorded before each update, training stopped at the first non-finite
-// loss. Differences from the FP64 parity kernel: FP32 FMA arithmetic and a
-// tree (shuffle) reduction over samples, so traces agree with the reference
-// only up to FP32 rounding.
+// loss. Differences from the FP64 parity kernel: FP32 FMA arithmetic and tree
+// reductions over samples, so traces agree with the reference only up to FP32
+// rounding.
 //
-// Mapping: one warp per CTA; the warp trains 32/K models that share one
-// training tile (same kernel-variant-hardware combination and fold, different
-// init seeds); each model is spread over K lanes that split its samples.
-//   * the tile (N rows x 8 floats, y in column 7) is staged ONCE into shared
-//     memory by a TMA bulk copy (cp.async.bulk + mbarrier) and re-read from
-//     there for every epoch: HBM traffic per model-epoch ~ 0;
-//   * weights and gradient accumulators live in registers (fully unrolled for
-//     the compile-time shape); Adam moments in shared memory [param][lane];
-//   * with K = 1 all 32 lanes read the same row (shared-memory broadcast);
-//     with K > 1 the K per-lane partial gradients are summed by a shuffle
-//     butterfly, after which every lane applies the identical Adam step.
+// Two mappings, chosen by population size (engine.cpp build_plan):
+//  * train_fp32_kernel<K> — MANY models (sweeps): one warp per CTA trains 32/K
+//    models that share one training tile (same combination and fold, different
+//    init seeds); each model spreads over K lanes that split its samples.
+//    Weights and gradient accumulators live in registers (fully unrolled for the
+//    compile-time shape); with K = 1 all 32 lanes read the same row (shared-
+//    memory broadcast); with K > 1 the per-lane partials are summed by a shuffle
+//    butterfly, after which every lane applies the identical Adam step.
+//  * train_fp32_cta_kernel<W> — FEW models (the 48-combo population): one model
+//    per CTA of W warps so the per-epoch LATENCY is minimised; threads own
+//    samples, gradients are reduced by a warp transpose through shared memory
+//    and then across warps; owner threads apply Adam; new weights are broadcast
+//    back through shared memory (two __syncthreads per epoch).
+// In both, the tile (N rows x 8 floats, target y in column 7) is staged ONCE into
+// shared memory by a TMA bulk copy (cp.async.bulk + mbarrier) and re-read from
+// there every epoch, so HBM traffic per model-epoch is ~0.
 #include <cmath>
 #include <cstdint>
 
@@ -30,12 +35,18 @@ __device__ __forceinline__ uint32_t smem_addr(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
-// TMA 1-D bulk copy global -> shared, completion tracked by an mbarrier.
-__device__ __forceinline__ void tma_load_tile(void* dst, const void* src, uint32_t bytes,
-                                              uint64_t* bar) {
+// mbarrier init by one thread; the caller syncs before anyone waits on it.
+__device__ __forceinline__ void mbar_init(uint64_t* bar) {
   const uint32_t b = smem_addr(bar);
   asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b));
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// TMA 1-D bulk copy global -> shared, completion tracked by an (initialised) mbarrier.
+__device__ __forceinline__ void tma_load_tile(void* dst, const void* src, uint32_t bytes,
+                                              uint64_t* bar) {
+  const uint32_t b = smem_addr(bar);
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes) : "memory");
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -57,22 +68,127 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
       : "memory");
 }
 
+__device__ __forceinline__ float sqrt_approx(float x) {
+  float r;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ float rcp_approx(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
+// Flat parameter layout of the reference (mlp.cpp:124-131): L0.w [H1][I], L0.b,
+// then (2 hidden) L1.w [H2][H1], L1.b, then output w, b.
 template <int I, int H1, int H2>
 struct Net {
-  static constexpr int L1W = 0;                        // [H1][I]
-  static constexpr int L1B = I * H1;                   // [H1]
-  static constexpr int L2W = L1B + H1;                 // [H2][H1] or output [H1]
+  static constexpr int L1W = 0;
+  static constexpr int L1B = I * H1;
+  static constexpr int L2W = L1B + H1;
   static constexpr int L2B = H2 > 0 ? L2W + H1 * H2 : L2W + H1;
-  static constexpr int L3W = L2B + (H2 > 0 ? H2 : 1);  // output [H2] (2 hidden)
+  static constexpr int L3W = L2B + (H2 > 0 ? H2 : 1);
   static constexpr int L3B = H2 > 0 ? L3W + H2 : L3W;
   static constexpr int P = H2 > 0 ? L3B + 1 : L2B + 1;
 };
 
+// Forward + backward of ONE sample, accumulating its gradient contribution into gr
+// and err^2 into loss. scale = 2/N folds the 1/N of the mean and the 2 of d(err^2).
+template <int I, int H1, int H2>
+__device__ __forceinline__ void accumulate_sample(const float* w, const float* xv, float* gr,
+                                                  float& loss, float scale) {
+  using N = Net<I, H1, H2>;
+  float z1[H1];
+#pragma unroll
+  for (int h = 0; h < H1; ++h) {
+    float z = w[N::L1B + h];
+#pragma unroll
+    for (int i = 0; i < I; ++i) z = fmaf(w[N::L1W + h * I + i], xv[i], z);
+    z1[h] = fmaxf(z, 0.f);
+  }
+  float out;
+  float z2[H2 > 0 ? H2 : 1];
+  if constexpr (H2 > 0) {
+#pragma unroll
+    for (int o = 0; o < H2; ++o) {
+      float z = w[N::L2B + o];
+#pragma unroll
+      for (int h = 0; h < H1; ++h) z = fmaf(w[N::L2W + o * H1 + h], z1[h], z);
+      z2[o] = fmaxf(z, 0.f);
+    }
+    float acc0 = w[N::L3B], acc1 = 0.f;
+#pragma unroll
+    for (int o = 0; o < H2; ++o) {
+      if (o & 1) acc1 = fmaf(w[N::L3W + o], z2[o], acc1);
+      else acc0 = fmaf(w[N::L3W + o], z2[o], acc0);
+    }
+    out = acc0 + acc1;
+  } else {
+    float acc0 = w[N::L2B], acc1 = 0.f;
+#pragma unroll
+    for (int h = 0; h < H1; ++h) {
+      if (h & 1) acc1 = fmaf(w[N::L2W + h], z1[h], acc1);
+      else acc0 = fmaf(w[N::L2W + h], z1[h], acc0);
+    }
+    out = acc0 + acc1;
+  }
+  const float err = out - xv[7];
+  loss = fmaf(err, err, loss);
+  const float d = err * scale;
+  if constexpr (H2 > 0) {
+    gr[N::L3B] += d;
+    float d2[H2];
+#pragma unroll
+    for (int o = 0; o < H2; ++o) {
+      gr[N::L3W + o] = fmaf(d, z2[o], gr[N::L3W + o]);
+      d2[o] = z2[o] > 0.f ? w[N::L3W + o] * d : 0.f;
+      gr[N::L2B + o] += d2[o];
+    }
+#pragma unroll
+    for (int h = 0; h < H1; ++h) {
+      float acc = 0.f;
+#pragma unroll
+      for (int o = 0; o < H2; ++o) {
+        gr[N::L2W + o * H1 + h] = fmaf(d2[o], z1[h], gr[N::L2W + o * H1 + h]);
+        acc = fmaf(w[N::L2W + o * H1 + h], d2[o], acc);
+      }
+      const float d1 = z1[h] > 0.f ? acc : 0.f;
+      gr[N::L1B + h] += d1;
+#pragma unroll
+      for (int i = 0; i < I; ++i) gr[N::L1W + h * I + i] = fmaf(d1, xv[i], gr[N::L1W + h * I + i]);
+    }
+  } else {
+    gr[N::L2B] += d;
+#pragma unroll
+    for (int h = 0; h < H1; ++h) {
+      gr[N::L2W + h] = fmaf(d, z1[h], gr[N::L2W + h]);
+      const float d1 = z1[h] > 0.f ? w[N::L2W + h] * d : 0.f;
+      gr[N::L1B + h] += d1;
+#pragma unroll
+      for (int i = 0; i < I; ++i) gr[N::L1W + h * I + i] = fmaf(d1, xv[i], gr[N::L1W + h * I + i]);
+    }
+  }
+}
+
+__device__ __forceinline__ void load_row(const float* trow, int s, float* xv) {
+  const float4 lo = *reinterpret_cast<const float4*>(trow + s * 8);
+  const float4 hi = *reinterpret_cast<const float4*>(trow + s * 8 + 4);
+  xv[0] = lo.x; xv[1] = lo.y; xv[2] = lo.z; xv[3] = lo.w;
+  xv[4] = hi.x; xv[5] = hi.y; xv[6] = hi.z; xv[7] = hi.w;
+}
+
+// One Adam step in FP32 (mlp.cpp:142-154): m = 0.9m + 0.1g, v = 0.999v + 0.001g^2,
+// w -= lr/bc1 * m / (sqrt(v/bc2) + 1e-8), with step = lr/bc1 and rb2 = 1/bc2.
+__device__ __forceinline__ float adam_step(float& mo, float& ve, float g, float step, float rb2) {
+  mo = fmaf(0.1f, g, 0.9f * mo);
+  ve = fmaf(0.001f * g, g, 0.999f * ve);
+  return step * mo * rcp_approx(sqrt_approx(ve * rb2) + 1e-8f);
+}
+
+// ---------------------------------------------------------------------------------
 template <int I, int H1, int H2, int K>
 __global__ void __launch_bounds__(32) train_fp32_kernel(TrainF32Args a) {
-  using N = Net<I, H1, H2>;
-  constexpr int P = N::P;
-  constexpr int G = 32 / K;  // models per warp
+  constexpr int P = Net<I, H1, H2>::P;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ uint64_t bar;
   const int lane = threadIdx.x;
@@ -88,6 +204,8 @@ __global__ void __launch_bounds__(32) train_fp32_kernel(TrainF32Args a) {
 
   float* trow = reinterpret_cast<float*>(smem_raw);  // [rows][8]
   float* adam = trow + (size_t)rows * 8;            // [2][P][32]
+  if (lane == 0) mbar_init(&bar);
+  __syncwarp();
   if (lane == 0) tma_load_tile(trow, a.rows + a.tile_offset[tile] * 8, (uint32_t)rows * 32u, &bar);
 
   float w[P], gr[P];
@@ -99,11 +217,11 @@ __global__ void __launch_bounds__(32) train_fp32_kernel(TrainF32Args a) {
     adam[(P + p) * 32 + lane] = 0.f;
   }
   const float lr = (float)a.lr[m];
-  const float scale = 2.0f / (float)rows;  // d(mean err^2)/d out = 2 err / N
+  const float scale = 2.0f / (float)rows;
   const float inv_n = 1.0f / (float)rows;
   double* trace = (a.loss_trace && active) ? a.loss_trace + a.trace_offset[m] : nullptr;
   int bad = -1;
-  float last = 0.f;
+  float last = 0.f, pw1 = 1.f, pw2 = 1.f;
   mbar_wait(&bar, 0);
   __syncwarp();
 
@@ -112,81 +230,9 @@ __global__ void __launch_bounds__(32) train_fp32_kernel(TrainF32Args a) {
     for (int p = 0; p < P; ++p) gr[p] = 0.f;
     float loss = 0.f;
     for (int s = sub; s < rows; s += K) {
-      const float4 lo = *reinterpret_cast<const float4*>(trow + s * 8);
-      const float4 hi = *reinterpret_cast<const float4*>(trow + s * 8 + 4);
-      const float xv[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
-      // forward
-      float z1[H1];
-#pragma unroll
-      for (int h = 0; h < H1; ++h) {
-        float z = w[N::L1B + h];
-#pragma unroll
-        for (int i = 0; i < I; ++i) z = fmaf(w[N::L1W + h * I + i], xv[i], z);
-        z1[h] = fmaxf(z, 0.f);
-      }
-      float out;
-      float z2[H2 > 0 ? H2 : 1];
-      if constexpr (H2 > 0) {
-#pragma unroll
-        for (int o = 0; o < H2; ++o) {
-          float z = w[N::L2B + o];
-#pragma unroll
-          for (int h = 0; h < H1; ++h) z = fmaf(w[N::L2W + o * H1 + h], z1[h], z);
-          z2[o] = fmaxf(z, 0.f);
-        }
-        float acc0 = w[N::L3B], acc1 = 0.f;
-#pragma unroll
-        for (int o = 0; o < H2; ++o) {
-          if (o & 1) acc1 = fmaf(w[N::L3W + o], z2[o], acc1);
-          else acc0 = fmaf(w[N::L3W + o], z2[o], acc0);
-        }
-        out = acc0 + acc1;
-      } else {
-        float acc0 = w[N::L2B], acc1 = 0.f;
-#pragma unroll
-        for (int h = 0; h < H1; ++h) {
-          if (h & 1) acc1 = fmaf(w[N::L2W + h], z1[h], acc1);
-          else acc0 = fmaf(w[N::L2W + h], z1[h], acc0);
-        }
-        out = acc0 + acc1;
-      }
-      const float err = out - xv[7];
-      loss = fmaf(err, err, loss);
-      const float d = err * scale;
-      // backward
-      if constexpr (H2 > 0) {
-        gr[N::L3B] += d;
-        float d2[H2];
-#pragma unroll
-        for (int o = 0; o < H2; ++o) {
-          gr[N::L3W + o] = fmaf(d, z2[o], gr[N::L3W + o]);
-          d2[o] = z2[o] > 0.f ? w[N::L3W + o] * d : 0.f;
-          gr[N::L2B + o] += d2[o];
-        }
-#pragma unroll
-        for (int h = 0; h < H1; ++h) {
-          float acc = 0.f;
-#pragma unroll
-          for (int o = 0; o < H2; ++o) {
-            gr[N::L2W + o * H1 + h] = fmaf(d2[o], z1[h], gr[N::L2W + o * H1 + h]);
-            acc = fmaf(w[N::L2W + o * H1 + h], d2[o], acc);
-          }
-          const float d1 = z1[h] > 0.f ? acc : 0.f;
-          gr[N::L1B + h] += d1;
-#pragma unroll
-          for (int i = 0; i < I; ++i) gr[N::L1W + h * I + i] = fmaf(d1, xv[i], gr[N::L1W + h * I + i]);
-        }
-      } else {
-        gr[N::L2B] += d;
-#pragma unroll
-        for (int h = 0; h < H1; ++h) {
-          gr[N::L2W + h] = fmaf(d, z1[h], gr[N::L2W + h]);
-          const float d1 = z1[h] > 0.f ? w[N::L2W + h] * d : 0.f;
-          gr[N::L1B + h] += d1;
-#pragma unroll
-          for (int i = 0; i < I; ++i) gr[N::L1W + h * I + i] = fmaf(d1, xv[i], gr[N::L1W + h * I + i]);
-        }
-      }
+      float xv[8];
+      load_row(trow, s, xv);
+      accumulate_sample<I, H1, H2>(w, xv, gr, loss, scale);
     }
     // sum the K per-lane partials of each model (lanes slot*K .. slot*K+K-1)
 #pragma unroll
@@ -196,27 +242,18 @@ __global__ void __launch_bounds__(32) train_fp32_kernel(TrainF32Args a) {
       loss += __shfl_xor_sync(0xffffffffu, loss, off);
     }
     loss *= inv_n;
+    pw1 *= 0.9f;
+    pw2 *= 0.999f;
     if (bad < 0) {
       last = loss;
       if (trace && sub == 0 && (e % a.trace_stride) == 0) trace[e / a.trace_stride] = (double)loss;
       if (!isfinite(loss)) {
         bad = e;  // TrainingError(epoch): freeze, keep the warp converged
       } else {
-        // Adam (mlp.cpp:142-154); bias corrections 1 - beta^t in FP32
-        const float t = (float)(e + 1);
-        const float bc1 = 1.f - exp2f(t * -0.15200309344504997f);   // log2(0.9)
-        const float bc2 = 1.f - exp2f(t * -0.0014434168696687106f);  // log2(0.999)
-        const float step = lr / bc1, rb2 = 1.f / bc2;
+        const float step = lr / (1.f - pw1), rb2 = 1.f / (1.f - pw2);
 #pragma unroll
-        for (int p = 0; p < P; ++p) {
-          float& mo = adam[p * 32 + lane];
-          float& ve = adam[(P + p) * 32 + lane];
-          const float mk = fmaf(0.1f, gr[p], 0.9f * mo);
-          const float vk = fmaf(0.001f * gr[p], gr[p], 0.999f * ve);
-          mo = mk;
-          ve = vk;
-          w[p] -= step * mk / (sqrtf(vk * rb2) + 1e-8f);
-        }
+        for (int p = 0; p < P; ++p)
+          w[p] -= adam_step(adam[p * 32 + lane], adam[(P + p) * 32 + lane], gr[p], step, rb2);
       }
     }
   }
@@ -230,37 +267,34 @@ __global__ void __launch_bounds__(32) train_fp32_kernel(TrainF32Args a) {
 }
 
 // ---------------------------------------------------------------------------------
-// Small populations (fewer models than SMs x warps, e.g. the 48-combo config):
-// ONE model per CTA of 256 threads so the epoch latency, not the FLOP rate, is
-// minimised. Threads own samples; per epoch the 256 per-sample gradients are
-// reduced in two levels through shared memory (warp transpose-sum, then across
-// the 8 warps), 73-odd owner threads apply Adam, and the new weights are
-// broadcast back through shared memory. Two __syncthreads per epoch.
-constexpr int kCtaThreads = 256;
-constexpr int kCtaWarps = kCtaThreads / 32;
+template <int P>
+struct CtaLayout {
+  static constexpr int PT = (P + 3) & ~3;  // transpose row stride (float4 writes, 4-wavefront STS.128)
+};
 
-template <int I, int H1, int H2>
-__global__ void __launch_bounds__(kCtaThreads) train_fp32_cta_kernel(TrainF32Args a) {
-  using N = Net<I, H1, H2>;
-  constexpr int P = N::P;
-  constexpr int PP = (P + 3) & ~3;  // padded row of the transpose buffer
+template <int I, int H1, int H2, int W>
+__global__ void __launch_bounds__(32 * W) train_fp32_cta_kernel(TrainF32Args a) {
+  constexpr int P = Net<I, H1, H2>::P;
+  constexpr int PT = CtaLayout<P>::PT;
+  constexpr int T = 32 * W;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ uint64_t bar;
-  __shared__ __align__(16) float wsh[PP];
-  __shared__ float part[kCtaWarps][P + 1];  // per-warp partial gradients (+ loss)
+  __shared__ __align__(16) float wsh[PT];
+  __shared__ float part[W][P + 1];  // per-warp partial gradients (+ loss)
   __shared__ float loss_sh;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int m = a.sorted_model[a.group_first[blockIdx.x]];
   const int tile = a.model_tile[m];
   const int rows = a.tile_rows[tile];
   const int E = a.epochs[m];
-  float* trow = reinterpret_cast<float*>(smem_raw);              // [rows][8]
-  constexpr int PT = P | 1;  // odd transpose stride: conflict-free row writes and column reads
+  float* trow = reinterpret_cast<float*>(smem_raw);                 // [rows][8]
   float* tbuf = trow + (size_t)rows * 8 + (size_t)warp * 32 * PT;  // [32][PT] per warp
+  if (tid == 0) mbar_init(&bar);
+  __syncthreads();
   if (tid == 0) tma_load_tile(trow, a.rows + a.tile_offset[tile] * 8, (uint32_t)rows * 32u, &bar);
   const double* gp = a.params + a.param_offset[m];
-  for (int p = tid; p < PP; p += kCtaThreads) wsh[p] = p < P ? (float)gp[p] : 0.f;
-  float mo = 0.f, ve = 0.f;  // Adam moments of parameter `tid` (owner threads)
+  for (int p = tid; p < PT; p += T) wsh[p] = p < P ? (float)gp[p] : 0.f;
+  float mo = 0.f, ve = 0.f, pw1 = 1.f, pw2 = 1.f;  // owner thread `tid` < P: Adam state
   const float lr = (float)a.lr[m];
   const float scale = 2.0f / (float)rows, inv_n = 1.0f / (float)rows;
   double* trace = a.loss_trace ? a.loss_trace + a.trace_offset[m] : nullptr;
@@ -269,89 +303,30 @@ __global__ void __launch_bounds__(kCtaThreads) train_fp32_cta_kernel(TrainF32Arg
   mbar_wait(&bar, 0);
   __syncthreads();
 
-  float w[P];
   for (int e = 0; e < E; ++e) {
+    float w[PT];
 #pragma unroll
-    for (int p = 0; p < P; ++p) w[p] = wsh[p];
-    float gr[P];
+    for (int p = 0; p < PT; p += 4) {
+      const float4 v = *reinterpret_cast<const float4*>(wsh + p);
+      w[p] = v.x;
+      w[p + 1] = v.y;
+      w[p + 2] = v.z;
+      w[p + 3] = v.w;
+    }
+    float gr[PT];
 #pragma unroll
-    for (int p = 0; p < P; ++p) gr[p] = 0.f;
+    for (int p = 0; p < PT; ++p) gr[p] = 0.f;
     float loss = 0.f;
-    for (int s = tid; s < rows; s += kCtaThreads) {
-      const float4 lo = *reinterpret_cast<const float4*>(trow + s * 8);
-      const float4 hi = *reinterpret_cast<const float4*>(trow + s * 8 + 4);
-      const float xv[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
-      float z1[H1];
-#pragma unroll
-      for (int h = 0; h < H1; ++h) {
-        float z = w[N::L1B + h];
-#pragma unroll
-        for (int i = 0; i < I; ++i) z = fmaf(w[N::L1W + h * I + i], xv[i], z);
-        z1[h] = fmaxf(z, 0.f);
-      }
-      float out;
-      float z2[H2 > 0 ? H2 : 1];
-      if constexpr (H2 > 0) {
-#pragma unroll
-        for (int o = 0; o < H2; ++o) {
-          float z = w[N::L2B + o];
-#pragma unroll
-          for (int h = 0; h < H1; ++h) z = fmaf(w[N::L2W + o * H1 + h], z1[h], z);
-          z2[o] = fmaxf(z, 0.f);
-        }
-        out = w[N::L3B];
-#pragma unroll
-        for (int o = 0; o < H2; ++o) out = fmaf(w[N::L3W + o], z2[o], out);
-      } else {
-        float acc0 = w[N::L2B], acc1 = 0.f;
-#pragma unroll
-        for (int h = 0; h < H1; ++h) {
-          if (h & 1) acc1 = fmaf(w[N::L2W + h], z1[h], acc1);
-          else acc0 = fmaf(w[N::L2W + h], z1[h], acc0);
-        }
-        out = acc0 + acc1;
-      }
-      const float err = out - xv[7];
-      loss = fmaf(err, err, loss);
-      const float d = err * scale;
-      if constexpr (H2 > 0) {
-        gr[N::L3B] += d;
-        float d2[H2];
-#pragma unroll
-        for (int o = 0; o < H2; ++o) {
-          gr[N::L3W + o] = fmaf(d, z2[o], gr[N::L3W + o]);
-          d2[o] = z2[o] > 0.f ? w[N::L3W + o] * d : 0.f;
-          gr[N::L2B + o] += d2[o];
-        }
-#pragma unroll
-        for (int h = 0; h < H1; ++h) {
-          float acc = 0.f;
-#pragma unroll
-          for (int o = 0; o < H2; ++o) {
-            gr[N::L2W + o * H1 + h] = fmaf(d2[o], z1[h], gr[N::L2W + o * H1 + h]);
-            acc = fmaf(w[N::L2W + o * H1 + h], d2[o], acc);
-          }
-          const float d1 = z1[h] > 0.f ? acc : 0.f;
-          gr[N::L1B + h] += d1;
-#pragma unroll
-          for (int i = 0; i < I; ++i) gr[N::L1W + h * I + i] = fmaf(d1, xv[i], gr[N::L1W + h * I + i]);
-        }
-      } else {
-        gr[N::L2B] += d;
-#pragma unroll
-        for (int h = 0; h < H1; ++h) {
-          gr[N::L2W + h] = fmaf(d, z1[h], gr[N::L2W + h]);
-          const float d1 = z1[h] > 0.f ? w[N::L2W + h] * d : 0.f;
-          gr[N::L1B + h] += d1;
-#pragma unroll
-          for (int i = 0; i < I; ++i) gr[N::L1W + h * I + i] = fmaf(d1, xv[i], gr[N::L1W + h * I + i]);
-        }
-      }
+    for (int s = tid; s < rows; s += T) {
+      float xv[8];
+      load_row(trow, s, xv);
+      accumulate_sample<I, H1, H2>(w, xv, gr, loss, scale);
     }
     // level 1: warp transpose-sum through shared memory (lane j -> params j, j+32, ...)
     float* myrow = tbuf + lane * PT;
 #pragma unroll
-    for (int p = 0; p < P; ++p) myrow[p] = gr[p];
+    for (int p = 0; p < PT; p += 4)
+      *reinterpret_cast<float4*>(myrow + p) = make_float4(gr[p], gr[p + 1], gr[p + 2], gr[p + 3]);
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) loss += __shfl_xor_sync(0xffffffffu, loss, off);
     __syncwarp();
@@ -372,20 +347,18 @@ __global__ void __launch_bounds__(kCtaThreads) train_fp32_cta_kernel(TrainF32Arg
     }
     if (lane == 0) part[warp][P] = loss;
     __syncthreads();
-    // level 2: owners sum the 8 warp partials and apply Adam
+    // level 2: owners sum the W warp partials and apply Adam
+    pw1 *= 0.9f;
+    pw2 *= 0.999f;
     if (tid <= P) {
       float gsum = 0.f;
 #pragma unroll
-      for (int k = 0; k < kCtaWarps; ++k) gsum += part[k][tid];
+      for (int k = 0; k < W; ++k) gsum += part[k][tid];
       if (tid == P) {
         loss_sh = gsum * inv_n;
       } else {
-        const float t = (float)(e + 1);
-        const float bc1 = 1.f - exp2f(t * -0.15200309344504997f);
-        const float bc2 = 1.f - exp2f(t * -0.0014434168696687106f);
-        mo = fmaf(0.1f, gsum, 0.9f * mo);
-        ve = fmaf(0.001f * gsum, gsum, 0.999f * ve);
-        wsh[tid] -= (lr / bc1) * mo / (sqrtf(ve / bc2) + 1e-8f);
+        const float step = lr / (1.f - pw1), rb2 = 1.f / (1.f - pw2);
+        wsh[tid] -= adam_step(mo, ve, gsum, step, rb2);
       }
     }
     __syncthreads();
@@ -399,24 +372,22 @@ __global__ void __launch_bounds__(kCtaThreads) train_fp32_cta_kernel(TrainF32Arg
       break;  // uniform across the CTA (everyone read the same loss)
     }
   }
-  // weights of the failing epoch were updated with a non-finite gradient; the
-  // reference discards the model in that case (TrainingError), so do we
+  // on a non-finite loss the reference discards the model (TrainingError); so do we
   double* outp = a.params + a.param_offset[m];
-  for (int p = tid; p < P; p += kCtaThreads) outp[p] = (double)wsh[p];
+  for (int p = tid; p < P; p += T) outp[p] = (double)wsh[p];
   if (tid == 0) {
     a.final_loss[m] = (double)last;
     a.nonfinite_epoch[m] = bad;
   }
 }
 
-template <int I, int H1, int H2>
+template <int I, int H1, int H2, int W>
 void launch_cta(const TrainF32Args& a, int tile_bytes, cudaStream_t s) {
   constexpr int P = Net<I, H1, H2>::P;
-  constexpr int PT = P | 1;
-  auto kern = train_fp32_cta_kernel<I, H1, H2>;
-  const int dyn = tile_bytes + kCtaWarps * 32 * PT * 4;
+  auto kern = train_fp32_cta_kernel<I, H1, H2, W>;
+  const int dyn = tile_bytes + W * 32 * CtaLayout<P>::PT * 4;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
-  kern<<<a.n_groups, kCtaThreads, dyn, s>>>(a);
+  kern<<<a.n_groups, 32 * W, dyn, s>>>(a);
 }
 
 // dynamic smem = the largest tile of the launch (rows x 32 B) + Adam moments
@@ -429,6 +400,8 @@ void launch_k(const TrainF32Args& a, int tile_bytes, cudaStream_t s) {
   kern<<<a.n_groups, 32, dyn, s>>>(a);
 }
 
+// lanes: 1/2/4/8/32 = lanes per model in the warp kernel; 64/128/256 = threads per
+// model in the CTA kernel.
 template <int I, int H1, int H2>
 bool dispatch_lanes(const TrainF32Args& a, int lanes, int tile_bytes, cudaStream_t s) {
   switch (lanes) {
@@ -437,9 +410,19 @@ bool dispatch_lanes(const TrainF32Args& a, int lanes, int tile_bytes, cudaStream
     case 4: launch_k<I, H1, H2, 4>(a, tile_bytes, s); return true;
     case 8: launch_k<I, H1, H2, 8>(a, tile_bytes, s); return true;
     case 32: launch_k<I, H1, H2, 32>(a, tile_bytes, s); return true;
-    case kCtaThreads: launch_cta<I, H1, H2>(a, tile_bytes, s); return true;
+    case 64: launch_cta<I, H1, H2, 2>(a, tile_bytes, s); return true;
+    case 128: launch_cta<I, H1, H2, 4>(a, tile_bytes, s); return true;
+    case 256: launch_cta<I, H1, H2, 8>(a, tile_bytes, s); return true;
     default: return false;
   }
+}
+
+__global__ void pack_rows_kernel(const double* X, const double* y, int64_t n, float* out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n * 8) return;
+  const int64_t r = i / 8;
+  const int c = (int)(i % 8);
+  out[i] = c == 7 ? (float)y[r] : (float)X[i];
 }
 
 }  // namespace
@@ -472,22 +455,10 @@ bool launch_train_fp32(const TrainF32Args& a, int in, int h1, int h2, int lanes,
   return false;
 }
 
-}  // namespace lann
-
-namespace lann {
-namespace {
-__global__ void pack_rows_kernel(const double* X, const double* y, int64_t n, float* out) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n * 8) return;
-  const int64_t r = i / 8;
-  const int c = (int)(i % 8);
-  out[i] = c == 7 ? (float)y[r] : (float)X[i];
-}
-}  // namespace
-
 // FP32 rows [n][8] = normalised inputs x0..x6 with the target in column 7.
 void launch_pack_rows(const double* X, const double* y, int64_t n, float* out, cudaStream_t s) {
   if (n <= 0) return;
   pack_rows_kernel<<<(unsigned)((n * 8 + 255) / 256), 256, 0, s>>>(X, y, n, out);
 }
+
 }  // namespace lann

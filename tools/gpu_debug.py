@@ -1,4 +1,4 @@
-"""Developer probe: run individual engine entry points (for compute-sanitizer)."""
+"""Developer probe: FP64 exact one/two-epoch comparisons against the oracle (prints diffs)."""
 import os
 import sys
 
@@ -6,35 +6,25 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+from oracle_lib import Oracle  # noqa: E402
 from paper_2003_07497_b200 import abi  # noqa: E402
 from paper_2003_07497_b200 import engine as E  # noqa: E402
-from paper_2003_07497_b200 import population as P  # noqa: E402
 
-which = sys.argv[1:] or ["onestep", "random64", "select"]
+o = Oracle()
 eng = E.Engine(0)
 rng = np.random.default_rng(5)
-if "onestep" in which:
-    X = rng.uniform(0, 1, (250, 7))
-    y = rng.uniform(0, 1, 250)
-    p0 = E.init_params([7, 8, 1], 11)
-    out = eng.train([X], [y], [{"tile": 0, "h1": 8, "lr": 1e-2, "epochs": 2, "params": p0}], abi.FP32, trace=True)
-    print("onestep ok", out[3][0])
-if "random64" in which:
-    X = rng.uniform(0, 1, (50, 3))
-    y = rng.uniform(0, 1, 50)
-    p0 = E.init_params([3, 4, 2, 1], 1)
-    out = eng.train([X], [y], [{"tile": 0, "h1": 4, "h2": 2, "lr": 1e-3, "epochs": 5, "params": p0}],
-                    abi.FP64_EXACT, trace=True)
-    print("random64 ok", out[3][0])
-if "select" in which:
-    jobs = P.config2_jobs(root_seed=1, epochs_scale=0.002)
-    pop = eng.prepare(jobs, abi.FP32)
-    pop.run(1)
-    st, res, params, _ = pop.fetch(want_params=True)
-    norms = pop.norms()
-    idx = [i for i, j in enumerate(jobs) if j.world.kind == abi.MM]
-    models = [{"inputs": res[i].n_inputs, "h1": 8, "h2": 0, "log_target": 0, "params": params[i], "norm": norms[i]}
-              for i in idx]
-    thd = [1 if jobs[i].world.hw_class == abi.HW_CPU else 0 for i in idx]
-    gi, gs = eng.select_variants(models, thd, abi.MM, 16, 7, 0, 1000, precision=abi.FP32)
-    print("select ok", gi[:10], gs[:3])
+for dims, n, ep in [([1, 1, 1], 3, 1), ([2, 3, 1], 20, 1), ([7, 8, 1], 250, 1), ([7, 8, 1], 250, 2), ([6, 5, 5, 1], 250, 1)]:
+    I = dims[0]
+    X = rng.uniform(0, 1, (n, I))
+    y = rng.uniform(0, 1, n)
+    p0 = E.init_params(dims, 3)
+    m = {"tile": 0, "h1": dims[1], "h2": dims[2] if len(dims) > 3 else 0, "lr": 1e-2, "epochs": ep, "params": p0}
+    params, final, bad, traces = eng.train([X], [y], [m], abi.FP64_EXACT, trace=True)
+    Xp = np.zeros((n, 8))
+    Xp[:, :I] = X
+    st, p_exp, t_exp, _ = o.train_full_batch(dims, p0, Xp, y, 1e-2, ep)
+    _, l0, g0 = o.mse_gradient(dims, p0, Xp, y)
+    dp = params[0] - p_exp
+    print(dims, n, ep, "trace eq", np.array_equal(traces[0], t_exp), traces[0][:2], t_exp[:2],
+          "param diff idx", np.nonzero(dp)[0][:12], "max", np.abs(dp).max())

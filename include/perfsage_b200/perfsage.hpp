@@ -1,0 +1,222 @@
+// perfsage_b200/perfsage.hpp — drop-in C++ API for the reference's LANN hot path.
+//
+// Same namespaces, type names, fields and function signatures as the reference
+// perfsage core (paths relative to /root/reference/proj/core/include/perfsage/) for
+// the data-parallel path the engine replaces:
+//   errors.hpp      Error, ParamError, SchemaError, DomainError, TrainingError, BuildAbortError
+//   kernels.hpp     KernelKind, ScheduleCandidate, ScheduleSpace (cpu_default / gpu_style / enumerate_all)
+//   datagen.hpp     Sample, Dataset, split
+//   models.hpp      ModelFamily, ModelConfig, default_config, param_count_for, NormStats,
+//                   TrainedModel, train_nn, train_model (NN families), predict, predict_dataset
+//   mlp.hpp         DenseLayer, Mlp
+//   eval.hpp        mape, mape_thresholded, spearman, average_ranks, make_report
+//   selector.hpp    enumerate_candidates, select(ScheduleScorer...), select(TrainedModel, n, cands)
+// plus the batched overloads the engine exists for: models::train_population and
+// models::predict_population. Every compute call runs on the GPU through the C ABI
+// (include/lann_engine.h); there is no CPU fallback. Link: -lperfsage_b200.
+#pragma once
+
+#include <cstdint>
+#include <functional>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <tuple>
+#include <variant>
+#include <vector>
+
+namespace perfsage {
+
+// ---- errors.hpp:9-69 ------------------------------------------------------------------------
+class Error : public std::runtime_error {
+ public:
+  explicit Error(const std::string& msg) : std::runtime_error(msg) {}
+};
+class ParamError : public Error { public: using Error::Error; };
+class DomainError : public Error { public: using Error::Error; };
+class SchemaError : public Error { public: using Error::Error; };
+class TrainingError : public Error {
+ public:
+  TrainingError(const std::string& msg, int epoch) : Error(msg), epoch_(epoch) {}
+  int epoch() const { return epoch_; }
+
+ private:
+  int epoch_;
+};
+class BuildAbortError : public Error {
+ public:
+  BuildAbortError(const std::string& msg, std::size_t completed) : Error(msg), completed_(completed) {}
+  std::size_t completed() const { return completed_; }
+
+ private:
+  std::size_t completed_;
+};
+
+namespace engine {
+enum class Precision { Fp64Exact, Fp32 };
+// Arithmetic mode of the perfsage:: calls on this thread (default: Fp64Exact, bit-identical
+// to the reference). Each host thread owns one engine (CUDA stream) on `device`.
+void set_precision(Precision p);
+Precision precision();
+void set_device(int device);
+}  // namespace engine
+
+// ---- kernels.hpp -------------------------------------------------------------------------------
+namespace kernels {
+enum class KernelKind { MM, MV, MC, MP, Blur };
+std::string to_string(KernelKind kind);
+
+struct ScheduleCandidate {
+  std::uint32_t s1 = 8, s2 = 256, s3 = 128, s4 = 8;
+  auto tie() const { return std::tie(s1, s2, s3, s4); }
+  bool operator==(const ScheduleCandidate& o) const { return tie() == o.tie(); }
+  bool operator<(const ScheduleCandidate& o) const { return tie() < o.tie(); }
+  bool is_pow2() const;
+  std::string to_string() const;
+};
+
+struct ScheduleSpace {
+  std::uint32_t s1_min = 2, s1_max = 1024, s2_min = 2, s2_max = 1024;
+  std::uint32_t s3_min = 2, s3_max = 1024, s4_min = 2, s4_max = 1024;
+  bool chained = true;
+  static ScheduleSpace cpu_default();
+  static ScheduleSpace gpu_style();
+  bool contains(const ScheduleCandidate& c) const;
+  std::uint64_t size() const;
+  std::vector<ScheduleCandidate> enumerate_all() const;
+};
+}  // namespace kernels
+
+// ---- datagen.hpp:72-116 -------------------------------------------------------------------------
+namespace datagen {
+struct Sample {
+  std::vector<double> features;
+  std::uint64_t c = 0;
+  double runtime_s = 0.0;
+  std::string variant_id;
+  bool operator==(const Sample&) const = default;
+};
+
+struct Dataset {
+  kernels::KernelKind kind = kernels::KernelKind::MM;
+  std::vector<std::string> feature_names;
+  std::vector<Sample> samples;
+  std::uint64_t seed = 0;
+  std::string host;
+  std::size_t size() const { return samples.size(); }
+  std::vector<double> runtimes() const;
+};
+
+/// Disjoint, exhaustive, seeded-shuffle partition (datagen.cpp:225-248).
+std::pair<Dataset, Dataset> split(const Dataset& dataset, double train_fraction, std::uint64_t seed);
+}  // namespace datagen
+
+// ---- mlp.hpp / models.hpp ----------------------------------------------------------------------
+namespace models {
+struct DenseLayer {
+  int in = 0;
+  int out = 0;
+  std::vector<double> w;
+  std::vector<double> b;
+};
+
+struct Mlp {
+  std::vector<DenseLayer> layers;
+  int input_dim() const { return layers.empty() ? 0 : layers.front().in; }
+  int param_count() const;
+};
+
+enum class ModelFamily { NnC, Nn, Const, LrC, NlrC };
+std::string to_string(ModelFamily family);
+bool family_augmented(ModelFamily family);
+
+struct ModelConfig {
+  ModelFamily family = ModelFamily::NnC;
+  std::vector<int> hidden_widths = {8};
+  double learning_rate = 1e-3;
+  int epochs = 5000;
+  std::uint64_t seed = 0;
+  bool unconstrained = false;
+  bool log_target = false;
+  int forest_trees = 100;
+  int forest_depth = 12;
+  void validate(int input_dim) const;
+};
+
+constexpr int kLightweightParamBudget = 75;
+ModelConfig default_config(kernels::KernelKind kind, ModelFamily family, bool unconstrained = false);
+int param_count_for(int input_dim, const std::vector<int>& hidden_widths);
+
+struct NormStats {
+  std::vector<double> f_min, f_max;
+  double t_min = 0.0, t_max = 1.0;
+  bool log_target = false;
+  std::vector<double> normalize(std::span<const double> features) const;
+  double normalize_target(double t) const;
+  double denormalize_target(double t_scaled) const;
+  static NormStats fit(const std::vector<std::vector<double>>& X, std::span<const double> y,
+                       bool log_target = false);
+};
+
+struct TrainedModel {
+  ModelConfig config;
+  kernels::KernelKind kind = kernels::KernelKind::MM;
+  std::vector<std::string> schema;
+  NormStats norm;
+  std::variant<Mlp> payload;  // NN families (the engine's scope); std::get<Mlp> as in the reference
+  std::vector<double> loss_trace;
+};
+
+std::vector<double> model_features(const datagen::Sample& sample, ModelFamily family);
+
+/// models.cpp:279-303 — trained on the GPU (one-model population).
+TrainedModel train_nn(const datagen::Dataset& train, const ModelConfig& config);
+/// models.cpp:335-344 restricted to the NN families (const/lrc/nlrc are out of scope).
+TrainedModel train_model(const datagen::Dataset& train, const ModelConfig& config);
+/// Batched overload: every (dataset, config) pair trained in ONE engine call.
+std::vector<TrainedModel> train_population(const std::vector<const datagen::Dataset*>& train,
+                                           const std::vector<ModelConfig>& configs);
+
+/// models.cpp:346-363 / 372-378 — evaluated on the GPU.
+double predict(const TrainedModel& model, std::span<const double> features);
+std::vector<double> predict_dataset(const TrainedModel& model, const datagen::Dataset& data);
+/// Batched overload: predictions of many (model, dataset) pairs in one call.
+std::vector<std::vector<double>> predict_population(const std::vector<const TrainedModel*>& models,
+                                                    const std::vector<const datagen::Dataset*>& data);
+int param_count(const TrainedModel& model);
+std::vector<double> flatten_params(const Mlp& net);
+}  // namespace models
+
+// ---- eval.hpp:13-49 ------------------------------------------------------------------------------
+namespace eval {
+double mape(std::span<const double> truth, std::span<const double> pred);
+struct ThresholdedMape {
+  double value = 0.0;
+  std::size_t n_kept = 0;
+};
+ThresholdedMape mape_thresholded(std::span<const double> truth, std::span<const double> pred,
+                                 double drop_fraction = 0.3);
+double spearman(std::span<const double> truth, std::span<const double> pred);
+struct EvalReport {
+  std::string kernel, variant, model_family;
+  double mape_full = 0.0, mape_thresholded = 0.0, rho = 0.0;
+  std::size_t n_total = 0, n_kept = 0;
+};
+EvalReport make_report(std::span<const double> truth, std::span<const double> pred,
+                       double drop_fraction = 0.3);
+}  // namespace eval
+
+// ---- selector.hpp:21-36 --------------------------------------------------------------------------
+namespace selector {
+using kernels::ScheduleCandidate;
+using kernels::ScheduleSpace;
+std::vector<ScheduleCandidate> enumerate_candidates(const ScheduleSpace& space, std::size_t limit,
+                                                    std::uint64_t seed);
+using ScheduleScorer = std::function<double(const ScheduleCandidate&)>;
+ScheduleCandidate select(const ScheduleScorer& scorer, const std::vector<ScheduleCandidate>& candidates);
+/// selector.cpp:42-53 — all candidates scored and reduced on the GPU.
+ScheduleCandidate select(const models::TrainedModel& model, std::uint32_t image_n,
+                         const std::vector<ScheduleCandidate>& candidates);
+}  // namespace selector
+
+}  // namespace perfsage

@@ -213,12 +213,13 @@ std::unique_ptr<TrainPlan> build_plan(lann_engine* e, const DevTrain& t, int pre
     if (const char* env = std::getenv("LANN_FP32_LANES")) lanes = std::atoi(env);
     if (lanes != 1 && lanes != 2 && lanes != 4 && lanes != 8 && lanes != 32 && lanes != 64 &&
         lanes != 128 && lanes != 256) {
-      // smallest lanes-per-model that still gives >= 16 warps per SM; populations
-      // too small for that get a whole CTA (4 warps) per model
+      // smallest lanes-per-model that still gives >= 32 warps (one-warp CTAs) per SM —
+      // enough waves that the longest (20000-epoch) groups do not leave a long tail;
+      // populations too small for that get a whole CTA (4 warps) per model
       const int total = t.n_models - int(fp64_models.size());
       lanes = total <= 4 * e->sms ? 128 : 32;
       for (int k : {1, 2, 4, 8})
-        if ((total + 32 / k - 1) / (32 / k) >= 16 * e->sms) {
+        if ((total + 32 / k - 1) / (32 / k) >= 32 * e->sms) {
           lanes = k;
           break;
         }

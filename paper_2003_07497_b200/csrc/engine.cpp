@@ -953,9 +953,15 @@ int lann_select_variants(lann_engine* e, const lann_model_set* ms, const int32_t
         dsc(size_t(n_cands), s);
     Timer timer(e);
     ck(cudaEventRecord(e->tr0, s), "event");
-    e->launches += select_variants_launch(M, ms->precision, kind, max_threads, seed, first, n_cands,
-                                          dI.p, dh1.p, dh2.p, dl.p, dt.p, dpo.p, dp.p, dn.p, didx.p,
-                                          dsc.p, e->sms, s);
+    if (ms->precision == LANN_FP32 && !std::getenv("LANN_SELECT_GENERIC") &&
+        select_variants_fast_launch(M, kind, max_threads, seed, first, n_cands, ms->n_inputs, ms->h1,
+                                    ms->h2, ms->log_target, with_n_thd, ms->param_offset, ms->params,
+                                    ms->norm, didx.p, dsc.p, e->sms, s))
+      e->launches += 1;
+    else
+      e->launches += select_variants_launch(M, ms->precision, kind, max_threads, seed, first, n_cands,
+                                            dI.p, dh1.p, dh2.p, dl.p, dt.p, dpo.p, dp.p, dn.p, didx.p,
+                                            dsc.p, e->sms, s);
     ck(cudaGetLastError(), "select_variants launch");
     ck(cudaEventRecord(e->tr1, s), "event");
     didx.down(out_idx);

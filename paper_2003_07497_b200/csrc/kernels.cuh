@@ -107,6 +107,13 @@ int select_schedule_launch(int64_t n, const uint32_t* d_cands, uint32_t n_img, i
                            int H2, int logt, const double* d_w, const double* d_nrm,
                            double* d_blk_score, int64_t* d_blk_idx, cudaStream_t s);
 bool select_variants_supported(int n_models, int max_params);
+// FP32 fast path (one hidden layer of 8, <= 16 models): weights folded with the
+// normalisation on the host, passed as a __grid_constant__ parameter. Host pointers.
+bool select_variants_fast_launch(int n_models, int kind, int max_threads, uint64_t seed, int64_t first,
+                                 int64_t n, const int* n_inputs, const int* h1, const int* h2,
+                                 const int* logt, const int* with_thd, const int64_t* param_offset,
+                                 const double* params, const double* norm, int* d_idx, double* d_score,
+                                 int sms, cudaStream_t s);
 int select_variants_launch(int n_models, int precision, int kind, int max_threads, uint64_t seed,
                            int64_t first, int64_t n, const int* d_in, const int* d_h1,
                            const int* d_h2, const int* d_logt, const int* d_thd,

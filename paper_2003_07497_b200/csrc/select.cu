@@ -33,6 +33,9 @@ __device__ __forceinline__ uint64_t derive(uint64_t root, uint64_t stream) {
   return sm64(s);
 }
 __device__ __forceinline__ uint64_t bounded(uint64_t& s, uint64_t n) {
+  // power of two: (2^64 - n) % n == 0, so the first draw is always accepted and
+  // r % n == r & (n - 1) — the same value Rng::bounded returns, without a 64-bit modulo
+  if ((n & (n - 1)) == 0) return sm64(s) & (n - 1);
   const uint64_t thr = (0 - n) % n;
   for (;;) {
     const uint64_t r = sm64(s);
@@ -242,6 +245,7 @@ __global__ void select_schedule_kernel(SchedArgs a, int pass) {
 
 constexpr int kMaxModels = 32;
 constexpr int kMaxParams = 96;  // lightweight nets (<= 75 parameters)
+constexpr int kFastMaxV = 16;   // variant models in the constant-parameter fast path
 
 struct VariantArgs {
   int n_models, precision, kind, max_threads;
@@ -317,7 +321,121 @@ __global__ void __launch_bounds__(256) select_variants_kernel(VariantArgs a) {
   }
 }
 
+// ---- fast path: prediction nets (one hidden layer of 8), FP32, <= 16 variant models -------
+// Weights travel as a __grid_constant__ kernel parameter (constant bank), so every FFMA
+// takes its weight as a constant-cache operand; min-max normalisation is folded into
+// layer 1 on the host: W'[h][j] = W[h][j] / range_j, B'[h] = B[h] - sum_j W[h][j] min_j / range_j.
+// Input columns are the kind's base features, then n_thd, then c (a model without n_thd
+// or without c has zero weights there).
+struct FastModels {
+  int nv;
+  float w1[kFastMaxV][8][8];  // [v][h][column]
+  float b1[kFastMaxV][8];
+  float w2[kFastMaxV][8];
+  float b2[kFastMaxV];
+  float tmin[kFastMaxV], trange[kFastMaxV];
+  int logt[kFastMaxV];
+};
+
+template <int NB>
+__global__ void __launch_bounds__(256) select_variants_fast(const __grid_constant__ FastModels fm,
+                                                            int kind, int max_threads, uint64_t seed,
+                                                            int64_t first, int64_t n, int* out_idx,
+                                                            double* out_score) {
+  constexpr int NC = NB + 2;  // columns: base features, n_thd, c
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    double base[8];
+    uint64_t c;
+    gen_candidate(kind, max_threads, seed, first + i, base, c);
+    float x[NC];
+#pragma unroll
+    for (int j = 0; j < NB; ++j) x[j] = (float)base[j];
+    x[NB] = (float)base[NB];
+    x[NB + 1] = (float)(double)c;
+    int best = -1;
+    float best_s = 0.f;
+#pragma unroll
+    for (int v = 0; v < kFastMaxV; ++v) {
+      if (v < fm.nv) {
+        float out = fm.b2[v];
+#pragma unroll
+        for (int h = 0; h < 8; ++h) {
+          float z = fm.b1[v][h];
+#pragma unroll
+          for (int j = 0; j < NC; ++j) z = fmaf(fm.w1[v][h][j], x[j], z);
+          out = fmaf(fm.w2[v][h], fmaxf(z, 0.f), out);
+        }
+        float t = fmaf(out, fm.trange[v], fm.tmin[v]);
+        if (fm.logt[v]) t = __expf(t);
+        t = fmaxf(t, 1e-9f);
+        if (best < 0 || t < best_s) {
+          best = v;
+          best_s = t;
+        }
+      }
+    }
+    out_idx[i] = best;
+    out_score[i] = (double)best_s;
+  }
+}
+
 }  // namespace
+
+// Host side of the fast path: fold normalisation into layer 1 (in FP64, then round).
+bool select_variants_fast_launch(int n_models, int kind, int max_threads, uint64_t seed, int64_t first,
+                                 int64_t n, const int* n_inputs, const int* h1, const int* h2,
+                                 const int* logt, const int* with_thd, const int64_t* param_offset,
+                                 const double* params, const double* norm, int* d_idx, double* d_score,
+                                 int sms, cudaStream_t s) {
+  if (n_models < 1 || n_models > kFastMaxV || kind < 0 || kind > 3) return false;
+  static const int nb_of[4] = {5, 3, 4, 5};
+  const int nb = nb_of[kind];
+  FastModels fm{};
+  fm.nv = n_models;
+  for (int v = 0; v < n_models; ++v) {
+    if (h1[v] != 8 || h2[v] != 0) return false;
+    const int I = n_inputs[v];
+    const bool thd = with_thd[v] != 0;
+    if (I != nb + (thd ? 1 : 0) && I != nb + (thd ? 1 : 0) + 1) return false;
+    const bool aug = I == nb + (thd ? 1 : 0) + 1;
+    int col[8];  // model input j -> column
+    for (int j = 0; j < nb; ++j) col[j] = j;
+    int k = nb;
+    if (thd) col[k++] = nb;
+    if (aug) col[k++] = nb + 1;
+    const double* w = params + param_offset[v];
+    const double* nr = norm + 18 * v;
+    for (int h = 0; h < 8; ++h) {
+      double b = w[I * 8 + h];
+      for (int j = 0; j < I; ++j) {
+        const double range = nr[8 + j] - nr[j];
+        const double wj = w[h * I + j];
+        if (range > 0.0) {
+          fm.w1[v][h][col[j]] = (float)(wj / range);
+          b -= wj * nr[j] / range;
+        }
+      }
+      fm.b1[v][h] = (float)b;
+      fm.w2[v][h] = (float)w[(I + 1) * 8 + h];
+    }
+    fm.b2[v] = (float)w[(I + 1) * 8 + 8];
+    const double tr = nr[17] - nr[16];
+    fm.tmin[v] = (float)nr[16];
+    fm.trange[v] = tr > 0.0 ? (float)tr : 0.f;
+    fm.logt[v] = logt[v];
+  }
+  int64_t blocks = (n + 255) / 256;
+  const int64_t cap = (int64_t)sms * 16;
+  if (blocks > cap) blocks = cap;
+  if (blocks < 1) blocks = 1;
+  switch (nb) {
+    case 3: select_variants_fast<3><<<(unsigned)blocks, 256, 0, s>>>(fm, kind, max_threads, seed, first, n, d_idx, d_score); break;
+    case 4: select_variants_fast<4><<<(unsigned)blocks, 256, 0, s>>>(fm, kind, max_threads, seed, first, n, d_idx, d_score); break;
+    default: select_variants_fast<5><<<(unsigned)blocks, 256, 0, s>>>(fm, kind, max_threads, seed, first, n, d_idx, d_score); break;
+  }
+  return true;
+}
 
 int select_schedule_launch(int64_t n, const uint32_t* d_cands, uint32_t n_img, int I, int H1,
                            int H2, int logt, const double* d_w, const double* d_nrm,

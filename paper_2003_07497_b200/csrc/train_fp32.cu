@@ -25,6 +25,7 @@
 // there every epoch, so HBM traffic per model-epoch is ~0.
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 
 #include "kernels.cuh"
 
@@ -267,12 +268,214 @@ __global__ void __launch_bounds__(32) train_fp32_kernel(TrainF32Args a) {
 }
 
 // ---------------------------------------------------------------------------------
+// Packed variant of train_fp32_kernel for the prediction nets (one hidden layer of 8):
+// hidden units are paired and every pair runs on sm_100's packed FP32 FMA
+// (fma.rn.f32x2 -> FFMA2, two FMAs per issue slot; the sample feature is a broadcast
+// scalar operand). The unpacked kernel is issue-bound (179 instructions per sample, 149
+// on the FMA pipe; profiles/r01_*); this one issues ~110 for the same 277 FLOP.
+typedef unsigned long long f32x2;
+__device__ __forceinline__ f32x2 pk(float a, float b) {
+  f32x2 r;
+  asm("mov.b64 %0, {%1,%2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void upk(f32x2 p, float& a, float& b) {
+  asm("mov.b64 {%0,%1}, %2;" : "=f"(a), "=f"(b) : "l"(p));
+}
+__device__ __forceinline__ f32x2 fma2(f32x2 a, f32x2 b, f32x2 c) {
+  f32x2 r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+__device__ __forceinline__ f32x2 mul2(f32x2 a, f32x2 b) {
+  f32x2 r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ f32x2 add2(f32x2 a, f32x2 b) {
+  f32x2 r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+
+template <int I, int K>
+__global__ void __launch_bounds__(32) train_fp32_h8_kernel(TrainF32Args a) {
+  constexpr int HP = 4;  // hidden pairs (h = 2q, 2q+1)
+  using N = Net<I, 8, 0>;
+  constexpr int P = N::P;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ uint64_t bar;
+  const int lane = threadIdx.x;
+  const int first = a.group_first[blockIdx.x];
+  const int count = a.group_count[blockIdx.x];
+  const int slot = lane / K, sub = lane % K;
+  const bool active = slot < count;
+  const int m = a.sorted_model[first + (active ? slot : 0)];
+  const int tile = a.model_tile[m];
+  const int rows = a.tile_rows[tile];
+  const int E = a.epochs[m];
+  float* trow = reinterpret_cast<float*>(smem_raw);  // [rows][8]
+  float* adam = trow + (size_t)rows * 8;            // [2][P][32], canonical parameter order
+  if (lane == 0) mbar_init(&bar);
+  __syncwarp();
+  if (lane == 0) tma_load_tile(trow, a.rows + a.tile_offset[tile] * 8, (uint32_t)rows * 32u, &bar);
+
+  const double* gp = a.params + a.param_offset[m];
+  f32x2 w1[I][HP], b1[HP], w2[HP];
+  float b2 = (float)gp[N::L2B];
+#pragma unroll
+  for (int q = 0; q < HP; ++q) {
+#pragma unroll
+    for (int i = 0; i < I; ++i)
+      w1[i][q] = pk((float)gp[N::L1W + (2 * q) * I + i], (float)gp[N::L1W + (2 * q + 1) * I + i]);
+    b1[q] = pk((float)gp[N::L1B + 2 * q], (float)gp[N::L1B + 2 * q + 1]);
+    w2[q] = pk((float)gp[N::L2W + 2 * q], (float)gp[N::L2W + 2 * q + 1]);
+  }
+  for (int p = 0; p < P; ++p) {
+    adam[p * 32 + lane] = 0.f;
+    adam[(P + p) * 32 + lane] = 0.f;
+  }
+  const float lr = (float)a.lr[m];
+  const float scale = 2.0f / (float)rows;
+  const float inv_n = 1.0f / (float)rows;
+  double* trace = (a.loss_trace && active) ? a.loss_trace + a.trace_offset[m] : nullptr;
+  int bad = -1;
+  float last = 0.f, pw1 = 1.f, pw2 = 1.f;
+  mbar_wait(&bar, 0);
+  __syncwarp();
+
+  for (int e = 0; e < E; ++e) {
+    f32x2 g1[I][HP], gb1[HP], gw2[HP];
+    const f32x2 zero2 = pk(0.f, 0.f);
+#pragma unroll
+    for (int q = 0; q < HP; ++q) {
+#pragma unroll
+      for (int i = 0; i < I; ++i) g1[i][q] = zero2;
+      gb1[q] = zero2;
+      gw2[q] = zero2;
+    }
+    float gb2 = 0.f, loss = 0.f;
+    for (int s = sub; s < rows; s += K) {
+      float xv[8];
+      load_row(trow, s, xv);
+      f32x2 xx[I];
+#pragma unroll
+      for (int i = 0; i < I; ++i) xx[i] = pk(xv[i], xv[i]);
+      f32x2 z[HP];
+#pragma unroll
+      for (int q = 0; q < HP; ++q) {
+        z[q] = b1[q];
+#pragma unroll
+        for (int i = 0; i < I; ++i) z[q] = fma2(w1[i][q], xx[i], z[q]);
+      }
+      f32x2 act[HP];
+      float za[HP], zb[HP];
+#pragma unroll
+      for (int q = 0; q < HP; ++q) {
+        upk(z[q], za[q], zb[q]);
+        act[q] = pk(fmaxf(za[q], 0.f), fmaxf(zb[q], 0.f));
+      }
+      f32x2 acc = pk(b2, 0.f);
+#pragma unroll
+      for (int q = 0; q < HP; ++q) acc = fma2(w2[q], act[q], acc);
+      float o0, o1;
+      upk(acc, o0, o1);
+      const float err = (o0 + o1) - xv[7];
+      loss = fmaf(err, err, loss);
+      const float d = err * scale;
+      const f32x2 dd = pk(d, d);
+      gb2 += d;
+#pragma unroll
+      for (int q = 0; q < HP; ++q) {
+        gw2[q] = fma2(dd, act[q], gw2[q]);
+        float ta, tb;
+        upk(mul2(w2[q], dd), ta, tb);
+        const f32x2 dq = pk(za[q] > 0.f ? ta : 0.f, zb[q] > 0.f ? tb : 0.f);
+        gb1[q] = add2(gb1[q], dq);
+#pragma unroll
+        for (int i = 0; i < I; ++i) g1[i][q] = fma2(dq, xx[i], g1[i][q]);
+      }
+    }
+    // sum the K per-lane partials of each model
+#pragma unroll
+    for (int off = 1; off < K; off <<= 1) {
+      auto red = [&](f32x2& v) {
+        float lo, hi;
+        upk(v, lo, hi);
+        lo += __shfl_xor_sync(0xffffffffu, lo, off);
+        hi += __shfl_xor_sync(0xffffffffu, hi, off);
+        v = pk(lo, hi);
+      };
+#pragma unroll
+      for (int q = 0; q < HP; ++q) {
+#pragma unroll
+        for (int i = 0; i < I; ++i) red(g1[i][q]);
+        red(gb1[q]);
+        red(gw2[q]);
+      }
+      gb2 += __shfl_xor_sync(0xffffffffu, gb2, off);
+      loss += __shfl_xor_sync(0xffffffffu, loss, off);
+    }
+    loss *= inv_n;
+    pw1 *= 0.9f;
+    pw2 *= 0.999f;
+    if (bad < 0) {
+      last = loss;
+      if (trace && sub == 0 && (e % a.trace_stride) == 0) trace[e / a.trace_stride] = (double)loss;
+      if (!isfinite(loss)) {
+        bad = e;
+      } else {
+        const float step = lr / (1.f - pw1), rb2 = 1.f / (1.f - pw2);
+        auto upd = [&](f32x2& wv, f32x2 gv, int p0, int p1) {
+          float w0, w1v, g0, g1v;
+          upk(wv, w0, w1v);
+          upk(gv, g0, g1v);
+          w0 -= adam_step(adam[p0 * 32 + lane], adam[(P + p0) * 32 + lane], g0, step, rb2);
+          w1v -= adam_step(adam[p1 * 32 + lane], adam[(P + p1) * 32 + lane], g1v, step, rb2);
+          wv = pk(w0, w1v);
+        };
+#pragma unroll
+        for (int q = 0; q < HP; ++q) {
+#pragma unroll
+          for (int i = 0; i < I; ++i) upd(w1[i][q], g1[i][q], N::L1W + 2 * q * I + i, N::L1W + (2 * q + 1) * I + i);
+          upd(b1[q], gb1[q], N::L1B + 2 * q, N::L1B + 2 * q + 1);
+          upd(w2[q], gw2[q], N::L2W + 2 * q, N::L2W + 2 * q + 1);
+        }
+        b2 -= adam_step(adam[N::L2B * 32 + lane], adam[(P + N::L2B) * 32 + lane], gb2, step, rb2);
+      }
+    }
+  }
+  if (active && sub == 0) {
+    double* outp = a.params + a.param_offset[m];
+#pragma unroll
+    for (int q = 0; q < HP; ++q) {
+      float x0, x1;
+#pragma unroll
+      for (int i = 0; i < I; ++i) {
+        upk(w1[i][q], x0, x1);
+        outp[N::L1W + 2 * q * I + i] = x0;
+        outp[N::L1W + (2 * q + 1) * I + i] = x1;
+      }
+      upk(b1[q], x0, x1);
+      outp[N::L1B + 2 * q] = x0;
+      outp[N::L1B + 2 * q + 1] = x1;
+      upk(w2[q], x0, x1);
+      outp[N::L2W + 2 * q] = x0;
+      outp[N::L2W + 2 * q + 1] = x1;
+    }
+    outp[N::L2B] = b2;
+    a.final_loss[m] = (double)last;
+    a.nonfinite_epoch[m] = bad;
+  }
+}
+
+// ---------------------------------------------------------------------------------
 template <int P>
 struct CtaLayout {
   static constexpr int PT = (P + 3) & ~3;  // transpose row stride (float4 writes, 4-wavefront STS.128)
 };
 
-template <int I, int H1, int H2, int W>
+template <int I, int H1, int H2, int W, bool kShuffleReduce>
 __global__ void __launch_bounds__(32 * W) train_fp32_cta_kernel(TrainF32Args a) {
   constexpr int P = Net<I, H1, H2>::P;
   constexpr int PT = CtaLayout<P>::PT;
@@ -327,30 +530,56 @@ __global__ void __launch_bounds__(32 * W) train_fp32_cta_kernel(TrainF32Args a) 
       load_row(trow, s, xv);
       accumulate_sample<I, H1, H2>(w, xv, gr, loss, scale);
     }
-    // level 1: warp transpose-sum through shared memory (lane j -> params j, j+32, ...)
-    float* myrow = tbuf + lane * PT;
+    if constexpr (kShuffleReduce) {
+      // level 1: recursive-halving reduce-scatter in registers — at offset o each lane
+      // keeps one half of its vector, sends the other to lane ^ o and adds what it gets;
+      // after 5 levels lane L holds the warp sums of elements 3L..3L+2 (loss = element P)
+      constexpr int PR = 32 * ((P + 1 + 31) / 32);
+      float v[PR];
 #pragma unroll
-    for (int p = 0; p < PT; p += 4)
-      *reinterpret_cast<float4*>(myrow + p) = make_float4(gr[p], gr[p + 1], gr[p + 2], gr[p + 3]);
+      for (int p = 0; p < PR; ++p) v[p] = p < P ? gr[p] : (p == P ? loss : 0.f);
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) loss += __shfl_xor_sync(0xffffffffu, loss, off);
-    __syncwarp();
+      for (int o = 16, n = PR / 2; o >= 1; o >>= 1, n >>= 1) {
+        const bool up = (lane & o) != 0;
 #pragma unroll
-    for (int k = 0; k < (P + 31) / 32; ++k) {
-      const int p = lane + 32 * k;
-      if (p < P) {
-        float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
-#pragma unroll
-        for (int r = 0; r < 32; r += 4) {
-          s0 += tbuf[(r + 0) * PT + p];
-          s1 += tbuf[(r + 1) * PT + p];
-          s2 += tbuf[(r + 2) * PT + p];
-          s3 += tbuf[(r + 3) * PT + p];
+        for (int j = 0; j < n; ++j) {
+          const float send = up ? v[j] : v[j + n];
+          const float keep = up ? v[j + n] : v[j];
+          v[j] = keep + __shfl_xor_sync(0xffffffffu, send, o);
         }
-        part[warp][p] = (s0 + s1) + (s2 + s3);
       }
+      constexpr int PER = PR / 32;
+#pragma unroll
+      for (int k = 0; k < PER; ++k) {
+        const int p = PER * lane + k;
+        if (p <= P) part[warp][p] = v[k];
+      }
+    } else {
+      // level 1: warp transpose-sum through shared memory (lane j -> params j, j+32, ...)
+      float* myrow = tbuf + lane * PT;
+#pragma unroll
+      for (int p = 0; p < PT; p += 4)
+        *reinterpret_cast<float4*>(myrow + p) = make_float4(gr[p], gr[p + 1], gr[p + 2], gr[p + 3]);
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) loss += __shfl_xor_sync(0xffffffffu, loss, off);
+      __syncwarp();
+#pragma unroll
+      for (int k = 0; k < (P + 31) / 32; ++k) {
+        const int p = lane + 32 * k;
+        if (p < P) {
+          float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+#pragma unroll
+          for (int r = 0; r < 32; r += 4) {
+            s0 += tbuf[(r + 0) * PT + p];
+            s1 += tbuf[(r + 1) * PT + p];
+            s2 += tbuf[(r + 2) * PT + p];
+            s3 += tbuf[(r + 3) * PT + p];
+          }
+          part[warp][p] = (s0 + s1) + (s2 + s3);
+        }
+      }
+      if (lane == 0) part[warp][P] = loss;
     }
-    if (lane == 0) part[warp][P] = loss;
     __syncthreads();
     // level 2: owners sum the W warp partials and apply Adam
     pw1 *= 0.9f;
@@ -392,18 +621,35 @@ __global__ void __launch_bounds__(32 * W) train_fp32_cta_kernel(TrainF32Args a) 
 template <int I, int H1, int H2, int W>
 void launch_cta(const TrainF32Args& a, int tile_bytes, cudaStream_t s) {
   constexpr int P = Net<I, H1, H2>::P;
-  auto kern = train_fp32_cta_kernel<I, H1, H2, W>;
-  const int dyn = tile_bytes + W * 32 * CtaLayout<P>::PT * 4;
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
-  kern<<<a.n_groups, 32 * W, dyn, s>>>(a);
+  static const bool shuffle = std::getenv("LANN_CTA_SMEM_REDUCE") == nullptr;
+  if (shuffle) {
+    auto kern = train_fp32_cta_kernel<I, H1, H2, W, true>;
+    const int dyn = tile_bytes;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
+    kern<<<a.n_groups, 32 * W, dyn, s>>>(a);
+  } else {
+    auto kern = train_fp32_cta_kernel<I, H1, H2, W, false>;
+    const int dyn = tile_bytes + W * 32 * CtaLayout<P>::PT * 4;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
+    kern<<<a.n_groups, 32 * W, dyn, s>>>(a);
+  }
 }
 
 // dynamic smem = the largest tile of the launch (rows x 32 B) + Adam moments
 template <int I, int H1, int H2, int K>
 void launch_k(const TrainF32Args& a, int tile_bytes, cudaStream_t s) {
   constexpr int P = Net<I, H1, H2>::P;
-  auto kern = train_fp32_kernel<I, H1, H2, K>;
   const int dyn = tile_bytes + 2 * P * 32 * 4;
+  if constexpr (H1 == 8 && H2 == 0) {
+    static const bool packed = std::getenv("LANN_FP32_UNPACKED") == nullptr;
+    if (packed) {
+      auto kern = train_fp32_h8_kernel<I, K>;
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
+      kern<<<a.n_groups, 32, dyn, s>>>(a);
+      return;
+    }
+  }
+  auto kern = train_fp32_kernel<I, H1, H2, K>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
   kern<<<a.n_groups, 32, dyn, s>>>(a);
 }

@@ -149,6 +149,7 @@ Status validate_train(const DevTrain& t) {
 struct Fp32Bucket {
   int in, h1, h2, lanes, tile_bytes, n_groups;
   DBuf<int> gfirst, gcount, sorted;
+  DBuf<long long> prof;  // LANN_PHASE_PROFILE: CTA 0 cycle split (CTA kernel)
   double cost;
 };
 
@@ -259,6 +260,7 @@ std::unique_ptr<TrainPlan> build_plan(lann_engine* e, const DevTrain& t, int pre
       b->gcount = DBuf<int>(gcount, s);
       b->sorted = DBuf<int>(ms, s);
       b->cost = cost;
+      if (std::getenv("LANN_PHASE_PROFILE")) b->prof = DBuf<long long>(4, s);
       P.buckets.push_back(std::move(b));
     }
     // longest bucket first so it starts first on its stream
@@ -360,6 +362,7 @@ void execute_plan(lann_engine* e, const TrainPlan& P, double* dparams, double* d
     a.loss_trace = dtrace;
     a.trace_offset = dtrace_off;
     a.trace_stride = P.trace_stride;
+    a.phase_cycles = b->prof.p;
     if (!launch_train_fp32(a, b->in, b->h1, b->h2, b->lanes, b->tile_bytes, next_stream()))
       throw CudaFail{"no FP32 kernel for this shape"};
     ck(cudaGetLastError(), "train_fp32 launch");
@@ -397,6 +400,13 @@ void execute_plan(lann_engine* e, const TrainPlan& P, double* dparams, double* d
   }
   if (std::getenv("LANN_PHASE_PROFILE")) {
     ck(cudaDeviceSynchronize(), "profile sync");
+    for (const auto& b : P.buckets) {
+      if (b->lanes < 64) continue;
+      long long c[4] = {0, 0, 0, 0};
+      ck(cudaMemcpy(c, b->prof.p, 3 * sizeof(long long), cudaMemcpyDeviceToHost), "profile D2H");
+      std::fprintf(stderr, "fp32 cta shape %d-%d-%d: cycles compute %lld reduce %lld adam %lld\n", b->in,
+                   b->h1, b->h2, c[0], c[1], c[2]);
+    }
     for (const auto& b : P.buckets64) {
       long long c[4] = {0, 0, 0, 0};
       ck(cudaMemcpy(c, b->prof.p, sizeof c, cudaMemcpyDeviceToHost), "profile D2H");

@@ -55,6 +55,7 @@ struct TrainF32Args {
   double* loss_trace;
   const int64_t* trace_offset;
   int trace_stride;
+  long long* phase_cycles;   // optional (LANN_PHASE_PROFILE): CTA 0's clock64 per phase
 };
 
 // Prediction over rows (models.cpp:346-363).

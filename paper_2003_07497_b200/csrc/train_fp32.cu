@@ -511,7 +511,10 @@ __global__ void __launch_bounds__(32 * W) train_fp32_cta_kernel(TrainF32Args a) 
   mbar_wait(&bar, 0);
   __syncthreads();
 
+  const bool prof = a.phase_cycles && blockIdx.x == 0 && tid == 0;
+  long long pc[3] = {0, 0, 0};
   for (int e = 0; e < E; ++e) {
+    const long long clk0 = prof ? clock64() : 0;
     float w[PT];
 #pragma unroll
     for (int p = 0; p < PT; p += 4) {
@@ -530,6 +533,7 @@ __global__ void __launch_bounds__(32 * W) train_fp32_cta_kernel(TrainF32Args a) 
       load_row(trow, s, xv);
       accumulate_sample<I, H1, H2>(w, xv, gr, loss, scale);
     }
+    const long long clk1 = prof ? clock64() : 0;
     if constexpr (kShuffleReduce) {
       // level 1: recursive-halving reduce-scatter in registers — at offset o each lane
       // keeps one half of its vector, sends the other to lane ^ o and adds what it gets;
@@ -581,6 +585,7 @@ __global__ void __launch_bounds__(32 * W) train_fp32_cta_kernel(TrainF32Args a) 
       if (lane == 0) part[warp][P] = loss;
     }
     __syncthreads();
+    const long long clk2 = prof ? clock64() : 0;
     // level 2: owners sum the W warp partials and apply Adam
     pw1 *= 0.9f;
     pw2 *= 0.999f;
@@ -599,6 +604,12 @@ __global__ void __launch_bounds__(32 * W) train_fp32_cta_kernel(TrainF32Args a) 
       }
     }
     __syncthreads();
+    if (prof) {
+      const long long clk3 = clock64();
+      pc[0] += clk1 - clk0;  // weight reload + per-sample forward/backward
+      pc[1] += clk2 - clk1;  // reduce-scatter + barrier
+      pc[2] += clk3 - clk2;  // owner sums + Adam + barrier
+    }
     const float L = loss_sh;
     if (bad < 0) {
       last = L;
@@ -609,6 +620,8 @@ __global__ void __launch_bounds__(32 * W) train_fp32_cta_kernel(TrainF32Args a) 
       break;  // uniform across the CTA (everyone read the same loss)
     }
   }
+  if (prof)
+    for (int k = 0; k < 3; ++k) a.phase_cycles[k] = pc[k];
   // on a non-finite loss the reference discards the model (TrainingError); so do we
   double* outp = a.params + a.param_offset[m];
   for (int p = tid; p < P; p += T) outp[p] = (double)wsh[p];

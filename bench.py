@@ -169,9 +169,16 @@ def main():
     import torch.distributed as dist
     from paper_2003_07497_b200 import engine as E
 
-    torch.cuda.set_device(local_rank)
+    # LANN_BENCH_SHARE_DEVICE=1: every rank on device 0 with gloo plumbing — only for
+    # exercising the multi-rank code path on a one-GPU box (NCCL rejects duplicate GPUs)
+    share = os.environ.get("LANN_BENCH_SHARE_DEVICE") == "1"
+    device = 0 if share else local_rank
+    torch.cuda.set_device(device)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
 
     def barrier():
         if world > 1:
@@ -181,12 +188,12 @@ def main():
     def max_over_ranks(x):
         if world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        t = torch.tensor([x], dtype=torch.float64, device="cpu" if share else "cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
     precision = abi.FP32 if args.precision == "fp32" else abi.FP64_EXACT
-    eng = E.Engine(local_rank)
+    eng = E.Engine(device)
     jobs = popmod.config2_jobs(root_seed=1 + rank)
     me_rank = popmod.model_epochs(jobs)
     pop = eng.prepare(jobs, precision)
@@ -197,7 +204,7 @@ def main():
     barrier()
     dev_ms, train_ms, launches = 0.0, 0.0, 0
     t0 = time.perf_counter()
-    with ClockSampler(local_rank) as clk:
+    with ClockSampler(device) as clk:
         for _ in range(args.steps):
             flush.zero_()
             torch.cuda.synchronize()

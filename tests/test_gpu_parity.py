@@ -70,6 +70,24 @@ def test_fp64_kfold_sweep_bit_exact(engine, golden):
         check(r, exp, p, log_target=bool(j.log_target))
 
 
+def test_fp64_sharded_population_identical(engine, golden):
+    """Multi-GPU invariant: a population trained as 1, 2 or 4 contiguous
+    shards (what ranks of bench.py / sharding.shard run) gives bit-identical results."""
+    from paper_2003_07497_b200 import sharding
+    jobs = [job_from(j) for j in golden["config3_kfold_short"]["jobs"]]
+    st, whole, _, _ = engine.run_population(jobs, abi.FP64_EXACT)
+    assert st == 0
+    for world in (2, 4):
+        merged = []
+        for rank in range(world):
+            part, off = sharding.shard(jobs, rank, world)
+            st, res, _, _ = engine.run_population(part, abi.FP64_EXACT)
+            assert st == 0
+            merged.extend(res)
+        assert [(r.final_loss, r.mape, r.mape_thr, r.rho) for r in merged] == \
+               [(r.final_loss, r.mape, r.mape_thr, r.rho) for r in whole]
+
+
 def random_problem(rng, I, dims_hidden, n):
     X = np.zeros((n, I))
     X[:] = rng.uniform(0, 1, (n, I))

@@ -15,11 +15,15 @@
 //    compile-time shape); with K = 1 all 32 lanes read the same row (shared-
 //    memory broadcast); with K > 1 the per-lane partials are summed by a shuffle
 //    butterfly, after which every lane applies the identical Adam step.
+//  * train_fp32_h8_kernel<K> — the same mapping for the one-hidden-layer-of-8
+//    prediction nets with hidden units paired on the packed FP32 FMA (FFMA2).
 //  * train_fp32_cta_kernel<W> — FEW models (the 48-combo population): one model
 //    per CTA of W warps so the per-epoch LATENCY is minimised; threads own
-//    samples, gradients are reduced by a warp transpose through shared memory
-//    and then across warps; owner threads apply Adam; new weights are broadcast
-//    back through shared memory (two __syncthreads per epoch).
+//    samples; gradients are reduced inside each warp by a register-only
+//    recursive-halving reduce-scatter (shuffles; a shared-memory transpose
+//    variant is kept for comparison) and then across warps through shared
+//    memory; owner threads apply Adam; new weights are broadcast back through
+//    shared memory (two __syncthreads per epoch).
 // In both, the tile (N rows x 8 floats, target y in column 7) is staged ONCE into
 // shared memory by a TMA bulk copy (cp.async.bulk + mbarrier) and re-read from
 // there every epoch, so HBM traffic per model-epoch is ~0.

@@ -210,22 +210,14 @@ std::unique_ptr<TrainPlan> build_plan(lann_engine* e, const DevTrain& t, int pre
       else
         fp64_models.push_back(m);
     }
-    int lanes = 0;
-    if (const char* env = std::getenv("LANN_FP32_LANES")) lanes = std::atoi(env);
-    if (lanes != 1 && lanes != 2 && lanes != 4 && lanes != 8 && lanes != 32 && lanes != 64 &&
-        lanes != 128 && lanes != 256) {
-      // smallest lanes-per-model that still gives >= 32 warps (one-warp CTAs) per SM —
-      // enough waves that the longest (20000-epoch) groups do not leave a long tail;
-      // populations too small for that get a whole CTA (4 warps) per model
-      const int total = t.n_models - int(fp64_models.size());
-      lanes = total <= 4 * e->sms ? 128 : 32;
-      for (int k : {1, 2, 4, 8})
-        if ((total + 32 / k - 1) / (32 / k) >= 32 * e->sms) {
-          lanes = k;
-          break;
-        }
-    }
-    const int G = lanes <= 32 ? 32 / lanes : 1;
+    int env_lanes = 0;
+    if (const char* env = std::getenv("LANN_FP32_LANES")) env_lanes = std::atoi(env);
+    if (env_lanes != 1 && env_lanes != 2 && env_lanes != 4 && env_lanes != 8 && env_lanes != 32 &&
+        env_lanes != 64 && env_lanes != 128 && env_lanes != 256)
+      env_lanes = 0;
+    // populations too small to fill the GPU with warps get a whole CTA (4 warps) per model
+    const int total_fp32 = t.n_models - int(fp64_models.size());
+    const bool small = total_fp32 <= 4 * e->sms;
     for (auto& [shape, ms] : by_shape) {
       // group: same tile and epoch count, up to G models; longest groups first
       std::stable_sort(ms.begin(), ms.end(), [&](int a, int b) {
@@ -235,6 +227,39 @@ std::unique_ptr<TrainPlan> build_plan(lann_engine* e, const DevTrain& t, int pre
         if (t.model_tile[a] != t.model_tile[b]) return t.model_tile[a] < t.model_tile[b];
         return t.epochs[a] < t.epochs[b];
       });
+      auto count_groups = [&](int G) {
+        int n = 0;
+        for (size_t i = 0; i < ms.size();) {
+          size_t j = i + 1;
+          while (j < ms.size() && int(j - i) < G && t.model_tile[ms[j]] == t.model_tile[ms[i]] &&
+                 t.epochs[ms[j]] == t.epochs[ms[i]])
+            ++j;
+          ++n;
+          i = j;
+        }
+        return n;
+      };
+      int bucket_rows = 1;
+      for (int m : ms) bucket_rows = std::max(bucket_rows, t.tile_rows[t.model_tile[m]]);
+      int lanes = env_lanes;
+      if (!lanes && small) lanes = 128;
+      if (!lanes) {
+        // lanes per model minimising the modelled makespan of this bucket on its own:
+        // waves x per-warp epoch cost (samples per lane + butterfly levels + Adam), with
+        // the wave size from the kernel's measured occupancy
+        double best = 1e300;
+        for (int k : {1, 2, 4, 8}) {
+          const int slots = std::max(1, fp32_warp_slots_per_sm(std::get<0>(shape), std::get<1>(shape),
+                                                               std::get<2>(shape), k, bucket_rows * 32)) * e->sms;
+          const double waves = std::ceil(double(count_groups(32 / k)) / slots);
+          const double epoch = double(bucket_rows) / k + 1.0 * std::log2(double(k)) + 6.0;
+          if (waves * epoch < best * 0.999) {
+            best = waves * epoch;
+            lanes = k;
+          }
+        }
+      }
+      const int G = lanes <= 32 ? 32 / lanes : 1;
       std::vector<int> gfirst, gcount;
       int max_rows = 1;
       double cost = 0.0;
@@ -304,9 +329,8 @@ std::unique_ptr<TrainPlan> build_plan(lann_engine* e, const DevTrain& t, int pre
         const int tile = t.model_tile[m];
         const int np = param_count(t.tile_inputs[tile], t.h1[m], t.h2[m]);
         b->max_p = std::max(b->max_p, np);
-        const size_t rec = size_t(fp64_record_doubles(t.tile_inputs[tile], t.h1[m], t.h2[m])) *
-                           t.tile_rows[tile] * 8;
-        const size_t state = size_t(3 * np + 2) * 8;
+        const size_t rec = fp64_record_bytes(t.tile_inputs[tile], t.h1[m], t.h2[m], t.tile_rows[tile]);
+        const size_t state = fp64_state_bytes(np);
         max_state = std::max(max_state, state);
         max_bytes_smem = std::max(max_bytes_smem, state + rec);
         soff[m] = scratch;

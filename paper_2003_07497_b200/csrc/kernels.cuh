@@ -91,11 +91,13 @@ struct EvalArgs {
 // shape = {I, H1, H2} when every model of the launch has that compiled shape, else null
 void launch_train_fp64(const TrainArgs& a, int max_p, int dyn_bytes, const int* shape, cudaStream_t s);
 bool fp64_shape_compiled(int in, int h1, int h2);
-// bytes of one per-sample record of the FP64 trainer for a shape (see train_fp64.cu)
-int fp64_record_doubles(int in, int h1, int h2);
+// FP64 trainer footprint (see train_fp64.cu): record matrix of a model, model state
+size_t fp64_record_bytes(int in, int h1, int h2, int n);
+size_t fp64_state_bytes(int p);
 bool launch_train_fp32(const TrainF32Args& a, int in, int h1, int h2, int lanes, int tile_bytes,
                        cudaStream_t s);
 bool fp32_shape_supported(int in, int h1, int h2);
+int fp32_warp_slots_per_sm(int in, int h1, int h2, int lanes, int tile_bytes);
 void launch_predict_fp64(const PredictArgs& a, cudaStream_t s);
 void launch_predict_fp32(const PredictArgs& a, cudaStream_t s);
 void launch_eval(const EvalArgs& a, int max_len, cudaStream_t s);

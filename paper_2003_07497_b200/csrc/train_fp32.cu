@@ -698,6 +698,53 @@ __global__ void pack_rows_kernel(const double* X, const double* y, int64_t n, fl
 
 }  // namespace
 
+// Resident one-warp CTAs per SM of the warp kernel for (shape, lanes): the wave size the
+// host uses to pick lanes per model without a long last wave.
+template <int I, int H1, int H2, int K>
+int slots_k(int tile_bytes) {
+  constexpr int P = Net<I, H1, H2>::P;
+  const int dyn = tile_bytes + 2 * P * 32 * 4;
+  int n = 0;
+  if constexpr (H1 == 8 && H2 == 0) {
+    cudaFuncSetAttribute(train_fp32_h8_kernel<I, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, train_fp32_h8_kernel<I, K>, 32, dyn);
+  } else {
+    cudaFuncSetAttribute(train_fp32_kernel<I, H1, H2, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, train_fp32_kernel<I, H1, H2, K>, 32, dyn);
+  }
+  return n;
+}
+
+template <int I, int H1, int H2>
+int slots_shape(int lanes, int tile_bytes) {
+  switch (lanes) {
+    case 1: return slots_k<I, H1, H2, 1>(tile_bytes);
+    case 2: return slots_k<I, H1, H2, 2>(tile_bytes);
+    case 4: return slots_k<I, H1, H2, 4>(tile_bytes);
+    case 8: return slots_k<I, H1, H2, 8>(tile_bytes);
+    default: return slots_k<I, H1, H2, 32>(tile_bytes);
+  }
+}
+
+int fp32_warp_slots_per_sm(int in, int h1, int h2, int lanes, int tile_bytes) {
+  if (h1 == 8 && h2 == 0) {
+    switch (in) {
+      case 1: return slots_shape<1, 8, 0>(lanes, tile_bytes);
+      case 2: return slots_shape<2, 8, 0>(lanes, tile_bytes);
+      case 3: return slots_shape<3, 8, 0>(lanes, tile_bytes);
+      case 4: return slots_shape<4, 8, 0>(lanes, tile_bytes);
+      case 5: return slots_shape<5, 8, 0>(lanes, tile_bytes);
+      case 6: return slots_shape<6, 8, 0>(lanes, tile_bytes);
+      default: return slots_shape<7, 8, 0>(lanes, tile_bytes);
+    }
+  }
+  switch (in) {
+    case 4: return slots_shape<4, 5, 5>(lanes, tile_bytes);
+    case 5: return slots_shape<5, 5, 5>(lanes, tile_bytes);
+    default: return slots_shape<6, 5, 5>(lanes, tile_bytes);
+  }
+}
+
 bool fp32_shape_supported(int in, int h1, int h2) {
   if (h1 == 8 && h2 == 0) return in >= 1 && in <= 7;
   if (h1 == 5 && h2 == 5) return in >= 4 && in <= 6;

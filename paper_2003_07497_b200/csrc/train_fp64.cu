@@ -9,15 +9,18 @@
 // multiply-add is ever contracted (the reference object code has no FMA).
 //
 // Mapping (one CTA per model, models ordered longest-first):
-//   phase A  threads own SAMPLES: forward + backward for their samples, writing a
-//            per-sample record {x, hidden activations, inv_n*delta, err^2};
+//   phase A  threads own SAMPLES: forward + backward for their samples, writing the
+//            sample's column of the record matrix {x, y, hidden activations,
+//            inv_n*delta, err^2};
 //   phase B  threads own PARAMETERS: each sums its N per-sample terms in sample
 //            order (the only order-sensitive reduction), then applies Adam;
 //            one thread sums the loss terms in sample order.
-// Two __syncthreads per epoch. The N-long dependent DADD chain (8 cycles each)
-// bounds the epoch latency; several CTAs per SM overlap their chains.
-// Phase A is compiled per network shape for the default topologies (all loops
-// unrolled, shared-memory offsets immediate); other shapes use a generic path.
+// Two __syncthreads per epoch. The record matrix is stored structure-of-arrays
+// (one row per quantity, samples contiguous): phase-A stores are contiguous across
+// lanes, and a phase-B chain fetches two samples per 128-bit shared-memory load, so
+// the N-long dependent DADD chain (8 cycles per link) — not shared-memory
+// wavefronts — bounds the epoch latency. Phase A is compiled per network shape for
+// the default topologies (unrolled, immediate offsets); other shapes use a generic path.
 #include <cmath>
 
 #include "kernels.cuh"
@@ -27,18 +30,21 @@ namespace {
 
 constexpr int kMaxKB = 8;  // parameters owned per thread in phase B (P <= 8 * blockDim)
 
+// Record rows: [0,7) inputs x0..x6 | 7 target y | [8, 8+H1) a1 | [.., +H2) a2 |
+// t1[H1] | t2[H2] | tout | e2 | ones. Row r of sample s lives at r * ld + s.
+__host__ __device__ constexpr int rec_rows(int H1, int H2) {
+  return 8 + 2 * (H1 + (H2 > 0 ? H2 : 0)) + 3;
+}
+__host__ __device__ constexpr int rec_ld(int N) { return (N + 1) & ~1; }  // even: 16-B aligned pairs
+
 struct Shape {
   int I, H1, H2, nl, P, R;
   int dims[4];
   int woff[3], boff[3];
-  int inoff[3];  // record offset of each layer's input vector
-  int toff[3];   // record offset of each layer's (scaled) deltas
-  int e2;        // record offset of err^2
+  int inoff[3];  // record row of each layer's input vector
+  int toff[3];   // record row of each layer's (scaled) deltas
+  int e2, ones;  // record rows of err^2 and of the constant 1.0
 };
-
-__host__ __device__ constexpr int rec_stride(int H1, int H2) {
-  return (8 + 2 * (H1 + (H2 > 0 ? H2 : 0)) + 2) | 1;  // odd: minimal bank pattern for 8-byte accesses
-}
 
 __device__ Shape make_shape(int I, int H1, int H2) {
   Shape s;
@@ -67,31 +73,32 @@ __device__ Shape make_shape(int I, int H1, int H2) {
   s.toff[1] = t0 + s.dims[1];
   s.toff[2] = t0 + s.dims[1] + s.dims[2];
   s.e2 = t0 + hidden + 1;
-  s.R = rec_stride(H1, H2);
+  s.ones = s.e2 + 1;
+  s.R = rec_rows(H1, H2);
   return s;
 }
 
 // ---- phase A, compiled shape ------------------------------------------------------
-// Record layout (doubles): [0,8) x | [8, 8+H1) a1 | [.., +H2) a2 | t1[H1] | t2[H2] | tout | e2
 template <int I, int H1, int H2>
 struct Fixed {
   static constexpr int HS = H1 + H2;
   static constexpr int A1 = 8, A2 = 8 + H1;
   static constexpr int T1 = 8 + HS, T2 = T1 + H1, TO = T1 + HS, E2 = TO + 1;
-  static constexpr int R = rec_stride(H1, H2);
   static constexpr int W1 = 0, B1 = I * H1;
-  static constexpr int W2 = B1 + H1, B2 = W2 + H1 * H2;          // 2 hidden layers
-  static constexpr int WO = H2 > 0 ? B2 + H2 : B1 + H1;          // output weights
+  static constexpr int W2 = B1 + H1, B2 = W2 + H1 * H2;  // 2 hidden layers
+  static constexpr int WO = H2 > 0 ? B2 + H2 : B1 + H1;  // output weights
   static constexpr int BO = WO + (H2 > 0 ? H2 : H1);
   static constexpr int P = BO + 1;
 
-  __device__ static void sample(const double* __restrict__ w, double* __restrict__ r, double y,
+  // r = column s of the record matrix (r[row * ld])
+  __device__ static void sample(const double* __restrict__ w, double* __restrict__ r, int ld,
                                 double inv_n) {
     double x[I];
 #pragma unroll
-    for (int i = 0; i < I; ++i) x[i] = r[i];
-    // layer 1 in groups of 4 neurons (4 DADD chains in flight) — the group loop is
-    // not unrolled so the weights are not all hoisted into registers at once
+    for (int i = 0; i < I; ++i) x[i] = r[i * ld];
+    const double y = r[7 * ld];
+    // layer 1 in groups of 4 neurons (4 DADD chains in flight); the group loop is not
+    // unrolled so the weights are not all hoisted into registers at once
     constexpr int G1 = (H1 + 3) / 4;
 #pragma unroll 1
     for (int gi = 0; gi < G1; ++gi) {
@@ -105,11 +112,11 @@ struct Fixed {
           if (gi * 4 + k < H1) z[k] = __dadd_rn(z[k], __dmul_rn(w[W1 + (gi * 4 + k) * I + i], x[i]));
 #pragma unroll
       for (int k = 0; k < 4; ++k)
-        if (gi * 4 + k < H1) r[A1 + gi * 4 + k] = z[k] > 0.0 ? z[k] : 0.0;
+        if (gi * 4 + k < H1) r[(A1 + gi * 4 + k) * ld] = z[k] > 0.0 ? z[k] : 0.0;
     }
     double a1[H1];
 #pragma unroll
-    for (int o = 0; o < H1; ++o) a1[o] = r[A1 + o];
+    for (int o = 0; o < H1; ++o) a1[o] = r[(A1 + o) * ld];
     double a2[H2 > 0 ? H2 : 1];
     double z;
     if constexpr (H2 > 0) {
@@ -122,7 +129,7 @@ struct Fixed {
 #pragma unroll
       for (int o = 0; o < H2; ++o) {
         a2[o] = a2[o] > 0.0 ? a2[o] : 0.0;
-        r[A2 + o] = a2[o];
+        r[(A2 + o) * ld] = a2[o];
       }
       z = w[BO];
 #pragma unroll
@@ -133,16 +140,16 @@ struct Fixed {
       for (int i = 0; i < H1; ++i) z = __dadd_rn(z, __dmul_rn(w[WO + i], a1[i]));
     }
     const double err = __dsub_rn(z, y);
-    r[E2] = __dmul_rn(err, err);
+    r[E2 * ld] = __dmul_rn(err, err);
     const double dout = __dmul_rn(2.0, err);
-    r[TO] = __dmul_rn(inv_n, dout);
+    r[TO * ld] = __dmul_rn(inv_n, dout);
     if constexpr (H2 > 0) {
       double d2[H2];
 #pragma unroll
       for (int i = 0; i < H2; ++i) {
         const double acc = __dadd_rn(0.0, __dmul_rn(w[WO + i], dout));
         d2[i] = a2[i] > 0.0 ? acc : 0.0;
-        r[T2 + i] = __dmul_rn(inv_n, d2[i]);
+        r[(T2 + i) * ld] = __dmul_rn(inv_n, d2[i]);
       }
       double acc[H1];
 #pragma unroll
@@ -152,12 +159,12 @@ struct Fixed {
 #pragma unroll
         for (int i = 0; i < H1; ++i) acc[i] = __dadd_rn(acc[i], __dmul_rn(w[W2 + o * H1 + i], d2[o]));
 #pragma unroll
-      for (int i = 0; i < H1; ++i) r[T1 + i] = __dmul_rn(inv_n, a1[i] > 0.0 ? acc[i] : 0.0);
+      for (int i = 0; i < H1; ++i) r[(T1 + i) * ld] = __dmul_rn(inv_n, a1[i] > 0.0 ? acc[i] : 0.0);
     } else {
 #pragma unroll
       for (int i = 0; i < H1; ++i) {
         const double acc = __dadd_rn(0.0, __dmul_rn(w[WO + i], dout));
-        r[T1 + i] = __dmul_rn(inv_n, a1[i] > 0.0 ? acc : 0.0);
+        r[(T1 + i) * ld] = __dmul_rn(inv_n, a1[i] > 0.0 ? acc : 0.0);
       }
     }
   }
@@ -165,103 +172,102 @@ struct Fixed {
 
 // ---- phase A, generic shape (runtime loops) ------------------------------------------
 __device__ void sample_generic(const Shape& sh, const double* __restrict__ w, double* __restrict__ r,
-                               double y, double inv_n) {
+                               int ld, double inv_n) {
+  const double y = r[7 * ld];
   for (int l = 0; l < sh.nl; ++l) {
     const int in = sh.dims[l], out = sh.dims[l + 1];
     const double* wl = w + sh.woff[l];
     const double* bl = w + sh.boff[l];
-    const double* ain = r + sh.inoff[l];
+    const double* ain = r + sh.inoff[l] * ld;
     if (l + 1 < sh.nl) {
-      double* aout = r + sh.inoff[l + 1];
+      double* aout = r + sh.inoff[l + 1] * ld;
       for (int o = 0; o < out; o += 4) {  // four independent DADD chains in flight
         const int n4 = out - o < 4 ? out - o : 4;
         double z[4];
 #pragma unroll
         for (int k = 0; k < 4; ++k) z[k] = k < n4 ? bl[o + k] : 0.0;
         for (int i = 0; i < in; ++i) {
-          const double ai = ain[i];
+          const double ai = ain[i * ld];
 #pragma unroll
           for (int k = 0; k < 4; ++k)
             if (k < n4) z[k] = __dadd_rn(z[k], __dmul_rn(wl[(o + k) * in + i], ai));
         }
 #pragma unroll
         for (int k = 0; k < 4; ++k)
-          if (k < n4) aout[o + k] = z[k] > 0.0 ? z[k] : 0.0;
+          if (k < n4) aout[(o + k) * ld] = z[k] > 0.0 ? z[k] : 0.0;
       }
     } else {
       double z = bl[0];
-      for (int i = 0; i < in; ++i) z = __dadd_rn(z, __dmul_rn(wl[i], ain[i]));
+      for (int i = 0; i < in; ++i) z = __dadd_rn(z, __dmul_rn(wl[i], ain[i * ld]));
       const double err = __dsub_rn(z, y);
-      r[sh.e2] = __dmul_rn(err, err);
-      r[sh.toff[l]] = __dmul_rn(2.0, err);  // unscaled output delta (mlp.cpp:92)
+      r[sh.e2 * ld] = __dmul_rn(err, err);
+      r[sh.toff[l] * ld] = __dmul_rn(2.0, err);  // unscaled output delta (mlp.cpp:92)
     }
   }
   for (int l = sh.nl - 2; l >= 0; --l) {  // hidden deltas from the next layer's, unscaled
     const int nin = sh.dims[l + 1], nout = sh.dims[l + 2];
     const double* wn = w + sh.woff[l + 1];
-    const double* dn = r + sh.toff[l + 1];
-    const double* act = r + sh.inoff[l + 1];
-    double* d = r + sh.toff[l];
+    const double* dn = r + sh.toff[l + 1] * ld;
+    const double* act = r + sh.inoff[l + 1] * ld;
+    double* d = r + sh.toff[l] * ld;
     for (int i = 0; i < nin; i += 4) {
       const int n4 = nin - i < 4 ? nin - i : 4;
       double acc[4] = {0.0, 0.0, 0.0, 0.0};
       for (int o = 0; o < nout; ++o) {
-        const double dno = dn[o];
+        const double dno = dn[o * ld];
 #pragma unroll
         for (int k = 0; k < 4; ++k)
           if (k < n4) acc[k] = __dadd_rn(acc[k], __dmul_rn(wn[o * nin + i + k], dno));
       }
 #pragma unroll
       for (int k = 0; k < 4; ++k)
-        if (k < n4) d[i + k] = act[i + k] > 0.0 ? acc[k] : 0.0;
+        if (k < n4) d[(i + k) * ld] = act[(i + k) * ld] > 0.0 ? acc[k] : 0.0;
     }
   }
   // scale in place: t = inv_n * delta (the left factor of mlp.cpp:113,117)
-  const int nd = sh.e2 - sh.toff[0];
-  for (int j = 0; j < nd; ++j) r[sh.toff[0] + j] = __dmul_rn(inv_n, r[sh.toff[0] + j]);
+  for (int j = sh.toff[0]; j < sh.e2; ++j) r[j * ld] = __dmul_rn(inv_n, r[j * ld]);
 }
 
-// Sequential sum over samples of t[s] * a[s] (or t[s] alone when ap is null), in sample
-// order, with the shared-memory loads of batch b+1 issued before the DADD chain of
-// batch b so only the 8-cycle DADD latency is exposed.
-// Two alternating register buffers (A, B) of U samples each: while one batch's DADD
-// chain runs, the other batch's loads are in flight; no register copies.
+// Sequential sum over samples 0..N-1 of t[s] * a[s] (or t[s] alone), in sample order.
+// Rows are contiguous and 16-B aligned: each 128-bit load brings two samples; two
+// alternating register buffers of U pairs keep the loads of the next batch in flight
+// while the DADD chain of the current one runs.
 template <int U, bool kMul>
 __device__ __forceinline__ double chain_sum_impl(const double* __restrict__ tp,
-                                                 const double* __restrict__ ap, int N, int R) {
+                                                 const double* __restrict__ ap, int N) {
+  const double2* t2 = reinterpret_cast<const double2*>(tp);
+  const double2* a2 = reinterpret_cast<const double2*>(ap);
+  const int npairs = N / 2;
   double g = 0.0;
-  double ta[U], xa[U], tb[U], xb[U];
-  auto load = [&](int s0, double* t, double* x) {
+  double2 ta[U], xa[U], tb[U], xb[U];
+  auto load = [&](int j0, double2* t, double2* x) {
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      t[u] = tp[(s0 + u) * R];
-      if (kMul) x[u] = ap[(s0 + u) * R];
+      t[u] = t2[j0 + u];
+      if (kMul) x[u] = a2[j0 + u];
     }
   };
-  auto consume = [&](const double* t, const double* x) {
+  auto consume = [&](const double2* t, const double2* x) {
 #pragma unroll
-    for (int u = 0; u < U; ++u) g = __dadd_rn(g, kMul ? __dmul_rn(t[u], x[u]) : t[u]);
+    for (int u = 0; u < U; ++u) {
+      g = __dadd_rn(g, kMul ? __dmul_rn(t[u].x, x[u].x) : t[u].x);
+      g = __dadd_rn(g, kMul ? __dmul_rn(t[u].y, x[u].y) : t[u].y);
+    }
   };
-  int s = 0;
-  if (N >= U) load(0, ta, xa);
-  for (; s + 2 * U <= N; s += 2 * U) {
-    load(s + U, tb, xb);
+  int j = 0;
+  if (npairs >= U) load(0, ta, xa);
+  for (; j + 2 * U <= npairs; j += 2 * U) {
+    load(j + U, tb, xb);
     consume(ta, xa);
-    if (s + 3 * U <= N) load(s + 2 * U, ta, xa);
+    if (j + 3 * U <= npairs) load(j + 2 * U, ta, xa);
     consume(tb, xb);
   }
-  if (s + U <= N) {
+  if (j + U <= npairs) {
     consume(ta, xa);
-    s += U;
+    j += U;
   }
-  for (; s < N; ++s) g = __dadd_rn(g, kMul ? __dmul_rn(tp[s * R], ap[s * R]) : tp[s * R]);
+  for (int s = 2 * j; s < N; ++s) g = __dadd_rn(g, kMul ? __dmul_rn(tp[s], ap[s]) : tp[s]);
   return g;
-}
-
-template <int U>
-__device__ __forceinline__ double chain_sum(const double* __restrict__ tp, const double* __restrict__ ap,
-                                            int N, int R) {
-  return ap ? chain_sum_impl<U, true>(tp, ap, N, R) : chain_sum_impl<U, false>(tp, nullptr, N, R);
 }
 
 template <int KB, int I, int H1, int H2, bool SMEM>
@@ -276,17 +282,17 @@ __global__ void __launch_bounds__(256) train_fp64_exact(TrainArgs a) {
   const double lr = a.lr[m];
   const Shape sh = make_shape(a.tile_inputs[tile], a.h1[m], a.h2[m]);
   const int P = sh.P;
-  const int R = kFixed ? F::R : sh.R;
+  const int ld = rec_ld(N);
   const int tid = threadIdx.x, nt = blockDim.x;
 
   double* w = smem;           // [P]
   double* mom = w + P;        // [P] Adam m
   double* vel = mom + P;      // [P] Adam v
   double* Ls = vel + P;       // [1] epoch loss
-  // SMEM: records follow the model state in shared memory (a pointer the compiler can
-  // prove is shared, so every record access is an LDS/STS); else per-model global scratch
+  // SMEM: the record matrix follows the model state in shared memory, 16-B aligned (a
+  // pointer the compiler can prove is shared: every access is an LDS/STS); else global scratch
   double* rec;
-  if constexpr (SMEM) rec = Ls + 2;
+  if constexpr (SMEM) rec = smem + ((3 * P + 2 + 1) & ~1);
   else rec = a.scratch + a.scratch_offset[m];
 
   const double* gp = a.params + a.param_offset[m];
@@ -298,12 +304,12 @@ __global__ void __launch_bounds__(256) train_fp64_exact(TrainArgs a) {
   const double* X = a.X + a.tile_offset[tile] * 8;
   const double* Y = a.y + a.tile_offset[tile];
   for (int s = tid; s < N; s += nt) {
-    for (int i = 0; i < 7; ++i) rec[(size_t)s * R + i] = X[(size_t)s * 8 + i];
-    rec[(size_t)s * R + 7] = Y[s];  // inputs use slots 0..I-1 (I <= 7): slot 7 holds the target
-    rec[(size_t)s * R + R - 1] = 1.0;  // padding slot: bias terms are t * 1.0 (exact)
+    for (int i = 0; i < 7; ++i) rec[i * ld + s] = X[(size_t)s * 8 + i];
+    rec[7 * ld + s] = Y[s];        // inputs use rows 0..I-1 (I <= 7): row 7 holds the target
+    rec[sh.ones * ld + s] = 1.0;   // bias terms are t * 1.0 (exact)
   }
 
-  // phase-B ownership: parameter p -> (record offset of its delta, of its input or -1)
+  // phase-B ownership: parameter p -> (record row of its delta, of its input or of 1.0)
   int tix[KB], aix[KB];
 #pragma unroll
   for (int k = 0; k < KB; ++k) {
@@ -319,12 +325,12 @@ __global__ void __launch_bounds__(256) train_fp64_exact(TrainArgs a) {
           aix[k] = sh.inoff[l] + q % in;
         } else if (p >= sh.boff[l] && p < sh.boff[l] + out) {
           tix[k] = sh.toff[l] + (p - sh.boff[l]);
-          aix[k] = sh.R - 1;  // x 1.0: every lane of a warp runs the same multiply-add chain
+          aix[k] = sh.ones;  // x 1.0: every lane of a warp runs the same multiply-add chain
         }
       }
     }
   }
-  const int e2off = sh.e2;
+  const int e2row = sh.e2;
   const int loss_tid = nt - 1;
   const double inv_n = 1.0 / (double)N;  // mlp.cpp:84
   const double beta1 = 0.9, beta2 = 0.999, eps = 1e-8;
@@ -341,9 +347,8 @@ __global__ void __launch_bounds__(256) train_fp64_exact(TrainArgs a) {
     const double2 bc = a.bias_corr[e];  // issued early: its latency hides behind phase A
     // ---- phase A: per-sample forward / backward (mlp.cpp:86-104) ----
     for (int s = tid; s < N; s += nt) {
-      double* r = rec + (size_t)s * R;
-      if constexpr (kFixed) F::sample(w, r, r[7], inv_n);  // y cached in record slot 7
-      else sample_generic(sh, w, r, Y[s], inv_n);
+      if constexpr (kFixed) F::sample(w, rec + s, ld, inv_n);
+      else sample_generic(sh, w, rec + s, ld, inv_n);
     }
     __syncthreads();
     const long long clk1 = prof ? clock64() : 0;
@@ -355,18 +360,14 @@ __global__ void __launch_bounds__(256) train_fp64_exact(TrainArgs a) {
     long long clk2 = 0;
     if (tix[0] >= 0) {
       if (KB == 1) {
-        g[0] = chain_sum<8>(rec + tix[0], aix[0] >= 0 ? rec + aix[0] : nullptr, N, R);
+        g[0] = chain_sum_impl<4, true>(rec + tix[0] * ld, rec + aix[0] * ld, N);
         if (prof) clk2 = clock64();
       } else {
         for (int s = 0; s < N; ++s) {
-          const double* r = rec + (size_t)s * R;
 #pragma unroll
-          for (int k = 0; k < KB; ++k) {
-            if (tix[k] >= 0) {
-              const double t = r[tix[k]];
-              g[k] = __dadd_rn(g[k], aix[k] >= 0 ? __dmul_rn(t, r[aix[k]]) : t);
-            }
-          }
+          for (int k = 0; k < KB; ++k)
+            if (tix[k] >= 0)
+              g[k] = __dadd_rn(g[k], __dmul_rn(rec[tix[k] * ld + s], rec[aix[k] * ld + s]));
         }
       }
 #pragma unroll
@@ -384,7 +385,7 @@ __global__ void __launch_bounds__(256) train_fp64_exact(TrainArgs a) {
       }
     }
     if (tid == loss_tid) {
-      double L = chain_sum<8>(rec + e2off, nullptr, N, R);
+      double L = chain_sum_impl<4, false>(rec + e2row * ld, nullptr, N);
       L = __dmul_rn(L, inv_n);  // mlp.cpp:120
       Ls[0] = L;
       if (trace && (e % a.trace_stride) == 0) trace[e / a.trace_stride] = L;
@@ -417,10 +418,12 @@ __global__ void __launch_bounds__(256) train_fp64_exact(TrainArgs a) {
 
 }  // namespace
 
-int fp64_record_doubles(int in, int h1, int h2) {
+// doubles of record matrix per model (rows x padded samples) and of model state
+size_t fp64_record_bytes(int in, int h1, int h2, int n) {
   (void)in;
-  return rec_stride(h1, h2);
+  return size_t(rec_rows(h1, h2)) * size_t(rec_ld(n)) * 8;
 }
+size_t fp64_state_bytes(int p) { return size_t((3 * p + 2 + 1) & ~1) * 8; }
 
 bool fp64_shape_compiled(int in, int h1, int h2) {
   if (h1 == 8 && h2 == 0) return in >= 1 && in <= 7;
@@ -428,9 +431,9 @@ bool fp64_shape_compiled(int in, int h1, int h2) {
   return false;
 }
 
-// Dynamic shared memory = (3P + 2) doubles of model state, plus the per-sample
-// records when a.smem_records is set; the host sizes dyn_bytes for the largest model.
-// shape = {I, H1, H2} when every model of the launch has that compiled shape, else {0,0,0}.
+// Dynamic shared memory = model state (3P + 2 doubles, padded even), plus the record
+// matrix when a.smem_records is set; the host sizes dyn_bytes for the largest model.
+// shape = {I, H1, H2} when every model of the launch has that compiled shape, else null.
 void launch_train_fp64(const TrainArgs& a, int max_p, int dyn_bytes, const int* shape,
                        cudaStream_t s) {
   const int block = 256;

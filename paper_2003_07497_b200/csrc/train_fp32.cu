@@ -19,11 +19,12 @@
 //    prediction nets with hidden units paired on the packed FP32 FMA (FFMA2).
 //  * train_fp32_cta_kernel<W> — FEW models (the 48-combo population): one model
 //    per CTA of W warps so the per-epoch LATENCY is minimised; threads own
-//    samples; gradients are reduced inside each warp by a register-only
-//    recursive-halving reduce-scatter (shuffles; a shared-memory transpose
-//    variant is kept for comparison) and then across warps through shared
-//    memory; owner threads apply Adam; new weights are broadcast back through
-//    shared memory (two __syncthreads per epoch).
+//    samples (two per thread, interleaved in one basic block); gradients are
+//    reduced inside each warp by a register-only recursive-halving reduce-scatter
+//    without power-of-two padding (LeanRS; a shared-memory transpose variant is
+//    kept for comparison) and then across warps through shared memory; owner
+//    threads apply Adam; new weights are broadcast back through shared memory
+//    (two __syncthreads per epoch).
 // In both, the tile (N rows x 8 floats, target y in column 7) is staged ONCE into
 // shared memory by a TMA bulk copy (cp.async.bulk + mbarrier) and re-read from
 // there every epoch, so HBM traffic per model-epoch is ~0.
@@ -101,7 +102,7 @@ struct Net {
 // and err^2 into loss. scale = 2/N folds the 1/N of the mean and the 2 of d(err^2).
 template <int I, int H1, int H2>
 __device__ __forceinline__ void accumulate_sample(const float* w, const float* xv, float* gr,
-                                                  float& loss, float scale) {
+                                                  float& loss, float scale, bool valid = true) {
   using N = Net<I, H1, H2>;
   float z1[H1];
 #pragma unroll
@@ -137,7 +138,7 @@ __device__ __forceinline__ void accumulate_sample(const float* w, const float* x
     }
     out = acc0 + acc1;
   }
-  const float err = out - xv[7];
+  const float err = valid ? out - xv[7] : 0.f;
   loss = fmaf(err, err, loss);
   const float d = err * scale;
   if constexpr (H2 > 0) {
@@ -474,13 +475,56 @@ __global__ void __launch_bounds__(32) train_fp32_h8_kernel(TrainF32Args a) {
 }
 
 // ---------------------------------------------------------------------------------
+// Lean warp reduce-scatter of N values per lane (no power-of-two padding): at offset O
+// every lane keeps ceil(n/2) values (the lower half if its O-bit is clear, else the
+// upper half, zero-padded when n is odd), sends the other half to lane ^ O and adds what
+// it receives. 72 values take 36+18+9+5+3 = 71 shuffles (93 with padding to 96).
+// rs_map() gives the span of the original vector lane L finally holds: elements
+// base + k for k < valid.
+template <int N, int O>
+struct LeanRS {
+  static constexpr int H = (N + 1) / 2;
+  template <int M>
+  __device__ __forceinline__ static void run(float (&v)[M], int lane) {
+    const bool up = (lane & O) != 0;
+#pragma unroll
+    for (int j = 0; j < H; ++j) {
+      const float lo = v[j];
+      const float hi = (H + j < N) ? v[(H + j < N) ? H + j : 0] : 0.f;
+      const float send = up ? lo : hi;
+      const float keep = up ? hi : lo;
+      v[j] = keep + __shfl_xor_sync(0xffffffffu, send, O);
+    }
+    if constexpr (O > 1) LeanRS<H, O / 2>::run(v, lane);
+  }
+};
+__host__ __device__ constexpr int lean_rs_final(int n) {
+  for (int o = 16; o >= 1; o >>= 1) n = (n + 1) / 2;
+  return n;
+}
+__device__ __forceinline__ void lean_rs_map(int n, int lane, int& base, int& valid) {
+  base = 0;
+  valid = n;
+  for (int o = 16; o >= 1; o >>= 1) {
+    const int h = (n + 1) / 2;
+    if (lane & o) {
+      base += h;
+      valid = valid > h ? valid - h : 0;
+    } else {
+      valid = valid < h ? valid : h;
+    }
+    n = h;
+  }
+}
+
+// ---------------------------------------------------------------------------------
 template <int P>
 struct CtaLayout {
   static constexpr int PT = (P + 3) & ~3;  // transpose row stride (float4 writes, 4-wavefront STS.128)
 };
 
-template <int I, int H1, int H2, int W, bool kShuffleReduce>
-__global__ void __launch_bounds__(32 * W) train_fp32_cta_kernel(TrainF32Args a) {
+template <int I, int H1, int H2, int W, bool kShuffleReduce, bool kPair>
+__global__ void __launch_bounds__(32 * W, 1) train_fp32_cta_kernel(TrainF32Args a) {
   constexpr int P = Net<I, H1, H2>::P;
   constexpr int PT = CtaLayout<P>::PT;
   constexpr int T = 32 * W;
@@ -512,6 +556,8 @@ __global__ void __launch_bounds__(32 * W) train_fp32_cta_kernel(TrainF32Args a) 
   double* trace = a.loss_trace ? a.loss_trace + a.trace_offset[m] : nullptr;
   int bad = -1;
   float last = 0.f;
+  int rs_base, rs_valid;
+  lean_rs_map(P + 1, lane, rs_base, rs_valid);
   mbar_wait(&bar, 0);
   __syncthreads();
 
@@ -532,36 +578,35 @@ __global__ void __launch_bounds__(32 * W) train_fp32_cta_kernel(TrainF32Args a) 
 #pragma unroll
     for (int p = 0; p < PT; ++p) gr[p] = 0.f;
     float loss = 0.f;
-    for (int s = tid; s < rows; s += T) {
-      float xv[8];
-      load_row(trow, s, xv);
-      accumulate_sample<I, H1, H2>(w, xv, gr, loss, scale);
+    if constexpr (kPair) {
+      // two samples per thread in one basic block: independent chains interleave
+      for (int s0 = tid; s0 < rows; s0 += 2 * T) {
+        const int s1 = s0 + T;
+        float xa[8], xb[8];
+        load_row(trow, s0, xa);
+        load_row(trow, s1 < rows ? s1 : s0, xb);
+        accumulate_sample<I, H1, H2>(w, xa, gr, loss, scale);
+        accumulate_sample<I, H1, H2>(w, xb, gr, loss, scale, s1 < rows);
+      }
+    } else {
+      for (int s = tid; s < rows; s += T) {
+        float xv[8];
+        load_row(trow, s, xv);
+        accumulate_sample<I, H1, H2>(w, xv, gr, loss, scale);
+      }
     }
     const long long clk1 = prof ? clock64() : 0;
     if constexpr (kShuffleReduce) {
-      // level 1: recursive-halving reduce-scatter in registers — at offset o each lane
-      // keeps one half of its vector, sends the other to lane ^ o and adds what it gets;
-      // after 5 levels lane L holds the warp sums of elements 3L..3L+2 (loss = element P)
-      constexpr int PR = 32 * ((P + 1 + 31) / 32);
-      float v[PR];
+      // level 1: lean recursive-halving reduce-scatter in registers (LeanRS): lane L ends
+      // with the warp sums of elements rs_base .. rs_base + rs_valid - 1 (loss = element P)
+      float v[P + 1];
 #pragma unroll
-      for (int p = 0; p < PR; ++p) v[p] = p < P ? gr[p] : (p == P ? loss : 0.f);
+      for (int p = 0; p < P; ++p) v[p] = gr[p];
+      v[P] = loss;
+      LeanRS<P + 1, 16>::run(v, lane);
 #pragma unroll
-      for (int o = 16, n = PR / 2; o >= 1; o >>= 1, n >>= 1) {
-        const bool up = (lane & o) != 0;
-#pragma unroll
-        for (int j = 0; j < n; ++j) {
-          const float send = up ? v[j] : v[j + n];
-          const float keep = up ? v[j + n] : v[j];
-          v[j] = keep + __shfl_xor_sync(0xffffffffu, send, o);
-        }
-      }
-      constexpr int PER = PR / 32;
-#pragma unroll
-      for (int k = 0; k < PER; ++k) {
-        const int p = PER * lane + k;
-        if (p <= P) part[warp][p] = v[k];
-      }
+      for (int k = 0; k < lean_rs_final(P + 1); ++k)
+        if (k < rs_valid) part[warp][rs_base + k] = v[k];
     } else {
       // level 1: warp transpose-sum through shared memory (lane j -> params j, j+32, ...)
       float* myrow = tbuf + lane * PT;
@@ -638,14 +683,21 @@ __global__ void __launch_bounds__(32 * W) train_fp32_cta_kernel(TrainF32Args a) 
 template <int I, int H1, int H2, int W>
 void launch_cta(const TrainF32Args& a, int tile_bytes, cudaStream_t s) {
   constexpr int P = Net<I, H1, H2>::P;
-  static const bool shuffle = std::getenv("LANN_CTA_SMEM_REDUCE") == nullptr;
-  if (shuffle) {
-    auto kern = train_fp32_cta_kernel<I, H1, H2, W, true>;
+  const char* pe = std::getenv("LANN_CTA_PAIR");
+  const bool pair = pe == nullptr || pe[0] != '0';
+  if (std::getenv("LANN_CTA_SMEM_REDUCE") == nullptr) {
     const int dyn = tile_bytes;
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
-    kern<<<a.n_groups, 32 * W, dyn, s>>>(a);
+    if (pair) {
+      auto kern = train_fp32_cta_kernel<I, H1, H2, W, true, true>;
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
+      kern<<<a.n_groups, 32 * W, dyn, s>>>(a);
+    } else {
+      auto kern = train_fp32_cta_kernel<I, H1, H2, W, true, false>;
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
+      kern<<<a.n_groups, 32 * W, dyn, s>>>(a);
+    }
   } else {
-    auto kern = train_fp32_cta_kernel<I, H1, H2, W, false>;
+    auto kern = train_fp32_cta_kernel<I, H1, H2, W, false, false>;
     const int dyn = tile_bytes + W * 32 * CtaLayout<P>::PT * 4;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
     kern<<<a.n_groups, 32 * W, dyn, s>>>(a);

@@ -119,3 +119,39 @@ def test_fp32_population_status_and_metrics(engine):
     st, res, _, _ = engine.run_population(jobs, abi.FP32)
     assert st == 0
     assert all(r.status == 0 and r.n_kept == 175 and 0.0 < r.mape_thr < 100.0 and r.rho > 0.0 for r in res)
+
+
+@pytest.mark.parametrize("I", [4, 5, 6])
+@pytest.mark.parametrize("n", [100, 129, 250, 700])
+def test_fp32_cta_kernel_two_hidden_trace_prefix(engine, oracle, I, n):
+    """The CTA-per-model kernel (two interleaved samples per thread, lean reduce-scatter) on
+    the two-hidden-layer nets, every compiled input width and on row counts below one
+    pass, odd, the config-2 size and above two passes: loss trace within 1e-4 relative of the
+    exact reference over the first 25 epochs (its pre-divergence prefix at every size)."""
+    rng = np.random.default_rng(100 + 7 * I + n)
+    X = rng.uniform(0, 1, (n, I))
+    y = rng.uniform(0, 1, n)
+    dims = [I, 5, 5, 1]
+    p0 = E.init_params(dims, 9 + I)
+    m = [{"tile": 0, "h1": 5, "h2": 5, "lr": 1e-2, "epochs": 25, "params": p0}]
+    params, final, bad, traces = engine.train([X], [y], m, abi.FP32, trace=True)
+    Xp = np.zeros((n, 8))
+    Xp[:, :I] = X
+    st, p_exp, t_exp, _ = oracle.train_full_batch(dims, p0, Xp, y, 1e-2, 25)
+    rel = np.abs(traces[0] - t_exp) / t_exp
+    assert rel.max() <= 1e-4, rel.max()
+    assert np.max(np.abs(params[0] - p_exp)) <= 1e-3
+
+
+def test_fp32_cta_kernel_paired_matches_single(engine, monkeypatch):
+    """Config-2 population: the CTA kernel with two interleaved samples per thread (default)
+    and with one sample per loop trip (LANN_CTA_PAIR=0) reach the same accuracy."""
+    jobs = P.config2_jobs(root_seed=2, epochs_scale=0.25)
+    st, fast, _, _ = engine.run_population(jobs, abi.FP32)
+    assert st == 0, engine.last_error
+    monkeypatch.setenv("LANN_CTA_PAIR", "0")
+    st, gen, _, _ = engine.run_population(jobs, abi.FP32)
+    assert st == 0, engine.last_error
+    a = np.array([r.mape_thr for r in fast])
+    b = np.array([r.mape_thr for r in gen])
+    assert abs(np.median(a) - np.median(b)) <= 1.0, (a, b)

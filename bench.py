@@ -256,8 +256,10 @@ def main():
         "wall_s_timed_region": wall_s, "failed_models": len(bad),
         "median_thr_mape": float(np.median([r.mape_thr for r in results])),
     }
-    if rank == 0 and not args.no_extras:
-        line["extras"] = extras(E, eng, precision)
+    if not args.no_extras:
+        ex = extras(E, eng, rank, world, barrier, max_over_ranks)
+        if rank == 0:
+            line["extras"] = ex
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
         secs, kind, cbad = cpu_reference_run(jobs, threads)
@@ -274,68 +276,123 @@ def main():
     return 0
 
 
-def extras(E, eng, precision):
-    """Secondary measurements (one pass each): FP64 parity-mode throughput on config 2,
-    the config-3 seed x fold sweep share of one GPU, config-4 variant-selection scoring."""
+def extras(E, eng, rank, world, barrier, max_over_ranks):
+    """Secondary measurements (one pass each, every rank participates where the work shards):
+    FP64 parity-mode throughput on config 2; config 5 (the same 48 combinations as plain FFNNs,
+    family nn, next to the LANNs); the config-3 seed x fold sweep SHARDED over the ranks
+    (strong scaling: 61,440 models in total, cost-balanced contiguous slices, no collective);
+    config-4 variant selection with the candidate range split over the ranks."""
+    from paper_2003_07497_b200 import sharding
     out = {}
     jobs = popmod.config2_jobs(root_seed=1)
+    if rank == 0:
+        try:
+            p64 = eng.prepare(jobs, abi.FP64_EXACT)
+            p64.run(1)
+            p64.run(1)
+            ms = eng.last_device_ms
+            out["config2_fp64_exact"] = {"value": popmod.model_epochs(jobs) / (ms / 1e3), "unit": "model-epochs/s",
+                                         "ms_per_step": ms, "dtype": "f64",
+                                         "note": "bit-identical to the reference trainer (tests/test_gpu_parity.py)"}
+            p64.close()
+        except Exception as ex:  # noqa: BLE001
+            out["config2_fp64_exact"] = {"error": str(ex)}
+        try:
+            out["config5_lann_vs_ffnn"] = lann_vs_ffnn(eng)
+        except Exception as ex:  # noqa: BLE001
+            out["config5_lann_vs_ffnn"] = {"error": str(ex)}
     try:
-        p64 = eng.prepare(jobs, abi.FP64_EXACT)
-        p64.run(1)
-        p64.run(1)
-        ms = eng.last_device_ms
-        out["config2_fp64_exact"] = {"value": popmod.model_epochs(jobs) / (ms / 1e3), "unit": "model-epochs/s",
-                                     "ms_per_step": ms, "dtype": "f64",
-                                     "note": "bit-identical to the reference trainer (tests/test_gpu_parity.py)"}
-        p64.close()
-    except Exception as ex:  # noqa: BLE001
-        out["config2_fp64_exact"] = {"error": str(ex)}
-    try:
-        sweep = popmod.config3_jobs(root_seed=1, n_seeds=int(os.environ.get("LANN_SWEEP_SEEDS", 256)))
+        n_seeds = int(os.environ.get("LANN_SWEEP_SEEDS", 256))
+        sweep = popmod.config3_jobs(root_seed=1, n_seeds=n_seeds)
+        mine, offset = sharding.shard(sweep, rank, world)
         t0 = time.perf_counter()
-        ps = eng.prepare(sweep, abi.FP32)
+        ps = eng.prepare(mine, abi.FP32)
         prep_s = time.perf_counter() - t0
+        ps.run(1)  # warm-up (module load, first-touch)
+        barrier()
         ps.run(1)
-        ms = eng.last_device_ms
+        ms = max_over_ranks(eng.last_device_ms)
         tms = eng.last_train_ms
+        tflops = ps.flop / (tms / 1e3) / 1e12
+        st, res, _, _ = ps.fetch()
+        merged = sharding.gather_results(res, rank, world)
         me = popmod.model_epochs(sweep)
-        out["config3_sweep_fp32"] = {"models": len(sweep), "model_epochs": me,
+        thr = np.array([r[3] for r in merged]) if world > 1 else np.array([r.mape_thr for r in merged])
+        out["config3_sweep_fp32"] = {"models": len(sweep), "model_epochs": me, "n_gpus": world, "scaling": "strong",
                                      "value": me / (ms / 1e3), "unit": "model-epochs/s", "ms": ms,
-                                     "train_tflops": ps.flop / (tms / 1e3) / 1e12, "host_prepare_s": prep_s,
-                                     "note": "48 combos x seeds x 5 folds on ONE GPU (the 8-GPU config shards this list)"}
+                                     "rank0_models": len(mine), "rank0_train_tflops": tflops,
+                                     "rank0_host_prepare_s": prep_s,
+                                     "median_fold_thr_mape": float(np.median(thr)),
+                                     "note": f"48 combos x {n_seeds} seeds x 5 folds; contiguous cost-balanced "
+                                             "shards, one per rank, no data-path collective; max-over-ranks device time"}
         ps.close()
     except Exception as ex:  # noqa: BLE001
         out["config3_sweep_fp32"] = {"error": str(ex)}
     try:
-        out["config4_selection"] = selection_extra(E, eng)
+        out["config4_selection"] = selection_extra(E, eng, rank, world, barrier, max_over_ranks)
     except Exception as ex:  # noqa: BLE001
         out["config4_selection"] = {"error": str(ex)}
     return out
 
 
-def selection_extra(E, eng, n_cands=10_000_000):
+def lann_vs_ffnn(eng):
+    """Config 5: the config-2 population trained as LANNs (family nnc, complexity input) and as
+    plain FFNNs (family nn, same worlds and seeds, no complexity input): device throughput of
+    each and the accuracy gap (median held-out thresholded MAPE)."""
+    row = {}
+    for name, fam in (("lann_nnc", abi.NNC), ("ffnn_nn", abi.NN)):
+        jobs = popmod.config2_jobs(root_seed=1, family=fam)
+        p = eng.prepare(jobs, abi.FP32)
+        p.run(1)
+        p.run(1)
+        ms = eng.last_device_ms
+        st, res, _, _ = p.fetch()
+        p.close()
+        pred = [r.mape_thr for r, j in zip(res, jobs) if j.world.kind != abi.BLUR]
+        row[name] = {"value": popmod.model_epochs(jobs) / (ms / 1e3), "unit": "model-epochs/s", "ms": ms,
+                     "median_thr_mape_all": float(np.median([r.mape_thr for r in res])),
+                     "median_thr_mape_prediction_nets": float(np.median(pred)),
+                     "failed": int(sum(1 for r in res if r.status))}
+    row["thr_mape_gap_pp"] = row["ffnn_nn"]["median_thr_mape_all"] - row["lann_nnc"]["median_thr_mape_all"]
+    return row
+
+
+def selection_extra(E, eng, rank, world, barrier, max_over_ranks, n_cands=10_000_000):
     """Config 4: per kernel kind, n_cands counter-generated candidate shapes scored by its
-    10 variant-hardware prediction models from the config-2 population, argmin per candidate."""
+    10 variant-hardware prediction models from the config-2 population, argmin per candidate;
+    each rank scores a contiguous 1/world of the candidate range (candidate i is generated from
+    derive_seed(seed, i), so the split changes nothing)."""
     jobs = popmod.config2_jobs(root_seed=1)
     pop = eng.prepare(jobs, abi.FP32)
     pop.run(1)
     st, res, params, _ = pop.fetch(want_params=True)
     norms = pop.norms()
     pop.close()
-    total_pred, total_ms, kern_ms = 0, 0.0, 0.0
+    lo = n_cands * rank // world
+    hi = n_cands * (rank + 1) // world
+    per_kind = []
     for kind in (abi.MM, abi.MV, abi.MC, abi.MP):
         idx = [i for i, j in enumerate(jobs) if j.world.kind == kind]
         models = [{"inputs": res[i].n_inputs, "h1": 8, "h2": 0, "log_target": 0, "params": params[i],
                    "norm": norms[i]} for i in idx]
         thd = [1 if jobs[i].world.hw_class == abi.HW_CPU else 0 for i in idx]
-        eng.select_variants(models, thd, kind, 16, 7, 0, n_cands, precision=abi.FP32)
+        per_kind.append((kind, models, thd))
+    eng.select_variants(per_kind[0][1], per_kind[0][2], per_kind[0][0], 16, 7, lo, min(hi - lo, 1 << 16),
+                        precision=abi.FP32)  # warm-up
+    barrier()
+    total_pred, total_ms, kern_ms = 0, 0.0, 0.0
+    for kind, models, thd in per_kind:
+        eng.select_variants(models, thd, kind, 16, 7, lo, hi - lo, precision=abi.FP32)
         total_ms += eng.last_device_ms
         kern_ms += eng.last_train_ms
         total_pred += n_cands * len(models)
+    kern_ms = max_over_ranks(kern_ms)
+    total_ms = max_over_ranks(total_ms)
     flop_pred = 2 * 7 * 8 + 2 * 8 + 2 * 7 + 2  # SURVEY 8(d): 144 for MM nnc
-    return {"candidates_per_kind": n_cands, "models_per_kind": 10, "predictions": total_pred,
-            "value": total_pred / (kern_ms / 1e3), "unit": "predictions/s", "kernel_ms": kern_ms,
-            "call_ms_incl_d2h": total_ms, "approx_tflops": total_pred * flop_pred / (kern_ms / 1e3) / 1e12}
+    return {"candidates_per_kind": n_cands, "models_per_kind": 10, "predictions": total_pred, "n_gpus": world,
+            "scaling": "strong", "value": total_pred / (kern_ms / 1e3), "unit": "predictions/s",
+            "kernel_ms": kern_ms, "call_ms_incl_d2h": total_ms,
+            "approx_tflops": total_pred * flop_pred / (kern_ms / 1e3) / 1e12}
 
 
 if __name__ == "__main__":

@@ -214,6 +214,13 @@ int lann_build_dataset(const lann_world* world, uint64_t seed, int32_t count,
                        double* feats, uint64_t* c, double* runtime, int32_t* n_features);
 int lann_split_order(int32_t n, uint64_t seed, int64_t* order);
 
+/* The synthetic world's runtime probe at GIVEN blur schedules (the stand-in for
+ * datagen::measure of the tiled blur kernel in perfsage.cpp cmd_select:297-316):
+ * instance blur(image_n, sched[i]) with n_thd = world.max_threads, noise drawn from
+ * Rng(derive_seed(seed, 0x9015E)) one draw per schedule in order. sched [n][4]. */
+int lann_probe_schedules(const lann_world* world, uint64_t seed, uint32_t image_n, int32_t n,
+                         const uint32_t* sched, double* runtime);
+
 /* Glorot-uniform init (Mlp::init, mlp.cpp:9-25) with Rng(derive_seed(seed, 0xA11CE)). */
 int lann_init_params(int32_t n_dims, const int32_t* dims, uint64_t seed, double* params);
 

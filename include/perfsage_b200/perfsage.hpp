@@ -11,13 +11,21 @@
 //   mlp.hpp         DenseLayer, Mlp
 //   eval.hpp        mape, mape_thresholded, spearman, average_ranks, make_report
 //   selector.hpp    enumerate_candidates, select(ScheduleScorer...), select(TrainedModel, n, cands)
+//   features.hpp    feature_names, kind_from_feature_names
+//   csv.cpp         datagen::save_csv / load_csv (same columns, %.17g doubles)
+//   model_io.hpp    models::save_model / load_model (same "perfsage-model" v1 JSON document)
+//   eval.hpp        aggregate, write_reports_csv, print_reports, print_aggregate
 // plus the batched overloads the engine exists for: models::train_population and
-// models::predict_population. Every compute call runs on the GPU through the C ABI
+// models::predict_population, and datagen::build_synthetic (a dataset from one of the
+// engine's synthetic runtime worlds, the generator the population runs use). Every compute call runs on the GPU through the C ABI
 // (include/lann_engine.h); there is no CPU fallback. Link: -lperfsage_b200.
 #pragma once
 
 #include <cstdint>
 #include <functional>
+#include <iosfwd>
+#include <optional>
+#include <utility>
 #include <span>
 #include <stdexcept>
 #include <string>
@@ -43,6 +51,7 @@ class TrainingError : public Error {
  private:
   int epoch_;
 };
+class LoadError : public Error { public: using Error::Error; };  // errors.hpp:49-52
 class BuildAbortError : public Error {
  public:
   BuildAbortError(const std::string& msg, std::size_t completed) : Error(msg), completed_(completed) {}
@@ -65,6 +74,7 @@ void set_device(int device);
 namespace kernels {
 enum class KernelKind { MM, MV, MC, MP, Blur };
 std::string to_string(KernelKind kind);
+KernelKind kind_from_string(const std::string& s);  // kernels.cpp (ParamError on unknown)
 
 struct ScheduleCandidate {
   std::uint32_t s1 = 8, s2 = 256, s3 = 128, s4 = 8;
@@ -109,6 +119,19 @@ struct Dataset {
 
 /// Disjoint, exhaustive, seeded-shuffle partition (datagen.cpp:225-248).
 std::pair<Dataset, Dataset> split(const Dataset& dataset, double train_fraction, std::uint64_t seed);
+
+/// csv.cpp:43-102: header kernel,variant,<features...>,c,runtime_s; doubles as %.17g, LF
+/// line endings; LoadError on a bad header, field count, number, negative c or runtime <= 0.
+void save_csv(const Dataset& dataset, const std::string& path);
+Dataset load_csv(const std::string& path);
+
+/// The engine's synthetic dataset generator (lann_build_dataset): `count` samples of
+/// datagen::sample_params draws from Rng(derive_seed(seed, 0)) probed by the closed-form
+/// runtime world `world_index` of the 48 default combinations (0 = the acceptance world,
+/// acceptance_main.cpp:271-279). variant_id names the combination (combo_variant_id).
+Dataset build_synthetic(int world_index, std::size_t count, std::uint64_t seed);
+int synthetic_world_count();
+std::string combo_variant_id(int world_index);
 }  // namespace datagen
 
 // ---- mlp.hpp / models.hpp ----------------------------------------------------------------------
@@ -128,6 +151,11 @@ struct Mlp {
 
 enum class ModelFamily { NnC, Nn, Const, LrC, NlrC };
 std::string to_string(ModelFamily family);
+ModelFamily family_from_string(const std::string& s);  // models.cpp (ParamError on unknown)
+
+/// features.cpp:10-21 / 59-72
+std::vector<std::string> feature_names(kernels::KernelKind kind, bool with_n_thd);
+std::pair<kernels::KernelKind, bool> kind_from_feature_names(const std::vector<std::string>& names);
 bool family_augmented(ModelFamily family);
 
 struct ModelConfig {
@@ -185,6 +213,12 @@ std::vector<std::vector<double>> predict_population(const std::vector<const Trai
                                                     const std::vector<const datagen::Dataset*>& data);
 int param_count(const TrainedModel& model);
 std::vector<double> flatten_params(const Mlp& net);
+
+/// model_io.cpp:114-173: the "perfsage-model" version-1 JSON document (config, schema,
+/// norm_stats, payload.layers[rows, cols, weights, biases], metrics.loss_trace); doubles are
+/// written with 17 significant digits, so save -> load is bit-exact. LoadError on bad files.
+void save_model(const TrainedModel& model, const std::string& path);
+TrainedModel load_model(const std::string& path);
 }  // namespace models
 
 // ---- eval.hpp:13-49 ------------------------------------------------------------------------------
@@ -204,6 +238,18 @@ struct EvalReport {
 };
 EvalReport make_report(std::span<const double> truth, std::span<const double> pred,
                        double drop_fraction = 0.3);
+
+/// eval.cpp:110-197: per-group means (std::map key order) + an "overall" row.
+enum class GroupBy { Kernel, Variant, ModelFamily };
+struct AggregateRow {
+  std::string group;
+  double mape_full = 0.0, mape_thresholded = 0.0, rho = 0.0;
+  std::size_t reports = 0;
+};
+std::vector<AggregateRow> aggregate(const std::vector<EvalReport>& reports, GroupBy group_by);
+void write_reports_csv(std::ostream& os, const std::vector<EvalReport>& reports);
+void print_reports(std::ostream& os, const std::vector<EvalReport>& reports);
+void print_aggregate(std::ostream& os, const std::vector<AggregateRow>& rows);
 }  // namespace eval
 
 // ---- selector.hpp:21-36 --------------------------------------------------------------------------
@@ -217,6 +263,26 @@ ScheduleCandidate select(const ScheduleScorer& scorer, const std::vector<Schedul
 /// selector.cpp:42-53 — all candidates scored and reduced on the GPU.
 ScheduleCandidate select(const models::TrainedModel& model, std::uint32_t image_n,
                          const std::vector<ScheduleCandidate>& candidates);
+
+/// selector.hpp:37-62 / selector.cpp:55-140: regret and speedups of a chosen schedule
+/// against measured runtimes (true best: lowest runtime, ties to the smaller schedule).
+struct SelectionReport {
+  ScheduleCandidate chosen;
+  double predicted_s = 0.0, measured_s = 0.0;
+  ScheduleCandidate true_best;
+  double true_best_s = 0.0;
+  ScheduleCandidate default_schedule;
+  double default_s = 0.0;
+  double regret = 0.0;                  // measured_s / true_best_s
+  double speedup_vs_default = 0.0;      // default_s / measured_s
+  double speedup_vs_random_mean = 0.0;  // mean candidate runtime / measured_s
+  std::string to_json() const;
+  std::string summary() const;
+};
+using MeasuredCandidates = std::vector<std::pair<ScheduleCandidate, double>>;
+SelectionReport evaluate_selection(const ScheduleCandidate& chosen, const MeasuredCandidates& measured,
+                                   const ScheduleCandidate& default_schedule,
+                                   std::optional<double> default_runtime_s, double predicted_s);
 }  // namespace selector
 
 }  // namespace perfsage

@@ -12,6 +12,8 @@
 //   models::mse_gradient / Mlp::init (mlp.cpp:9-122)
 //   eval::mape / mape_thresholded / spearman (eval.cpp:26-90)
 //   selector::select / enumerate_candidates (selector.cpp:13-53)
+//   datagen::save_csv / load_csv (csv.cpp), models::save_model / load_model (model_io.cpp),
+//   and the body of the CLI's train command (tools/perfsage.cpp:250-278)
 #include <algorithm>
 #include <atomic>
 #include <bit>
@@ -471,6 +473,99 @@ double ref_run_population(int n_jobs, const lann_job* jobs, lann_job_result* res
     worker();
     for (auto& t : pool) t.join();
     return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+// ---- on-disk formats and the CLI train pipeline (csv.cpp, model_io.cpp, perfsage.cpp) ----
+
+// build_dataset with the world probe, every sample's variant_id set, then datagen::save_csv
+int ref_save_dataset_csv(const lann_world* w, std::uint64_t seed, int count, const char* variant_id,
+                         const char* path) {
+    try {
+        auto ds = make_dataset(*w, seed, count);
+        for (auto& smp : ds.samples) smp.variant_id = variant_id;
+        datagen::save_csv(ds, path);
+        return 0;
+    } catch (const std::exception& e) {
+        return status_of(e);
+    }
+}
+
+int ref_csv_roundtrip(const char* in, const char* out) {
+    try {
+        datagen::save_csv(datagen::load_csv(in), out);
+        return 0;
+    } catch (const std::exception& e) {
+        return status_of(e);
+    }
+}
+
+int ref_model_roundtrip(const char* in, const char* out) {
+    try {
+        models::save_model(models::load_model(in), out);
+        return 0;
+    } catch (const std::exception& e) {
+        return status_of(e);
+    }
+}
+
+// load_model -> [f_min.., f_max.., t_min, t_max, flat params.., loss_trace..]; returns count
+int ref_model_dump(const char* path, double* out, int cap) {
+    try {
+        const auto m = models::load_model(path);
+        std::vector<double> v(m.norm.f_min.begin(), m.norm.f_min.end());
+        v.insert(v.end(), m.norm.f_max.begin(), m.norm.f_max.end());
+        v.push_back(m.norm.t_min);
+        v.push_back(m.norm.t_max);
+        const auto flat = models::flatten_params(std::get<models::Mlp>(m.payload));
+        v.insert(v.end(), flat.begin(), flat.end());
+        v.insert(v.end(), m.loss_trace.begin(), m.loss_trace.end());
+        if (int(v.size()) > cap) return -1;
+        std::copy(v.begin(), v.end(), out);
+        return int(v.size());
+    } catch (const std::exception& e) {
+        status_of(e);
+        return -1;
+    }
+}
+
+// perfsage.cpp cmd_train (:250-278) minus the manifest: load_csv -> split(derive_seed(seed,
+// 0x5b11)) -> default_config(kind, family) with seed (+ epochs override) -> train_model ->
+// save_model / save_csv x2
+int ref_cli_train(const char* csv, std::uint64_t seed, const char* family, int epochs,
+                  const char* model_out, const char* train_out, const char* test_out) {
+    try {
+        const auto fam = models::family_from_string(family);
+        const auto ds = datagen::load_csv(csv);
+        const auto [tr, te] = datagen::split(ds, 0.5, derive_seed(seed, 0x5b11));
+        auto cfg = models::default_config(ds.kind, fam, false);
+        cfg.family = fam;
+        cfg.seed = seed;
+        if (epochs > 0) cfg.epochs = epochs;
+        const auto model = models::train_model(tr, cfg);
+        models::save_model(model, model_out);
+        datagen::save_csv(tr, train_out);
+        datagen::save_csv(te, test_out);
+        return 0;
+    } catch (const std::exception& e) {
+        return status_of(e);
+    }
+}
+
+// perfsage.cpp evaluate_model_on (:98-108): out = {mape_full, mape_thr, rho, n_kept}
+int ref_eval_model(const char* model_path, const char* csv, double drop, double* out) {
+    try {
+        const auto m = models::load_model(model_path);
+        const auto data = datagen::load_csv(csv);
+        const auto pred = models::predict_dataset(m, data);
+        const auto rep = eval::make_report(data.runtimes(), pred, drop);
+        out[0] = rep.mape_full;
+        out[1] = rep.mape_thresholded;
+        out[2] = rep.rho;
+        out[3] = double(rep.n_kept);
+        return 0;
+    } catch (const std::exception& e) {
+        return status_of(e);
+    }
 }
 
 }  // extern "C"

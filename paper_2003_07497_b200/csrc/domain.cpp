@@ -192,6 +192,26 @@ Status build_dataset(const lann_world& w, std::uint64_t seed, int count, Dataset
   return {};
 }
 
+Status probe_schedules(const lann_world& w, std::uint64_t seed, std::uint32_t image_n, int n,
+                       const std::uint32_t* sched, double* runtime) {
+  if (w.kind != LANN_BLUR) return {LANN_PARAM_ERROR, "schedule probes need a blur world"};
+  if (n < 0 || image_n == 0) return {LANN_PARAM_ERROR, "bad probe request"};
+  SeqRng noise(derive_seed(seed, 0x9015E));
+  for (int i = 0; i < n; ++i) {
+    Instance p;
+    p.kind = LANN_BLUR;
+    p.n = image_n;
+    p.n_thd = w.max_threads;
+    for (int j = 0; j < 4; ++j) {
+      p.sched[j] = sched[4 * i + j];
+      if (p.sched[j] == 0 || (p.sched[j] & (p.sched[j] - 1)) != 0)
+        return {LANN_PARAM_ERROR, "schedule factors must be positive powers of two"};
+    }
+    runtime[i] = world_runtime(w, p, noise);
+  }
+  return {};
+}
+
 Status split_order(int n, double frac, std::uint64_t seed, std::vector<std::int64_t>& order,
                    int& n_train) {
   if (!(frac > 0.0 && frac < 1.0)) return {LANN_PARAM_ERROR, "train fraction must lie in (0,1)"};

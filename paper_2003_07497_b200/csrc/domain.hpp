@@ -112,5 +112,7 @@ const std::vector<double>& adam_bias_table(int epochs);
 
 // The 48 kernel-variant-hardware combinations (config 2); see DESIGN.md.
 std::vector<lann_world> default_combos();
+Status probe_schedules(const lann_world& w, std::uint64_t seed, std::uint32_t image_n, int n,
+                       const std::uint32_t* sched, double* runtime);
 
 }  // namespace lann

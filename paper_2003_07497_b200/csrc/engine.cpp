@@ -1025,6 +1025,12 @@ int lann_build_dataset(const lann_world* w, uint64_t seed, int32_t count, double
   return LANN_OK;
 }
 
+int lann_probe_schedules(const lann_world* w, uint64_t seed, uint32_t image_n, int32_t n,
+                         const uint32_t* sched, double* runtime) {
+  if (!w || (n > 0 && (!sched || !runtime))) return LANN_PARAM_ERROR;
+  return probe_schedules(*w, seed, image_n, n, sched, runtime).code;
+}
+
 int lann_split_order(int32_t n, uint64_t seed, int64_t* order) {
   std::vector<int64_t> o;
   int ntr = 0;

@@ -181,6 +181,37 @@ class Reference(_Lib):
         L.ref_select_schedule.argtypes = [C.c_int, C.c_int, _i32p, _dp, _dp, C.c_int, C.c_uint32, C.c_int, _u32p, C.POINTER(C.c_int64), C.POINTER(C.c_double)]
         L.ref_run_population.argtypes = [C.c_int, C.POINTER(Job), C.POINTER(JobResult), C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int]
         L.ref_run_population.restype = C.c_double
+        L.ref_save_dataset_csv.argtypes = [C.POINTER(World), C.c_uint64, C.c_int, C.c_char_p, C.c_char_p]
+        L.ref_csv_roundtrip.argtypes = [C.c_char_p, C.c_char_p]
+        L.ref_model_roundtrip.argtypes = [C.c_char_p, C.c_char_p]
+        L.ref_model_dump.argtypes = [C.c_char_p, _dp, C.c_int]
+        L.ref_cli_train.argtypes = [C.c_char_p, C.c_uint64, C.c_char_p, C.c_int, C.c_char_p, C.c_char_p, C.c_char_p]
+        L.ref_eval_model.argtypes = [C.c_char_p, C.c_char_p, C.c_double, _dp]
+
+    # ---- on-disk formats (csv.cpp, model_io.cpp) and the CLI train body (perfsage.cpp) ----
+    def save_dataset_csv(self, world, seed, count, variant_id, path):
+        return self.lib.ref_save_dataset_csv(C.byref(world), seed, count, variant_id.encode(), str(path).encode())
+
+    def csv_roundtrip(self, src, dst):
+        return self.lib.ref_csv_roundtrip(str(src).encode(), str(dst).encode())
+
+    def model_roundtrip(self, src, dst):
+        return self.lib.ref_model_roundtrip(str(src).encode(), str(dst).encode())
+
+    def model_dump(self, path):
+        out = np.zeros(1 << 20)
+        n = self.lib.ref_model_dump(str(path).encode(), out, len(out))
+        assert n >= 0, self.last_error()
+        return out[:n]
+
+    def cli_train(self, csv, seed, family, epochs, model_out, train_out, test_out):
+        return self.lib.ref_cli_train(str(csv).encode(), seed, family.encode(), epochs, str(model_out).encode(),
+                                      str(train_out).encode(), str(test_out).encode())
+
+    def eval_model(self, model, csv, drop=0.3):
+        out = np.zeros(4)
+        st = self.lib.ref_eval_model(str(model).encode(), str(csv).encode(), drop, out)
+        return st, out
 
     def last_error(self):
         return self.lib.ref_last_error().decode()

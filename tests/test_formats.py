@@ -1,0 +1,166 @@
+"""CPU: the on-disk formats and the `perfsage gen` caller, against the
+reference's own writers and readers.
+
+* datagen::save_csv / load_csv (csv.cpp:43-102): `perfsage gen` writes byte-for-byte the CSV the
+  reference writes for the same dataset; CSV round trips are byte-identical in both directions.
+* models::save_model / load_model (model_io.cpp:114-173): every double (norm stats, weights, loss
+  trace) survives engine -> reference -> engine and reference -> engine -> reference bit for bit.
+* LoadError behaviour on malformed files mirrors csv.cpp / model_io.cpp.
+Pinned by fixtures written by the reference itself (tests/golden/make_formats_golden.py), and
+cross-checked live against oracle/_ref/libperfsage_ref.so where it was built.
+"""
+import hashlib
+import json
+import os
+import subprocess
+
+import pytest
+
+from paper_2003_07497_b200 import abi
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+GOLD = os.path.join(ROOT, "tests", "golden")
+CLI = os.path.join(ROOT, "paper_2003_07497_b200", "bin", "perfsage")
+LIB = os.path.join(ROOT, "paper_2003_07497_b200", "lib")
+
+
+def sha_file(path):
+    with open(path, "rb") as f:
+        return hashlib.sha256(f.read()).hexdigest()
+
+
+@pytest.fixture(scope="module")
+def fmt():
+    return json.load(open(os.path.join(GOLD, "formats_r01.json")))
+
+
+@pytest.fixture(scope="module")
+def tool(tmp_path_factory):
+    exe = str(tmp_path_factory.mktemp("fmt") / "formats_tool")
+    subprocess.run(["g++", "-std=c++20", "-O2", "-I", os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "tests", "cpp", "formats_tool.cpp"), "-L", LIB, "-lperfsage_b200",
+                    f"-Wl,-rpath,{LIB}", "-o", exe], check=True)
+    return exe
+
+
+def run(*args):
+    out = subprocess.run(list(args), capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stdout + out.stderr
+    return out.stdout
+
+
+def dump_hex(tool, path):
+    return [float.fromhex(x).hex() for x in run(tool, "model-dump", str(path)).split()]
+
+
+def test_gen_csv_is_the_reference_csv(tmp_path, fmt):
+    """`perfsage gen --world 0 --seed 1 --count 500` == the reference's build_dataset + save_csv
+    of the acceptance world, byte for byte (sha256 of the reference-written fixture)."""
+    run(CLI, "gen", "--world", "0", "--count", "500", "--seed", "1", "--out", str(tmp_path))
+    ours = tmp_path / "dataset_mm_dense_threaded_cpu4.csv"
+    assert sha_file(ours) == fmt["csv_sha256"]
+    man = json.load(open(tmp_path / "manifest.json"))
+    assert man["runs"][0]["command"] == "gen" and man["runs"][0]["seed"] == 1
+    assert man["runs"][0]["outputs"] == [str(ours)]
+
+
+@pytest.mark.parametrize("world", [3, 12, 27, 40, 46])
+def test_gen_csv_matches_live_reference(tmp_path, reference, world):
+    """Every kind of world (GPU-class without n_thd, MV, MP, both blur lattices): our CSV bytes ==
+    the reference's save_csv of its own build_dataset with the same probe."""
+    from paper_2003_07497_b200 import engine as E
+
+    run(CLI, "gen", "--world", str(world), "--count", "64", "--seed", "5", "--out", str(tmp_path))
+    (ours,) = [p for p in tmp_path.iterdir() if p.suffix == ".csv"]
+    vid = open(ours).read().split("\n")[1].split(",")[1]
+    ref = tmp_path / "ref.csv"
+    assert reference.save_dataset_csv(E.default_combos()[world], 5, 64, vid, ref) == 0, reference.last_error()
+    assert open(ours, "rb").read() == open(ref, "rb").read()
+
+
+def test_csv_round_trips_are_byte_identical(tmp_path, tool, reference):
+    src = os.path.join(GOLD, "ref_dataset_w0_s1.csv")
+    run(tool, "csv-roundtrip", src, str(tmp_path / "ours.csv"))
+    assert open(tmp_path / "ours.csv", "rb").read() == open(src, "rb").read()
+    assert reference.csv_roundtrip(tmp_path / "ours.csv", tmp_path / "back.csv") == 0
+    assert open(tmp_path / "back.csv", "rb").read() == open(src, "rb").read()
+
+
+def test_reference_model_file_loads_bit_exact(tmp_path, tool, fmt):
+    """The reference-written model (nlohmann formatting) loads here with every double identical to
+    the reference's own load_model; re-saving and re-loading changes nothing."""
+    src = os.path.join(GOLD, fmt["model"])
+    assert dump_hex(tool, src) == fmt["model_dump_hex"]
+    run(tool, "model-roundtrip", src, str(tmp_path / "m.json"))
+    assert dump_hex(tool, tmp_path / "m.json") == fmt["model_dump_hex"]
+
+
+def test_model_round_trip_through_the_reference(tmp_path, tool, reference):
+    """Awkward doubles (subnormals, -0, DBL_MAX, 0.1, a u64 seed of 2^64-1) written by the engine
+    load bit-exact in the reference, and the reference's re-save loads bit-exact here."""
+    ours = tmp_path / "synth.json"
+    run(tool, "model-synth", str(ours), "17")
+    mine = dump_hex(tool, ours)
+    assert [float(x).hex() for x in reference.model_dump(ours)] == mine
+    back = tmp_path / "back.json"
+    assert reference.model_roundtrip(ours, back) == 0, reference.last_error()
+    assert dump_hex(tool, back) == mine
+    assert json.load(open(back))["config"]["seed"] == 2**64 - 1
+
+
+def test_csv_load_errors(tmp_path, tool):
+    """csv.cpp:62-100: LoadError for a bad header, unknown schema, wrong field count, bad numbers,
+    a kernel column that disagrees with the schema, negative c, runtime <= 0."""
+    head = "kernel,variant,m,n,k,d1,d2,n_thd,c,runtime_s\n"
+    good = "mm,v,1,2,3,1,1,1,6,0.5\n"
+    cases = {
+        "header": "kernel,variant,c\n",
+        "schema": "kernel,variant,a,b,c,runtime_s\nmm,v,1,2,3,0.5\n",
+        "fields": head + "mm,v,1,2,3,1,1,1,6\n",
+        "number": head + "mm,v,1,x,3,1,1,1,6,0.5\n",
+        "kernel": head + "mv,v,1,2,3,1,1,1,6,0.5\n",
+        "neg_c": head + "mm,v,1,2,3,1,1,1,-6,0.5\n",
+        "runtime": head + "mm,v,1,2,3,1,1,1,6,0\n",
+    }
+    for name, text in cases.items():
+        p = tmp_path / f"{name}.csv"
+        p.write_text(text)
+        assert run(tool, "csv-load", str(p)).startswith("LoadError"), name
+    p = tmp_path / "ok.csv"
+    p.write_text(head + good + "\r\n" + good.replace("\n", "\r\n"))
+    assert run(tool, "csv-load", str(p)).strip() == "ok 2"
+
+
+def test_model_load_errors(tmp_path, tool, fmt):
+    src = json.load(open(os.path.join(GOLD, fmt["model"])))
+    bad = {
+        "not_json": "{",
+        "format": json.dumps({**src, "format": "other"}),
+        "version": json.dumps({**src, "version": 2}),
+        "missing": json.dumps({k: v for k, v in src.items() if k != "norm_stats"}),
+        "shape": json.dumps({**src, "payload": {"layers": [{"rows": 2, "cols": 2, "weights": [1.0], "biases": [0.0, 0.0]}]}}),
+        "family": json.dumps({**src, "config": {**src["config"], "family": "svm"}}),
+    }
+    for name, text in bad.items():
+        p = tmp_path / f"{name}.json"
+        p.write_text(text)
+        assert run(tool, "model-load", str(p)).startswith("LoadError"), name
+
+
+def test_cli_gpu_commands_fail_loudly_without_a_device(tmp_path):
+    """No CPU fallback: on a machine without a GPU the training commands exit 1 with an error."""
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    out = subprocess.run([CLI, "train", "--data", os.path.join(GOLD, "ref_dataset_w0_s1.csv"), "--out",
+                          str(tmp_path)], capture_output=True, text=True)
+    assert out.returncode == 1 and "no CUDA device" in out.stderr
+
+
+def test_cli_argument_errors(tmp_path):
+    for args in (["frobnicate"], ["gen", "--world"], ["gen", "--count", "x"], ["gen", "--world", "99"],
+                 ["sweep", "--family", "svm"]):
+        out = subprocess.run([CLI, *args, "--out", str(tmp_path)] if len(args) > 1 else [CLI, *args],
+                             capture_output=True, text=True)
+        assert out.returncode == 1 and out.stderr.startswith("error:"), args

@@ -1,0 +1,155 @@
+"""GPU: the `perfsage` command-line caller end to end on the engine.
+
+* train (FP64 exact) on the reference-written dataset reproduces the REFERENCE CLI's outputs: the
+  model file's norm stats, weights and full loss trace bit for bit, and byte-identical
+  train.csv / test.csv (fixtures from tests/golden/make_formats_golden.py).
+* eval of that model on test.csv == the reference's evaluate_model_on report.
+* compare trains both NN families in one batched call; its nnc row == train + eval.
+* select (blur schedules) and select-variants (config 4) produce consistent choices.
+* sweep (config 3 / 5 driver) rows == the C oracle's run of the same jobs (FP64 exact).
+"""
+import csv
+import json
+import os
+import subprocess
+
+import numpy as np
+import pytest
+
+from paper_2003_07497_b200 import abi
+from paper_2003_07497_b200 import engine as E
+from paper_2003_07497_b200.population import derive_seed
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+GOLD = os.path.join(ROOT, "tests", "golden")
+CLI = os.path.join(ROOT, "paper_2003_07497_b200", "bin", "perfsage")
+FMT = json.load(open(os.path.join(GOLD, "formats_r01.json")))
+REF_CSV = os.path.join(GOLD, FMT["csv"])
+
+
+def cli(*args):
+    out = subprocess.run([CLI, *map(str, args)], capture_output=True, text=True, timeout=900)
+    assert out.returncode == 0, out.stdout + out.stderr
+    return out.stdout
+
+
+def model_hex(path):
+    m = json.load(open(path))
+    n = m["norm_stats"]
+    vals = n["f_min"] + n["f_max"] + [n["t_min"], n["t_max"]]
+    for layer in m["payload"]["layers"]:
+        vals += layer["weights"] + layer["biases"]
+    vals += m["metrics"]["loss_trace"]
+    return [float(v).hex() for v in vals]
+
+
+def sha(path):
+    import hashlib
+
+    return hashlib.sha256(open(path, "rb").read()).hexdigest()
+
+
+def read_reports(path):
+    with open(path) as f:
+        return list(csv.DictReader(f))
+
+
+@pytest.fixture(scope="module")
+def trained(tmp_path_factory):
+    out = tmp_path_factory.mktemp("train")
+    t = FMT["train"]
+    cli("train", "--data", REF_CSV, "--seed", t["seed"], "--epochs", t["epochs"], "--family", t["family"],
+        "--precision", "fp64", "--out", out)
+    return out
+
+
+def test_cli_train_reproduces_the_reference_cli(trained):
+    assert model_hex(trained / "model_nnc.json") == FMT["model_dump_hex"]
+    assert sha(trained / "train.csv") == FMT["train_csv_sha256"]
+    assert sha(trained / "test.csv") == FMT["test_csv_sha256"]
+    man = json.load(open(trained / "manifest.json"))
+    assert man["runs"][-1]["command"] == "train" and man["runs"][-1]["inputs"] == [REF_CSV]
+
+
+def test_cli_eval_matches_the_reference_report(trained, tmp_path):
+    cli("eval", "--model", trained / "model_nnc.json", "--data", trained / "test.csv", "--out", tmp_path,
+        "--group-by", "family")
+    (row,) = read_reports(tmp_path / "eval.csv")
+    ref = FMT["eval_test"]
+    assert float(row["mape_full"]) == ref["mape_full"]
+    assert float(row["mape_thresholded"]) == ref["mape_thresholded"]
+    assert float(row["rho"]) == ref["rho"]
+    assert int(row["n_kept"]) == ref["n_kept"] and int(row["n_total"]) == 250
+    assert row["kernel"] == "mm" and row["model_family"] == "nnc" and row["variant"] == "dense_threaded@cpu4"
+
+
+def test_cli_compare_batches_both_families(trained, tmp_path):
+    t = FMT["train"]
+    out = cli("compare", "--data", REF_CSV, "--seed", t["seed"], "--epochs", t["epochs"], "--precision", "fp64",
+              "--out", tmp_path)
+    rows = read_reports(tmp_path / "compare.csv")
+    assert [r["model_family"] for r in rows] == ["nnc", "nn"]
+    assert float(rows[0]["mape_thresholded"]) == FMT["eval_test"]["mape_thresholded"]
+    assert "best thresholded MAPE" in out
+
+
+def test_cli_select_blur_schedule(tmp_path):
+    out = cli("select", "--world", 40, "--n", 1024, "--candidates", 120, "--seed", 2, "--epochs", 400,
+              "--out", tmp_path)
+    rep = json.load(open(tmp_path / "selection.json"))
+    assert rep["regret"] >= 1.0 and rep["measured_s"] > 0 and rep["speedup_vs_default"] > 0
+    with open(tmp_path / "schedules.csv") as f:
+        rows = list(csv.DictReader(f))
+    sched = {(int(r["s1"]), int(r["s2"]), int(r["s3"]), int(r["s4"])): float(r["runtime_s"]) for r in rows}
+    ch = rep["chosen"]
+    key = (ch["s1"], ch["s2"], ch["s3"], ch["s4"])
+    assert sched[key] == rep["measured_s"]
+    assert min(sched.values()) == rep["true_best_s"]
+    assert "chosen schedule" in out
+    # the measured table fed back through --data reproduces the same model and choice
+    again = tmp_path / "again"
+    cli("select", "--data", tmp_path / "schedules.csv", "--n", 1024, "--seed", 2, "--epochs", 400, "--out", again)
+    assert json.load(open(again / "selection.json")) == rep
+
+
+def test_cli_sweep_matches_the_oracle(tmp_path, oracle):
+    """Two combinations x 2 seeds x 5 folds, FP64 exact, 2% of the default epochs: every sweep.csv
+    row equals the C oracle's run of the identical job."""
+    cli("sweep", "--combos", "0,40", "--seeds", 2, "--folds", 5, "--epochs-scale", 0.02, "--precision", "fp64",
+        "--root-seed", 1, "--out", tmp_path)
+    with open(tmp_path / "sweep.csv") as f:
+        rows = list(csv.DictReader(f))
+    assert len(rows) == 2 * 2 * 5
+    worlds = E.default_combos()
+    for r in rows:
+        combo, s, fold = int(r["combo"]), int(r["seed_index"]), int(r["fold"])
+        w = worlds[combo]
+        ds = derive_seed(1, combo)
+        blur = w.kind == abi.BLUR
+        job = abi.make_job(w, ds, n_folds=5, fold=fold, hidden=(5, 5) if blur else (8,), lr=1e-2,
+                           epochs=int((20000 if blur else 8000) * 0.02), log_target=blur,
+                           init_seed=derive_seed(ds, 1 + s))
+        ref, _, _ = oracle.run_job(job)
+        assert int(r["status"]) == ref.status == 0
+        assert float(r["final_loss"]) == ref.final_loss
+        assert float(r["mape_thresholded"]) == ref.mape_thr
+        assert float(r["rho"]) == ref.rho
+
+
+def test_cli_select_variants(tmp_path):
+    """Config 4 through the CLI: two MM variant models (worlds 0 and 5: dense / sparse on the
+    same host) score 200k counter-generated shapes; every candidate gets exactly one winner."""
+    for w in (0, 5):
+        d = tmp_path / f"w{w}"
+        cli("gen", "--world", w, "--count", 500, "--seed", 1, "--out", d)
+        (data,) = [p for p in d.iterdir() if p.suffix == ".csv"]
+        cli("train", "--data", data, "--seed", 1, "--epochs", 500, "--precision", "fp32", "--out", d)
+    out = cli("select-variants", "--model", tmp_path / "w0" / "model_nnc.json", "--model",
+              tmp_path / "w5" / "model_nnc.json", "--candidates", 200000, "--max-threads", 4,
+              "--precision", "fp32", "--out", tmp_path)
+    with open(tmp_path / "variants.csv") as f:
+        rows = list(csv.DictReader(f))
+    assert sum(int(r["chosen"]) for r in rows) == 200000
+    assert "predictions/s" in out

@@ -116,7 +116,7 @@ def test_cli_select_blur_schedule(tmp_path):
 
 def test_cli_sweep_matches_the_oracle(tmp_path, oracle):
     """Two combinations x 2 seeds x 5 folds, FP64 exact, 2% of the default epochs: every sweep.csv
-    row equals the C oracle's run of the identical job."""
+    row equals the C oracle's run of the identical job (training bit-exact; blur metrics to 1e-12)."""
     cli("sweep", "--combos", "0,40", "--seeds", 2, "--folds", 5, "--epochs-scale", 0.02, "--precision", "fp64",
         "--root-seed", 1, "--out", tmp_path)
     with open(tmp_path / "sweep.csv") as f:
@@ -134,8 +134,12 @@ def test_cli_sweep_matches_the_oracle(tmp_path, oracle):
         ref, _, _ = oracle.run_job(job)
         assert int(r["status"]) == ref.status == 0
         assert float(r["final_loss"]) == ref.final_loss
-        assert float(r["mape_thresholded"]) == ref.mape_thr
-        assert float(r["rho"]) == ref.rho
+        if blur:  # log-target predictions go through CUDA exp (<= 1 ulp from glibc): DESIGN.md 4
+            assert float(r["mape_thresholded"]) == pytest.approx(ref.mape_thr, rel=1e-12)
+            assert float(r["rho"]) == pytest.approx(ref.rho, rel=1e-12)
+        else:
+            assert float(r["mape_thresholded"]) == ref.mape_thr
+            assert float(r["rho"]) == ref.rho
 
 
 def test_cli_select_variants(tmp_path):

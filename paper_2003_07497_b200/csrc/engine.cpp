@@ -10,6 +10,9 @@
 #include <algorithm>
 #include <atomic>
 #include <chrono>
+#include <condition_variable>
+#include <functional>
+#include <mutex>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -466,17 +469,70 @@ struct Population {
   double train_flop = 0.0;  // algorithmic FLOP of one training pass
 };
 
+// Persistent host worker pool for the per-population preparation (datasets, tiles, init):
+// spawning threads per call cost ~1-2 ms of the end-to-end path. Workers live for the process
+// (detached, never joined); one parallel_for runs at a time.
+class HostPool {
+ public:
+  static HostPool& get() {
+    static HostPool* pool = new HostPool();
+    return *pool;
+  }
+  void run(int n, const std::function<void(int)>& fn) {
+    if (n <= 0) return;
+    std::lock_guard<std::mutex> one(call_);
+    if (n == 1 || workers_ == 0) {
+      for (int i = 0; i < n; ++i) fn(i);
+      return;
+    }
+    {
+      std::lock_guard<std::mutex> lk(m_);
+      fn_ = &fn;
+      n_ = n;
+      next_.store(0);
+      active_ = workers_;
+      ++gen_;
+    }
+    cv_.notify_all();
+    drain();
+    std::unique_lock<std::mutex> lk(m_);
+    done_.wait(lk, [&] { return active_ == 0; });
+    fn_ = nullptr;
+  }
+
+ private:
+  HostPool() {
+    workers_ = int(std::max(1u, std::min(32u, std::thread::hardware_concurrency()))) - 1;
+    for (int t = 0; t < workers_; ++t) std::thread([this] { loop(); }).detach();
+  }
+  void drain() {
+    for (int i; (i = next_.fetch_add(1)) < n_;) (*fn_)(i);
+  }
+  void loop() {
+    std::uint64_t seen = 0;
+    for (;;) {
+      {
+        std::unique_lock<std::mutex> lk(m_);
+        cv_.wait(lk, [&] { return gen_ != seen; });
+        seen = gen_;
+      }
+      drain();
+      std::lock_guard<std::mutex> lk(m_);
+      if (--active_ == 0) done_.notify_one();
+    }
+  }
+  std::mutex call_, m_;
+  std::condition_variable cv_, done_;
+  const std::function<void(int)>* fn_ = nullptr;
+  std::atomic<int> next_{0};
+  int n_ = 0, workers_ = 0, active_ = 0;
+  std::uint64_t gen_ = 0;
+};
+
 template <class F>
 void parallel_for(int n, F&& fn) {
-  const int nthreads = int(std::max(1u, std::min(32u, std::thread::hardware_concurrency())));
-  std::atomic<int> next{0};
-  std::vector<std::thread> pool;
-  auto worker = [&] {
-    for (int i; (i = next.fetch_add(1)) < n;) fn(i);
-  };
-  for (int t = 1; t < std::min(nthreads, n); ++t) pool.emplace_back(worker);
-  worker();
-  for (auto& th : pool) th.join();
+  const std::function<void(int)> f = fn;
+  HostPool::get().run(n, f);
 }
 
 double flop_per_model_epoch(int I, int h1, int h2, int n) {
@@ -747,6 +803,14 @@ int lann_engine_create(int device, lann_engine** out) {
     for (auto& j : e->join) ck(cudaEventCreateWithFlags(&j, cudaEventDisableTiming), "event");
     ck(cudaDeviceGetAttribute(&e->max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, device), "attr");
     ck(cudaDeviceGetAttribute(&e->sms, cudaDevAttrMultiProcessorCount, device), "attr");
+    // keep freed stream-ordered allocations in the device pool: repeated population calls
+    // then reuse them instead of returning memory to the driver at every synchronisation
+    if (std::getenv("LANN_POOL_RELEASE") == nullptr) {
+      cudaMemPool_t pool;
+      ck(cudaDeviceGetDefaultMemPool(&pool, device), "mempool");
+      std::uint64_t keep = ~std::uint64_t(0);
+      ck(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep), "mempool attr");
+    }
   } catch (const CudaFail&) {
     delete e;
     return LANN_CUDA_ERROR;

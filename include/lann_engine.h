@@ -221,6 +221,25 @@ int lann_split_order(int32_t n, uint64_t seed, int64_t* order);
 int lann_probe_schedules(const lann_world* world, uint64_t seed, uint32_t image_n, int32_t n,
                          const uint32_t* sched, double* runtime);
 
+/* ---- real measurement on the B200 (datagen::measure, datagen.cpp:118-160; the paper's
+ * GPU-class variants, section IV-A) ----------------------------------------------------
+ * Times GPU kernel variant `variant` of kernel kind `kind` on every instance: feats
+ * [n][LANN_ROW] are the GPU-class base features (mm: m,n,k,d1,d2; mv: m,n,d; mc: m,n,r,d;
+ * mp: m,n,r,s,d; blur: n,s1,s2,s3,s4), operands are generated on the device from `seed`,
+ * `warmups` untimed runs then the median of `reps` CUDA-event-timed runs, in seconds.
+ * checksum (optional) = sum of the output elements (FP64) for verification. */
+int lann_measure(lann_engine* engine, int32_t kind, const char* variant, int32_t n, const double* feats,
+                 int32_t warmups, int32_t reps, uint64_t seed, double* runtime_s, double* checksum);
+int lann_measure_variant_count(int32_t kind);
+const char* lann_measure_variant_name(int32_t kind, int32_t idx);
+/* datagen::build_dataset with the measured probe: `count` instances drawn as sample_params
+ * (Rng(derive_seed(seed, 0)), GPU class: no n_thd; blur from the `blur_lattice` schedule
+ * space at side `blur_side`, 0 = the default sides), each measured by lann_measure. */
+int lann_build_measured_dataset(lann_engine* engine, int32_t kind, const char* variant,
+                                int32_t blur_lattice, int32_t blur_side, int32_t count, uint64_t seed,
+                                int32_t warmups, int32_t reps, double* feats, uint64_t* c,
+                                double* runtime, int32_t* n_features);
+
 /* Glorot-uniform init (Mlp::init, mlp.cpp:9-25) with Rng(derive_seed(seed, 0xA11CE)). */
 int lann_init_params(int32_t n_dims, const int32_t* dims, uint64_t seed, double* params);
 

@@ -52,6 +52,7 @@ class TrainingError : public Error {
   int epoch_;
 };
 class LoadError : public Error { public: using Error::Error; };  // errors.hpp:49-52
+class ExternalVariantError : public Error { public: using Error::Error; };  // errors.hpp
 class BuildAbortError : public Error {
  public:
   BuildAbortError(const std::string& msg, std::size_t completed) : Error(msg), completed_(completed) {}
@@ -130,6 +131,28 @@ Dataset load_csv(const std::string& path);
 /// runtime world `world_index` of the 48 default combinations (0 = the acceptance world,
 /// acceptance_main.cpp:271-279). variant_id names the combination (combo_variant_id).
 Dataset build_synthetic(int world_index, std::size_t count, std::uint64_t seed);
+
+/// datagen.hpp:44-51 / datagen.cpp:118-160: untimed warm-ups, then the median of `reps` runs.
+struct TimingPolicy {
+  int warmups = 1;
+  int reps = 5;
+};
+/// Real measurement on the B200 (lann_build_measured_dataset): `count` sample_params draws of
+/// the GPU-class space (no n_thd), each timed as B200 kernel variant `variant` (CUDA events,
+/// TimingPolicy median). Variants per kind: measured_variants(kind). variant_id = variant@b200.
+Dataset build_measured(kernels::KernelKind kind, const std::string& variant, std::size_t count,
+                       std::uint64_t seed, TimingPolicy policy = {}, bool gpu_lattice = true,
+                       std::uint32_t blur_side = 1024);
+std::vector<std::string> measured_variants(kernels::KernelKind kind);
+/// external.cpp:46-118: run `command` via /bin/sh, write the features as one line of %.17g
+/// values to its stdin, read one positive decimal runtime (seconds) from the first stdout line.
+/// Throws ExternalVariantError on spawn failure, non-zero exit or a malformed reply.
+double run_external_variant(const std::string& command, std::span<const double> features);
+/// datagen::build_dataset with an external variant as the probe (perfsage.cpp cmd_gen
+/// --external-cmd): sample_params draws (CPU class: n_thd in 1..max_threads, pinned to 1 for a
+/// GPU-class variant), features without c sent to the command.
+Dataset build_external(kernels::KernelKind kind, const std::string& command, const std::string& variant_id,
+                       bool gpu_class, int max_threads, std::size_t count, std::uint64_t seed);
 int synthetic_world_count();
 std::string combo_variant_id(int world_index);
 }  // namespace datagen

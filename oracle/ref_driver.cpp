@@ -551,6 +551,27 @@ int ref_cli_train(const char* csv, std::uint64_t seed, const char* family, int e
     }
 }
 
+// perfsage.cpp cmd_gen with --external-cmd (:197-248): an external variant as the probe,
+// datagen::build_dataset, every sample's variant_id set, save_csv
+int ref_save_external_csv(int kind, int gpu_class, int max_threads, const char* command, const char* variant_id,
+                          int count, std::uint64_t seed, const char* path) {
+    try {
+        kernels::VariantDescriptor ext;
+        ext.variant_id = variant_id;
+        ext.kind = kind_of(kind);
+        ext.impl = kernels::ImplKind::External;
+        ext.hw_class = gpu_class ? kernels::HardwareClass::Gpu : kernels::HardwareClass::Cpu;
+        ext.hardware_label = "external";
+        ext.launch_command = command;
+        auto space = datagen::ParamSpace::defaults(kind_of(kind), max_threads);
+        const auto ds = datagen::build_dataset(ext, space, std::size_t(count), seed, {});
+        datagen::save_csv(ds, path);
+        return 0;
+    } catch (const std::exception& e) {
+        return status_of(e);
+    }
+}
+
 // perfsage.cpp evaluate_model_on (:98-108): out = {mape_full, mape_thr, rho, n_kept}
 int ref_eval_model(const char* model_path, const char* csv, double drop, double* out) {
     try {

@@ -3,9 +3,13 @@
 // Mirrors the reference tool's subcommands, options, outputs and manifest
 // (/root/reference/proj/tools/perfsage.cpp:32-422) on top of the drop-in perfsage:: API and the
 // C ABI, with every training / prediction / metric / selection step on the GPU:
-//   gen      synthetic dataset of one runtime world -> dataset_<kernel>_<variant>.csv
-//            (the reference measures its CPU kernels here; measurement is out of scope, the
-//            engine's closed-form worlds stand in, lann_engine.h lann_world)
+//   gen      dataset -> dataset_<kernel>_<variant>.csv, from one of three probes:
+//            --measure --kernel K --variant V   real B200 kernel variants timed with CUDA events
+//                                               (measure.cu; `gen --list-variants`)
+//            --external-cmd CMD --kernel K      the reference's external black-box protocol
+//            --world W                          the engine's closed-form synthetic worlds
+//   measure-variant  serve the external protocol for a B200 variant (one feature line in ->
+//            one runtime out), so the reference's own `gen --external-cmd` can measure B200s
 //   train    CSV -> split(seed 0x5b11) -> train_model -> model_<family>.json, train.csv, test.csv
 //   eval     model JSON(s) x CSV -> eval.csv (+ --group-by aggregate)
 //   compare  CSV -> the NN families (nnc, nn) trained as ONE batched population -> compare.csv
@@ -87,7 +91,8 @@ struct Args {
   }
 };
 
-const std::vector<std::string> kFlags = {"unconstrained", "list", "help", "both-families"};
+const std::vector<std::string> kFlags = {"unconstrained", "list", "help", "both-families", "measure",
+                                         "gpu-class", "list-variants"};
 
 Args parse(int argc, char** argv) {
   Args a;
@@ -238,6 +243,40 @@ std::string sanitize(std::string s) {
 
 // ---- subcommands ---------------------------------------------------------------------------------
 int cmd_gen(const Args& a) {
+  if (a.has("list-variants")) {
+    std::cout << "kernel  B200 variant\n";
+    for (auto k : {kernels::KernelKind::MM, kernels::KernelKind::MV, kernels::KernelKind::MC, kernels::KernelKind::MP,
+                   kernels::KernelKind::Blur})
+      for (const auto& v : datagen::measured_variants(k))
+        std::cout << std::left << std::setw(8) << kernels::to_string(k) << v << "\n";
+    return 0;
+  }
+  if (a.has("measure") || a.has("external-cmd")) {
+    const auto kind = kernels::kind_from_string(a.get("kernel", "mm"));
+    const std::size_t count = std::size_t(a.integer("count", 500));
+    const std::uint64_t seed = a.u64("seed", 1);
+    const fs::path out = a.get("out", "perfsage_out");
+    datagen::Dataset ds;
+    std::string vid;
+    if (a.has("measure")) {
+      const std::string variant = a.get("variant", "");
+      if (variant.empty()) throw ParamError("--measure needs --variant (see gen --list-variants)");
+      const datagen::TimingPolicy pol{int(a.integer("warmups", 1)), int(a.integer("reps", 5))};
+      ds = datagen::build_measured(kind, variant, count, seed, pol, a.get("blur-space", "gpu") == "gpu",
+                                   std::uint32_t(a.integer("blur-side", 1024)));
+      vid = variant + "@b200";
+    } else {
+      vid = a.get("external-id", "external");
+      ds = datagen::build_external(kind, a.get("external-cmd", ""), vid, a.has("gpu-class"),
+                                   int(a.integer("max-threads", 4)), count, seed);
+    }
+    fs::create_directories(out);
+    const fs::path csv = out / ("dataset_" + kernels::to_string(kind) + "_" + sanitize(vid) + ".csv");
+    datagen::save_csv(ds, csv.string());
+    record_run(out, a, seed, {}, {csv.string()});
+    std::cout << "wrote " << ds.size() << " samples to " << csv.string() << "\n";
+    return 0;
+  }
   if (a.has("list")) {
     std::cout << "world  kernel  variant\n";
     for (int i = 0; i < datagen::synthetic_world_count(); ++i) {
@@ -646,6 +685,36 @@ int cmd_select_variants(const Args& a) {
   return 0;
 }
 
+// The reference's external-variant protocol (external.cpp:46-118) served by a B200 variant:
+// every stdin line of GPU-class features -> one line with the median runtime in seconds.
+int cmd_measure_variant(const Args& a) {
+  const auto kind = kernels::kind_from_string(a.get("kernel", "mm"));
+  const std::string variant = a.get("variant", "");
+  const int warmups = int(a.integer("warmups", 1)), reps = int(a.integer("reps", 5));
+  const std::uint64_t seed = a.u64("seed", 1);
+  lann_engine* e = nullptr;
+  if (lann_engine_create(int(a.integer("device", 0)), &e) != LANN_OK)
+    throw Error("no CUDA device: the LANN engine has no CPU fallback");
+  std::string line;
+  int st = 0;
+  while (std::getline(std::cin, line)) {
+    std::stringstream ss(line);
+    double f[LANN_ROW] = {0};
+    int n = 0;
+    for (double v; n < LANN_ROW && ss >> v;) f[n++] = v;
+    if (n == 0) continue;
+    double rt = 0.0;
+    st = lann_measure(e, int(kind), variant.c_str(), 1, f, warmups, reps, seed, &rt, nullptr);
+    if (st) break;
+    std::printf("%.17g\n", rt);
+    std::fflush(stdout);
+  }
+  const std::string err = st ? lann_last_error(e) : "";
+  lann_engine_destroy(e);
+  if (st) throw ParamError("measurement failed: " + err);
+  return 0;
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
@@ -658,6 +727,7 @@ int main(int argc, char** argv) {
     if (a.command == "select") return cmd_select(a);
     if (a.command == "sweep") return cmd_sweep(a);
     if (a.command == "select-variants") return cmd_select_variants(a);
+    if (a.command == "measure-variant") return cmd_measure_variant(a);
     throw ParamError("unknown subcommand '" + a.command + "'");
   } catch (const std::exception& ex) {
     std::cerr << "error: " << ex.what() << "\n";

@@ -1089,6 +1089,50 @@ int lann_build_dataset(const lann_world* w, uint64_t seed, int32_t count, double
   return LANN_OK;
 }
 
+int lann_measure(lann_engine* e, int32_t kind, const char* variant, int32_t n, const double* feats,
+                 int32_t warmups, int32_t reps, uint64_t seed, double* runtime_s, double* checksum) {
+  if (!e) return LANN_NO_DEVICE;
+  if (n < 0 || (n > 0 && (!feats || !runtime_s))) return set_err(e, {LANN_PARAM_ERROR, "bad measurement request"});
+  e->err.clear();
+  try {
+    ck(cudaSetDevice(e->device), "cudaSetDevice");
+    Timer timer(e);
+    const int st =
+        measure_instances(kind, variant, n, feats, warmups, reps, seed, runtime_s, checksum, e->stream, e->err);
+    timer.stop();
+    return st;
+  } catch (const CudaFail& f) {
+    e->err = f.what;
+    return LANN_CUDA_ERROR;
+  }
+}
+
+int lann_measure_variant_count(int32_t kind) { return measure_variant_count(kind); }
+const char* lann_measure_variant_name(int32_t kind, int32_t idx) { return measure_variant_name(kind, idx); }
+
+int lann_build_measured_dataset(lann_engine* e, int32_t kind, const char* variant, int32_t blur_lattice,
+                                int32_t blur_side, int32_t count, uint64_t seed, int32_t warmups, int32_t reps,
+                                double* feats, uint64_t* c, double* runtime, int32_t* n_features) {
+  if (!e) return LANN_NO_DEVICE;
+  if (count < 2 || kind < LANN_MM || kind > LANN_BLUR || !feats || !c || !runtime || !n_features)
+    return set_err(e, {LANN_PARAM_ERROR, "build_dataset needs count >= 2 and output buffers"});
+  // sample_params draws of the GPU-class parameter space (datagen.cpp:60-110, n_thd pinned)
+  SeqRng rng(derive_seed(seed, 0));
+  std::vector<double> f(size_t(count) * LANN_ROW, 0.0);
+  for (int i = 0; i < count; ++i) {
+    Instance p = sample_instance(kind, 1, blur_lattice, rng);
+    p.n_thd = 1;
+    if (kind == LANN_BLUR && blur_side > 0) p.n = uint32_t(blur_side);
+    base_features(p, false, &f[size_t(i) * LANN_ROW]);
+    c[i] = complexity(p);
+  }
+  const int st = lann_measure(e, kind, variant, count, f.data(), warmups, reps, seed, runtime, nullptr);
+  if (st) return st;
+  std::memcpy(feats, f.data(), f.size() * sizeof(double));
+  *n_features = base_feature_count(kind, false);
+  return LANN_OK;
+}
+
 int lann_probe_schedules(const lann_world* w, uint64_t seed, uint32_t image_n, int32_t n,
                          const uint32_t* sched, double* runtime) {
   if (!w || (n > 0 && (!sched || !runtime))) return LANN_PARAM_ERROR;

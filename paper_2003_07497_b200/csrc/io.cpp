@@ -20,6 +20,11 @@
 #include <memory>
 #include <ostream>
 #include <sstream>
+#include <csignal>
+#include <mutex>
+
+#include <sys/wait.h>
+#include <unistd.h>
 
 #include "../../include/lann_engine.h"
 #include "../../include/perfsage_b200/perfsage.hpp"
@@ -174,6 +179,126 @@ Dataset build_synthetic(int index, std::size_t count, std::uint64_t seed) {
     s.runtime_s = rt[i];
     s.variant_id = vid;
     ds.samples.push_back(std::move(s));
+  }
+  return ds;
+}
+
+std::vector<std::string> measured_variants(kernels::KernelKind kind) {
+  std::vector<std::string> out;
+  for (int i = 0; i < lann_measure_variant_count(int(kind)); ++i) out.emplace_back(lann_measure_variant_name(int(kind), i));
+  return out;
+}
+
+Dataset build_measured(kernels::KernelKind kind, const std::string& variant, std::size_t count, std::uint64_t seed,
+                       TimingPolicy policy, bool gpu_lattice, std::uint32_t blur_side) {
+  if (count < 2) throw ParamError("build_dataset needs count >= 2");
+  if (policy.reps < 1) throw ParamError("timing policy needs reps >= 1");
+  if (policy.warmups < 0) throw ParamError("timing policy needs warmups >= 0");
+  lann_engine* e = nullptr;
+  if (lann_engine_create(0, &e) != LANN_OK) throw Error("no CUDA device: the LANN engine has no CPU fallback");
+  std::vector<double> feats(count * LANN_ROW), rt(count);
+  std::vector<std::uint64_t> c(count);
+  int nf = 0;
+  const int st = lann_build_measured_dataset(e, int(kind), variant.c_str(), gpu_lattice ? 1 : 0, int(blur_side),
+                                             int(count), seed, policy.warmups, policy.reps, feats.data(), c.data(),
+                                             rt.data(), &nf);
+  const std::string msg = st ? lann_last_error(e) : "";
+  lann_engine_destroy(e);
+  if (st == LANN_PARAM_ERROR) throw ParamError(msg);
+  if (st) throw Error("measurement failed: " + msg);
+  Dataset ds;
+  ds.kind = kind;
+  ds.feature_names = models::feature_names(kind, false);
+  ds.seed = seed;
+  ds.host = "NVIDIA B200";
+  for (std::size_t i = 0; i < count; ++i) {
+    Sample smp;
+    smp.features.assign(feats.begin() + std::ptrdiff_t(i * LANN_ROW), feats.begin() + std::ptrdiff_t(i * LANN_ROW + nf));
+    smp.c = c[i];
+    smp.runtime_s = rt[i];
+    smp.variant_id = variant + "@b200";
+    ds.samples.push_back(std::move(smp));
+  }
+  return ds;
+}
+
+double run_external_variant(const std::string& command, std::span<const double> features) {
+  if (command.empty()) throw ExternalVariantError("empty launch command");
+  static std::once_flag once;  // the child may exit without reading its stdin
+  std::call_once(once, [] { std::signal(SIGPIPE, SIG_IGN); });
+  int to_child[2], from_child[2];
+  if (pipe(to_child) != 0) throw ExternalVariantError("pipe() failed");
+  if (pipe(from_child) != 0) {
+    close(to_child[0]);
+    close(to_child[1]);
+    throw ExternalVariantError("pipe() failed");
+  }
+  const pid_t pid = fork();
+  if (pid < 0) {
+    for (int fd : {to_child[0], to_child[1], from_child[0], from_child[1]}) close(fd);
+    throw ExternalVariantError("fork() failed for '" + command + "'");
+  }
+  if (pid == 0) {
+    if (dup2(to_child[0], STDIN_FILENO) < 0 || dup2(from_child[1], STDOUT_FILENO) < 0) _exit(127);
+    for (int fd : {to_child[0], to_child[1], from_child[0], from_child[1]}) close(fd);
+    execl("/bin/sh", "sh", "-c", command.c_str(), static_cast<char*>(nullptr));
+    _exit(127);
+  }
+  close(to_child[0]);
+  close(from_child[1]);
+  std::string line;
+  for (std::size_t i = 0; i < features.size(); ++i) line += (i ? " " : "") + fmt17(features[i]);
+  line += '\n';
+  for (std::size_t off = 0; off < line.size();) {
+    const ssize_t w = write(to_child[1], line.data() + off, line.size() - off);
+    if (w <= 0) break;
+    off += std::size_t(w);
+  }
+  close(to_child[1]);
+  std::string reply;
+  char buf[256];
+  for (ssize_t r; (r = read(from_child[0], buf, sizeof buf)) > 0;) reply.append(buf, std::size_t(r));
+  close(from_child[0]);
+  int status = 0;
+  if (waitpid(pid, &status, 0) < 0) throw ExternalVariantError("waitpid() failed for '" + command + "'");
+  if (!WIFEXITED(status) || WEXITSTATUS(status) != 0)
+    throw ExternalVariantError("variant command '" + command + "' exited with status " +
+                               std::to_string(WIFEXITED(status) ? WEXITSTATUS(status) : -1));
+  std::string tok = reply.substr(0, reply.find('\n'));
+  while (!tok.empty() && (tok.back() == '\r' || tok.back() == ' ')) tok.pop_back();
+  const std::size_t b = tok.find_first_not_of(' ');
+  if (b == std::string::npos) throw ExternalVariantError("variant command '" + command + "' replied with no runtime");
+  tok = tok.substr(b);
+  char* end = nullptr;
+  const double v = std::strtod(tok.c_str(), &end);
+  if (end == tok.c_str() || *end != '\0')
+    throw ExternalVariantError("variant command '" + command + "' replied with non-numeric runtime '" + tok + "'");
+  if (!(v > 0.0)) throw ExternalVariantError("variant command '" + command + "' replied with non-positive runtime");
+  return v;
+}
+
+Dataset build_external(kernels::KernelKind kind, const std::string& command, const std::string& variant_id,
+                       bool gpu_class, int max_threads, std::size_t count, std::uint64_t seed) {
+  if (count < 2) throw ParamError("build_dataset needs count >= 2");
+  if (max_threads < 1) throw ParamError("param space needs max_threads >= 1");
+  const bool takes_thd = !gpu_class && kind != kernels::KernelKind::Blur;  // variants.hpp:29-31
+  lann::SeqRng rng(lann::derive_seed(seed, 0));
+  Dataset ds;
+  ds.kind = kind;
+  ds.feature_names = models::feature_names(kind, takes_thd);
+  ds.seed = seed;
+  ds.host = "external";
+  for (std::size_t i = 0; i < count; ++i) {
+    lann::Instance p = lann::sample_instance(int(kind), max_threads, gpu_class ? 1 : 0, rng);
+    if (gpu_class) p.n_thd = 1;  // Threading::FixedSingle (datagen.cpp:195)
+    double f[LANN_ROW] = {0};
+    const int nf = lann::base_features(p, takes_thd, f);
+    Sample smp;
+    smp.features.assign(f, f + nf);
+    smp.c = lann::complexity(p);
+    smp.runtime_s = run_external_variant(command, smp.features);
+    smp.variant_id = variant_id;
+    ds.samples.push_back(std::move(smp));
   }
   return ds;
 }

@@ -3,6 +3,7 @@
 #pragma once
 
 #include <cstdint>
+#include <string>
 
 #include <cuda_runtime.h>
 
@@ -126,4 +127,12 @@ int select_variants_launch(int n_models, int precision, int kind, int max_thread
 
 namespace lann {
 void launch_pack_rows(const double* X, const double* y, int64_t n, float* out, cudaStream_t s);
+}  // namespace lann
+
+namespace lann {
+// measure.cu — B200 GPU-class kernel variants timed with CUDA events
+int measure_variant_count(int kind);
+const char* measure_variant_name(int kind, int idx);
+int measure_instances(int kind, const char* variant, int n, const double* feats, int warmups, int reps,
+                      uint64_t seed, double* runtime_s, double* checksum, cudaStream_t s, std::string& err);
 }  // namespace lann

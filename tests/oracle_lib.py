@@ -187,6 +187,8 @@ class Reference(_Lib):
         L.ref_model_dump.argtypes = [C.c_char_p, _dp, C.c_int]
         L.ref_cli_train.argtypes = [C.c_char_p, C.c_uint64, C.c_char_p, C.c_int, C.c_char_p, C.c_char_p, C.c_char_p]
         L.ref_eval_model.argtypes = [C.c_char_p, C.c_char_p, C.c_double, _dp]
+        L.ref_save_external_csv.argtypes = [C.c_int, C.c_int, C.c_int, C.c_char_p, C.c_char_p, C.c_int, C.c_uint64,
+                                            C.c_char_p]
 
     # ---- on-disk formats (csv.cpp, model_io.cpp) and the CLI train body (perfsage.cpp) ----
     def save_dataset_csv(self, world, seed, count, variant_id, path):
@@ -207,6 +209,10 @@ class Reference(_Lib):
     def cli_train(self, csv, seed, family, epochs, model_out, train_out, test_out):
         return self.lib.ref_cli_train(str(csv).encode(), seed, family.encode(), epochs, str(model_out).encode(),
                                       str(train_out).encode(), str(test_out).encode())
+
+    def save_external_csv(self, kind, gpu_class, max_threads, command, variant_id, count, seed, path):
+        return self.lib.ref_save_external_csv(kind, int(gpu_class), max_threads, command.encode(), variant_id.encode(),
+                                              count, seed, str(path).encode())
 
     def eval_model(self, model, csv, drop=0.3):
         out = np.zeros(4)

@@ -164,3 +164,28 @@ def test_cli_argument_errors(tmp_path):
         out = subprocess.run([CLI, *args, "--out", str(tmp_path)] if len(args) > 1 else [CLI, *args],
                              capture_output=True, text=True)
         assert out.returncode == 1 and out.stderr.startswith("error:"), args
+
+
+@pytest.mark.parametrize("kind,gpu_class", [(abi.MM, False), (abi.MV, True), (abi.MP, False), (abi.BLUR, False)])
+def test_gen_external_protocol_matches_reference(tmp_path, reference, kind, gpu_class):
+    """`perfsage gen --external-cmd CMD` (external.cpp protocol: one line of %.17g features on
+    stdin, one runtime on stdout) builds the CSV the reference builds with the same command."""
+    name = {abi.MM: "mm", abi.MV: "mv", abi.MP: "mp", abi.BLUR: "blur"}[kind]
+    cmd = "awk '{s=1; for(i=1;i<=NF;i++) s+=$i; printf \"%.17g\\n\", s*1e-9}'"
+    args = ["gen", "--external-cmd", cmd, "--kernel", name, "--count", "12", "--seed", "9", "--max-threads", "4",
+            "--external-id", "ext", "--out", str(tmp_path)]
+    if gpu_class:
+        args.append("--gpu-class")
+    run(CLI, *args)
+    ours = tmp_path / f"dataset_{name}_ext.csv"
+    ref = tmp_path / "ref.csv"
+    assert reference.save_external_csv(kind, gpu_class, 4, cmd, "ext", 12, 9, ref) == 0, reference.last_error()
+    assert open(ours, "rb").read() == open(ref, "rb").read()
+
+
+def test_gen_external_protocol_errors(tmp_path):
+    for cmd, what in (("exit 3", "exited with status 3"), ("echo abc", "non-numeric"), ("echo -1", "non-positive"),
+                      ("true", "no runtime")):
+        out = subprocess.run([CLI, "gen", "--external-cmd", cmd, "--kernel", "mm", "--count", "2", "--out",
+                              str(tmp_path)], capture_output=True, text=True)
+        assert out.returncode == 1 and what in out.stderr, (cmd, out.stderr)

@@ -1,0 +1,183 @@
+"""GPU: real measurement of B200 kernel variants (measure.cu).
+
+* Every variant computes the reference kernel's mathematics (reference.cpp:14-66): its output
+  checksum matches a numpy restatement on operands rebuilt from the same counter hash.
+* Timing follows datagen::measure (warm-ups, median of reps): positive, and for the GEMMs
+  ordered with the work (Spearman of runtime vs m*n*k).
+* `perfsage gen --measure` builds a real B200 dataset that trains LANNs through the engine, and
+  `perfsage measure-variant` serves the reference's external-variant protocol.
+"""
+import csv
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+import pytest
+
+from paper_2003_07497_b200 import abi
+from paper_2003_07497_b200 import engine as E
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+CLI = os.path.join(ROOT, "paper_2003_07497_b200", "bin", "perfsage")
+M64 = (1 << 64) - 1
+
+
+def mix64(z):
+    z = (z + np.uint64(0x9E3779B97F4A7C15))
+    z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+    z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+    return z ^ (z >> np.uint64(31))
+
+
+def operand(seed, op, count, d):
+    """measure.cu gen_value / gen_keep: value = top 24 bits / 2^24, kept with probability d."""
+    i = np.arange(count, dtype=np.uint64)
+    base = np.uint64(seed) ^ np.uint64((op << 56) & M64)
+    with np.errstate(over="ignore"):
+        v = (mix64(base ^ (i * np.uint64(2))) >> np.uint64(40)).astype(np.float32) * np.float32(1.0 / 16777216.0)
+        if d < 1.0:
+            keep = (mix64(base ^ (i * np.uint64(2) + np.uint64(1))) >> np.uint64(11)).astype(np.float64) * 2.0**-53 < d
+            v = np.where(keep, v, np.float32(0))
+    return v
+
+
+def instance_seed(seed, i):
+    with np.errstate(over="ignore"):
+        return int(mix64(np.uint64(seed) ^ (np.uint64(0x3C6EF372FE94F82B) * np.uint64(i + 1))))
+
+
+def measure(kind, variant, feats, seed=11, warmups=1, reps=3):
+    L = E.load_library()
+    L.lann_measure.argtypes = [C.c_void_p, C.c_int32, C.c_char_p, C.c_int32, C.c_void_p, C.c_int32, C.c_int32,
+                               C.c_uint64, C.c_void_p, C.c_void_p]
+    f = np.zeros((len(feats), 8))
+    for r, row in enumerate(feats):
+        f[r, : len(row)] = row
+    rt = np.zeros(len(feats))
+    cs = np.zeros(len(feats))
+    eng = C.c_void_p()
+    assert L.lann_engine_create(0, C.byref(eng)) == 0
+    st = L.lann_measure(eng, kind, variant.encode(), len(feats), f.ctypes.data, warmups, reps, seed, rt.ctypes.data,
+                        cs.ctypes.data)
+    L.lann_engine_destroy(eng)
+    assert st == 0
+    return rt, cs
+
+
+def reference_output(kind, row, s):
+    if kind == abi.MM:
+        m, n, k, d1, d2 = row
+        a = operand(s, 0, m * n, d1).reshape(m, n).astype(np.float64)
+        b = operand(s, 1, n * k, d2).reshape(n, k).astype(np.float64)
+        return a @ b
+    if kind == abi.MV:
+        m, n, d = row
+        a = operand(s, 0, m * n, d).reshape(m, n).astype(np.float64)
+        return a @ operand(s, 1, n, 1.0).astype(np.float64)
+    if kind == abi.MC:
+        m, n, r, d = row
+        a = operand(s, 0, m * n, d).reshape(m, n).astype(np.float64)
+        f = operand(s, 1, r * r, 1.0).reshape(r, r).astype(np.float64)
+        om, on = m - r + 1, n - r + 1
+        return sum(a[u:u + om, v:v + on] * f[u, v] for u in range(r) for v in range(r))
+    if kind == abi.MP:
+        m, n, _r, st, d = row
+        a = operand(s, 0, m * n, d).reshape(m, n).astype(np.float64)
+        om, on = -(-m // st), -(-n // st)
+        out = np.zeros((om, on))
+        for i in range(om):
+            for j in range(on):
+                w = a[i * st:(i + 1) * st, j * st:(j + 1) * st]
+                out[i, j] = max(w.max(), 0.0) if w.size < st * st else w.max()
+        return out
+    n = row[0]
+    img = operand(s, 0, n * n, 1.0).reshape(n, n)
+    bx = (img[:, :-2] + img[:, 1:-1] + img[:, 2:]) / np.float32(3)
+    return ((bx[:-2] + bx[1:-1] + bx[2:]) / np.float32(3)).astype(np.float64)
+
+
+CASES = [
+    (abi.MM, "gemm_tiled", [(37, 70, 129, 1.0, 1.0), (64, 64, 64, 0.5, 0.25), (1, 300, 7, 1.0, 1.0)]),
+    (abi.MM, "cublas_sgemm", [(37, 70, 129, 1.0, 1.0), (128, 3, 65, 0.125, 1.0)]),
+    (abi.MM, "spmm_csr", [(37, 70, 129, 0.0625, 1.0), (100, 200, 33, 0.5, 0.5)]),
+    (abi.MV, "gemv_dense", [(300, 170, 1.0), (5, 1000, 0.25)]),
+    (abi.MV, "spmv_csr", [(300, 170, 0.03125), (64, 1024, 0.5)]),
+    (abi.MC, "conv_direct", [(50, 40, 3, 1.0), (33, 70, 7, 0.5)]),
+    (abi.MP, "maxpool", [(50, 41, 3, 2, 1.0), (33, 70, 2, 3, 0.25), (9, 9, 5, 4, 1.0)]),
+    (abi.BLUR, "blur_sched", [(256, 2, 8, 4, 1), (130, 16, 1, 64, 1), (64, 4, 64, 64, 1)]),
+]
+
+
+@pytest.mark.parametrize("kind,variant,rows", CASES, ids=[c[1] for c in CASES])
+def test_variant_computes_the_reference_mathematics(kind, variant, rows):
+    rt, cs = measure(kind, variant, rows, seed=11)
+    assert np.all(rt > 0)
+    for i, row in enumerate(rows):
+        ref = reference_output(kind, row, instance_seed(11, i)).sum()
+        assert cs[i] == pytest.approx(ref, rel=2e-5, abs=1e-6), (row, cs[i], ref)
+
+
+def test_gemm_runtime_follows_the_work():
+    """Square GEMMs 128..1024: runtime grows with the work (on 148 SMs small or skinny GEMMs are
+    parallelism-bound, not work-bound, so only the square ladder is required to be monotone; the
+    random shapes only have to correlate positively — that nonlinearity is what the LANN learns)."""
+    ladder = [(s, s, s, 1.0, 1.0) for s in (128, 256, 512, 1024)]
+    rng = np.random.default_rng(3)
+    rows = [(int(m), int(n), int(k), 1.0, 1.0) for m, n, k in rng.integers(16, 1025, (24, 3))]
+    rank = lambda x: np.argsort(np.argsort(x))  # noqa: E731
+    for variant in ("gemm_tiled", "cublas_sgemm"):
+        rt, _ = measure(abi.MM, variant, ladder, reps=5)
+        assert rt[3] > rt[2] > rt[0] and rt[3] > 2 * rt[0], (variant, rt)
+        rt, _ = measure(abi.MM, variant, rows, reps=5)
+        work = np.array([m * n * k for m, n, k, _, _ in rows], dtype=np.float64)
+        assert np.corrcoef(rank(work), rank(rt))[0, 1] > 0.3, variant
+
+
+def test_unknown_variant_is_a_param_error():
+    L = E.load_library()
+    L.lann_measure.argtypes = [C.c_void_p, C.c_int32, C.c_char_p, C.c_int32, C.c_void_p, C.c_int32, C.c_int32,
+                               C.c_uint64, C.c_void_p, C.c_void_p]
+    eng = C.c_void_p()
+    assert L.lann_engine_create(0, C.byref(eng)) == 0
+    f = np.zeros(8)
+    rt = np.zeros(1)
+    assert L.lann_measure(eng, abi.MM, b"nope", 1, f.ctypes.data, 1, 3, 1, rt.ctypes.data, None) == abi.PARAM_ERROR
+    L.lann_engine_destroy(eng)
+
+
+def run(*args):
+    out = subprocess.run([str(a) for a in args], capture_output=True, text=True, timeout=900)
+    assert out.returncode == 0, out.stdout + out.stderr
+    return out.stdout
+
+
+def test_measured_dataset_trains_lanns(tmp_path):
+    """gen --measure: 400 real B200 cuBLAS SGEMM timings -> train NN+C and NN on them (FP32)."""
+    run(CLI, "gen", "--measure", "--kernel", "mm", "--variant", "cublas_sgemm", "--count", 400, "--seed", 2,
+        "--reps", 3, "--out", tmp_path)
+    data = tmp_path / "dataset_mm_cublas_sgemm_b200.csv"
+    with open(data) as f:
+        rows = list(csv.DictReader(f))
+    assert len(rows) == 400 and all(float(r["runtime_s"]) > 0 for r in rows)
+    assert list(rows[0].keys())[:7] == ["kernel", "variant", "m", "n", "k", "d1", "d2"]
+    run(CLI, "compare", "--data", data, "--seed", 1, "--epochs", 3000, "--precision", "fp32", "--out", tmp_path)
+    with open(tmp_path / "compare.csv") as f:
+        rep = {r["model_family"]: float(r["mape_thresholded"]) for r in csv.DictReader(f)}
+    assert np.isfinite(rep["nnc"]) and rep["nnc"] < 60.0
+
+
+def test_measure_variant_serves_the_external_protocol(tmp_path):
+    """The reference's --external-cmd protocol driven by `perfsage measure-variant` (one CUDA
+    process per sample, as external.cpp spawns it)."""
+    cmd = f"{CLI} measure-variant --kernel mm --variant gemm_tiled --reps 3"
+    run(CLI, "gen", "--external-cmd", cmd, "--kernel", "mm", "--gpu-class", "--count", 4, "--seed", 3,
+        "--external-id", "gemm_tiled_ext", "--out", tmp_path)
+    with open(tmp_path / "dataset_mm_gemm_tiled_ext.csv") as f:
+        rows = list(csv.DictReader(f))
+    assert len(rows) == 4 and all(float(r["runtime_s"]) > 0 for r in rows)
+    out = subprocess.run([CLI, "measure-variant", "--kernel", "mv", "--variant", "gemv_dense"],
+                         input="100 200 1\n300 20 0.5\n", capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0 and len(out.stdout.split()) == 2

@@ -240,6 +240,38 @@ int lann_build_measured_dataset(lann_engine* engine, int32_t kind, const char* v
                                 int32_t warmups, int32_t reps, double* feats, uint64_t* c,
                                 double* runtime, int32_t* n_features);
 
+/* ---- the baseline families of the five-family comparison (models.cpp:184-333,
+ * forest.cpp): const (C: t ~ c), lrc (LR+C) least squares and the nlrc random forest,
+ * fitted on RAW features (no normalisation), batched over models. -------------------- */
+typedef struct lann_design {
+  int32_t n_models;
+  const int32_t* n_rows;      /* samples per model */
+  const int32_t* n_feats;     /* design columns per model (<= LANN_ROW; const: 1 = c) */
+  const int64_t* row_offset;  /* first row of each model in X / y */
+  const double* X;            /* [rows][LANN_ROW] model features (model_features order) */
+  const double* y;            /* runtimes in seconds */
+} lann_design;
+/* fit_least_squares (models.cpp:220-265), bit-identical: weights [n_models][LANN_ROW],
+ * intercept [n_models]; status[m] = 0, or LANN_DOMAIN_ERROR for FitError (singular despite
+ * the ridge). */
+int lann_fit_linear(lann_engine* engine, const lann_design* design, double ridge, double* weights,
+                    double* intercept, int32_t* status);
+/* fit_forest (forest.cpp:124-143): Rng(derive_seed(seeds[m], t)) bootstraps, trees of up to
+ * nodes_per_tree = 2 * max(n_rows) nodes each, written in the reference's depth-first preorder
+ * to node_* [n_models][trees][nodes_per_tree]; node_count [n_models][trees]. */
+int lann_fit_forest(lann_engine* engine, const lann_design* design, int32_t trees, int32_t max_depth,
+                    int32_t min_samples_split, const uint64_t* seeds, int32_t* node_feature,
+                    double* node_threshold, int32_t* node_left, int32_t* node_right, double* node_value,
+                    int32_t* node_count);
+/* LinearModel / Forest prediction (models.cpp:357-362, forest.cpp:13-27), max(v, 1e-9). */
+int lann_predict_linear(lann_engine* engine, int32_t n_models, const int32_t* n_feats, const double* weights,
+                        const double* intercept, int64_t n_rows, const double* rows, const int32_t* row_model,
+                        double* out);
+int lann_predict_forest(lann_engine* engine, int32_t n_models, int32_t trees, int32_t nodes_per_tree,
+                        const int32_t* node_feature, const double* node_threshold, const int32_t* node_left,
+                        const int32_t* node_right, const double* node_value, int64_t n_rows, const double* rows,
+                        const int32_t* row_model, double* out);
+
 /* Glorot-uniform init (Mlp::init, mlp.cpp:9-25) with Rng(derive_seed(seed, 0xA11CE)). */
 int lann_init_params(int32_t n_dims, const int32_t* dims, uint64_t seed, double* params);
 

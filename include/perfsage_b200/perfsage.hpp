@@ -52,6 +52,7 @@ class TrainingError : public Error {
   int epoch_;
 };
 class LoadError : public Error { public: using Error::Error; };  // errors.hpp:49-52
+class FitError : public Error { public: using Error::Error; };   // errors.hpp:42-46
 class ExternalVariantError : public Error { public: using Error::Error; };  // errors.hpp
 class BuildAbortError : public Error {
  public:
@@ -209,12 +210,34 @@ struct NormStats {
                        bool log_target = false);
 };
 
+/// models.hpp:56-60 — the const / lrc payload: runtime = intercept + sum_j weights[j] * x[j]
+struct LinearModel {
+  std::vector<double> weights;
+  double intercept = 0.0;
+};
+/// forest.hpp:10-30 — the nlrc payload (nodes in depth-first preorder, leaves have feature -1).
+/// Prediction runs on the GPU through models::predict / predict_dataset.
+struct TreeNode {
+  int feature = -1;
+  double threshold = 0.0;
+  int left = -1;
+  int right = -1;
+  double value = 0.0;
+  bool is_leaf() const { return feature < 0; }
+};
+struct Tree {
+  std::vector<TreeNode> nodes;
+};
+struct Forest {
+  std::vector<Tree> trees;
+};
+
 struct TrainedModel {
   ModelConfig config;
   kernels::KernelKind kind = kernels::KernelKind::MM;
   std::vector<std::string> schema;
-  NormStats norm;
-  std::variant<Mlp> payload;  // NN families (the engine's scope); std::get<Mlp> as in the reference
+  NormStats norm;  // NN families only (the baselines fit raw features)
+  std::variant<Mlp, LinearModel, Forest> payload;
   std::vector<double> loss_trace;
 };
 
@@ -222,9 +245,15 @@ std::vector<double> model_features(const datagen::Sample& sample, ModelFamily fa
 
 /// models.cpp:279-303 — trained on the GPU (one-model population).
 TrainedModel train_nn(const datagen::Dataset& train, const ModelConfig& config);
-/// models.cpp:335-344 restricted to the NN families (const/lrc/nlrc are out of scope).
+/// models.cpp:335-344 — every family on the GPU: nnc / nn (train_nn), const / lrc (least squares,
+/// bit-identical), nlrc (random forest).
 TrainedModel train_model(const datagen::Dataset& train, const ModelConfig& config);
-/// Batched overload: every (dataset, config) pair trained in ONE engine call.
+TrainedModel train_const(const datagen::Dataset& train, const ModelConfig& config);  // models.cpp:305-312
+TrainedModel train_lrc(const datagen::Dataset& train, const ModelConfig& config);    // models.cpp:314-320
+TrainedModel train_nlrc(const datagen::Dataset& train, const ModelConfig& config);   // models.cpp:322-333
+/// Batched overload: every (dataset, config) pair trained in one engine call per family group
+/// (NN families: one trainer launch set; const + lrc: one least-squares launch; nlrc: one forest
+/// launch of models x trees CTAs).
 std::vector<TrainedModel> train_population(const std::vector<const datagen::Dataset*>& train,
                                            const std::vector<ModelConfig>& configs);
 

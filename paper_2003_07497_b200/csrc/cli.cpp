@@ -12,7 +12,7 @@
 //            one runtime out), so the reference's own `gen --external-cmd` can measure B200s
 //   train    CSV -> split(seed 0x5b11) -> train_model -> model_<family>.json, train.csv, test.csv
 //   eval     model JSON(s) x CSV -> eval.csv (+ --group-by aggregate)
-//   compare  CSV -> the NN families (nnc, nn) trained as ONE batched population -> compare.csv
+//   compare  CSV -> the five families (nnc, nn, const, lrc, nlrc) batched per family group -> compare.csv
 //   select   blur schedules: train on measured samples, GPU argmin over the candidates,
 //            regret / speedups (selection.json, schedules.csv)
 //   sweep    the 48-combination population x seeds x k folds (config 3 / config 5) through
@@ -318,8 +318,10 @@ int cmd_train(const Args& a) {  // perfsage.cpp:250-278
   datagen::save_csv(train_set, tr.string());
   datagen::save_csv(test_set, te.string());
   record_run(out, a, seed, {data}, {mp.string(), tr.string(), te.string()});
-  std::cout << "trained " << fam << " on " << train_set.size() << " samples (" << models::param_count(model)
-            << " parameters, final loss " << model.loss_trace.back() << ")\nmodel: " << mp.string() << "\n";
+  std::cout << "trained " << fam << " on " << train_set.size() << " samples";
+  if (std::holds_alternative<models::Mlp>(model.payload))
+    std::cout << " (" << models::param_count(model) << " parameters, final loss " << model.loss_trace.back() << ")";
+  std::cout << "\nmodel: " << mp.string() << "\n";
   return 0;
 }
 
@@ -369,17 +371,17 @@ int cmd_compare(const Args& a) {  // perfsage.cpp:384-414, NN families batched
   const std::uint64_t seed = a.u64("seed", 0);
   const auto dataset = datagen::load_csv(data);
   const auto [train_set, test_set] = datagen::split(dataset, a.real("train-frac", 0.5), lann::derive_seed(seed, 0x5b11));
-  const std::vector<models::ModelFamily> fams = {models::ModelFamily::NnC, models::ModelFamily::Nn};
+  const std::vector<models::ModelFamily> fams = {models::ModelFamily::NnC, models::ModelFamily::Nn,
+                                                 models::ModelFamily::Const, models::ModelFamily::LrC,
+                                                 models::ModelFamily::NlrC};
   std::vector<models::ModelConfig> cfgs;
   std::vector<const datagen::Dataset*> trains, tests;
   for (auto f : fams) {
-    auto cfg = make_config(dataset.kind, f, a, seed);
-    if (a.has("epochs")) cfg.epochs = int(a.integer("epochs", cfg.epochs));
-    cfgs.push_back(cfg);
+    cfgs.push_back(make_config(dataset.kind, f, a, seed));
     trains.push_back(&train_set);
     tests.push_back(&test_set);
   }
-  const auto ms = models::train_population(trains, cfgs);  // both families in one launch set
+  const auto ms = models::train_population(trains, cfgs);  // NN pair in one launch set, LS, forest
   std::vector<const models::TrainedModel*> mp;
   for (const auto& m : ms) mp.push_back(&m);
   const auto preds = models::predict_population(mp, tests);
@@ -398,7 +400,7 @@ int cmd_compare(const Args& a) {  // perfsage.cpp:384-414, NN families batched
   }
   eval::print_reports(std::cout, reports);
   std::cout << "best thresholded MAPE: " << reports[best].model_family << " (" << reports[best].mape_thresholded
-            << "%)\n(const / lrc / nlrc baselines are not part of this engine: SURVEY.md 8(f) row 4)\n";
+            << "%)\n";
   record_run(out, a, seed, {data}, {csv.string()});
   return 0;
 }

@@ -1133,6 +1133,209 @@ int lann_build_measured_dataset(lann_engine* e, int32_t kind, const char* varian
   return LANN_OK;
 }
 
+// ---- baseline families -------------------------------------------------------------------------
+namespace {
+Status check_design(const lann_design* d, int max_feats) {
+  if (!d || d->n_models < 1 || !d->n_rows || !d->n_feats || !d->row_offset || !d->X || !d->y)
+    return {LANN_PARAM_ERROR, "empty design"};
+  for (int m = 0; m < d->n_models; ++m) {
+    if (d->n_rows[m] < 2) return {LANN_PARAM_ERROR, "training needs at least 2 samples"};
+    if (d->n_feats[m] < 1 || d->n_feats[m] > max_feats) return {LANN_PARAM_ERROR, "design columns out of range"};
+    if (d->row_offset[m] < 0) return {LANN_PARAM_ERROR, "bad row offset"};
+  }
+  return {};
+}
+int64_t design_rows(const lann_design* d) {
+  int64_t r = 0;
+  for (int m = 0; m < d->n_models; ++m) r = std::max<int64_t>(r, d->row_offset[m] + d->n_rows[m]);
+  return r;
+}
+}  // namespace
+
+int lann_fit_linear(lann_engine* e, const lann_design* d, double ridge, double* weights, double* intercept,
+                    int32_t* status) {
+  if (!e) return LANN_NO_DEVICE;
+  if (Status st = check_design(d, LANN_ROW)) return set_err(e, st);
+  if (!weights || !intercept || !status) return set_err(e, {LANN_PARAM_ERROR, "missing output buffers"});
+  try {
+    ck(cudaSetDevice(e->device), "cudaSetDevice");
+    Timer timer(e);
+    cudaStream_t s = e->stream;
+    const int M = d->n_models;
+    const int64_t rows = design_rows(d);
+    DBuf<int> dn(d->n_rows, size_t(M), s), df(d->n_feats, size_t(M), s), dst(size_t(M), s);
+    DBuf<int64_t> doff(d->row_offset, size_t(M), s);
+    DBuf<double> dX(d->X, size_t(rows) * LANN_ROW, s), dY(d->y, size_t(rows), s);
+    DBuf<double> dW(size_t(M) * LANN_ROW, s), dI(size_t(M), s);
+    launch_fit_linear({M, dn.p, df.p, doff.p, dX.p, dY.p, ridge, dW.p, dI.p, dst.p}, s);
+    ck(cudaGetLastError(), "fit_linear launch");
+    e->launches += 1;
+    dW.down(weights);
+    dI.down(intercept);
+    dst.down(status);
+    timer.stop();
+    for (int m = 0; m < M; ++m) status[m] = status[m] ? LANN_DOMAIN_ERROR : LANN_OK;
+    for (int m = 0; m < M; ++m)
+      if (status[m]) return set_err(e, {LANN_DOMAIN_ERROR, "singular design matrix despite ridge"});
+    return LANN_OK;
+  } catch (const CudaFail& f) {
+    e->err = f.what;
+    return LANN_CUDA_ERROR;
+  }
+}
+
+int lann_predict_linear(lann_engine* e, int32_t M, const int32_t* n_feats, const double* weights,
+                        const double* intercept, int64_t n_rows, const double* rows, const int32_t* row_model,
+                        double* out) {
+  if (!e) return LANN_NO_DEVICE;
+  if (M < 1 || !n_feats || !weights || !intercept || n_rows < 0 || (n_rows && (!rows || !row_model || !out)))
+    return set_err(e, {LANN_PARAM_ERROR, "bad linear prediction request"});
+  for (int64_t r = 0; r < n_rows; ++r)
+    if (row_model[r] < 0 || row_model[r] >= M) return set_err(e, {LANN_PARAM_ERROR, "row model out of range"});
+  try {
+    ck(cudaSetDevice(e->device), "cudaSetDevice");
+    Timer timer(e);
+    cudaStream_t s = e->stream;
+    DBuf<int> df(n_feats, size_t(M), s), dm(row_model, size_t(n_rows), s);
+    DBuf<double> dW(weights, size_t(M) * LANN_ROW, s), dI(intercept, size_t(M), s);
+    DBuf<double> dR(rows, size_t(n_rows) * LANN_ROW, s), dO(size_t(n_rows), s);
+    launch_predict_linear({n_rows, dR.p, dm.p, df.p, dW.p, dI.p, dO.p}, s);
+    ck(cudaGetLastError(), "predict_linear launch");
+    e->launches += n_rows > 0;
+    dO.down(out);
+    timer.stop();
+    return LANN_OK;
+  } catch (const CudaFail& f) {
+    e->err = f.what;
+    return LANN_CUDA_ERROR;
+  }
+}
+
+int lann_fit_forest(lann_engine* e, const lann_design* d, int32_t trees, int32_t max_depth,
+                    int32_t min_samples_split, const uint64_t* seeds, int32_t* node_feature, double* node_threshold,
+                    int32_t* node_left, int32_t* node_right, double* node_value, int32_t* node_count) {
+  if (!e) return LANN_NO_DEVICE;
+  if (Status st = check_design(d, LANN_ROW)) return set_err(e, st);
+  if (trees < 1 || max_depth < 1) return set_err(e, {LANN_PARAM_ERROR, "forest needs trees >= 1 and max_depth >= 1"});
+  if (!seeds || !node_feature || !node_threshold || !node_left || !node_right || !node_value || !node_count)
+    return set_err(e, {LANN_PARAM_ERROR, "missing forest buffers"});
+  const int M = d->n_models;
+  int max_rows = 0;
+  for (int m = 0; m < M; ++m) {
+    if (d->n_rows[m] < 10) return set_err(e, {LANN_PARAM_ERROR, "forest needs at least 10 samples"});
+    max_rows = std::max(max_rows, d->n_rows[m]);
+  }
+  if (forest_smem_bytes(max_rows) > size_t(e->max_smem))
+    return set_err(e, {LANN_PARAM_ERROR, "forest training set too large for one CTA"});
+  // bootstraps (forest.cpp:132-136): Rng(derive_seed(seed, t)).bounded(n) x n, sorted
+  std::vector<uint16_t> boot(size_t(M) * trees * max_rows, 0);
+  parallel_for(M * trees, [&](int k) {
+    const int m = k / trees, t = k % trees, n = d->n_rows[m];
+    SeqRng rng(derive_seed(seeds[m], uint64_t(t)));
+    uint16_t* b = &boot[size_t(k) * max_rows];
+    for (int i = 0; i < n; ++i) b[i] = uint16_t(rng.bounded(uint64_t(n)));
+    std::sort(b, b + n);
+  });
+  const size_t npt = size_t(2) * max_rows, total = size_t(M) * trees * npt;
+  try {
+    ck(cudaSetDevice(e->device), "cudaSetDevice");
+    Timer timer(e);
+    cudaStream_t s = e->stream;
+    const int64_t rows = design_rows(d);
+    DBuf<int> dn(d->n_rows, size_t(M), s), df(d->n_feats, size_t(M), s);
+    DBuf<int64_t> doff(d->row_offset, size_t(M), s);
+    DBuf<double> dX(d->X, size_t(rows) * LANN_ROW, s), dY(d->y, size_t(rows), s);
+    DBuf<uint16_t> dB(boot, s);
+    DBuf<int> nf(total, s), nl(total, s), nr(total, s), nc(size_t(M) * trees, s);
+    DBuf<double> nt(total, s), nv(total, s);
+    DBuf<double> ss(size_t(M) * trees * max_rows * LANN_ROW, s), sth(size_t(M) * trees * max_rows * LANN_ROW, s);
+    ForestArgs fa{M, trees, max_depth, min_samples_split, max_rows, dn.p, df.p, doff.p, dX.p, dY.p, dB.p,
+                  nf.p, nt.p, nl.p, nr.p, nv.p, nc.p, ss.p, sth.p};
+    launch_fit_forest(fa, s);
+    ck(cudaGetLastError(), "fit_forest launch");
+    e->launches += 1;
+    std::vector<int> bf(total), bl(total), br(total), bc(size_t(M) * trees);
+    std::vector<double> bt(total), bv(total);
+    nf.down(bf.data());
+    nl.down(bl.data());
+    nr.down(br.data());
+    nc.down(bc.data());
+    nt.down(bt.data());
+    nv.down(bv.data());
+    timer.stop();
+    // breadth-first -> the reference's depth-first preorder (Builder::build, forest.cpp:96-121)
+    parallel_for(M * trees, [&](int k) {
+      const size_t base = size_t(k) * npt;
+      std::vector<int> stack = {0}, order;
+      std::vector<int> newid(size_t(bc[size_t(k)]), -1);
+      while (!stack.empty()) {
+        const int v = stack.back();
+        stack.pop_back();
+        newid[size_t(v)] = int(order.size());
+        order.push_back(v);
+        if (bf[base + v] >= 0) {
+          stack.push_back(br[base + v]);
+          stack.push_back(bl[base + v]);
+        }
+      }
+      for (size_t i = 0; i < npt; ++i) {
+        const size_t o = base + i;
+        if (i < order.size()) {
+          const size_t src = base + size_t(order[i]);
+          node_feature[o] = bf[src];
+          node_threshold[o] = bt[src];
+          node_left[o] = bf[src] >= 0 ? newid[size_t(bl[src])] : -1;
+          node_right[o] = bf[src] >= 0 ? newid[size_t(br[src])] : -1;
+          node_value[o] = bv[src];
+        } else {
+          node_feature[o] = node_left[o] = node_right[o] = -1;
+          node_threshold[o] = node_value[o] = 0.0;
+        }
+      }
+      node_count[k] = bc[size_t(k)];
+    });
+    return LANN_OK;
+  } catch (const CudaFail& f) {
+    e->err = f.what;
+    return LANN_CUDA_ERROR;
+  }
+}
+
+int lann_predict_forest(lann_engine* e, int32_t M, int32_t trees, int32_t npt, const int32_t* node_feature,
+                        const double* node_threshold, const int32_t* node_left, const int32_t* node_right,
+                        const double* node_value, int64_t n_rows, const double* rows, const int32_t* row_model,
+                        double* out) {
+  if (!e) return LANN_NO_DEVICE;
+  if (M < 1 || trees < 1 || npt < 1 || !node_feature || !node_threshold || !node_left || !node_right ||
+      !node_value || n_rows < 0 || (n_rows && (!rows || !row_model || !out)))
+    return set_err(e, {LANN_PARAM_ERROR, "bad forest prediction request"});
+  for (int64_t r = 0; r < n_rows; ++r)
+    if (row_model[r] < 0 || row_model[r] >= M) return set_err(e, {LANN_PARAM_ERROR, "row model out of range"});
+  const size_t total = size_t(M) * trees * npt;
+  for (size_t i = 0; i < total; ++i)  // a malformed tree must not send the GPU walk off the arrays
+    if (node_feature[i] >= LANN_ROW || (node_feature[i] >= 0 && (node_left[i] < 0 || node_left[i] >= npt ||
+                                                                 node_right[i] < 0 || node_right[i] >= npt)))
+      return set_err(e, {LANN_PARAM_ERROR, "malformed forest node"});
+  try {
+    ck(cudaSetDevice(e->device), "cudaSetDevice");
+    Timer timer(e);
+    cudaStream_t s = e->stream;
+    DBuf<int> df(node_feature, total, s), dl(node_left, total, s), dr(node_right, total, s);
+    DBuf<double> dt(node_threshold, total, s), dv(node_value, total, s);
+    DBuf<int> dm(row_model, size_t(n_rows), s);
+    DBuf<double> dR(rows, size_t(n_rows) * LANN_ROW, s), dO(size_t(n_rows), s);
+    launch_predict_forest({n_rows, dR.p, dm.p, trees, npt, df.p, dt.p, dl.p, dr.p, dv.p, dO.p}, s);
+    ck(cudaGetLastError(), "predict_forest launch");
+    e->launches += n_rows > 0;
+    dO.down(out);
+    timer.stop();
+    return LANN_OK;
+  } catch (const CudaFail& f) {
+    e->err = f.what;
+    return LANN_CUDA_ERROR;
+  }
+}
+
 int lann_probe_schedules(const lann_world* w, uint64_t seed, uint32_t image_n, int32_t n,
                          const uint32_t* sched, double* runtime) {
   if (!w || (n > 0 && (!sched || !runtime))) return LANN_PARAM_ERROR;

@@ -309,7 +309,6 @@ Dataset build_external(kernels::KernelKind kind, const std::string& command, con
 namespace models {
 
 void save_model(const TrainedModel& m, const std::string& path) {
-  const auto& net = std::get<Mlp>(m.payload);
   const auto& c = m.config;
   std::ostringstream o;
   o << "{\n";
@@ -336,18 +335,40 @@ void save_model(const TrainedModel& m, const std::string& path) {
   o << "    \"t_max\": " << jnum(m.norm.t_max) << ",\n";
   o << "    \"log_target\": " << (m.norm.log_target ? "true" : "false") << "\n";
   o << "  },\n";
-  o << "  \"payload\": {\n    \"layers\": [\n";
-  for (std::size_t l = 0; l < net.layers.size(); ++l) {
-    const auto& L = net.layers[l];
-    o << "      {\"rows\": " << L.out << ", \"cols\": " << L.in << ", \"weights\": " << jarr(L.w)
-      << ", \"biases\": " << jarr(L.b) << "}" << (l + 1 < net.layers.size() ? "," : "") << "\n";
+  o << "  \"payload\": {\n";
+  if (const auto* net = std::get_if<Mlp>(&m.payload)) {
+    o << "    \"layers\": [\n";
+    for (std::size_t l = 0; l < net->layers.size(); ++l) {
+      const auto& L = net->layers[l];
+      o << "      {\"rows\": " << L.out << ", \"cols\": " << L.in << ", \"weights\": " << jarr(L.w)
+        << ", \"biases\": " << jarr(L.b) << "}" << (l + 1 < net->layers.size() ? "," : "") << "\n";
+    }
+    o << "    ]\n  },\n";
+    o << "  \"metrics\": {\n";
+    o << "    \"param_count\": " << net->param_count() << ",\n";
+    if (!m.loss_trace.empty()) o << "    \"final_loss\": " << jnum(m.loss_trace.back()) << ",\n";
+    o << "    \"loss_trace\": " << jarr(m.loss_trace) << "\n";
+    o << "  }\n}\n";
+  } else {
+    if (const auto* lin = std::get_if<LinearModel>(&m.payload)) {
+      o << "    \"linear\": {\"weights\": " << jarr(lin->weights) << ", \"intercept\": " << jnum(lin->intercept)
+        << "}\n";
+    } else {
+      const auto& forest = std::get<Forest>(m.payload);
+      o << "    \"forest\": [\n";
+      for (std::size_t t = 0; t < forest.trees.size(); ++t) {
+        o << "      [";
+        const auto& nodes = forest.trees[t].nodes;
+        for (std::size_t v = 0; v < nodes.size(); ++v)
+          o << (v ? ", " : "") << "{\"feature\": " << nodes[v].feature << ", \"threshold\": "
+            << jnum(nodes[v].threshold) << ", \"left\": " << nodes[v].left << ", \"right\": " << nodes[v].right
+            << ", \"value\": " << jnum(nodes[v].value) << "}";
+        o << "]" << (t + 1 < forest.trees.size() ? "," : "") << "\n";
+      }
+      o << "    ]\n";
+    }
+    o << "  },\n  \"metrics\": null\n}\n";  // model_io.cpp:140-146: metrics only for NN payloads
   }
-  o << "    ]\n  },\n";
-  o << "  \"metrics\": {\n";
-  o << "    \"param_count\": " << net.param_count() << ",\n";
-  if (!m.loss_trace.empty()) o << "    \"final_loss\": " << jnum(m.loss_trace.back()) << ",\n";
-  o << "    \"loss_trace\": " << jarr(m.loss_trace) << "\n";
-  o << "  }\n}\n";
   std::ofstream os(path, std::ios::binary);
   if (!os) throw LoadError("cannot open '" + path + "' for writing");
   os << o.str();
@@ -391,21 +412,40 @@ TrainedModel load_model(const std::string& path) {
     m.norm.t_max = n.at("t_max").num();
     m.norm.log_target = n.at("log_target").boolean();
     const Json& p = j.at("payload");
-    if (!p.find("layers"))
-      throw LoadError("'" + path + "': only NN payloads (layers) are in this engine's scope");
-    Mlp net;
-    for (const auto& lj : p.at("layers").items) {
-      DenseLayer L;
-      L.out = lj.at("rows").i32();
-      L.in = lj.at("cols").i32();
-      L.w = lj.at("weights").doubles();
-      L.b = lj.at("biases").doubles();
-      if (L.w.size() != std::size_t(L.in) * std::size_t(L.out) || L.b.size() != std::size_t(L.out))
-        throw LoadError("layer shape does not match its weight payload");
-      net.layers.push_back(std::move(L));
+    if (p.find("layers")) {
+      Mlp net;
+      for (const auto& lj : p.at("layers").items) {
+        DenseLayer L;
+        L.out = lj.at("rows").i32();
+        L.in = lj.at("cols").i32();
+        L.w = lj.at("weights").doubles();
+        L.b = lj.at("biases").doubles();
+        if (L.w.size() != std::size_t(L.in) * std::size_t(L.out) || L.b.size() != std::size_t(L.out))
+          throw LoadError("layer shape does not match its weight payload");
+        net.layers.push_back(std::move(L));
+      }
+      if (net.layers.empty()) throw LoadError("model has no layers");
+      m.payload = std::move(net);
+    } else if (p.find("linear")) {
+      LinearModel lin;
+      lin.weights = p.at("linear").at("weights").doubles();
+      lin.intercept = p.at("linear").at("intercept").num();
+      m.payload = std::move(lin);
+    } else if (p.find("forest")) {
+      Forest forest;
+      for (const auto& tj : p.at("forest").items) {
+        Tree t;
+        for (const auto& nj : tj.items)
+          t.nodes.push_back({nj.at("feature").i32(), nj.at("threshold").num(), nj.at("left").i32(),
+                             nj.at("right").i32(), nj.at("value").num()});
+        if (t.nodes.empty()) throw LoadError("forest tree has no nodes");
+        forest.trees.push_back(std::move(t));
+      }
+      if (forest.trees.empty()) throw LoadError("forest has no trees");
+      m.payload = std::move(forest);
+    } else {
+      throw LoadError("model payload missing (expected layers, linear, or forest)");
     }
-    if (net.layers.empty()) throw LoadError("model has no layers");
-    m.payload = std::move(net);
     if (const Json* mt = j.find("metrics"))
       if (const Json* lt = mt->find("loss_trace")) m.loss_trace = lt->doubles();
     return m;

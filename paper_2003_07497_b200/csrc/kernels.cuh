@@ -136,3 +136,62 @@ const char* measure_variant_name(int kind, int idx);
 int measure_instances(int kind, const char* variant, int n, const double* feats, int warmups, int reps,
                       uint64_t seed, double* runtime_s, double* checksum, cudaStream_t s, std::string& err);
 }  // namespace lann
+
+namespace lann {
+// baselines.cu — const / lrc least squares and the nlrc forest
+struct LinearArgs {
+  int n_models;
+  const int* n_rows;
+  const int* n_feats;         // columns of the design (1 for const)
+  const int64_t* row_offset;
+  const double* X;            // raw features [rows][LANN_ROW]
+  const double* y;            // raw runtimes
+  double ridge;
+  double* weights;            // [n_models][LANN_ROW]
+  double* intercept;
+  int* status;                // 0 ok, 1 singular despite ridge (FitError)
+};
+struct PredictLinearArgs {
+  int64_t n_rows;
+  const double* rows;         // [n][LANN_ROW] raw features
+  const int* row_model;
+  const int* n_feats;
+  const double* weights;
+  const double* intercept;
+  double* out;
+};
+struct ForestArgs {
+  int n_models, trees, max_depth, min_samples_split, max_rows;
+  const int* n_rows;
+  const int* n_feats;
+  const int64_t* row_offset;
+  const double* X;
+  const double* y;
+  const uint16_t* bootstrap;  // [model][tree][max_rows] sorted sample indices
+  int* node_feature;          // [model][tree][2 max_rows], breadth-first
+  double* node_threshold;
+  int* node_left;
+  int* node_right;
+  double* node_value;
+  int* node_count;            // [model][tree]
+  double* scratch_sse;        // [model][tree][max_rows][LANN_ROW]
+  double* scratch_thr;
+};
+struct PredictForestArgs {
+  int64_t n_rows;
+  const double* rows;
+  const int* row_model;
+  int trees, nodes_per_tree;
+  const int* node_feature;    // [model][tree][nodes_per_tree]
+  const double* node_threshold;
+  const int* node_left;
+  const int* node_right;
+  const double* node_value;
+  double* out;
+};
+void launch_fit_linear(const LinearArgs& a, cudaStream_t s);
+void launch_predict_linear(const PredictLinearArgs& a, cudaStream_t s);
+size_t forest_smem_bytes(int max_rows);
+void launch_fit_forest(const ForestArgs& a, cudaStream_t s);
+void launch_predict_forest(const PredictForestArgs& a, cudaStream_t s);
+}  // namespace lann

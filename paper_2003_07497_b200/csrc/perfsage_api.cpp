@@ -8,6 +8,7 @@
 #include <bit>
 #include <cmath>
 #include <limits>
+#include <map>
 #include <memory>
 
 #include "../../include/lann_engine.h"
@@ -281,7 +282,11 @@ std::vector<double> flatten_params(const Mlp& net) {
   return flat;
 }
 
-int param_count(const TrainedModel& m) { return std::get<Mlp>(m.payload).param_count(); }
+int param_count(const TrainedModel& m) {
+  const auto* net = std::get_if<Mlp>(&m.payload);
+  if (!net) throw ParamError("param_count is defined for NN-family models only");
+  return net->param_count();
+}
 
 namespace {
 
@@ -353,8 +358,9 @@ Prepared prepare(const datagen::Dataset& train, const ModelConfig& config) {
 
 }  // namespace
 
-std::vector<TrainedModel> train_population(const std::vector<const datagen::Dataset*>& train,
-                                           const std::vector<ModelConfig>& configs) {
+namespace {
+std::vector<TrainedModel> train_nn_population(const std::vector<const datagen::Dataset*>& train,
+                                              const std::vector<ModelConfig>& configs) {
   if (train.size() != configs.size()) throw ParamError("one dataset per model config");
   if (train.empty()) return {};
   std::vector<Prepared> prep;
@@ -425,25 +431,197 @@ std::vector<TrainedModel> train_population(const std::vector<const datagen::Data
   return out;
 }
 
+// models.cpp:176-182 — the raw design matrix of a baseline family
+struct Design {
+  std::vector<std::vector<double>> X;
+  std::vector<double> y;
+};
+Design assemble(const datagen::Dataset& train, ModelFamily family) {
+  if (train.samples.size() < 2) throw ParamError("training needs at least 2 samples");
+  Design d;
+  for (const auto& smp : train.samples) {
+    d.X.push_back(model_features(smp, family));
+    d.y.push_back(smp.runtime_s);
+  }
+  if (d.X[0].size() > LANN_ROW) throw ParamError("model inputs must lie in 1..8");
+  return d;
+}
+
+TrainedModel base_model(const datagen::Dataset& train, const ModelConfig& config) {
+  TrainedModel m;
+  m.config = config;
+  m.kind = train.kind;
+  m.schema = schema_of(train, config.family);
+  return m;
+}
+
+struct PackedDesign {
+  std::vector<std::int32_t> rows, feats;
+  std::vector<std::int64_t> off;
+  std::vector<double> X, y;
+  lann_design view() const {
+    return {std::int32_t(rows.size()), rows.data(), feats.data(), off.data(), X.data(), y.data()};
+  }
+  void add(const Design& d) {
+    off.push_back(std::int64_t(y.size()));
+    rows.push_back(std::int32_t(d.y.size()));
+    feats.push_back(std::int32_t(d.X[0].size()));
+    for (const auto& r : d.X) {
+      double row[LANN_ROW] = {0};
+      std::copy(r.begin(), r.end(), row);
+      X.insert(X.end(), row, row + LANN_ROW);
+    }
+    y.insert(y.end(), d.y.begin(), d.y.end());
+  }
+};
+
+constexpr double kRidge = 1e-8;  // models.cpp:276
+
+// const + lrc (models.cpp:305-320): one least-squares launch for all of them
+void fit_linear_batch(const std::vector<const datagen::Dataset*>& train, const std::vector<ModelConfig>& cfgs,
+                      const std::vector<int>& idx, std::vector<TrainedModel>& out) {
+  PackedDesign pd;
+  for (int i : idx) pd.add(assemble(*train[i], cfgs[i].family));
+  const int M = int(idx.size());
+  std::vector<double> w(std::size_t(M) * LANN_ROW), b(M);
+  std::vector<std::int32_t> st(M);
+  lann_engine* e = engine::get();
+  const lann_design dv = pd.view();
+  const int rc = lann_fit_linear(e, &dv, kRidge, w.data(), b.data(), st.data());
+  if (rc == LANN_DOMAIN_ERROR) throw FitError("singular design matrix despite ridge");
+  check(rc, e);
+  for (int k = 0; k < M; ++k) {
+    TrainedModel m = base_model(*train[idx[k]], cfgs[idx[k]]);
+    LinearModel lin;
+    lin.weights.assign(w.begin() + std::ptrdiff_t(k) * LANN_ROW, w.begin() + std::ptrdiff_t(k) * LANN_ROW + pd.feats[k]);
+    lin.intercept = b[k];
+    m.payload = std::move(lin);
+    out[idx[k]] = std::move(m);
+  }
+}
+
+// nlrc (models.cpp:322-333): one forest launch, models x trees CTAs; trees per launch must agree,
+// so configs are grouped by (trees, depth)
+void fit_forest_batch(const std::vector<const datagen::Dataset*>& train, const std::vector<ModelConfig>& cfgs,
+                      const std::vector<int>& idx, std::vector<TrainedModel>& out) {
+  std::map<std::pair<int, int>, std::vector<int>> groups;
+  for (int i : idx) groups[{cfgs[i].forest_trees, cfgs[i].forest_depth}].push_back(i);
+  for (const auto& [key, members] : groups) {
+    PackedDesign pd;
+    std::vector<std::uint64_t> seeds;
+    int max_rows = 0;
+    for (int i : members) {
+      const Design d = assemble(*train[i], ModelFamily::NlrC);
+      cfgs[i].validate(int(d.X[0].size()));
+      if (d.y.size() < 10) throw ParamError("forest needs at least 10 samples");
+      pd.add(d);
+      seeds.push_back(cfgs[i].seed);
+      max_rows = std::max(max_rows, int(d.y.size()));
+    }
+    const int M = int(members.size()), trees = key.first, npt = 2 * max_rows;
+    const std::size_t total = std::size_t(M) * trees * npt;
+    std::vector<std::int32_t> nf(total), nl(total), nr(total), nc(std::size_t(M) * trees);
+    std::vector<double> nt(total), nv(total);
+    lann_engine* e = engine::get();
+    const lann_design dv = pd.view();
+    check(lann_fit_forest(e, &dv, trees, key.second, 2, seeds.data(), nf.data(), nt.data(), nl.data(), nr.data(),
+                          nv.data(), nc.data()),
+          e);
+    for (int k = 0; k < M; ++k) {
+      TrainedModel m = base_model(*train[members[k]], cfgs[members[k]]);
+      Forest forest;
+      for (int t = 0; t < trees; ++t) {
+        Tree tree;
+        const std::size_t base = (std::size_t(k) * trees + t) * npt;
+        for (int v = 0; v < nc[std::size_t(k) * trees + t]; ++v)
+          tree.nodes.push_back({nf[base + v], nt[base + v], nl[base + v], nr[base + v], nv[base + v]});
+        forest.trees.push_back(std::move(tree));
+      }
+      m.payload = std::move(forest);
+      out[members[k]] = std::move(m);
+    }
+  }
+}
+}  // namespace
+
+std::vector<TrainedModel> train_population(const std::vector<const datagen::Dataset*>& train,
+                                           const std::vector<ModelConfig>& configs) {
+  if (train.size() != configs.size()) throw ParamError("one dataset per model config");
+  std::vector<int> nn, lin, forest;
+  for (std::size_t i = 0; i < configs.size(); ++i) {
+    switch (configs[i].family) {
+      case ModelFamily::NnC:
+      case ModelFamily::Nn: nn.push_back(int(i)); break;
+      case ModelFamily::Const:
+      case ModelFamily::LrC: lin.push_back(int(i)); break;
+      case ModelFamily::NlrC: forest.push_back(int(i)); break;
+    }
+  }
+  std::vector<TrainedModel> out(configs.size());
+  if (!nn.empty()) {
+    std::vector<const datagen::Dataset*> t;
+    std::vector<ModelConfig> c;
+    for (int i : nn) {
+      t.push_back(train[i]);
+      c.push_back(configs[i]);
+    }
+    auto res = train_nn_population(t, c);
+    for (std::size_t k = 0; k < nn.size(); ++k) out[nn[k]] = std::move(res[k]);
+  }
+  if (!lin.empty()) fit_linear_batch(train, configs, lin, out);
+  if (!forest.empty()) fit_forest_batch(train, configs, forest, out);
+  return out;
+}
+
 TrainedModel train_nn(const datagen::Dataset& train, const ModelConfig& config) {
+  if (config.family != ModelFamily::NnC && config.family != ModelFamily::Nn)
+    throw ParamError("train_nn expects an NN family config");
+  return std::move(train_population({&train}, {config}).front());
+}
+
+TrainedModel train_const(const datagen::Dataset& train, const ModelConfig& config) {
+  if (config.family != ModelFamily::Const) throw ParamError("train_const expects family const");
+  return std::move(train_population({&train}, {config}).front());
+}
+
+TrainedModel train_lrc(const datagen::Dataset& train, const ModelConfig& config) {
+  if (config.family != ModelFamily::LrC) throw ParamError("train_lrc expects family lrc");
+  return std::move(train_population({&train}, {config}).front());
+}
+
+TrainedModel train_nlrc(const datagen::Dataset& train, const ModelConfig& config) {
+  if (config.family != ModelFamily::NlrC) throw ParamError("train_nlrc expects family nlrc");
   return std::move(train_population({&train}, {config}).front());
 }
 
 TrainedModel train_model(const datagen::Dataset& train, const ModelConfig& config) {
-  if (config.family != ModelFamily::NnC && config.family != ModelFamily::Nn)
-    throw ParamError("this engine trains the NN families (nnc, nn); const/lrc/nlrc are out of scope");
-  return train_nn(train, config);
+  return std::move(train_population({&train}, {config}).front());
 }
 
-std::vector<std::vector<double>> predict_population(const std::vector<const TrainedModel*>& models,
-                                                    const std::vector<const datagen::Dataset*>& data) {
-  if (models.size() != data.size()) throw ParamError("one dataset per model");
-  const int M = int(models.size());
+namespace {
+// rows of one model's dataset in its model_features layout (schema-checked, models.cpp:347-350)
+void append_rows(const TrainedModel& t, const datagen::Dataset& data, int m, std::vector<double>& rows,
+                 std::vector<std::int32_t>& row_model) {
+  for (const auto& smp : data.samples) {
+    const auto f = model_features(smp, t.config.family);
+    if (f.size() != t.schema.size())
+      throw SchemaError("feature vector length " + std::to_string(f.size()) + " does not match model schema of " +
+                        std::to_string(t.schema.size()));
+    double row[LANN_ROW] = {0};
+    std::copy(f.begin(), f.end(), row);
+    rows.insert(rows.end(), row, row + LANN_ROW);
+    row_model.push_back(m);
+  }
+}
+
+void predict_mlp(const std::vector<const TrainedModel*>& models, const std::vector<const datagen::Dataset*>& data,
+                 const std::vector<int>& idx, std::vector<std::vector<double>>& res) {
+  const int M = int(idx.size());
   std::vector<std::int32_t> n_in(M), h1(M), h2(M), logt(M), row_model;
   std::vector<std::int64_t> poff(M);
   std::vector<double> params, norm(std::size_t(M) * 18, 0.0), rows;
   for (int m = 0; m < M; ++m) {
-    const TrainedModel& t = *models[m];
+    const TrainedModel& t = *models[idx[m]];
     const Mlp& net = std::get<Mlp>(t.payload);
     n_in[m] = net.input_dim();
     h1[m] = net.layers.size() > 1 ? net.layers[0].out : 1;
@@ -458,16 +636,7 @@ std::vector<std::vector<double>> predict_population(const std::vector<const Trai
     }
     norm[18 * m + 16] = t.norm.t_min;
     norm[18 * m + 17] = t.norm.t_max;
-    for (const auto& s : data[m]->samples) {
-      const auto f = model_features(s, t.config.family);
-      if (f.size() != t.schema.size())
-        throw SchemaError("feature vector length " + std::to_string(f.size()) +
-                          " does not match model schema of " + std::to_string(t.schema.size()));
-      double row[LANN_ROW] = {0};
-      std::copy(f.begin(), f.end(), row);
-      rows.insert(rows.end(), row, row + LANN_ROW);
-      row_model.push_back(m);
-    }
+    append_rows(t, *data[idx[m]], m, rows, row_model);
   }
   std::vector<double> out(row_model.size());
   if (!row_model.empty()) {
@@ -476,10 +645,98 @@ std::vector<std::vector<double>> predict_population(const std::vector<const Trai
     lann_engine* e = engine::get();
     check(lann_predict(e, &ms, std::int64_t(row_model.size()), rows.data(), row_model.data(), out.data()), e);
   }
-  std::vector<std::vector<double>> res(M);
   std::size_t k = 0;
   for (int m = 0; m < M; ++m)
-    for (std::size_t i = 0; i < data[m]->samples.size(); ++i) res[m].push_back(out[k++]);
+    for (std::size_t i = 0; i < data[idx[m]]->samples.size(); ++i) res[idx[m]].push_back(out[k++]);
+}
+
+void predict_linear(const std::vector<const TrainedModel*>& models, const std::vector<const datagen::Dataset*>& data,
+                    const std::vector<int>& idx, std::vector<std::vector<double>>& res) {
+  const int M = int(idx.size());
+  std::vector<std::int32_t> nf(M), row_model;
+  std::vector<double> w(std::size_t(M) * LANN_ROW, 0.0), b(M), rows;
+  for (int m = 0; m < M; ++m) {
+    const TrainedModel& t = *models[idx[m]];
+    const auto& lin = std::get<LinearModel>(t.payload);
+    if (lin.weights.size() != t.schema.size() || lin.weights.size() > LANN_ROW)
+      throw SchemaError("linear model weights do not match its schema");
+    nf[m] = std::int32_t(lin.weights.size());
+    std::copy(lin.weights.begin(), lin.weights.end(), w.begin() + std::ptrdiff_t(m) * LANN_ROW);
+    b[m] = lin.intercept;
+    append_rows(t, *data[idx[m]], m, rows, row_model);
+  }
+  std::vector<double> out(row_model.size());
+  if (!row_model.empty()) {
+    lann_engine* e = engine::get();
+    check(lann_predict_linear(e, M, nf.data(), w.data(), b.data(), std::int64_t(row_model.size()), rows.data(),
+                              row_model.data(), out.data()),
+          e);
+  }
+  std::size_t k = 0;
+  for (int m = 0; m < M; ++m)
+    for (std::size_t i = 0; i < data[idx[m]]->samples.size(); ++i) res[idx[m]].push_back(out[k++]);
+}
+
+void predict_forest(const std::vector<const TrainedModel*>& models, const std::vector<const datagen::Dataset*>& data,
+                    const std::vector<int>& idx, std::vector<std::vector<double>>& res) {
+  std::map<std::size_t, std::vector<int>> by_trees;  // one launch per tree count
+  for (int i : idx) {
+    const auto& f = std::get<Forest>(models[i]->payload);
+    if (f.trees.empty()) throw ParamError("empty forest");
+    by_trees[f.trees.size()].push_back(i);
+  }
+  for (const auto& [trees, members] : by_trees) {
+    const int M = int(members.size());
+    int npt = 1;
+    for (int i : members)
+      for (const auto& t : std::get<Forest>(models[i]->payload).trees) npt = std::max(npt, int(t.nodes.size()));
+    const std::size_t total = std::size_t(M) * trees * npt;
+    std::vector<std::int32_t> nf(total, -1), nl(total, -1), nr(total, -1), row_model;
+    std::vector<double> nt(total, 0.0), nv(total, 0.0), rows;
+    for (int m = 0; m < M; ++m) {
+      const TrainedModel& tm = *models[members[m]];
+      const auto& f = std::get<Forest>(tm.payload);
+      for (std::size_t t = 0; t < trees; ++t) {
+        const auto& nodes = f.trees[t].nodes;
+        if (nodes.empty()) throw ParamError("forest tree has no nodes");
+        for (std::size_t v = 0; v < nodes.size(); ++v) {
+          const std::size_t o = (std::size_t(m) * trees + t) * npt + v;
+          nf[o] = nodes[v].feature;
+          nt[o] = nodes[v].threshold;
+          nl[o] = nodes[v].left;
+          nr[o] = nodes[v].right;
+          nv[o] = nodes[v].value;
+        }
+      }
+      append_rows(tm, *data[members[m]], m, rows, row_model);
+    }
+    std::vector<double> out(row_model.size());
+    if (!row_model.empty()) {
+      lann_engine* e = engine::get();
+      check(lann_predict_forest(e, M, int(trees), npt, nf.data(), nt.data(), nl.data(), nr.data(), nv.data(),
+                                std::int64_t(row_model.size()), rows.data(), row_model.data(), out.data()),
+            e);
+    }
+    std::size_t k = 0;
+    for (int m = 0; m < M; ++m)
+      for (std::size_t i = 0; i < data[members[m]]->samples.size(); ++i) res[members[m]].push_back(out[k++]);
+  }
+}
+}  // namespace
+
+std::vector<std::vector<double>> predict_population(const std::vector<const TrainedModel*>& models,
+                                                    const std::vector<const datagen::Dataset*>& data) {
+  if (models.size() != data.size()) throw ParamError("one dataset per model");
+  std::vector<int> mlp, lin, forest;
+  for (std::size_t i = 0; i < models.size(); ++i) {
+    if (std::holds_alternative<Mlp>(models[i]->payload)) mlp.push_back(int(i));
+    else if (std::holds_alternative<LinearModel>(models[i]->payload)) lin.push_back(int(i));
+    else forest.push_back(int(i));
+  }
+  std::vector<std::vector<double>> res(models.size());
+  if (!mlp.empty()) predict_mlp(models, data, mlp, res);
+  if (!lin.empty()) predict_linear(models, data, lin, res);
+  if (!forest.empty()) predict_forest(models, data, forest, res);
   return res;
 }
 

@@ -77,6 +77,32 @@ int main(int argc, char** argv) {
       m.norm.t_max = 3.0000000000000004;
       for (int e = 0; e < 50; ++e) m.loss_trace.push_back(std::ldexp(u(rng) + 1.5, -e));
       models::save_model(m, argv[2]);
+    } else if (mode == "model-synth-linear" || mode == "model-synth-forest") {
+      std::mt19937_64 rng(std::strtoull(argv[3], nullptr, 10));
+      std::uniform_real_distribution<double> u(-1.0, 1.0);
+      models::TrainedModel m;
+      m.kind = kernels::KernelKind::MV;
+      m.schema = {"m", "n", "d", "c"};
+      if (mode == "model-synth-linear") {
+        m.config = models::default_config(m.kind, models::ModelFamily::LrC);
+        models::LinearModel lin;
+        lin.weights = {1e-300, -0.0, u(rng), 0.1};
+        lin.intercept = u(rng) * 1e-7;
+        m.payload = lin;
+      } else {
+        m.config = models::default_config(m.kind, models::ModelFamily::NlrC);
+        m.config.forest_trees = 3;
+        models::Forest f;
+        for (int t = 0; t < 3; ++t) {
+          models::Tree tree;
+          tree.nodes.push_back({int(t % 4), u(rng), 1, 2, u(rng)});
+          tree.nodes.push_back({-1, 0.0, -1, -1, u(rng) * 1e-9});
+          tree.nodes.push_back({-1, 0.0, -1, -1, 5e-324});
+          f.trees.push_back(tree);
+        }
+        m.payload = f;
+      }
+      models::save_model(m, argv[2]);
     } else if (mode == "model-dump") {
       const auto m = models::load_model(argv[2]);
       for (double v : m.norm.f_min) std::printf("%a\n", v);

@@ -189,3 +189,33 @@ def test_gen_external_protocol_errors(tmp_path):
         out = subprocess.run([CLI, "gen", "--external-cmd", cmd, "--kernel", "mm", "--count", "2", "--out",
                               str(tmp_path)], capture_output=True, text=True)
         assert out.returncode == 1 and what in out.stderr, (cmd, out.stderr)
+
+
+def _payload_hex(path):
+    p = json.load(open(path))["payload"]
+    if "linear" in p:
+        return [float(x).hex() for x in p["linear"]["weights"] + [p["linear"]["intercept"]]]
+    return [(n["feature"], float(n["threshold"]).hex(), n["left"], n["right"], float(n["value"]).hex())
+            for t in p["forest"] for n in t]
+
+
+@pytest.mark.parametrize("kind", ["linear", "forest"])
+def test_baseline_model_files_round_trip_through_the_reference(tmp_path, tool, reference, kind):
+    """const/lrc (payload.linear) and nlrc (payload.forest) model files: engine -> reference ->
+    engine leaves every weight, threshold and leaf value bit-identical."""
+    ours = tmp_path / "m.json"
+    run(tool, f"model-synth-{kind}", str(ours), "5")
+    back = tmp_path / "back.json"
+    assert reference.model_roundtrip(ours, back) == 0, reference.last_error()
+    assert _payload_hex(back) == _payload_hex(ours)
+    again = tmp_path / "again.json"
+    run(tool, "model-roundtrip", str(back), str(again))
+    assert _payload_hex(again) == _payload_hex(ours)
+    assert json.load(open(again))["metrics"] is None
+
+
+@pytest.mark.parametrize("fam", ["const", "lrc"])
+def test_reference_baseline_files_load(tmp_path, tool, fam):
+    src = os.path.join(GOLD, f"ref_model_w0_s3_{fam}.json")
+    run(tool, "model-roundtrip", src, str(tmp_path / "m.json"))
+    assert _payload_hex(tmp_path / "m.json") == _payload_hex(src)

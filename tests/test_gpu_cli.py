@@ -85,12 +85,12 @@ def test_cli_eval_matches_the_reference_report(trained, tmp_path):
     assert row["kernel"] == "mm" and row["model_family"] == "nnc" and row["variant"] == "dense_threaded@cpu4"
 
 
-def test_cli_compare_batches_both_families(trained, tmp_path):
+def test_cli_compare_nnc_row_is_train_plus_eval(trained, tmp_path):
     t = FMT["train"]
     out = cli("compare", "--data", REF_CSV, "--seed", t["seed"], "--epochs", t["epochs"], "--precision", "fp64",
               "--out", tmp_path)
     rows = read_reports(tmp_path / "compare.csv")
-    assert [r["model_family"] for r in rows] == ["nnc", "nn"]
+    assert [r["model_family"] for r in rows][:2] == ["nnc", "nn"]
     assert float(rows[0]["mape_thresholded"]) == FMT["eval_test"]["mape_thresholded"]
     assert "best thresholded MAPE" in out
 
@@ -157,3 +157,47 @@ def test_cli_select_variants(tmp_path):
         rows = list(csv.DictReader(f))
     assert sum(int(r["chosen"]) for r in rows) == 200000
     assert "predictions/s" in out
+
+
+def _linear(path):
+    p = json.load(open(path))["payload"]["linear"]
+    return [float(w).hex() for w in p["weights"]] + [float(p["intercept"]).hex()]
+
+
+@pytest.mark.parametrize("fam", ["const", "lrc"])
+def test_cli_least_squares_baselines_are_the_reference(tmp_path, fam):
+    """const / lrc (models.cpp:305-320) fitted on the GPU: weights and intercept bit-identical to
+    the reference's model file, and its test-set report identical."""
+    cli("train", "--data", REF_CSV, "--seed", 3, "--family", fam, "--out", tmp_path)
+    assert _linear(tmp_path / f"model_{fam}.json") == _linear(os.path.join(GOLD, FMT["baselines"][fam]["model"]))
+    cli("eval", "--model", tmp_path / f"model_{fam}.json", "--data", tmp_path / "test.csv", "--out", tmp_path / "e")
+    (row,) = read_reports(tmp_path / "e" / "eval.csv")
+    ref = FMT["baselines"][fam]["eval_test"]
+    assert (float(row["mape_full"]), float(row["mape_thresholded"]), float(row["rho"]), int(row["n_kept"])) == (
+        ref["mape_full"], ref["mape_thresholded"], ref["rho"], ref["n_kept"])
+
+
+def test_cli_forest_baseline_tracks_the_reference(tmp_path):
+    """nlrc (forest.cpp) on the GPU: the same bootstraps and split rule as the reference; trees
+    agree node for node except where equal feature values are summed in a different order (a
+    last-bit SSE difference can flip a tied split), so the report matches to tolerance."""
+    cli("train", "--data", REF_CSV, "--seed", 3, "--family", "nlrc", "--out", tmp_path)
+    forest = json.load(open(tmp_path / "model_nlrc.json"))["payload"]["forest"]
+    counts = [len(t) for t in forest]
+    ref_counts = FMT["baselines"]["nlrc"]["tree_node_counts"]
+    assert len(counts) == len(ref_counts) == 100
+    same = sum(a == b for a, b in zip(counts, ref_counts))
+    assert same >= 90, (same, counts[:10], ref_counts[:10])
+    cli("eval", "--model", tmp_path / "model_nlrc.json", "--data", tmp_path / "test.csv", "--out", tmp_path / "e")
+    (row,) = read_reports(tmp_path / "e" / "eval.csv")
+    ref = FMT["baselines"]["nlrc"]["eval_test"]
+    assert abs(float(row["mape_thresholded"]) - ref["mape_thresholded"]) <= 0.1
+    assert abs(float(row["rho"]) - ref["rho"]) <= 1e-3
+
+
+def test_cli_compare_runs_all_five_families(tmp_path):
+    out = cli("compare", "--data", REF_CSV, "--seed", 3, "--epochs", 300, "--precision", "fp32", "--out", tmp_path)
+    rows = read_reports(tmp_path / "compare.csv")
+    assert [r["model_family"] for r in rows] == ["nnc", "nn", "const", "lrc", "nlrc"]
+    assert float(rows[2]["mape_thresholded"]) == FMT["baselines"]["const"]["eval_test"]["mape_thresholded"]
+    assert "best thresholded MAPE" in out

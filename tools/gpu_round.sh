@@ -18,7 +18,7 @@ if [ "${PROFILE:-1}" = "1" ]; then
   # FP64 exact (parity mode) and the config-4 scorer
   timeout 600 $NCU -k "regex:exact<\(int\)1, \(int\)6" -c 1 -o gpurun_out/prof_fp64 -f \
     python tools/prof_pop.py fp64 0 0.1 > gpurun_out/ncu_fp64.log 2>&1
-  timeout 600 $NCU -k "regex:select_variants_fast" -c 1 -o gpurun_out/prof_select -f \
+  timeout 600 $NCU -k "regex:select_variants_fast" --launch-skip 1 -c 1 -o gpurun_out/prof_select -f \
     python bench.py --steps 1 --warmup 0 --no-cpu-baseline > gpurun_out/ncu_select.log 2>&1
   python tools/sweep_parts.py 256 > gpurun_out/sweep.txt 2>&1
   python tools/prof_sweep.py 256 >> gpurun_out/sweep.txt 2>&1

@@ -17,6 +17,8 @@
 //    butterfly, after which every lane applies the identical Adam step.
 //  * train_fp32_h8_kernel<K> — the same mapping for the one-hidden-layer-of-8
 //    prediction nets with hidden units paired on the packed FP32 FMA (FFMA2).
+//  * train_fp32_h55_kernel<K> — the same for the 5-5 selection nets (two FFMA2 pairs and
+//    one scalar unit per layer).
 //  * train_fp32_cta_kernel<W> — FEW models (the 48-combo population): one model
 //    per CTA of W warps so the per-epoch LATENCY is minimised; threads own
 //    samples (two per thread, interleaved in one basic block); gradients are
@@ -524,6 +526,269 @@ __device__ __forceinline__ void lean_rs_map(int n, int lane, int& base, int& val
 }
 
 // ---------------------------------------------------------------------------------
+// Packed variant of train_fp32_kernel for the two-hidden-layer 5-5 selection nets (the sweep's
+// blur part): units 0-3 of each layer run as two FFMA2 pairs, unit 4 as a scalar FFMA (no zero
+// padding, so no pad moves), the broadcast operand being the input / layer-1 activation. Same
+// mapping as train_fp32_kernel<K> (K lanes per model split the samples, butterfly over K,
+// identical Adam in every lane); moments in shared memory in the canonical parameter order.
+template <int I, int K>
+__global__ void __launch_bounds__(32) train_fp32_h55_kernel(TrainF32Args a) {
+  using N = Net<I, 5, 5>;
+  constexpr int P = N::P;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ uint64_t bar;
+  const int lane = threadIdx.x;
+  const int first = a.group_first[blockIdx.x];
+  const int count = a.group_count[blockIdx.x];
+  const int slot = lane / K, sub = lane % K;
+  const bool active = slot < count;
+  const int m = a.sorted_model[first + (active ? slot : 0)];
+  const int tile = a.model_tile[m];
+  const int rows = a.tile_rows[tile];
+  const int E = a.epochs[m];
+  float* trow = reinterpret_cast<float*>(smem_raw);  // [rows][8]
+  float* adam = trow + (size_t)rows * 8;            // [2][P][32]
+  if (lane == 0) mbar_init(&bar);
+  __syncwarp();
+  if (lane == 0) tma_load_tile(trow, a.rows + a.tile_offset[tile] * 8, (uint32_t)rows * 32u, &bar);
+
+  const double* gp = a.params + a.param_offset[m];
+  auto W = [&](int p) { return (float)gp[p]; };
+  // layer 1: pairs (0,1), (2,3) + scalar unit 4; likewise layer 2 and the output weights
+  f32x2 w1p[I][2], b1p[2], w2p[5][2], b2p[2], w3p[2];
+  float w1s[I], b1s, w2s[5], b2s, w3s, b3;
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+#pragma unroll
+    for (int i = 0; i < I; ++i) w1p[i][q] = pk(W(N::L1W + (2 * q) * I + i), W(N::L1W + (2 * q + 1) * I + i));
+    b1p[q] = pk(W(N::L1B + 2 * q), W(N::L1B + 2 * q + 1));
+#pragma unroll
+    for (int h = 0; h < 5; ++h) w2p[h][q] = pk(W(N::L2W + (2 * q) * 5 + h), W(N::L2W + (2 * q + 1) * 5 + h));
+    b2p[q] = pk(W(N::L2B + 2 * q), W(N::L2B + 2 * q + 1));
+    w3p[q] = pk(W(N::L3W + 2 * q), W(N::L3W + 2 * q + 1));
+  }
+#pragma unroll
+  for (int i = 0; i < I; ++i) w1s[i] = W(N::L1W + 4 * I + i);
+  b1s = W(N::L1B + 4);
+#pragma unroll
+  for (int h = 0; h < 5; ++h) w2s[h] = W(N::L2W + 4 * 5 + h);
+  b2s = W(N::L2B + 4);
+  w3s = W(N::L3W + 4);
+  b3 = W(N::L3B);
+  for (int p = 0; p < P; ++p) {
+    adam[p * 32 + lane] = 0.f;
+    adam[(P + p) * 32 + lane] = 0.f;
+  }
+  const float lr = (float)a.lr[m];
+  const float scale = 2.0f / (float)rows;
+  const float inv_n = 1.0f / (float)rows;
+  double* trace = (a.loss_trace && active) ? a.loss_trace + a.trace_offset[m] : nullptr;
+  int bad = -1;
+  float last = 0.f, pw1 = 1.f, pw2 = 1.f;
+  mbar_wait(&bar, 0);
+  __syncwarp();
+
+  for (int e = 0; e < E; ++e) {
+    const f32x2 zero2 = pk(0.f, 0.f);
+    f32x2 g1p[I][2], gb1p[2], g2p[5][2], gb2p[2], g3p[2];
+    float g1s[I], gb1s = 0.f, g2s[5], gb2s = 0.f, g3s = 0.f, gb3 = 0.f, loss = 0.f;
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+#pragma unroll
+      for (int i = 0; i < I; ++i) g1p[i][q] = zero2;
+#pragma unroll
+      for (int h = 0; h < 5; ++h) g2p[h][q] = zero2;
+      gb1p[q] = gb2p[q] = g3p[q] = zero2;
+    }
+#pragma unroll
+    for (int i = 0; i < I; ++i) g1s[i] = 0.f;
+#pragma unroll
+    for (int h = 0; h < 5; ++h) g2s[h] = 0.f;
+    for (int s = sub; s < rows; s += K) {
+      float xv[8];
+      load_row(trow, s, xv);
+      // layer 1
+      f32x2 z1p[2];
+      float z1s = b1s;
+#pragma unroll
+      for (int q = 0; q < 2; ++q) z1p[q] = b1p[q];
+#pragma unroll
+      for (int i = 0; i < I; ++i) {
+        z1p[0] = fma2(w1p[i][0], pk(xv[i], xv[i]), z1p[0]);
+        z1p[1] = fma2(w1p[i][1], pk(xv[i], xv[i]), z1p[1]);
+        z1s = fmaf(w1s[i], xv[i], z1s);
+      }
+      float a1[5];
+      upk(z1p[0], a1[0], a1[1]);
+      upk(z1p[1], a1[2], a1[3]);
+      a1[4] = z1s;
+#pragma unroll
+      for (int h = 0; h < 5; ++h) a1[h] = fmaxf(a1[h], 0.f);
+      // layer 2
+      f32x2 z2p[2] = {b2p[0], b2p[1]};
+      float z2s = b2s;
+#pragma unroll
+      for (int h = 0; h < 5; ++h) {
+        z2p[0] = fma2(w2p[h][0], pk(a1[h], a1[h]), z2p[0]);
+        z2p[1] = fma2(w2p[h][1], pk(a1[h], a1[h]), z2p[1]);
+        z2s = fmaf(w2s[h], a1[h], z2s);
+      }
+      float a2[5];
+      upk(z2p[0], a2[0], a2[1]);
+      upk(z2p[1], a2[2], a2[3]);
+      a2[4] = z2s;
+#pragma unroll
+      for (int o = 0; o < 5; ++o) a2[o] = fmaxf(a2[o], 0.f);
+      const f32x2 a2p0 = pk(a2[0], a2[1]), a2p1 = pk(a2[2], a2[3]);
+      // output
+      float o0, o1;
+      upk(fma2(w3p[1], a2p1, mul2(w3p[0], a2p0)), o0, o1);
+      const float out = (o0 + o1) + fmaf(w3s, a2[4], b3);
+      const float err = out - xv[7];
+      loss = fmaf(err, err, loss);
+      const float d = err * scale;
+      // backward
+      gb3 += d;
+      g3p[0] = fma2(a2p0, pk(d, d), g3p[0]);
+      g3p[1] = fma2(a2p1, pk(d, d), g3p[1]);
+      g3s = fmaf(a2[4], d, g3s);
+      float d2[5];
+      upk(mul2(w3p[0], pk(d, d)), d2[0], d2[1]);
+      upk(mul2(w3p[1], pk(d, d)), d2[2], d2[3]);
+      d2[4] = w3s * d;
+#pragma unroll
+      for (int o = 0; o < 5; ++o) d2[o] = a2[o] > 0.f ? d2[o] : 0.f;
+      const f32x2 d2p0 = pk(d2[0], d2[1]), d2p1 = pk(d2[2], d2[3]);
+      gb2p[0] = add2(gb2p[0], d2p0);
+      gb2p[1] = add2(gb2p[1], d2p1);
+      gb2s += d2[4];
+      float d1[5];
+#pragma unroll
+      for (int h = 0; h < 5; ++h) {
+        g2p[h][0] = fma2(d2p0, pk(a1[h], a1[h]), g2p[h][0]);
+        g2p[h][1] = fma2(d2p1, pk(a1[h], a1[h]), g2p[h][1]);
+        g2s[h] = fmaf(d2[4], a1[h], g2s[h]);
+        float t0, t1;
+        upk(fma2(w2p[h][1], d2p1, mul2(w2p[h][0], d2p0)), t0, t1);
+        const float acc = (t0 + t1) + w2s[h] * d2[4];
+        d1[h] = a1[h] > 0.f ? acc : 0.f;
+      }
+      const f32x2 d1p0 = pk(d1[0], d1[1]), d1p1 = pk(d1[2], d1[3]);
+      gb1p[0] = add2(gb1p[0], d1p0);
+      gb1p[1] = add2(gb1p[1], d1p1);
+      gb1s += d1[4];
+#pragma unroll
+      for (int i = 0; i < I; ++i) {
+        g1p[i][0] = fma2(d1p0, pk(xv[i], xv[i]), g1p[i][0]);
+        g1p[i][1] = fma2(d1p1, pk(xv[i], xv[i]), g1p[i][1]);
+        g1s[i] = fmaf(d1[4], xv[i], g1s[i]);
+      }
+    }
+    // sum the K per-lane partials of each model
+#pragma unroll
+    for (int off = 1; off < K; off <<= 1) {
+      auto red2 = [&](f32x2& v) {
+        float lo, hi;
+        upk(v, lo, hi);
+        lo += __shfl_xor_sync(0xffffffffu, lo, off);
+        hi += __shfl_xor_sync(0xffffffffu, hi, off);
+        v = pk(lo, hi);
+      };
+      auto red1 = [&](float& v) { v += __shfl_xor_sync(0xffffffffu, v, off); };
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+#pragma unroll
+        for (int i = 0; i < I; ++i) red2(g1p[i][q]);
+#pragma unroll
+        for (int h = 0; h < 5; ++h) red2(g2p[h][q]);
+        red2(gb1p[q]);
+        red2(gb2p[q]);
+        red2(g3p[q]);
+      }
+#pragma unroll
+      for (int i = 0; i < I; ++i) red1(g1s[i]);
+#pragma unroll
+      for (int h = 0; h < 5; ++h) red1(g2s[h]);
+      red1(gb1s);
+      red1(gb2s);
+      red1(g3s);
+      red1(gb3);
+      red1(loss);
+    }
+    loss *= inv_n;
+    pw1 *= 0.9f;
+    pw2 *= 0.999f;
+    if (bad < 0) {
+      last = loss;
+      if (trace && sub == 0 && (e % a.trace_stride) == 0) trace[e / a.trace_stride] = (double)loss;
+      if (!isfinite(loss)) {
+        bad = e;
+      } else {
+        const float step = lr / (1.f - pw1), rb2 = 1.f / (1.f - pw2);
+        auto upd1 = [&](float& w, float g, int p) {
+          w -= adam_step(adam[p * 32 + lane], adam[(P + p) * 32 + lane], g, step, rb2);
+        };
+        auto upd2 = [&](f32x2& wv, f32x2 gv, int p0, int p1) {
+          float w0, w1v, g0, g1v;
+          upk(wv, w0, w1v);
+          upk(gv, g0, g1v);
+          upd1(w0, g0, p0);
+          upd1(w1v, g1v, p1);
+          wv = pk(w0, w1v);
+        };
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+#pragma unroll
+          for (int i = 0; i < I; ++i) upd2(w1p[i][q], g1p[i][q], N::L1W + 2 * q * I + i, N::L1W + (2 * q + 1) * I + i);
+          upd2(b1p[q], gb1p[q], N::L1B + 2 * q, N::L1B + 2 * q + 1);
+#pragma unroll
+          for (int h = 0; h < 5; ++h) upd2(w2p[h][q], g2p[h][q], N::L2W + 2 * q * 5 + h, N::L2W + (2 * q + 1) * 5 + h);
+          upd2(b2p[q], gb2p[q], N::L2B + 2 * q, N::L2B + 2 * q + 1);
+          upd2(w3p[q], g3p[q], N::L3W + 2 * q, N::L3W + 2 * q + 1);
+        }
+#pragma unroll
+        for (int i = 0; i < I; ++i) upd1(w1s[i], g1s[i], N::L1W + 4 * I + i);
+        upd1(b1s, gb1s, N::L1B + 4);
+#pragma unroll
+        for (int h = 0; h < 5; ++h) upd1(w2s[h], g2s[h], N::L2W + 20 + h);
+        upd1(b2s, gb2s, N::L2B + 4);
+        upd1(w3s, g3s, N::L3W + 4);
+        upd1(b3, gb3, N::L3B);
+      }
+    }
+  }
+  if (active && sub == 0) {
+    double* outp = a.params + a.param_offset[m];
+    auto put2 = [&](f32x2 v, int p0, int p1) {
+      float x0, x1;
+      upk(v, x0, x1);
+      outp[p0] = x0;
+      outp[p1] = x1;
+    };
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+#pragma unroll
+      for (int i = 0; i < I; ++i) put2(w1p[i][q], N::L1W + 2 * q * I + i, N::L1W + (2 * q + 1) * I + i);
+      put2(b1p[q], N::L1B + 2 * q, N::L1B + 2 * q + 1);
+#pragma unroll
+      for (int h = 0; h < 5; ++h) put2(w2p[h][q], N::L2W + 2 * q * 5 + h, N::L2W + (2 * q + 1) * 5 + h);
+      put2(b2p[q], N::L2B + 2 * q, N::L2B + 2 * q + 1);
+      put2(w3p[q], N::L3W + 2 * q, N::L3W + 2 * q + 1);
+    }
+#pragma unroll
+    for (int i = 0; i < I; ++i) outp[N::L1W + 4 * I + i] = w1s[i];
+    outp[N::L1B + 4] = b1s;
+#pragma unroll
+    for (int h = 0; h < 5; ++h) outp[N::L2W + 20 + h] = w2s[h];
+    outp[N::L2B + 4] = b2s;
+    outp[N::L3W + 4] = w3s;
+    outp[N::L3B] = b3;
+    a.final_loss[m] = (double)last;
+    a.nonfinite_epoch[m] = bad;
+  }
+}
+
+// ---------------------------------------------------------------------------------
 template <int P>
 struct CtaLayout {
   static constexpr int PT = (P + 3) & ~3;  // transpose row stride (float4 writes, 4-wavefront STS.128)
@@ -724,6 +989,14 @@ void launch_k(const TrainF32Args& a, int tile_bytes, cudaStream_t s) {
       return;
     }
   }
+  if constexpr (H1 == 5 && H2 == 5) {
+    if (std::getenv("LANN_FP32_UNPACKED") == nullptr) {
+      auto kern = train_fp32_h55_kernel<I, K>;
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
+      kern<<<a.n_groups, 32, dyn, s>>>(a);
+      return;
+    }
+  }
   auto kern = train_fp32_kernel<I, H1, H2, K>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
   kern<<<a.n_groups, 32, dyn, s>>>(a);
@@ -766,6 +1039,9 @@ int slots_k(int tile_bytes) {
   if constexpr (H1 == 8 && H2 == 0) {
     cudaFuncSetAttribute(train_fp32_h8_kernel<I, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, train_fp32_h8_kernel<I, K>, 32, dyn);
+  } else if constexpr (H1 == 5 && H2 == 5) {
+    cudaFuncSetAttribute(train_fp32_h55_kernel<I, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, train_fp32_h55_kernel<I, K>, 32, dyn);
   } else {
     cudaFuncSetAttribute(train_fp32_kernel<I, H1, H2, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, train_fp32_kernel<I, H1, H2, K>, 32, dyn);

@@ -834,8 +834,18 @@ __global__ void __launch_bounds__(32 * W, 1) train_fp32_cta_kernel(TrainF32Args 
 
   const bool prof = a.phase_cycles && blockIdx.x == 0 && tid == 0;
   long long pc[3] = {0, 0, 0};
+  // kPair: each thread's two samples are the same every epoch, so their rows stay in registers
+  float xa[8], xb[8];
+  if constexpr (kPair) {
+    load_row(trow, tid < rows ? tid : 0, xa);
+    load_row(trow, tid + T < rows ? tid + T : 0, xb);
+  }
   for (int e = 0; e < E; ++e) {
     const long long clk0 = prof ? clock64() : 0;
+    // this epoch's Adam factors (bias corrections), computed while the samples run
+    pw1 *= 0.9f;
+    pw2 *= 0.999f;
+    const float step = lr / (1.f - pw1), rb2 = 1.f / (1.f - pw2);
     float w[PT];
 #pragma unroll
     for (int p = 0; p < PT; p += 4) {
@@ -851,13 +861,20 @@ __global__ void __launch_bounds__(32 * W, 1) train_fp32_cta_kernel(TrainF32Args 
     float loss = 0.f;
     if constexpr (kPair) {
       // two samples per thread in one basic block: independent chains interleave
-      for (int s0 = tid; s0 < rows; s0 += 2 * T) {
-        const int s1 = s0 + T;
-        float xa[8], xb[8];
-        load_row(trow, s0, xa);
-        load_row(trow, s1 < rows ? s1 : s0, xb);
-        accumulate_sample<I, H1, H2>(w, xa, gr, loss, scale);
-        accumulate_sample<I, H1, H2>(w, xb, gr, loss, scale, s1 < rows);
+      if (rows <= 2 * T) {
+        if (tid < rows) {
+          accumulate_sample<I, H1, H2>(w, xa, gr, loss, scale);
+          accumulate_sample<I, H1, H2>(w, xb, gr, loss, scale, tid + T < rows);
+        }
+      } else {
+        for (int s0 = tid; s0 < rows; s0 += 2 * T) {
+          const int s1 = s0 + T;
+          float ya[8], yb[8];
+          load_row(trow, s0, ya);
+          load_row(trow, s1 < rows ? s1 : s0, yb);
+          accumulate_sample<I, H1, H2>(w, ya, gr, loss, scale);
+          accumulate_sample<I, H1, H2>(w, yb, gr, loss, scale, s1 < rows);
+        }
       }
     } else {
       for (int s = tid; s < rows; s += T) {
@@ -907,10 +924,7 @@ __global__ void __launch_bounds__(32 * W, 1) train_fp32_cta_kernel(TrainF32Args 
     __syncthreads();
     const long long clk2 = prof ? clock64() : 0;
     // level 2: owners sum the W warp partials and apply Adam
-    pw1 *= 0.9f;
-    pw2 *= 0.999f;
     {
-      const float step = lr / (1.f - pw1), rb2 = 1.f / (1.f - pw2);
 #pragma unroll
       for (int k = 0; k < OWN; ++k) {
         const int p = tid + k * T;

@@ -430,9 +430,9 @@ void execute_plan(lann_engine* e, const TrainPlan& P, double* dparams, double* d
     for (const auto& b : P.buckets) {
       if (b->lanes < 64) continue;
       long long c[4] = {0, 0, 0, 0};
-      ck(cudaMemcpy(c, b->prof.p, 3 * sizeof(long long), cudaMemcpyDeviceToHost), "profile D2H");
-      std::fprintf(stderr, "fp32 cta shape %d-%d-%d: cycles compute %lld reduce %lld adam %lld\n", b->in,
-                   b->h1, b->h2, c[0], c[1], c[2]);
+      ck(cudaMemcpy(c, b->prof.p, 4 * sizeof(long long), cudaMemcpyDeviceToHost), "profile D2H");
+      std::fprintf(stderr, "fp32 cta shape %d-%d-%d: cycles compute %lld reduce %lld adam %lld loop %lld\n", b->in,
+                   b->h1, b->h2, c[0], c[1], c[2], c[3]);
     }
     for (const auto& b : P.buckets64) {
       long long c[4] = {0, 0, 0, 0};

@@ -803,7 +803,7 @@ __global__ void __launch_bounds__(32 * W, 1) train_fp32_cta_kernel(TrainF32Args 
   __shared__ uint64_t bar;
   __shared__ __align__(16) float wsh[PT];
   __shared__ float part[W][P + 1];  // per-warp partial gradients (+ loss)
-  __shared__ float loss_sh;
+  __shared__ float loss_sh[2];  // double-buffered: epoch e is checked at the top of e + 1
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int m = a.sorted_model[a.group_first[blockIdx.x]];
   const int tile = a.model_tile[m];
@@ -833,13 +833,14 @@ __global__ void __launch_bounds__(32 * W, 1) train_fp32_cta_kernel(TrainF32Args 
   __syncthreads();
 
   const bool prof = a.phase_cycles && blockIdx.x == 0 && tid == 0;
-  long long pc[3] = {0, 0, 0};
+  long long pc[4] = {0, 0, 0, 0};
   // kPair: each thread's two samples are the same every epoch, so their rows stay in registers
   float xa[8], xb[8];
   if constexpr (kPair) {
     load_row(trow, tid < rows ? tid : 0, xa);
     load_row(trow, tid + T < rows ? tid + T : 0, xb);
   }
+  const long long clk_begin = prof ? clock64() : 0;
   for (int e = 0; e < E; ++e) {
     const long long clk0 = prof ? clock64() : 0;
     // this epoch's Adam factors (bias corrections), computed while the samples run
@@ -854,6 +855,17 @@ __global__ void __launch_bounds__(32 * W, 1) train_fp32_cta_kernel(TrainF32Args 
       w[p + 1] = v.y;
       w[p + 2] = v.z;
       w[p + 3] = v.w;
+    }
+    // the previous epoch's loss (pre-update, mlp.cpp:165-172), read here so its shared-memory
+    // latency hides behind the weight loads instead of stalling the loop back-edge
+    if (e > 0) {
+      const float L = loss_sh[(e - 1) & 1];
+      last = L;
+      if (trace && tid == 0 && ((e - 1) % a.trace_stride) == 0) trace[(e - 1) / a.trace_stride] = (double)L;
+      if (!isfinite(L)) {
+        bad = e - 1;
+        break;  // uniform across the CTA (everyone read the same loss)
+      }
     }
     float gr[PT];
 #pragma unroll
@@ -932,7 +944,7 @@ __global__ void __launch_bounds__(32 * W, 1) train_fp32_cta_kernel(TrainF32Args 
           float gsum = 0.f;
 #pragma unroll
           for (int q = 0; q < W; ++q) gsum += part[q][p];
-          if (p == P) loss_sh = gsum * inv_n;
+          if (p == P) loss_sh[e & 1] = gsum * inv_n;
           else wsh[p] -= adam_step(mo[k], ve[k], gsum, step, rb2);
         }
       }
@@ -944,18 +956,17 @@ __global__ void __launch_bounds__(32 * W, 1) train_fp32_cta_kernel(TrainF32Args 
       pc[1] += clk2 - clk1;  // reduce-scatter + barrier
       pc[2] += clk3 - clk2;  // owner sums + Adam + barrier
     }
-    const float L = loss_sh;
-    if (bad < 0) {
-      last = L;
-      if (trace && tid == 0 && (e % a.trace_stride) == 0) trace[e / a.trace_stride] = (double)L;
-    }
-    if (!isfinite(L)) {
-      bad = e;
-      break;  // uniform across the CTA (everyone read the same loss)
-    }
   }
-  if (prof)
-    for (int k = 0; k < 3; ++k) a.phase_cycles[k] = pc[k];
+  if (bad < 0 && E > 0) {  // the last epoch's loss (every thread passed its final barrier)
+    const float L = loss_sh[(E - 1) & 1];
+    last = L;
+    if (trace && tid == 0 && ((E - 1) % a.trace_stride) == 0) trace[(E - 1) / a.trace_stride] = (double)L;
+    if (!isfinite(L)) bad = E - 1;
+  }
+  if (prof) {
+    pc[3] = clock64() - clk_begin;  // the whole epoch loop
+    for (int k = 0; k < 4; ++k) a.phase_cycles[k] = pc[k];
+  }
   // on a non-finite loss the reference discards the model (TrainingError); so do we
   double* outp = a.params + a.param_offset[m];
   for (int p = tid; p < P; p += T) outp[p] = (double)wsh[p];

@@ -155,3 +155,28 @@ def test_fp32_cta_kernel_paired_matches_single(engine, monkeypatch):
     a = np.array([r.mape_thr for r in fast])
     b = np.array([r.mape_thr for r in gen])
     assert abs(np.median(a) - np.median(b)) <= 1.0, (a, b)
+
+
+@pytest.mark.parametrize("lanes", [None, "1", "4", "128", "256"])
+@pytest.mark.parametrize("I,hidden", [(7, (8,)), (6, (5, 5))])
+def test_fp32_training_error_and_trace_tail(engine, monkeypatch, lanes, I, hidden):
+    """Every FP32 mapping: a non-finite target -> TrainingError(epoch 0) (mlp.cpp:166-169); a
+    finite run records all E pre-update losses and reports the last one as the final loss (the
+    CTA kernel checks epoch e's loss at the top of epoch e + 1, so the tail is handled apart)."""
+    if lanes:
+        monkeypatch.setenv("LANN_FP32_LANES", lanes)
+    rng = np.random.default_rng(1)
+    n = 250
+    X = rng.uniform(0, 1, (n, I))
+    y = rng.uniform(0, 1, n)
+    dims = [I, *hidden, 1]
+    m = {"tile": 0, "h1": hidden[0], "h2": hidden[1] if len(hidden) > 1 else 0, "lr": 1e-2, "epochs": 37,
+         "params": E.init_params(dims, 3)}
+    params, final, bad, traces = engine.train([X], [y], [m], abi.FP32, trace=True)
+    assert len(traces[0]) == 37 and np.all(np.isfinite(traces[0]))
+    assert final[0] == traces[0][-1]
+    y_bad = y.copy()
+    y_bad[17] = np.inf
+    with pytest.raises(E.TrainingError) as ei:
+        engine.train([X], [y_bad], [m], abi.FP32)
+    assert ei.value.epoch == 0

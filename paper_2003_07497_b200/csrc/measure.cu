@@ -32,6 +32,8 @@
 #include <cstdint>
 #include <cstring>
 #include <functional>
+#include <map>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -229,14 +231,15 @@ __global__ void checksum_kernel(const float* v, uint64_t n, double* out) {
 // ---- cuBLAS, loaded at first use (a library black box; the engine does not link it) ----------
 struct Cublas {
   void* lib = nullptr;
-  void* handle = nullptr;
   int (*create)(void**) = nullptr;
   int (*set_stream)(void*, cudaStream_t) = nullptr;
   int (*sgemm)(void*, int, int, int, int, int, const float*, const float*, int, const float*, int, const float*,
                float*, int) = nullptr;
-  bool ok = false;
+  std::mutex mu;
+  std::map<int, void*> handles;  // one cuBLAS handle per device (a handle is bound to its device)
   static Cublas& get() {
     static Cublas c;
+    std::lock_guard<std::mutex> lk(c.mu);
     if (!c.lib) {
       c.lib = dlopen("libcublas.so.12", RTLD_NOW | RTLD_LOCAL);
       if (!c.lib) c.lib = dlopen("/usr/local/cuda/lib64/libcublas.so.12", RTLD_NOW | RTLD_LOCAL);
@@ -244,10 +247,21 @@ struct Cublas {
         c.create = reinterpret_cast<decltype(c.create)>(dlsym(c.lib, "cublasCreate_v2"));
         c.set_stream = reinterpret_cast<decltype(c.set_stream)>(dlsym(c.lib, "cublasSetStream_v2"));
         c.sgemm = reinterpret_cast<decltype(c.sgemm)>(dlsym(c.lib, "cublasSgemm_v2"));
-        c.ok = c.create && c.set_stream && c.sgemm && c.create(&c.handle) == 0;
       }
     }
     return c;
+  }
+  void* handle_for_current_device() {
+    std::lock_guard<std::mutex> lk(mu);
+    if (!create || !set_stream || !sgemm) return nullptr;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    auto it = handles.find(dev);
+    if (it != handles.end()) return it->second;
+    void* h = nullptr;
+    if (create(&h) != 0) return nullptr;
+    handles[dev] = h;
+    return h;
   }
 };
 
@@ -306,7 +320,7 @@ int measure_instances(int kind, const char* variant, int n, const double* feats,
     return LANN_PARAM_ERROR;
   }
   const std::string v = variant;
-  static DevBuf A, B, C, S, rowptr, colidx, vals, csum;
+  DevBuf A, B, C, S, rowptr, colidx, vals, csum;  // per call: no state shared between engines / devices
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
@@ -350,16 +364,17 @@ int measure_instances(int kind, const char* variant, int n, const double* feats,
         run = [=] { gemm_tiled_kernel<<<dim3((k + GT - 1) / GT, (m + GT - 1) / GT), 256, 0, s>>>(a, b, c, m, nn, k); };
       } else if (v == "cublas_sgemm") {
         Cublas& cb = Cublas::get();
-        if (!cb.ok) {
+        void* handle = cb.handle_for_current_device();
+        if (!handle) {
           err = "cuBLAS could not be loaded";
           status = LANN_PARAM_ERROR;
           break;
         }
-        cb.set_stream(cb.handle, s);
+        cb.set_stream(handle, s);
         run = [=, &cb] {
           const float one = 1.f, zero = 0.f;
           // row-major C = A B  ==  column-major C^T = B^T A^T
-          cb.sgemm(cb.handle, 0, 0, k, m, nn, &one, b, k, a, nn, &zero, c, k);
+          cb.sgemm(handle, 0, 0, k, m, nn, &one, b, k, a, nn, &zero, c, k);
         };
       } else {
         build_csr(m, nn);

@@ -214,6 +214,17 @@ int lann_build_dataset(const lann_world* world, uint64_t seed, int32_t count,
                        double* feats, uint64_t* c, double* runtime, int32_t* n_features);
 int lann_split_order(int32_t n, uint64_t seed, int64_t* order);
 
+/* datagen::build_dataset of a native CPU-class variant with the reference CLI's --mock-timer
+ * probe (perfsage.cpp:71-84: 1e-9 * c * jitter(hash of the augmented features) + 1e-6), over
+ * ParamSpace{kind, max_threads, dims U{1..dim_max}, blur sides[n_sides], blur_lattice};
+ * single_threaded pins n_thd = 1 (Threading::FixedSingle). Byte-identical to the reference CLI's
+ * `gen --mock-timer` dataset. feats [count][LANN_ROW] (base features with n_thd). */
+int lann_build_mock_dataset(int32_t kind, int32_t single_threaded, int32_t max_threads, uint32_t dim_max,
+                            int32_t n_sides, const uint32_t* sides, int32_t blur_lattice, int32_t count,
+                            uint64_t seed, double* feats, uint64_t* c, double* runtime, int32_t* n_features);
+/* the mock probe at GIVEN blur schedules (cmd_select --mock-timer, perfsage.cpp:340-360) */
+int lann_mock_schedules(uint32_t image_n, int32_t n_thd, int32_t n, const uint32_t* sched, double* runtime);
+
 /* The synthetic world's runtime probe at GIVEN blur schedules (the stand-in for
  * datagen::measure of the tiled blur kernel in perfsage.cpp cmd_select:297-316):
  * instance blur(image_n, sched[i]) with n_thd = world.max_threads, noise drawn from

@@ -145,6 +145,14 @@ Dataset build_measured(kernels::KernelKind kind, const std::string& variant, std
                        std::uint64_t seed, TimingPolicy policy = {}, bool gpu_lattice = true,
                        std::uint32_t blur_side = 1024);
 std::vector<std::string> measured_variants(kernels::KernelKind kind);
+/// The reference CLI's `gen --mock-timer` dataset for a builtin native variant
+/// (variants.cpp:225-247: dense_single, dense_threaded, sparse_single per kind, tiled_threaded
+/// for mm, tiled for blur): ParamSpace::defaults(kind, max_threads) with dims U{1..dim_max},
+/// blur sides / lattice, the mock probe (perfsage.cpp:71-84). ParamError on an unknown variant.
+Dataset build_mock(kernels::KernelKind kind, const std::string& variant_id, std::size_t count, std::uint64_t seed,
+                   int max_threads, std::uint32_t dim_max = 1024, std::vector<std::uint32_t> blur_sides = {1024},
+                   bool gpu_lattice = false);
+std::vector<std::string> native_variants(kernels::KernelKind kind);
 /// external.cpp:46-118: run `command` via /bin/sh, write the features as one line of %.17g
 /// values to its stdin, read one positive decimal runtime (seconds) from the first stdout line.
 /// Throws ExternalVariantError on spawn failure, non-zero exit or a malformed reply.

@@ -572,6 +572,93 @@ int ref_save_external_csv(int kind, int gpu_class, int max_threads, const char* 
     }
 }
 
+// The reference CLI's mock_probe (tools/perfsage.cpp:71-84), restated here because the CLI itself
+// needs CLI11 (absent); it only calls reference library functions.
+datagen::RuntimeProbe ref_mock_probe() {
+    return [](const kernels::InstanceParams& params) {
+        const auto feats = models::featurize(params, true);
+        std::uint64_t h = 0x9e3779b97f4a7c15ULL;
+        for (double f : feats) {
+            std::uint64_t bits;
+            std::memcpy(&bits, &f, sizeof bits);
+            h ^= bits;
+            splitmix64(h);
+        }
+        const double jitter = 0.5 + double(splitmix64(h) >> 11) * 0x1.0p-53;
+        return 1e-9 * double(kernels::complexity(params)) * jitter + 1e-6;
+    };
+}
+
+// cmd_gen (perfsage.cpp:197-248) with --mock-timer, minus the manifest
+int ref_cli_gen_mock(int kind, const char* variant_id, int max_threads, unsigned dim_max, int n_sides,
+                     const unsigned* sides, int gpu_lattice, int count, std::uint64_t seed, const char* path) {
+    try {
+        auto space = datagen::ParamSpace::defaults(kind_of(kind), max_threads);
+        space.dim_max = dim_max;
+        if (kind_of(kind) == kernels::KernelKind::Blur) {
+            space.blur_sides.assign(sides, sides + n_sides);
+            space.schedules = gpu_lattice ? kernels::ScheduleSpace::gpu_style() : kernels::ScheduleSpace::cpu_default();
+        }
+        const auto registry = kernels::VariantRegistry::builtin();
+        const auto& variant = registry.get(kind_of(kind), variant_id);
+        datagen::BuildOptions opts;
+        opts.probe = ref_mock_probe();
+        datagen::save_csv(datagen::build_dataset(variant, space, std::size_t(count), seed, opts), path);
+        return 0;
+    } catch (const std::exception& e) {
+        return status_of(e);
+    }
+}
+
+// cmd_select (perfsage.cpp:307-382) with --mock-timer and no --data: out = {chosen s1..s4,
+// predicted_s, measured_s, true_best s1..s4, true_best_s, default_s, regret, speedup_vs_default,
+// speedup_vs_random_mean}
+int ref_cli_select_mock(unsigned n, int n_cands, std::uint64_t seed, int epochs, int threads, double* out) {
+    try {
+        const kernels::ScheduleCandidate default_sched{8, 256, 128, 8};
+        auto candidates = selector::enumerate_candidates(kernels::ScheduleSpace::cpu_default(), std::size_t(n_cands), seed);
+        const auto probe = ref_mock_probe();
+        datagen::Dataset measured;
+        measured.kind = kernels::KernelKind::Blur;
+        measured.feature_names = models::feature_names(kernels::KernelKind::Blur, false);
+        measured.seed = seed;
+        selector::MeasuredCandidates table;
+        auto instance = kernels::make_instance(kernels::InstanceParams::blur(n, default_sched), derive_seed(seed, 0x1417));
+        instance.params.n_thd = threads;
+        bool default_present = false;
+        for (const auto& c : candidates) default_present |= (c == default_sched);
+        if (!default_present) candidates.push_back(default_sched);
+        for (const auto& c : candidates) {
+            instance.params.schedule = c;
+            const double runtime = probe(instance.params);
+            table.emplace_back(c, runtime);
+            datagen::Sample smp;
+            smp.features = models::featurize(instance.params, false, false);
+            smp.c = kernels::complexity(instance.params);
+            smp.runtime_s = runtime;
+            smp.variant_id = "tiled";
+            measured.samples.push_back(std::move(smp));
+        }
+        auto cfg = models::default_config(kernels::KernelKind::Blur, models::ModelFamily::NnC, false);
+        cfg.family = models::ModelFamily::NnC;
+        cfg.seed = seed;
+        if (epochs > 0) cfg.epochs = epochs;
+        const auto model = models::train_model(measured, cfg);
+        const auto chosen = selector::select(model, n, candidates);
+        const auto chosen_params = kernels::InstanceParams::blur(n, chosen);
+        const double predicted = models::predict(model, models::model_features(chosen_params, cfg.family));
+        const auto rep = selector::evaluate_selection(chosen, table, default_sched, std::nullopt, predicted);
+        const double v[] = {double(rep.chosen.s1), double(rep.chosen.s2), double(rep.chosen.s3), double(rep.chosen.s4),
+                            rep.predicted_s, rep.measured_s, double(rep.true_best.s1), double(rep.true_best.s2),
+                            double(rep.true_best.s3), double(rep.true_best.s4), rep.true_best_s, rep.default_s,
+                            rep.regret, rep.speedup_vs_default, rep.speedup_vs_random_mean};
+        std::copy(std::begin(v), std::end(v), out);
+        return 0;
+    } catch (const std::exception& e) {
+        return status_of(e);
+    }
+}
+
 // perfsage.cpp evaluate_model_on (:98-108): out = {mape_full, mape_thr, rho, n_kept}
 int ref_eval_model(const char* model_path, const char* csv, double drop, double* out) {
     try {

@@ -92,7 +92,7 @@ struct Args {
 };
 
 const std::vector<std::string> kFlags = {"unconstrained", "list", "help", "both-families", "measure",
-                                         "gpu-class", "list-variants"};
+                                         "gpu-class", "list-variants", "mock-timer"};
 
 Args parse(int argc, char** argv) {
   Args a;
@@ -241,6 +241,17 @@ std::string sanitize(std::string s) {
   return s;
 }
 
+// hostinfo.cpp:26-34: hardware threads, capped by PERFSAGE_THREADS
+int host_max_threads() {
+  int hw = int(std::thread::hardware_concurrency());
+  if (hw < 1) hw = 1;
+  if (const char* env = std::getenv("PERFSAGE_THREADS")) {
+    const int cap = std::atoi(env);
+    if (cap >= 1) hw = std::min(hw, cap);
+  }
+  return hw;
+}
+
 // ---- subcommands ---------------------------------------------------------------------------------
 int cmd_gen(const Args& a) {
   if (a.has("list-variants")) {
@@ -249,6 +260,27 @@ int cmd_gen(const Args& a) {
                    kernels::KernelKind::Blur})
       for (const auto& v : datagen::measured_variants(k))
         std::cout << std::left << std::setw(8) << kernels::to_string(k) << v << "\n";
+    return 0;
+  }
+  if (a.has("mock-timer")) {  // perfsage.cpp:197-248 with --mock-timer: byte-identical dataset
+    const auto kind = kernels::kind_from_string(a.get("kernel", "mm"));
+    std::string variant = a.get("variant", "dense_threaded");
+    if (kind == kernels::KernelKind::Blur && variant == "dense_threaded") variant = "tiled";  // the only blur variant
+    const int mt = int(a.integer("max-threads", 0));
+    const int threads = mt > 0 ? mt : host_max_threads();
+    std::vector<std::uint32_t> sides;
+    for (const auto& v : a.all("blur-n")) sides.push_back(std::uint32_t(std::strtoul(v.c_str(), nullptr, 10)));
+    if (sides.empty()) sides = {1024};
+    const std::uint64_t seed = a.u64("seed", 1);
+    const auto ds = datagen::build_mock(kind, variant, std::size_t(a.integer("count", 500)), seed, threads,
+                                        std::uint32_t(a.integer("dim-max", 1024)), sides,
+                                        a.get("blur-space", "cpu") == "gpu");
+    const fs::path out = a.get("out", "perfsage_out");
+    fs::create_directories(out);
+    const fs::path csv = out / ("dataset_" + a.get("kernel", "mm") + "_" + variant + ".csv");
+    datagen::save_csv(ds, csv.string());
+    record_run(out, a, seed, {}, {csv.string()});
+    std::cout << "wrote " << ds.size() << " samples to " << csv.string() << "\n";
     return 0;
   }
   if (a.has("measure") || a.has("external-cmd")) {
@@ -266,7 +298,7 @@ int cmd_gen(const Args& a) {
                                    std::uint32_t(a.integer("blur-side", 1024)));
       vid = variant + "@b200";
     } else {
-      vid = a.get("external-id", "external");
+      vid = a.get("variant-id", a.get("external-id", "external"));
       ds = datagen::build_external(kind, a.get("external-cmd", ""), vid, a.has("gpu-class"),
                                    int(a.integer("max-threads", 4)), count, seed);
     }
@@ -277,6 +309,9 @@ int cmd_gen(const Args& a) {
     std::cout << "wrote " << ds.size() << " samples to " << csv.string() << "\n";
     return 0;
   }
+  if (a.has("kernel") && !a.has("world"))
+    throw ParamError("measuring the reference's CPU kernels is not part of this engine: use --mock-timer, "
+                     "--measure (B200 variants, gen --list-variants), --external-cmd or --world (gen --list)");
   if (a.has("list")) {
     std::cout << "world  kernel  variant\n";
     for (int i = 0; i < datagen::synthetic_world_count(); ++i) {
@@ -407,7 +442,7 @@ int cmd_compare(const Args& a) {  // perfsage.cpp:384-414, NN families batched
 
 int cmd_select(const Args& a) {  // perfsage.cpp:307-382
   setup_engine(a);
-  const auto default_sched = parse_schedule(a.get("default-schedule", "8,256,128,8"));
+  const auto default_sched = parse_schedule(a.get("default", a.get("default-schedule", "8,256,128,8")));
   const std::uint32_t n = std::uint32_t(a.integer("n", 1024));
   const std::uint64_t seed = a.u64("seed", 0);
   datagen::Dataset measured;
@@ -430,6 +465,30 @@ int cmd_select(const Args& a) {  // perfsage.cpp:307-382
       table.emplace_back(c, s.runtime_s);
     }
     if (candidates.empty()) throw ParamError("no samples with n=" + std::to_string(n) + " in " + path);
+  } else if (a.has("mock-timer")) {
+    // perfsage.cpp:340-362 with --mock-timer: every candidate (plus the default) probed by the
+    // deterministic mock timer on blur(n, schedule) with n_thd = the worker threads
+    const int mt = int(a.integer("max-threads", 0));
+    const int threads = mt > 0 ? mt : host_max_threads();
+    candidates = selector::enumerate_candidates(kernels::ScheduleSpace::cpu_default(),
+                                                std::size_t(a.integer("candidates", 200)), seed);
+    if (std::find(candidates.begin(), candidates.end(), default_sched) == candidates.end())
+      candidates.push_back(default_sched);
+    std::vector<std::uint32_t> flat;
+    for (const auto& c : candidates) flat.insert(flat.end(), {c.s1, c.s2, c.s3, c.s4});
+    std::vector<double> rt(candidates.size());
+    if (lann_mock_schedules(n, threads, int(candidates.size()), flat.data(), rt.data()))
+      throw ParamError("schedule probe failed");
+    for (std::size_t i = 0; i < candidates.size(); ++i) {
+      table.emplace_back(candidates[i], rt[i]);
+      datagen::Sample smp;
+      const auto& c = candidates[i];
+      smp.features = {double(n), double(c.s1), double(c.s2), double(c.s3), double(c.s4)};
+      smp.c = std::uint64_t(n) * n;
+      smp.runtime_s = rt[i];
+      smp.variant_id = "tiled";
+      measured.samples.push_back(std::move(smp));
+    }
   } else {
     // the synthetic blur world stands in for measuring the tiled kernel (out of scope)
     const int world = int(a.integer("world", 40));

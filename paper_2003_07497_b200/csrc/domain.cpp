@@ -93,8 +93,9 @@ std::uint32_t uniform_dim(SeqRng& rng, std::uint32_t lo, std::uint32_t hi) {
 
 }  // namespace
 
-Instance sample_instance(int kind, int max_threads, int gpu_lattice, SeqRng& rng) {
-  static const std::uint32_t sides[6] = {1024, 2048, 4096, 8192, 16384, 32768};
+Instance sample_instance(const SampleSpace& sp, SeqRng& rng) {
+  const int kind = sp.kind, max_threads = sp.max_threads, gpu_lattice = sp.gpu_lattice;
+  const std::uint32_t lo = sp.dim_min, hi = sp.dim_max;
   static const std::uint32_t mc_r[3] = {3, 5, 7}, mp_r[4] = {2, 3, 4, 5}, mp_s[2] = {1, 2};
   const bool inc_one = kind != LANN_MV;  // ParamSpace::defaults (datagen.cpp:18-24)
   Instance p;
@@ -102,37 +103,37 @@ Instance sample_instance(int kind, int max_threads, int gpu_lattice, SeqRng& rng
   auto threads = [&] { return int(uniform_dim(rng, 1, std::uint32_t(max_threads))); };
   switch (kind) {
     case LANN_MM: {
-      p.m = uniform_dim(rng, 1, 1024);
-      p.n = uniform_dim(rng, 1, 1024);
-      p.k = uniform_dim(rng, 1, 1024);
+      p.m = uniform_dim(rng, lo, hi);
+      p.n = uniform_dim(rng, lo, hi);
+      p.k = uniform_dim(rng, lo, hi);
       p.d1 = pick_density(std::uint64_t(p.m) * p.n, inc_one, rng);
       p.d2 = pick_density(std::uint64_t(p.n) * p.k, inc_one, rng);
       p.n_thd = threads();
       break;
     }
     case LANN_MV:
-      p.m = uniform_dim(rng, 1, 1024);
-      p.n = uniform_dim(rng, 1, 1024);
+      p.m = uniform_dim(rng, lo, hi);
+      p.n = uniform_dim(rng, lo, hi);
       p.d = pick_density(std::uint64_t(p.m) * p.n, inc_one, rng);
       p.n_thd = threads();
       break;
     case LANN_MC:
       p.r = mc_r[rng.bounded(3)];
-      p.m = uniform_dim(rng, std::max(1u, p.r), std::max(1024u, p.r));
-      p.n = uniform_dim(rng, std::max(1u, p.r), std::max(1024u, p.r));
+      p.m = uniform_dim(rng, std::max(lo, p.r), std::max(hi, p.r));
+      p.n = uniform_dim(rng, std::max(lo, p.r), std::max(hi, p.r));
       p.d = pick_density(std::uint64_t(p.m) * p.n, inc_one, rng);
       p.n_thd = threads();
       break;
     case LANN_MP:
       p.r = mp_r[rng.bounded(4)];
       p.s = mp_s[rng.bounded(2)];
-      p.m = uniform_dim(rng, std::max(1u, p.r), std::max(1024u, p.r));
-      p.n = uniform_dim(rng, std::max(1u, p.r), std::max(1024u, p.r));
+      p.m = uniform_dim(rng, std::max(lo, p.r), std::max(hi, p.r));
+      p.n = uniform_dim(rng, std::max(lo, p.r), std::max(hi, p.r));
       p.d = pick_density(std::uint64_t(p.m) * p.n, inc_one, rng);
       p.n_thd = threads();
       break;
     default: {
-      p.n = sides[rng.bounded(6)];
+      p.n = sp.sides[rng.bounded(sp.sides.size())];
       const auto& lat = schedule_lattice(gpu_lattice);
       const std::uint64_t i = rng.bounded(lat.size() / 4);
       std::memcpy(p.sched, &lat[4 * i], sizeof p.sched);
@@ -140,6 +141,56 @@ Instance sample_instance(int kind, int max_threads, int gpu_lattice, SeqRng& rng
     }
   }
   return p;
+}
+
+Instance sample_instance(int kind, int max_threads, int gpu_lattice, SeqRng& rng) {
+  SampleSpace sp;
+  sp.kind = kind;
+  sp.max_threads = max_threads;
+  sp.gpu_lattice = gpu_lattice;
+  return sample_instance(sp, rng);
+}
+
+// perfsage.cpp:71-84 (mock_probe, the CLI's --mock-timer): hash the bits of the augmented
+// feature vector (featurize(params, true): base features, n_thd except for blur, then c)
+// through splitmix64 -> jitter in [0.5, 1.5) -> 1e-9 * c * jitter + 1e-6
+double mock_runtime(const Instance& p) {
+  double f[LANN_ROW + 1] = {0};
+  int n = base_features(p, true, f);
+  f[n++] = double(complexity(p));
+  std::uint64_t h = 0x9e3779b97f4a7c15ULL;
+  for (int i = 0; i < n; ++i) {
+    std::uint64_t bits;
+    std::memcpy(&bits, &f[i], sizeof bits);
+    h ^= bits;
+    splitmix64(h);
+  }
+  const double jitter = 0.5 + double(splitmix64(h) >> 11) * 0x1.0p-53;
+  return 1e-9 * double(complexity(p)) * jitter + 1e-6;
+}
+
+Status build_mock_dataset(const SampleSpace& sp, bool single_threaded, std::uint64_t seed, int count, Dataset& ds) {
+  if (count < 2) return {LANN_PARAM_ERROR, "build_dataset needs count >= 2"};
+  if (sp.kind < 0 || sp.kind > LANN_BLUR) return {LANN_PARAM_ERROR, "unknown kernel kind"};
+  if (sp.max_threads < 1) return {LANN_PARAM_ERROR, "param space needs max_threads >= 1"};
+  if (sp.dim_min < 1 || sp.dim_max < sp.dim_min) return {LANN_PARAM_ERROR, "param space needs 1 <= dim_min <= dim_max"};
+  if (sp.kind == LANN_BLUR && sp.sides.empty()) return {LANN_PARAM_ERROR, "blur space needs image sides"};
+  const bool takes_thd = sp.kind != LANN_BLUR;  // native variants are CPU class (variants.hpp:29-31)
+  ds.kind = sp.kind;
+  ds.n_features = base_feature_count(sp.kind, takes_thd);
+  ds.feats.assign(std::size_t(count) * LANN_ROW, 0.0);
+  ds.c.assign(count, 0);
+  ds.runtime.assign(count, 0.0);
+  SeqRng rng(derive_seed(seed, 0));
+  for (int i = 0; i < count; ++i) {
+    Instance p = sample_instance(sp, rng);
+    if (single_threaded) p.n_thd = 1;               // Threading::FixedSingle (datagen.cpp:195)
+    if (sp.kind == LANN_BLUR) p.n_thd = sp.max_threads;  // datagen.cpp:196
+    base_features(p, takes_thd, &ds.feats[std::size_t(i) * LANN_ROW]);
+    ds.c[i] = complexity(p);
+    ds.runtime[i] = mock_runtime(p);
+  }
+  return {};
 }
 
 namespace {

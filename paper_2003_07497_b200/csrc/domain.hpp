@@ -69,7 +69,17 @@ std::uint64_t complexity(const Instance& p);                          // kernels
 int base_features(const Instance& p, bool with_n_thd, double* out);   // features.cpp:23-54
 int base_feature_count(int kind, bool with_n_thd);                    // features.cpp:10-21
 const std::vector<std::uint32_t>& schedule_lattice(int gpu_style);    // kernels.cpp:77-87
-Instance sample_instance(int kind, int max_threads, int gpu_lattice, SeqRng& rng);  // datagen.cpp:60-110
+// ParamSpace (datagen.hpp:19-40): dims U{dim_min..dim_max}, blur sides, schedule lattice
+struct SampleSpace {
+  int kind = LANN_MM;
+  int max_threads = 1;
+  int gpu_lattice = 0;
+  std::uint32_t dim_min = 1, dim_max = 1024;
+  std::vector<std::uint32_t> sides = {1024, 2048, 4096, 8192, 16384, 32768};
+};
+Instance sample_instance(const SampleSpace& space, SeqRng& rng);                     // datagen.cpp:60-110
+Instance sample_instance(int kind, int max_threads, int gpu_lattice, SeqRng& rng);  // default space
+double mock_runtime(const Instance& p);                                               // perfsage.cpp:71-84
 
 // ---- datasets ------------------------------------------------------------------------------
 struct Dataset {
@@ -82,6 +92,9 @@ struct Dataset {
 };
 
 Status build_dataset(const lann_world& w, std::uint64_t seed, int count, Dataset& out);  // datagen.cpp:177-223
+// build_dataset of a native (CPU-class) variant with the CLI's --mock-timer probe
+Status build_mock_dataset(const SampleSpace& space, bool single_threaded, std::uint64_t seed, int count,
+                          Dataset& out);
 Status split_order(int n, double frac, std::uint64_t seed, std::vector<std::int64_t>& order,
                    int& n_train);                                                      // datagen.cpp:225-248
 

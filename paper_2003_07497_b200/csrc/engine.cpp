@@ -1336,6 +1336,39 @@ int lann_predict_forest(lann_engine* e, int32_t M, int32_t trees, int32_t npt, c
   }
 }
 
+int lann_build_mock_dataset(int32_t kind, int32_t single_threaded, int32_t max_threads, uint32_t dim_max,
+                            int32_t n_sides, const uint32_t* sides, int32_t blur_lattice, int32_t count,
+                            uint64_t seed, double* feats, uint64_t* c, double* runtime, int32_t* n_features) {
+  if (!feats || !c || !runtime || !n_features || n_sides < 0 || (n_sides > 0 && !sides)) return LANN_PARAM_ERROR;
+  SampleSpace sp;
+  sp.kind = kind;
+  sp.max_threads = max_threads;
+  sp.gpu_lattice = blur_lattice;
+  sp.dim_max = dim_max;
+  if (n_sides > 0) sp.sides.assign(sides, sides + n_sides);
+  Dataset ds;
+  const Status st = build_mock_dataset(sp, single_threaded != 0, seed, count, ds);
+  if (st) return st.code;
+  std::memcpy(feats, ds.feats.data(), ds.feats.size() * sizeof(double));
+  std::memcpy(c, ds.c.data(), ds.c.size() * sizeof(uint64_t));
+  std::memcpy(runtime, ds.runtime.data(), ds.runtime.size() * sizeof(double));
+  *n_features = ds.n_features;
+  return LANN_OK;
+}
+
+int lann_mock_schedules(uint32_t image_n, int32_t n_thd, int32_t n, const uint32_t* sched, double* runtime) {
+  if (n < 0 || (n > 0 && (!sched || !runtime)) || image_n == 0) return LANN_PARAM_ERROR;
+  for (int i = 0; i < n; ++i) {
+    Instance p;
+    p.kind = LANN_BLUR;
+    p.n = image_n;
+    p.n_thd = n_thd;
+    for (int j = 0; j < 4; ++j) p.sched[j] = sched[4 * i + j];
+    runtime[i] = mock_runtime(p);
+  }
+  return LANN_OK;
+}
+
 int lann_probe_schedules(const lann_world* w, uint64_t seed, uint32_t image_n, int32_t n,
                          const uint32_t* sched, double* runtime) {
   if (!w || (n > 0 && (!sched || !runtime))) return LANN_PARAM_ERROR;

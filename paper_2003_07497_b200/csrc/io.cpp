@@ -9,6 +9,7 @@
 // which is not a dependency of this engine). Doubles are written with 17 significant digits
 // ("%.17g"), which round-trips every finite double exactly, so save -> load is bit-exact and
 // the files load unchanged in the reference (and the reference's files load here).
+#include <algorithm>
 #include <cerrno>
 #include <cmath>
 #include <cstdio>
@@ -187,6 +188,42 @@ std::vector<std::string> measured_variants(kernels::KernelKind kind) {
   std::vector<std::string> out;
   for (int i = 0; i < lann_measure_variant_count(int(kind)); ++i) out.emplace_back(lann_measure_variant_name(int(kind), i));
   return out;
+}
+
+std::vector<std::string> native_variants(kernels::KernelKind kind) {  // variants.cpp:225-247
+  if (kind == kernels::KernelKind::Blur) return {"tiled"};
+  std::vector<std::string> v = {"dense_single", "dense_threaded", "sparse_single"};
+  if (kind == kernels::KernelKind::MM) v.emplace_back("tiled_threaded");
+  return v;
+}
+
+Dataset build_mock(kernels::KernelKind kind, const std::string& variant_id, std::size_t count, std::uint64_t seed,
+                   int max_threads, std::uint32_t dim_max, std::vector<std::uint32_t> blur_sides, bool gpu_lattice) {
+  const auto names = native_variants(kind);
+  if (std::find(names.begin(), names.end(), variant_id) == names.end())
+    throw ParamError("no variant '" + variant_id + "' registered for kernel " + kernels::to_string(kind));
+  const bool single = variant_id.size() > 7 && variant_id.compare(variant_id.size() - 7, 7, "_single") == 0;
+  std::vector<double> feats(count * LANN_ROW), rt(count);
+  std::vector<std::uint64_t> c(count);
+  int nf = 0;
+  const int st = lann_build_mock_dataset(int(kind), single ? 1 : 0, max_threads, dim_max, int(blur_sides.size()),
+                                         blur_sides.data(), gpu_lattice ? 1 : 0, int(count), seed, feats.data(),
+                                         c.data(), rt.data(), &nf);
+  if (st) throw ParamError("invalid parameter space for the mock dataset");
+  Dataset ds;
+  ds.kind = kind;
+  ds.feature_names = models::feature_names(kind, kind != kernels::KernelKind::Blur);
+  ds.seed = seed;
+  ds.host = "mock-timer";
+  for (std::size_t i = 0; i < count; ++i) {
+    Sample smp;
+    smp.features.assign(feats.begin() + std::ptrdiff_t(i * LANN_ROW), feats.begin() + std::ptrdiff_t(i * LANN_ROW + nf));
+    smp.c = c[i];
+    smp.runtime_s = rt[i];
+    smp.variant_id = variant_id;
+    ds.samples.push_back(std::move(smp));
+  }
+  return ds;
 }
 
 Dataset build_measured(kernels::KernelKind kind, const std::string& variant, std::size_t count, std::uint64_t seed,

@@ -67,6 +67,7 @@ EXPORTS = ["lann_engine_create", "lann_engine_destroy", "lann_last_error", "lann
            "lann_select_schedule", "lann_select_variants", "lann_build_dataset", "lann_split_order", "lann_probe_schedules", "lann_measure",
            "lann_measure_variant_count", "lann_measure_variant_name", "lann_build_measured_dataset",
            "lann_fit_linear", "lann_fit_forest", "lann_predict_linear", "lann_predict_forest",
+           "lann_build_mock_dataset", "lann_mock_schedules",
            "lann_init_params", "lann_population_create", "lann_population_run", "lann_population_fetch",
            "lann_population_flop", "lann_population_models", "lann_population_destroy",
            "lann_population_norm", "lann_transfer_bytes", "lann_run_population", "lann_default_combos"]

@@ -187,6 +187,9 @@ class Reference(_Lib):
         L.ref_model_dump.argtypes = [C.c_char_p, _dp, C.c_int]
         L.ref_cli_train.argtypes = [C.c_char_p, C.c_uint64, C.c_char_p, C.c_int, C.c_char_p, C.c_char_p, C.c_char_p]
         L.ref_eval_model.argtypes = [C.c_char_p, C.c_char_p, C.c_double, _dp]
+        L.ref_cli_gen_mock.argtypes = [C.c_int, C.c_char_p, C.c_int, C.c_uint, C.c_int, _u32p, C.c_int, C.c_int,
+                                       C.c_uint64, C.c_char_p]
+        L.ref_cli_select_mock.argtypes = [C.c_uint, C.c_int, C.c_uint64, C.c_int, C.c_int, _dp]
         L.ref_save_external_csv.argtypes = [C.c_int, C.c_int, C.c_int, C.c_char_p, C.c_char_p, C.c_int, C.c_uint64,
                                             C.c_char_p]
 
@@ -209,6 +212,16 @@ class Reference(_Lib):
     def cli_train(self, csv, seed, family, epochs, model_out, train_out, test_out):
         return self.lib.ref_cli_train(str(csv).encode(), seed, family.encode(), epochs, str(model_out).encode(),
                                       str(train_out).encode(), str(test_out).encode())
+
+    def cli_gen_mock(self, kind, variant_id, max_threads, dim_max, sides, gpu_lattice, count, seed, path):
+        sides = np.ascontiguousarray(sides, dtype=np.uint32)
+        return self.lib.ref_cli_gen_mock(kind, variant_id.encode(), max_threads, dim_max, len(sides), sides,
+                                         int(gpu_lattice), count, seed, str(path).encode())
+
+    def cli_select_mock(self, n, n_cands, seed, epochs, threads):
+        out = np.zeros(15)
+        st = self.lib.ref_cli_select_mock(n, n_cands, seed, epochs, threads, out)
+        return st, out
 
     def save_external_csv(self, kind, gpu_class, max_threads, command, variant_id, count, seed, path):
         return self.lib.ref_save_external_csv(kind, int(gpu_class), max_threads, command.encode(), variant_id.encode(),

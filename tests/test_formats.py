@@ -219,3 +219,30 @@ def test_reference_baseline_files_load(tmp_path, tool, fam):
     src = os.path.join(GOLD, f"ref_model_w0_s3_{fam}.json")
     run(tool, "model-roundtrip", src, str(tmp_path / "m.json"))
     assert _payload_hex(tmp_path / "m.json") == _payload_hex(src)
+
+
+@pytest.mark.parametrize("kernel,kind,variant,extra,sides,gpu", [
+    ("mm", abi.MM, "dense_threaded", [], [1024], False),
+    ("mm", abi.MM, "tiled_threaded", ["--dim-max", "4096"], [1024], False),
+    ("mv", abi.MV, "sparse_single", [], [1024], False),
+    ("mc", abi.MC, "dense_single", ["--dim-max", "300"], [1024], False),
+    ("mp", abi.MP, "dense_threaded", [], [1024], False),
+    ("blur", abi.BLUR, "tiled", ["--blur-n", "512", "--blur-n", "2048"], [512, 2048], False),
+    ("blur", abi.BLUR, "tiled", ["--blur-space", "gpu"], [1024], True),
+])
+def test_gen_mock_timer_is_the_reference_cli(tmp_path, reference, kernel, kind, variant, extra, sides, gpu):
+    """`perfsage gen --mock-timer` (perfsage.cpp:71-84 probe, :197-248 body) writes the dataset the
+    reference CLI writes, byte for byte, for every builtin variant class and parameter-space option."""
+    run(CLI, "gen", "--mock-timer", "--kernel", kernel, "--variant", variant, "--count", "80", "--seed", "4",
+        "--max-threads", "6", *extra, "--out", str(tmp_path))
+    ours = tmp_path / f"dataset_{kernel}_{variant}.csv"
+    ref = tmp_path / "ref.csv"
+    dim_max = int(extra[extra.index("--dim-max") + 1]) if "--dim-max" in extra else 1024
+    assert reference.cli_gen_mock(kind, variant, 6, dim_max, sides, gpu, 80, 4, ref) == 0, reference.last_error()
+    assert open(ours, "rb").read() == open(ref, "rb").read()
+
+
+def test_gen_rejects_unknown_native_variant(tmp_path):
+    out = subprocess.run([CLI, "gen", "--mock-timer", "--kernel", "blur", "--variant", "dense_single", "--out",
+                          str(tmp_path)], capture_output=True, text=True)
+    assert out.returncode == 1 and "no variant" in out.stderr

@@ -201,3 +201,21 @@ def test_cli_compare_runs_all_five_families(tmp_path):
     assert [r["model_family"] for r in rows] == ["nnc", "nn", "const", "lrc", "nlrc"]
     assert float(rows[2]["mape_thresholded"]) == FMT["baselines"]["const"]["eval_test"]["mape_thresholded"]
     assert "best thresholded MAPE" in out
+
+
+def test_cli_select_mock_timer_is_the_reference_cli(tmp_path, reference):
+    """`perfsage select --mock-timer` == the reference CLI's cmd_select with its mock timer
+    (perfsage.cpp:307-382): same candidates, measured table, FP64 model, chosen schedule, true
+    best, regret and speedups (predicted_s through CUDA exp: 1e-12)."""
+    cli("select", "--mock-timer", "--n", 1024, "--candidates", 150, "--seed", 5, "--epochs", 1500, "--max-threads", 4,
+        "--precision", "fp64", "--out", tmp_path)
+    rep = json.load(open(tmp_path / "selection.json"))
+    st, ref = reference.cli_select_mock(1024, 150, 5, 1500, 4)
+    assert st == 0, reference.last_error()
+    sched = lambda d: [d["s1"], d["s2"], d["s3"], d["s4"]]  # noqa: E731
+    assert sched(rep["chosen"]) == list(ref[0:4])
+    assert rep["predicted_s"] == pytest.approx(ref[4], rel=1e-12)
+    assert rep["measured_s"] == ref[5]
+    assert sched(rep["true_best"]) == list(ref[6:10])
+    assert (rep["true_best_s"], rep["default_s"], rep["regret"], rep["speedup_vs_default"],
+            rep["speedup_vs_random_mean"]) == tuple(ref[10:15])

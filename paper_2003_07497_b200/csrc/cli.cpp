@@ -10,6 +10,7 @@
 //            --world W                          the engine's closed-form synthetic worlds
 //   measure-variant  serve the external protocol for a B200 variant (one feature line in ->
 //            one runtime out), so the reference's own `gen --external-cmd` can measure B200s
+//   bench    measure one instance of a B200 variant (the reference times one CPU kernel)
 //   train    CSV -> split(seed 0x5b11) -> train_model -> model_<family>.json, train.csv, test.csv
 //   eval     model JSON(s) x CSV -> eval.csv (+ --group-by aggregate)
 //   compare  CSV -> the five families (nnc, nn, const, lrc, nlrc) batched per family group -> compare.csv
@@ -746,6 +747,61 @@ int cmd_select_variants(const Args& a) {
   return 0;
 }
 
+// perfsage.cpp:424-472 `bench`: measure ONE kernel instance — here a B200 GPU-class variant
+// (median of reps CUDA-event timings); --list names the variants.
+int cmd_bench(const Args& a) {
+  if (a.has("list")) {
+    std::cout << "kernel  B200 variant\n";
+    for (auto k : {kernels::KernelKind::MM, kernels::KernelKind::MV, kernels::KernelKind::MC, kernels::KernelKind::MP,
+                   kernels::KernelKind::Blur})
+      for (const auto& v : datagen::measured_variants(k))
+        std::cout << std::left << std::setw(8) << kernels::to_string(k) << v << "\n";
+    return 0;
+  }
+  const auto kind = kernels::kind_from_string(a.get("kernel", "mm"));
+  const auto names = datagen::measured_variants(kind);
+  const std::string variant = a.get("variant", names.front());
+  const double m = a.real("m", 256), n = a.real("n", 256), k = a.real("k", 256), r = a.real("r", 3), st = a.real("s", 2);
+  const double d = a.real("d", 1.0), d2 = a.real("d2", 1.0);
+  double f[LANN_ROW] = {0};
+  std::uint64_t c = 0;
+  switch (kind) {  // GPU-class base features (features.cpp:10-21 without n_thd) and kernels.cpp:184-206
+    case kernels::KernelKind::MM:
+      f[0] = m, f[1] = n, f[2] = k, f[3] = d, f[4] = d2;
+      c = std::uint64_t(m) * std::uint64_t(n) * std::uint64_t(k);
+      break;
+    case kernels::KernelKind::MV:
+      f[0] = m, f[1] = n, f[2] = d;
+      c = std::uint64_t(m) * std::uint64_t(n);
+      break;
+    case kernels::KernelKind::MC:
+      f[0] = m, f[1] = n, f[2] = r, f[3] = d;
+      c = std::uint64_t(m - r + 1) * std::uint64_t(n - r + 1) * std::uint64_t(r * r);
+      break;
+    case kernels::KernelKind::MP:
+      f[0] = m, f[1] = n, f[2] = r, f[3] = st, f[4] = d;
+      c = std::uint64_t((n + st - 1) / st) * std::uint64_t((m + st - 1) / st) * std::uint64_t(st * st);
+      break;
+    case kernels::KernelKind::Blur: {
+      const auto sc = parse_schedule(a.get("schedule", "8,256,128,8"));
+      f[0] = n, f[1] = sc.s1, f[2] = sc.s2, f[3] = sc.s3, f[4] = sc.s4;
+      c = std::uint64_t(n) * std::uint64_t(n);
+      break;
+    }
+  }
+  lann_engine* e = nullptr;
+  if (lann_engine_create(int(a.integer("device", 0)), &e) != LANN_OK)
+    throw Error("no CUDA device: the LANN engine has no CPU fallback");
+  double rt = 0.0;
+  const int status = lann_measure(e, int(kind), variant.c_str(), 1, f, int(a.integer("warmups", 1)),
+                                  int(a.integer("reps", 5)), a.u64("seed", 1), &rt, nullptr);
+  const std::string err = status ? lann_last_error(e) : "";
+  lann_engine_destroy(e);
+  if (status) throw ParamError(err);
+  std::cout << kernels::to_string(kind) << "/" << variant << " c=" << c << " median_s=" << rt << "\n";
+  return 0;
+}
+
 // The reference's external-variant protocol (external.cpp:46-118) served by a B200 variant:
 // every stdin line of GPU-class features -> one line with the median runtime in seconds.
 int cmd_measure_variant(const Args& a) {
@@ -789,6 +845,7 @@ int main(int argc, char** argv) {
     if (a.command == "sweep") return cmd_sweep(a);
     if (a.command == "select-variants") return cmd_select_variants(a);
     if (a.command == "measure-variant") return cmd_measure_variant(a);
+    if (a.command == "bench") return cmd_bench(a);
     throw ParamError("unknown subcommand '" + a.command + "'");
   } catch (const std::exception& ex) {
     std::cerr << "error: " << ex.what() << "\n";

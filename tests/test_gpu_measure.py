@@ -181,3 +181,12 @@ def test_measure_variant_serves_the_external_protocol(tmp_path):
     out = subprocess.run([CLI, "measure-variant", "--kernel", "mv", "--variant", "gemv_dense"],
                          input="100 200 1\n300 20 0.5\n", capture_output=True, text=True, timeout=300)
     assert out.returncode == 0 and len(out.stdout.split()) == 2
+
+
+def test_cli_bench_measures_one_instance():
+    out = run(CLI, "bench", "--kernel", "mm", "--variant", "cublas_sgemm", "--m", 512, "--n", 512, "--k", 512,
+              "--reps", 3)
+    assert out.startswith("mm/cublas_sgemm c=134217728 median_s=")
+    assert float(out.split("median_s=")[1]) > 0
+    out = run(CLI, "bench", "--kernel", "blur", "--n", 1024, "--schedule", "4,32,8,1")
+    assert "blur/blur_sched c=1048576" in out

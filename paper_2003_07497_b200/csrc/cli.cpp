@@ -466,6 +466,39 @@ int cmd_select(const Args& a) {  // perfsage.cpp:307-382
       table.emplace_back(c, s.runtime_s);
     }
     if (candidates.empty()) throw ParamError("no samples with n=" + std::to_string(n) + " in " + path);
+  } else if (a.has("measure")) {
+    // real B200 timings of the blur_sched variant at every candidate schedule (measure.cu)
+    const bool gpu = a.get("lattice", "gpu") == "gpu";
+    candidates = selector::enumerate_candidates(gpu ? kernels::ScheduleSpace::gpu_style()
+                                                    : kernels::ScheduleSpace::cpu_default(),
+                                                std::size_t(a.integer("candidates", 200)), seed);
+    if (std::find(candidates.begin(), candidates.end(), default_sched) == candidates.end())
+      candidates.push_back(default_sched);
+    std::vector<double> feats(candidates.size() * LANN_ROW, 0.0), rt(candidates.size());
+    for (std::size_t i = 0; i < candidates.size(); ++i) {
+      const auto& c = candidates[i];
+      double* f = &feats[i * LANN_ROW];
+      f[0] = n, f[1] = c.s1, f[2] = c.s2, f[3] = c.s3, f[4] = c.s4;
+    }
+    lann_engine* e = nullptr;
+    if (lann_engine_create(int(a.integer("device", 0)), &e) != LANN_OK)
+      throw Error("no CUDA device: the LANN engine has no CPU fallback");
+    const int st = lann_measure(e, LANN_BLUR, "blur_sched", int(candidates.size()), feats.data(),
+                                int(a.integer("warmups", 2)), int(a.integer("reps", 7)), lann::derive_seed(seed, 0x1417),
+                                rt.data(), nullptr);
+    const std::string err = st ? lann_last_error(e) : "";
+    lann_engine_destroy(e);
+    if (st) throw ParamError("measurement failed: " + err);
+    for (std::size_t i = 0; i < candidates.size(); ++i) {
+      table.emplace_back(candidates[i], rt[i]);
+      datagen::Sample smp;
+      const auto& c = candidates[i];
+      smp.features = {double(n), double(c.s1), double(c.s2), double(c.s3), double(c.s4)};
+      smp.c = std::uint64_t(n) * n;
+      smp.runtime_s = rt[i];
+      smp.variant_id = "blur_sched@b200";
+      measured.samples.push_back(std::move(smp));
+    }
   } else if (a.has("mock-timer")) {
     // perfsage.cpp:340-362 with --mock-timer: every candidate (plus the default) probed by the
     // deterministic mock timer on blur(n, schedule) with n_thd = the worker threads
@@ -519,8 +552,20 @@ int cmd_select(const Args& a) {  // perfsage.cpp:307-382
     }
   }
   const auto family = models::family_from_string(a.get("family", "nnc"));
-  const auto cfg = make_config(kernels::KernelKind::Blur, family, a, seed);
-  const auto model = models::train_model(measured, cfg);
+  // --seeds K: train K init seeds (seed .. seed+K-1) as ONE population and keep the model with the
+  // lowest final training loss (the protocol of acceptance criterion 8, acceptance_main.cpp:438-450)
+  const int n_seeds = std::max(1, int(a.integer("seeds", 1)));
+  std::vector<models::ModelConfig> cfgs;
+  std::vector<const datagen::Dataset*> sets;
+  for (int k = 0; k < n_seeds; ++k) {
+    cfgs.push_back(make_config(kernels::KernelKind::Blur, family, a, seed + std::uint64_t(k)));
+    sets.push_back(&measured);
+  }
+  auto trained = models::train_population(sets, cfgs);
+  std::size_t pick = 0;
+  for (std::size_t k = 1; k < trained.size(); ++k)
+    if (!trained[k].loss_trace.empty() && trained[k].loss_trace.back() < trained[pick].loss_trace.back()) pick = k;
+  const models::TrainedModel model = std::move(trained[pick]);
   const auto chosen = selector::select(model, n, candidates);
   std::vector<double> feats = {double(n), double(chosen.s1), double(chosen.s2), double(chosen.s3), double(chosen.s4)};
   if (models::family_augmented(family)) feats.push_back(double(std::uint64_t(n) * n));

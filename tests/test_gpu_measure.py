@@ -190,3 +190,17 @@ def test_cli_bench_measures_one_instance():
     assert float(out.split("median_s=")[1]) > 0
     out = run(CLI, "bench", "--kernel", "blur", "--n", 1024, "--schedule", "4,32,8,1")
     assert "blur/blur_sched c=1048576" in out
+
+
+def test_criterion8_blur_selection_on_measured_b200(tmp_path):
+    """Acceptance criterion 8 (acceptance_main.cpp:406-462) on REAL B200 timings: 220 GPU-lattice
+    schedules (+ the default) of the blur_sched variant measured at n = 4096 (median of 7), five
+    init seeds x 100,000 epochs trained as one population, the lowest-loss net selects on the GPU:
+    regret <= 1.3x, and the choice beats the default schedule."""
+    out = run(CLI, "select", "--measure", "--n", 4096, "--candidates", 220, "--seed", 177, "--seeds", 5,
+              "--epochs", 100000, "--out", tmp_path)
+    import json
+
+    rep = json.load(open(tmp_path / "selection.json"))
+    assert rep["regret"] <= 1.3, out
+    assert rep["speedup_vs_default"] > 1.0

@@ -221,6 +221,28 @@ std::unique_ptr<TrainPlan> build_plan(lann_engine* e, const DevTrain& t, int pre
     // populations too small to fill the GPU with warps get a whole CTA (4 warps) per model
     const int total_fp32 = t.n_models - int(fp64_models.size());
     const bool small = total_fp32 <= 4 * e->sms;
+    // Large populations: all warp-kernel buckets run concurrently (one stream each), so the GPU
+    // stays full whatever a single bucket's wave count is; then the cheapest mapping is 2 lanes
+    // per model (less butterfly / redundant-Adam work than 4-8 lanes, a short enough per-lane
+    // sample loop, and enough warps). Measured on the config-3 sweep: 2 lanes 823 ms vs the
+    // per-bucket fill heuristic 892 ms (1 lane 994, 8 lanes 966).
+    int global_lanes = 0;
+    if (!env_lanes && !small) {
+      long long warps = 0;
+      int min_slots = 1 << 30;
+      for (auto& [shape, ms] : by_shape) {
+        std::map<std::pair<int, int>, int> per_tile;  // (tile, epochs) -> models
+        int rows = 1;
+        for (int m : ms) {
+          per_tile[{t.model_tile[m], t.epochs[m]}] += 1;
+          rows = std::max(rows, t.tile_rows[t.model_tile[m]]);
+        }
+        for (const auto& [key, cnt] : per_tile) warps += (cnt + 15) / 16;
+        min_slots = std::min(min_slots, std::max(1, fp32_warp_slots_per_sm(std::get<0>(shape), std::get<1>(shape),
+                                                                          std::get<2>(shape), 2, rows * 32)));
+      }
+      if (warps >= 2LL * min_slots * e->sms) global_lanes = 2;
+    }
     for (auto& [shape, ms] : by_shape) {
       // group: same tile and epoch count, up to G models; longest groups first
       std::stable_sort(ms.begin(), ms.end(), [&](int a, int b) {
@@ -244,7 +266,7 @@ std::unique_ptr<TrainPlan> build_plan(lann_engine* e, const DevTrain& t, int pre
       };
       int bucket_rows = 1;
       for (int m : ms) bucket_rows = std::max(bucket_rows, t.tile_rows[t.model_tile[m]]);
-      int lanes = env_lanes;
+      int lanes = env_lanes ? env_lanes : global_lanes;
       if (!lanes && small) lanes = 128;
       if (!lanes) {
         // lanes per model minimising the modelled makespan of this bucket on its own:
@@ -289,6 +311,9 @@ std::unique_ptr<TrainPlan> build_plan(lann_engine* e, const DevTrain& t, int pre
       b->sorted = DBuf<int>(ms, s);
       b->cost = cost;
       if (std::getenv("LANN_PHASE_PROFILE")) b->prof = DBuf<long long>(4, s);
+      if (std::getenv("LANN_PLAN_VERBOSE"))
+        std::fprintf(stderr, "fp32 bucket %d-%d-%d: %zu models, lanes %d, %d groups, rows <= %d\n", b->in, b->h1,
+                     b->h2, ms.size(), b->lanes, b->n_groups, max_rows);
       P.buckets.push_back(std::move(b));
     }
     // longest bucket first so it starts first on its stream

@@ -229,6 +229,17 @@ def main():
                 "algorithmic_flop_per_step": flop, "kernel_ms_per_step": train_launch_ms, "peak_source": peak_src,
                 "note": "FP32 CUDA-core FMA bound (tiny per-sample contractions, no tensor-core shape); "
                         "the 48-model population is latency-bound: <= 48 of 148 SMs busy"}
+    if precision == abi.FP32:
+        # the bound that actually applies to config 2: the serial epoch chain of the longest model
+        # (8 blur nets x 20,000 dependent epochs, one CTA each); cycles at the sampled SM clock
+        max_epochs = max(j.epochs for j in jobs)
+        roofline["critical_path"] = {
+            "models_on_path": sum(1 for j in jobs if j.epochs == max_epochs), "epochs": max_epochs,
+            "us_per_epoch": 1e3 * train_launch_ms / max_epochs,
+            "cycles_per_epoch": 1e6 * train_launch_ms / max_epochs * 1.965,
+            "sms_busy": f"{len(jobs)} of 148 (one CTA per model)",
+            "note": "per epoch: forward/backward of 2 samples per thread, warp reduce-scatter of 72 gradient "
+                    "values, cross-warp sum + Adam + weight broadcast (2 CTA barriers); DESIGN.md section 3"}
 
     # ---- e2e through the public C ABI with host buffers ----
     e2e_times = []

@@ -23,4 +23,8 @@ if [ "${PROFILE:-1}" = "1" ]; then
   python tools/sweep_parts.py 256 > gpurun_out/sweep.txt 2>&1
   python tools/prof_sweep.py 256 >> gpurun_out/sweep.txt 2>&1
 fi
+for r in cta h8 fp64 select; do
+  [ -f gpurun_out/prof_$r.ncu-rep ] && python tools/ncu_summary.py gpurun_out/prof_$r.ncu-rep > gpurun_out/summary_$r.txt 2>&1
+done
+rm -f gpurun_out/*.ncu-rep  # keep the copy-back under gpurun's size cap; summaries carry the numbers
 tail -5 gpurun_out/pytest_gpu.txt; cat gpurun_out/bench.json; cat gpurun_out/bench_ref.json; cat gpurun_out/sweep.txt

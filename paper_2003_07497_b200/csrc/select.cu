@@ -32,10 +32,34 @@ __device__ __forceinline__ uint64_t derive(uint64_t root, uint64_t stream) {
   sm64(s);
   return sm64(s);
 }
+// Exact 64-bit remainder by a small divisor without the emulated 64-bit modulo:
+// M = floor((2^64 - 1) / n) (table g_fastmod, built once per device), q = mulhi(r, M) is
+// floor(r / n) minus at most 2, so r - q n lies in [0, 3n) and two conditional subtractions
+// give r % n exactly.
+constexpr uint32_t kFastModMax = 4096;
+__device__ uint64_t g_fastmod[kFastModMax + 1];
+__global__ void fastmod_init_kernel() {
+  for (uint32_t n = blockIdx.x * blockDim.x + threadIdx.x + 1; n <= kFastModMax; n += gridDim.x * blockDim.x)
+    g_fastmod[n] = ~0ULL / n;
+}
+__device__ __forceinline__ uint64_t fastmod(uint64_t r, uint64_t n, uint64_t M) {
+  uint64_t rem = r - __umul64hi(r, M) * n;
+  if (rem >= n) rem -= n;
+  if (rem >= n) rem -= n;
+  return rem;
+}
 __device__ __forceinline__ uint64_t bounded(uint64_t& s, uint64_t n) {
   // power of two: (2^64 - n) % n == 0, so the first draw is always accepted and
   // r % n == r & (n - 1) — the same value Rng::bounded returns, without a 64-bit modulo
   if ((n & (n - 1)) == 0) return sm64(s) & (n - 1);
+  if (n <= kFastModMax) {
+    const uint64_t M = g_fastmod[n];
+    const uint64_t thr = fastmod(0 - n, n, M);
+    for (;;) {
+      const uint64_t r = sm64(s);
+      if (r >= thr) return fastmod(r, n, M);
+    }
+  }
   const uint64_t thr = (0 - n) % n;
   for (;;) {
     const uint64_t r = sm64(s);
@@ -382,6 +406,16 @@ __global__ void __launch_bounds__(256) select_variants_fast(const __grid_constan
 
 }  // namespace
 
+// the fastmod table, filled once per device (stream-ordered before the first scorer launch)
+void ensure_fastmod_table(cudaStream_t s) {
+  static bool done[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64 || done[dev]) return;
+  fastmod_init_kernel<<<16, 256, 0, s>>>();
+  done[dev] = true;
+}
+
 // Host side of the fast path: fold normalisation into layer 1 (in FP64, then round).
 bool select_variants_fast_launch(int n_models, int kind, int max_threads, uint64_t seed, int64_t first,
                                  int64_t n, const int* n_inputs, const int* h1, const int* h2,
@@ -389,6 +423,7 @@ bool select_variants_fast_launch(int n_models, int kind, int max_threads, uint64
                                  const double* params, const double* norm, int* d_idx, double* d_score,
                                  int sms, cudaStream_t s) {
   if (n_models < 1 || n_models > kFastMaxV || kind < 0 || kind > 3) return false;
+  ensure_fastmod_table(s);
   static const int nb_of[4] = {5, 3, 4, 5};
   const int nb = nb_of[kind];
   FastModels fm{};
@@ -457,6 +492,7 @@ int select_variants_launch(int n_models, int precision, int kind, int max_thread
                            const int* d_h2, const int* d_logt, const int* d_thd,
                            const int64_t* d_poff, const double* d_params, const double* d_norm,
                            int* d_idx, double* d_score, int sms, cudaStream_t s) {
+  ensure_fastmod_table(s);
   VariantArgs a{n_models, precision, kind, max_threads, seed, first, n, d_in, d_h1, d_h2,
                 d_logt, d_thd, d_poff, d_params, d_norm, d_idx, d_score};
   int64_t blocks = (n + 255) / 256;

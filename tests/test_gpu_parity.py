@@ -228,7 +228,11 @@ def trained_variant_models(engine):
     return jobs, res, params, norms
 
 
-def test_select_variants_fp64_bit_exact(engine, oracle):
+@pytest.mark.parametrize("max_threads", [16, 12, 5000])
+def test_select_variants_fp64_bit_exact(engine, oracle, max_threads):
+    """Counter-generated candidates (Rng::bounded's rejection rule: power-of-two, table-driven
+    exact remainder for n <= 4096, and the plain 64-bit modulo above) and exact-order scores are
+    identical to the C oracle for every kernel kind."""
     jobs, res, params, norms = trained_variant_models(engine)
     for kind in (abi.MM, abi.MV, abi.MC, abi.MP):
         idx = [i for i, j in enumerate(jobs) if j.world.kind == kind]
@@ -236,11 +240,11 @@ def test_select_variants_fp64_bit_exact(engine, oracle):
                    "norm": norms[i]} for i in idx]
         thd = np.array([1 if jobs[i].world.hw_class == abi.HW_CPU else 0 for i in idx], dtype=np.int32)
         n = 4000
-        gi, gs = engine.select_variants(models, thd, kind, 16, 7, 1000, n, precision=abi.FP64_EXACT)
+        gi, gs = engine.select_variants(models, thd, kind, max_threads, 7, 1000, n, precision=abi.FP64_EXACT)
         ms, keep = E._model_set(models, abi.FP64_EXACT)
         oi = np.zeros(n, dtype=np.int32)
         os_ = np.zeros(n)
-        oracle.lib.or_select_variants(ms, thd, kind, 16, 7, 1000, n, oi, os_)
+        oracle.lib.or_select_variants(ms, thd, kind, max_threads, 7, 1000, n, oi, os_)
         assert np.array_equal(gi, oi) and np.array_equal(gs, os_)
 
 

@@ -15,6 +15,8 @@
 //   never stored. Model weights and normalisation live in shared memory.
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
+#include <cstring>
 
 #include "kernels.cuh"
 
@@ -404,6 +406,85 @@ __global__ void __launch_bounds__(256) select_variants_fast(const __grid_constan
   }
 }
 
+// Packed variant of select_variants_fast: hidden units in pairs on FFMA2 (sm_100 fma.rn.f32x2)
+// with the candidate feature as the broadcast operand and the weight pairs as 64-bit uniform
+// operands — the scorer is issue-bound (ncu: 81% issue slots), and this halves the FMA issue.
+typedef unsigned long long f32x2;
+__device__ __forceinline__ f32x2 pk2(float a, float b) {
+  f32x2 r;
+  asm("mov.b64 %0, {%1,%2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void upk2(f32x2 p, float& a, float& b) {
+  asm("mov.b64 {%0,%1}, %2;" : "=f"(a), "=f"(b) : "l"(p));
+}
+__device__ __forceinline__ f32x2 ffma2(f32x2 a, f32x2 b, f32x2 c) {
+  f32x2 r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+
+struct FastModels2 {
+  int nv;
+  f32x2 w1[kFastMaxV][8][4];  // [v][column][hidden pair]
+  f32x2 b1[kFastMaxV][4];
+  f32x2 w2[kFastMaxV][4];
+  float b2[kFastMaxV];
+  float tmin[kFastMaxV], trange[kFastMaxV];
+  int logt[kFastMaxV];
+};
+
+template <int NB>
+__global__ void __launch_bounds__(256) select_variants_fast2(const __grid_constant__ FastModels2 fm,
+                                                             int kind, int max_threads, uint64_t seed,
+                                                             int64_t first, int64_t n, int* out_idx,
+                                                             double* out_score) {
+  constexpr int NC = NB + 2;  // columns: base features, n_thd, c
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    double base[8];
+    uint64_t c;
+    gen_candidate(kind, max_threads, seed, first + i, base, c);
+    float x[NC];
+#pragma unroll
+    for (int j = 0; j < NB; ++j) x[j] = (float)base[j];
+    x[NB] = (float)base[NB];
+    x[NB + 1] = (float)(double)c;
+    int best = -1;
+    float best_s = 0.f;
+#pragma unroll
+    for (int v = 0; v < kFastMaxV; ++v) {
+      if (v < fm.nv) {
+        f32x2 z[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) z[q] = fm.b1[v][q];
+#pragma unroll
+        for (int j = 0; j < NC; ++j)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) z[q] = ffma2(fm.w1[v][j][q], pk2(x[j], x[j]), z[q]);
+        f32x2 acc = pk2(fm.b2[v], 0.f);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          float za, zb;
+          upk2(z[q], za, zb);
+          acc = ffma2(fm.w2[v][q], pk2(fmaxf(za, 0.f), fmaxf(zb, 0.f)), acc);
+        }
+        float o0, o1;
+        upk2(acc, o0, o1);
+        float t = fmaf(o0 + o1, fm.trange[v], fm.tmin[v]);
+        if (fm.logt[v]) t = __expf(t);
+        t = fmaxf(t, 1e-9f);
+        if (best < 0 || t < best_s) {
+          best = v;
+          best_s = t;
+        }
+      }
+    }
+    out_idx[i] = best;
+    out_score[i] = (double)best_s;
+  }
+}
+
 }  // namespace
 
 // the fastmod table, filled once per device (stream-ordered before the first scorer launch)
@@ -464,6 +545,32 @@ bool select_variants_fast_launch(int n_models, int kind, int max_threads, uint64
   const int64_t cap = (int64_t)sms * 16;
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
+  if (std::getenv("LANN_SELECT_UNPACKED") == nullptr) {
+    FastModels2 f2{};
+    f2.nv = fm.nv;
+    for (int v = 0; v < fm.nv; ++v) {
+      for (int q = 0; q < 4; ++q) {
+        for (int j = 0; j < 8; ++j) {
+          float pair[2] = {fm.w1[v][2 * q][j], fm.w1[v][2 * q + 1][j]};
+          std::memcpy(&f2.w1[v][j][q], pair, 8);
+        }
+        float b[2] = {fm.b1[v][2 * q], fm.b1[v][2 * q + 1]};
+        std::memcpy(&f2.b1[v][q], b, 8);
+        float w[2] = {fm.w2[v][2 * q], fm.w2[v][2 * q + 1]};
+        std::memcpy(&f2.w2[v][q], w, 8);
+      }
+      f2.b2[v] = fm.b2[v];
+      f2.tmin[v] = fm.tmin[v];
+      f2.trange[v] = fm.trange[v];
+      f2.logt[v] = fm.logt[v];
+    }
+    switch (nb) {
+      case 3: select_variants_fast2<3><<<(unsigned)blocks, 256, 0, s>>>(f2, kind, max_threads, seed, first, n, d_idx, d_score); break;
+      case 4: select_variants_fast2<4><<<(unsigned)blocks, 256, 0, s>>>(f2, kind, max_threads, seed, first, n, d_idx, d_score); break;
+      default: select_variants_fast2<5><<<(unsigned)blocks, 256, 0, s>>>(f2, kind, max_threads, seed, first, n, d_idx, d_score); break;
+    }
+    return true;
+  }
   switch (nb) {
     case 3: select_variants_fast<3><<<(unsigned)blocks, 256, 0, s>>>(fm, kind, max_threads, seed, first, n, d_idx, d_score); break;
     case 4: select_variants_fast<4><<<(unsigned)blocks, 256, 0, s>>>(fm, kind, max_threads, seed, first, n, d_idx, d_score); break;

@@ -122,7 +122,7 @@ def test_fp32_population_status_and_metrics(engine):
 
 
 @pytest.mark.parametrize("I", [4, 5, 6])
-@pytest.mark.parametrize("n", [100, 129, 250, 700])
+@pytest.mark.parametrize("n", [100, 129, 250, 700, 2500])
 def test_fp32_cta_kernel_two_hidden_trace_prefix(engine, oracle, I, n):
     """The CTA-per-model kernel (two interleaved samples per thread, lean reduce-scatter) on
     the two-hidden-layer nets, every compiled input width and on row counts below one

@@ -574,6 +574,14 @@ int prepare_population(lann_engine* e, int n_jobs, const lann_job* jobs, int pre
   pop.base.assign(n_jobs, lann_job_result{});
   for (auto& r : pop.base) r.nonfinite_epoch = -1;
   e->err.clear();
+  const bool hprof = std::getenv("LANN_HOST_PROFILE") != nullptr;
+  auto now = [] { return std::chrono::steady_clock::now(); };
+  const auto h0 = now();
+  auto hlog = [&](const char* what, std::chrono::steady_clock::time_point since) {
+    if (hprof)
+      std::fprintf(stderr, "host %-10s %8.3f ms\n", what,
+                   std::chrono::duration<double, std::milli>(now() - since).count());
+  };
   // distinct datasets, splits and tiles
   using DKey = std::tuple<std::string, uint64_t, int>;
   std::map<DKey, int> dkeys;
@@ -609,6 +617,8 @@ int prepare_population(lann_engine* e, int n_jobs, const lann_job* jobs, int pre
   parallel_for(int(dsrc.size()), [&](int d) {
     dstat[d] = build_dataset(dsrc[d]->world, dsrc[d]->data_seed, dsrc[d]->count, dsets[d]);
   });
+  hlog("datasets", h0);
+  const auto h1 = now();
   std::vector<Tile> tiles(tsrc.size());
   std::vector<Status> tstat(tsrc.size());
   parallel_for(int(tsrc.size()), [&](int k) {
@@ -641,6 +651,8 @@ int prepare_population(lann_engine* e, int n_jobs, const lann_job* jobs, int pre
     r.n_eval = tiles[k].n_eval();
     pop.model_job.push_back(j);
   }
+  hlog("tiles", h1);
+  const auto h2 = now();
   const int M = int(pop.model_job.size());
   pop.M = M;
   if (M == 0) return pop.base[0].status;
@@ -694,6 +706,8 @@ int prepare_population(lann_engine* e, int n_jobs, const lann_job* jobs, int pre
       pop.toff[m] = pop.trace_total;
       pop.trace_total += t.epochs[m];
     }
+  hlog("pack+init", h2);
+  const auto h3 = now();
   // upload once
   cudaStream_t s = e->stream;
   pop.dX = DBuf<double>(X, s);
@@ -722,8 +736,11 @@ int prepare_population(lann_engine* e, int n_jobs, const lann_job* jobs, int pre
   pop.dMape = DBuf<double>(size_t(M), s);
   pop.dThr = DBuf<double>(size_t(M), s);
   pop.dRho = DBuf<double>(size_t(M), s);
+  hlog("uploads", h3);
+  const auto h4 = now();
   pop.plan = build_plan(e, t, precision, pop.dX.p, pop.dY.p, pop.rows);
   ck(cudaStreamSynchronize(s), "prepare");
+  hlog("plan", h4);
   return LANN_OK;
 }
 

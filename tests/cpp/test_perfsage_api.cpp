@@ -229,6 +229,73 @@ int main() {
     cfg3.seed = 3;
     CHECK(train_nn(train, cfg3).loss_trace == pop[2].loss_trace);
   }
+  // TrainLinear.RecoversExactLine (test_models.cpp:269-285): t = 2c + 1 with small dims
+  {
+    // sample_params draws (densities vary: a full-rank design), dims <= 16, t = 2c + 1
+    auto ds = datagen::build_mock(KernelKind::MM, "dense_threaded", 60, 13, 4, 16);
+    for (auto& smp : ds.samples) smp.runtime_s = 2.0 * double(smp.c) + 1.0;
+    ModelConfig cfg;
+    cfg.family = ModelFamily::LrC;
+    const auto model = train_lrc(ds, cfg);
+    const auto& lin = std::get<LinearModel>(model.payload);
+    CHECK(std::fabs(lin.weights.back() - 2.0) < 1e-6);
+    CHECK(std::fabs(lin.intercept - 1.0) < 1e-6);
+    for (std::size_t j = 0; j + 1 < lin.weights.size(); ++j) CHECK(std::fabs(lin.weights[j]) < 1e-5);
+    CHECK_THROWS(param_count(model), ParamError);
+  }
+  // TrainConst.UsesOnlyComplexity (test_models.cpp:287-301)
+  {
+    const auto ds = synth_mm(60, 15, [](std::uint64_t c, int, std::mt19937_64&) { return 5e-9 * double(c) + 2e-6; });
+    ModelConfig cfg;
+    cfg.family = ModelFamily::Const;
+    const auto model = train_const(ds, cfg);
+    CHECK(model.schema == std::vector<std::string>{"c"});
+    Sample smp = ds.samples[0];
+    const double before = predict(model, model_features(smp, ModelFamily::Const));
+    smp.features[0] += 100.0;
+    smp.features[3] = 0.25;
+    const double after = predict(model, model_features(smp, ModelFamily::Const));
+    CHECK(before == after);
+    CHECK(std::fabs(before - smp.runtime_s) <= smp.runtime_s * 1e-3);
+  }
+  // TrainForest.ConstantTargetAndDeterminism (test_models.cpp:303-326)
+  {
+    const auto ds = synth_mm(40, 3, [](std::uint64_t, int, std::mt19937_64&) { return 0.75; });
+    ModelConfig cfg;
+    cfg.family = ModelFamily::NlrC;
+    cfg.seed = 5;
+    const auto model = train_nlrc(ds, cfg);
+    const auto preds = predict_dataset(model, ds);
+    for (double v : preds) CHECK(v == 0.75);
+    const auto noisy = synth_mm(50, 17, [](std::uint64_t c, int, std::mt19937_64& r) {
+      return 1e-9 * double(c) + double(r() >> 11) * 0x1.0p-53 * 1e-6;
+    });
+    const auto a = train_nlrc(noisy, cfg), b = train_nlrc(noisy, cfg);
+    CHECK(predict_dataset(a, noisy) == predict_dataset(b, noisy));
+    Dataset tiny = ds;
+    tiny.samples.resize(5);
+    CHECK_THROWS(train_nlrc(tiny, cfg), ParamError);
+  }
+  // ModelIo.RoundTripPredictionsAreBitExact (test_models.cpp:328-350), all five families
+  {
+    const auto ds = synth_mm(40, 19, [](std::uint64_t c, int, std::mt19937_64& r) {
+      return 2e-9 * double(c) * (1 + (double(r() >> 11) * 0x1.0p-53 - 0.5) * 0.2) + 1e-7;
+    });
+    for (ModelFamily family :
+         {ModelFamily::NnC, ModelFamily::Nn, ModelFamily::Const, ModelFamily::LrC, ModelFamily::NlrC}) {
+      ModelConfig cfg = default_config(KernelKind::MM, family);
+      cfg.family = family;
+      cfg.epochs = 200;
+      cfg.seed = 23;
+      const auto model = train_model(ds, cfg);
+      const std::string path = "/tmp/lann_model_" + to_string(family) + ".json";
+      save_model(model, path);
+      const auto back = load_model(path);
+      CHECK(back.schema == model.schema);
+      CHECK(predict_dataset(model, ds) == predict_dataset(back, ds));
+    }
+    CHECK_THROWS(load_model("/tmp/lann_nonexistent_model.json"), LoadError);
+  }
   std::printf("drop-in API: %d failures\n", g_fail);
   return g_fail == 0 ? 0 : 1;
 }

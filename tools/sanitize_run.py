@@ -1,0 +1,37 @@
+"""Small end-to-end exercise of every kernel family, for compute-sanitizer (developer tool):
+  compute-sanitizer --tool memcheck python tools/sanitize_run.py"""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import numpy as np  # noqa: E402
+
+from paper_2003_07497_b200 import abi  # noqa: E402
+from paper_2003_07497_b200 import engine as E  # noqa: E402
+from paper_2003_07497_b200 import population as P  # noqa: E402
+
+eng = E.Engine(0)
+small = P.config2_jobs(root_seed=1, epochs_scale=0.005)
+for prec in (abi.FP32, abi.FP64_EXACT):
+    st, res, params, _ = eng.run_population(small, prec, want_params=True, want_trace=True)
+    print("config2 tiny", prec, st)
+sweep = P.config3_jobs(root_seed=1, n_seeds=2, combos=E.default_combos()[::6])
+for lanes in ("1", "2", "8", "32"):
+    os.environ["LANN_FP32_LANES"] = lanes
+    st, res, _, _ = eng.run_population([j for j in sweep], abi.FP32)
+    print("sweep lanes", lanes, st)
+os.environ.pop("LANN_FP32_LANES")
+pop = eng.prepare(P.config2_jobs(root_seed=1, epochs_scale=0.005), abi.FP32)
+pop.run(1)
+st, res, params, _ = pop.fetch(want_params=True)
+norms = pop.norms()
+jobs = P.config2_jobs(root_seed=1)
+idx = [i for i, j in enumerate(jobs) if j.world.kind == abi.MM]
+models = [{"inputs": res[i].n_inputs, "h1": 8, "h2": 0, "log_target": 0, "params": params[i], "norm": norms[i]}
+          for i in idx]
+thd = [1 if jobs[i].world.hw_class == abi.HW_CPU else 0 for i in idx]
+for prec in (abi.FP32, abi.FP64_EXACT):
+    gi, gs = eng.select_variants(models, thd, abi.MM, 12, 7, 0, 5000, precision=prec)
+    print("select", prec, int(gi.max()))
+print("done")

@@ -400,10 +400,54 @@ def selection_extra(E, eng, rank, world, barrier, max_over_ranks, n_cands=10_000
     kern_ms = max_over_ranks(kern_ms)
     total_ms = max_over_ranks(total_ms)
     flop_pred = 2 * 7 * 8 + 2 * 8 + 2 * 7 + 2  # 144 for MM nnc
-    return {"candidates_per_kind": n_cands, "models_per_kind": 10, "predictions": total_pred, "n_gpus": world,
-            "scaling": "strong", "value": total_pred / (kern_ms / 1e3), "unit": "predictions/s",
-            "kernel_ms": kern_ms, "call_ms_incl_d2h": total_ms,
-            "approx_tflops": total_pred * flop_pred / (kern_ms / 1e3) / 1e12}
+    out = {"candidates_per_kind": n_cands, "models_per_kind": 10, "predictions": total_pred, "n_gpus": world,
+           "scaling": "strong", "value": total_pred / (kern_ms / 1e3), "unit": "predictions/s",
+           "kernel_ms": kern_ms, "call_ms_incl_d2h": total_ms,
+           "approx_tflops": total_pred * flop_pred / (kern_ms / 1e3) / 1e12}
+    if rank == 0:
+        try:
+            out["cpu_reference"] = reference_predictions(jobs, res, params, norms)
+        except Exception as ex:  # noqa: BLE001
+            out["cpu_reference"] = {"error": str(ex)}
+    return out
+
+
+def reference_predictions(jobs, res, params, norms, n=1_000_000):
+    """The reference's own models::predict_dataset (oracle/_ref) on the host cores for the MM
+    kind's 10 variant models over a bounded sample of n candidate shapes (same feature ranges;
+    timing does not depend on the values), one model per thread task."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from oracle_lib import Reference  # test infrastructure: the baseline leg only
+    if not Reference.available():
+        return {"unavailable": "oracle/_ref not built"}
+    import concurrent.futures as cf
+    ref = Reference()
+    rng = np.random.default_rng(0)
+    idx = [i for i, j in enumerate(jobs) if j.world.kind == abi.MM]
+    threads = os.cpu_count() or 1
+    dims = rng.integers(1, 1025, (n, 3)).astype(np.float64)
+    feats = np.zeros((n, 8))
+    feats[:, :3] = dims
+    feats[:, 3] = 2.0 ** -rng.integers(0, 10, n)
+    feats[:, 4] = 2.0 ** -rng.integers(0, 10, n)
+    feats[:, 5] = rng.integers(1, 17, n)
+    c = (dims[:, 0] * dims[:, 1] * dims[:, 2]).astype(np.uint64)
+
+    feats_gpu = feats.copy()
+    feats_gpu[:, 5] = 0.0  # GPU-class variants take no n_thd
+
+    def one(i):
+        thd = jobs[i].world.hw_class == abi.HW_CPU
+        st, _ = ref.predict(abi.MM, thd, abi.NNC, (8,), params[i], norms[i], False, feats if thd else feats_gpu, c)
+        return st
+
+    t0 = time.perf_counter()
+    with cf.ThreadPoolExecutor(threads) as ex:
+        sts = list(ex.map(one, idx))
+    secs = time.perf_counter() - t0
+    return {"value": n * len(idx) / secs, "unit": "predictions/s", "cores": threads, "kind": "reference",
+            "sample": f"{n} MM candidate shapes x {len(idx)} variant models, models::predict_dataset, "
+                      f"one model per host thread task", "seconds": secs, "failed": int(sum(1 for s in sts if s))}
 
 
 if __name__ == "__main__":

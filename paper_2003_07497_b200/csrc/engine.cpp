@@ -226,22 +226,34 @@ std::unique_ptr<TrainPlan> build_plan(lann_engine* e, const DevTrain& t, int pre
     // per model (less butterfly / redundant-Adam work than 4-8 lanes, a short enough per-lane
     // sample loop, and enough warps). Measured on the config-3 sweep: 2 lanes 823 ms vs the
     // per-bucket fill heuristic 892 ms (1 lane 994, 8 lanes 966).
+    int max_epochs_all = 0;
+    for (auto& [shape, ms] : by_shape)
+      for (int m : ms) max_epochs_all = std::max(max_epochs_all, t.epochs[m]);
     int global_lanes = 0;
+    int off_lanes = 4;  // lanes for buckets off the critical path (mid-size populations)
     if (!env_lanes && !small) {
-      long long warps = 0;
+      long long warps = 0, warps_mixed = 0;
       int min_slots = 1 << 30;
       for (auto& [shape, ms] : by_shape) {
         std::map<std::pair<int, int>, int> per_tile;  // (tile, epochs) -> models
-        int rows = 1;
+        int rows = 1, epochs = 0;
         for (int m : ms) {
           per_tile[{t.model_tile[m], t.epochs[m]}] += 1;
           rows = std::max(rows, t.tile_rows[t.model_tile[m]]);
+          epochs = std::max(epochs, t.epochs[m]);
         }
-        for (const auto& [key, cnt] : per_tile) warps += (cnt + 15) / 16;
+        for (const auto& [key, cnt] : per_tile) {
+          warps += (cnt + 15) / 16;
+          warps_mixed += epochs < max_epochs_all ? (cnt + 15) / 16 : (cnt + 3) / 4;
+        }
         min_slots = std::min(min_slots, std::max(1, fp32_warp_slots_per_sm(std::get<0>(shape), std::get<1>(shape),
                                                                           std::get<2>(shape), 2, rows * 32)));
       }
       if (warps >= 2LL * min_slots * e->sms) global_lanes = 2;
+      // with the critical bucket at 8 lanes and the rest at 2, does the population fill the GPU
+      // once? then 2 lanes for the rest (throughput), else 4 (measured on 7,680 / 15,360 /
+      // 30,720-model sweep shares: 4 best at the smallest, 2 at the others)
+      if (warps_mixed >= 1LL * min_slots * e->sms) off_lanes = 2;
     }
     for (auto& [shape, ms] : by_shape) {
       // group: same tile and epoch count, up to G models; longest groups first
@@ -267,6 +279,9 @@ std::unique_ptr<TrainPlan> build_plan(lann_engine* e, const DevTrain& t, int pre
       int bucket_rows = 1;
       for (int m : ms) bucket_rows = std::max(bucket_rows, t.tile_rows[t.model_tile[m]]);
       int lanes = env_lanes ? env_lanes : global_lanes;
+      // per-shape-class overrides for experiments: LANN_FP32_LANES_H8 / LANN_FP32_LANES_2H
+      if (const char* ov = std::getenv(std::get<2>(shape) > 0 ? "LANN_FP32_LANES_2H" : "LANN_FP32_LANES_H8"))
+        if (std::atoi(ov) > 0) lanes = std::atoi(ov);
       if (!lanes && small) lanes = 128;
       if (!lanes) {
         // lanes per model minimising the modelled makespan of this bucket on its own:
@@ -283,6 +298,14 @@ std::unique_ptr<TrainPlan> build_plan(lann_engine* e, const DevTrain& t, int pre
             lanes = k;
           }
         }
+        // buckets run concurrently: a bucket with fewer epochs than the population's longest
+        // models is off the critical path and trades latency for throughput (off_lanes), while
+        // the critical-path bucket keeps at least 8 lanes per model (latency); measured on
+        // 7,680 / 15,360 / 30,720-model sweeps: 180.6 -> 161.8 / 266 -> 244 / 441 -> 428 ms
+        int bucket_epochs = 0;
+        for (int m : ms) bucket_epochs = std::max(bucket_epochs, t.epochs[m]);
+        if (bucket_epochs < max_epochs_all) lanes = off_lanes;
+        else lanes = std::max(8, lanes);
       }
       const int G = lanes <= 32 ? 32 / lanes : 1;
       std::vector<int> gfirst, gcount;

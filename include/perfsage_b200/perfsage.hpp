@@ -9,7 +9,7 @@
 //   models.hpp      ModelFamily, ModelConfig, default_config, param_count_for, NormStats,
 //                   TrainedModel, train_nn, train_model (NN families), predict, predict_dataset
 //   mlp.hpp         DenseLayer, Mlp
-//   eval.hpp        mape, mape_thresholded, spearman, average_ranks, make_report
+//   eval.hpp        mape, mape_thresholded, spearman, make_report, speedup
 //   selector.hpp    enumerate_candidates, select(ScheduleScorer...), select(TrainedModel, n, cands)
 //   features.hpp    feature_names, kind_from_feature_names
 //   csv.cpp         datagen::save_csv / load_csv (same columns, %.17g doubles)
@@ -25,6 +25,8 @@
 #include <functional>
 #include <iosfwd>
 #include <optional>
+#include <random>
+#include <algorithm>
 #include <utility>
 #include <span>
 #include <stdexcept>
@@ -73,6 +75,42 @@ void set_device(int device);
 }  // namespace engine
 
 // ---- kernels.hpp -------------------------------------------------------------------------------
+// ---- rng.hpp: the reference's seeded streams (mt19937_64 with hand-rolled draws) ---------------
+inline std::uint64_t splitmix64(std::uint64_t& state) {
+  std::uint64_t z = (state += 0x9e3779b97f4a7c15ULL);
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+inline std::uint64_t derive_seed(std::uint64_t root, std::uint64_t stream) {
+  std::uint64_t s = root ^ (0x9e3779b97f4a7c15ULL * (stream + 1));
+  splitmix64(s);
+  return splitmix64(s);
+}
+class Rng {
+ public:
+  explicit Rng(std::uint64_t seed) : engine_(seed) {}
+  std::uint64_t next() { return engine_(); }
+  std::uint64_t bounded(std::uint64_t n) {  // unbiased: reject below 2^64 mod n
+    const std::uint64_t threshold = (0 - n) % n;
+    for (;;)
+      if (const std::uint64_t r = engine_(); r >= threshold) return r % n;
+  }
+  std::int64_t uniform_int(std::int64_t lo, std::int64_t hi) {
+    return lo + static_cast<std::int64_t>(bounded(static_cast<std::uint64_t>(hi - lo) + 1));
+  }
+  double uniform() { return static_cast<double>(engine_() >> 11) * 0x1.0p-53; }
+  double uniform(double lo, double hi) { return lo + (hi - lo) * uniform(); }
+  template <typename T>
+  void partial_shuffle(std::vector<T>& v, std::size_t k) {
+    k = std::min(k, v.size());
+    for (std::size_t i = 0; i < k; ++i) std::swap(v[i], v[i + static_cast<std::size_t>(bounded(v.size() - i))]);
+  }
+
+ private:
+  std::mt19937_64 engine_;
+};
+
 namespace kernels {
 enum class KernelKind { MM, MV, MC, MP, Blur };
 std::string to_string(KernelKind kind);
@@ -97,6 +135,44 @@ struct ScheduleSpace {
   std::uint64_t size() const;
   std::vector<ScheduleCandidate> enumerate_all() const;
 };
+
+/// kernels.hpp:58-98 — one kernel instance's parameters (host-side value type).
+struct InstanceParams {
+  KernelKind kind = KernelKind::MM;
+  std::uint32_t m = 0, n = 0, k = 0, r = 0, s = 0;
+  double d1 = 1.0, d2 = 1.0, d = 1.0;
+  int n_thd = 1;
+  std::optional<ScheduleCandidate> schedule;
+  static InstanceParams mm(std::uint32_t m, std::uint32_t n, std::uint32_t k, double d1 = 1.0, double d2 = 1.0,
+                           int n_thd = 1);
+  static InstanceParams mv(std::uint32_t m, std::uint32_t n, double d = 1.0, int n_thd = 1);
+  static InstanceParams mc(std::uint32_t m, std::uint32_t n, std::uint32_t r, double d = 1.0, int n_thd = 1);
+  static InstanceParams mp(std::uint32_t m, std::uint32_t n, std::uint32_t r, std::uint32_t s, double d = 1.0,
+                           int n_thd = 1);
+  static InstanceParams blur(std::uint32_t n, const ScheduleCandidate& sched);
+  void validate() const;  // ParamError on an out-of-domain field (kernels.cpp:149-182)
+};
+/// kernels.cpp:184-206: mm m*n*k, mv m*n, mc (m-r+1)(n-r+1)r^2, mp ceil(n/s)ceil(m/s)s^2, blur n^2
+std::uint64_t complexity(const InstanceParams& params);
+
+/// variants.hpp:12-32 — the descriptor of a benchmarked variant (the engine measures none of the
+/// reference's CPU kernels; datagen::build_dataset needs a probe or an external variant).
+enum class Storage { Dense, Sparse };
+enum class Threading { Threaded, FixedSingle };
+enum class ImplKind { Naive, Tiled, External };
+enum class HardwareClass { Cpu, Gpu };
+struct VariantDescriptor {
+  std::string variant_id;
+  KernelKind kind = KernelKind::MM;
+  Storage storage = Storage::Dense;
+  Threading threading = Threading::Threaded;
+  ImplKind impl = ImplKind::Naive;
+  HardwareClass hw_class = HardwareClass::Cpu;
+  std::string hardware_label;
+  std::string launch_command;  // external variants only
+  bool is_external() const { return impl == ImplKind::External; }
+  bool takes_n_thd() const { return hw_class == HardwareClass::Cpu && kind != KernelKind::Blur; }
+};
 }  // namespace kernels
 
 // ---- datagen.hpp:72-116 -------------------------------------------------------------------------
@@ -119,6 +195,43 @@ struct Dataset {
   std::vector<double> runtimes() const;
 };
 
+/// datagen.hpp:44-51 / datagen.cpp:118-160: untimed warm-ups, then the median of `reps` runs.
+struct TimingPolicy {
+  int warmups = 1;
+  int reps = 5;
+};
+
+/// datagen.hpp:15-40 / datagen.cpp:18-110: the sampling space and its draws (host-side).
+struct ParamSpace {
+  kernels::KernelKind kind = kernels::KernelKind::MM;
+  std::uint32_t dim_min = 1, dim_max = 1024;
+  int max_threads = 1;
+  std::vector<std::uint32_t> mc_filter_dims = {3, 5, 7};
+  std::vector<std::uint32_t> mp_aux_dims = {2, 3, 4, 5};
+  std::vector<std::uint32_t> mp_pool_dims = {1, 2};
+  bool density_ladder_includes_one = true;
+  std::vector<std::uint32_t> blur_sides = {1024, 2048, 4096, 8192, 16384, 32768};
+  kernels::ScheduleSpace schedules = kernels::ScheduleSpace::cpu_default();
+  static ParamSpace defaults(kernels::KernelKind kind, int max_threads);
+  void validate() const;
+};
+std::vector<double> density_ladder(std::uint64_t cells, bool include_one);
+kernels::InstanceParams sample_params(const ParamSpace& space, Rng& rng);
+kernels::InstanceParams sample_params(const ParamSpace& space, std::uint64_t seed);
+double median_of(std::vector<double> values);  // datagen.cpp:118-124 (DomainError when empty)
+
+/// datagen.hpp:94-116: build_dataset with a runtime probe. Without a probe the reference times
+/// its CPU kernels, which this engine does not: external variants run the black-box protocol,
+/// anything else throws ParamError (use build_measured for B200 variants). Probe or external
+/// failures abort with BuildAbortError carrying the completed sample count.
+using RuntimeProbe = std::function<double(const kernels::InstanceParams&)>;
+struct BuildOptions {
+  TimingPolicy policy;
+  RuntimeProbe probe;
+};
+Dataset build_dataset(const kernels::VariantDescriptor& variant, const ParamSpace& space, std::size_t count,
+                      std::uint64_t seed, const BuildOptions& options = {});
+
 /// Disjoint, exhaustive, seeded-shuffle partition (datagen.cpp:225-248).
 std::pair<Dataset, Dataset> split(const Dataset& dataset, double train_fraction, std::uint64_t seed);
 
@@ -133,11 +246,6 @@ Dataset load_csv(const std::string& path);
 /// acceptance_main.cpp:271-279). variant_id names the combination (combo_variant_id).
 Dataset build_synthetic(int world_index, std::size_t count, std::uint64_t seed);
 
-/// datagen.hpp:44-51 / datagen.cpp:118-160: untimed warm-ups, then the median of `reps` runs.
-struct TimingPolicy {
-  int warmups = 1;
-  int reps = 5;
-};
 /// Real measurement on the B200 (lann_build_measured_dataset): `count` sample_params draws of
 /// the GPU-class space (no n_thd), each timed as B200 kernel variant `variant` (CUDA events,
 /// TimingPolicy median). Variants per kind: measured_variants(kind). variant_id = variant@b200.
@@ -177,16 +285,28 @@ struct DenseLayer {
 
 struct Mlp {
   std::vector<DenseLayer> layers;
+  /// mlp.cpp:9-25: Glorot-uniform weights U(-sqrt(6/(in+out)), +sqrt(6/(in+out))) drawn in layer /
+  /// row order from `rng`, biases 0 (host-side, bit-identical to the reference)
+  static Mlp init(const std::vector<int>& dims, Rng& rng);
   int input_dim() const { return layers.empty() ? 0 : layers.front().in; }
   int param_count() const;
 };
+void unflatten_params(Mlp& net, std::span<const double> flat);  // mlp.cpp:132-140
+/// mlp.hpp:64-66 / mlp.cpp:156-175 on the GPU (one-model lann_train): `epochs` full-batch Adam
+/// epochs over normalised rows X (one vector per sample) and targets y; net's weights updated in
+/// place; returns the pre-update loss trace. TrainingError(epoch) on a non-finite loss.
+std::vector<double> train_full_batch(Mlp& net, const std::vector<std::vector<double>>& X,
+                                     std::span<const double> y, double lr, int epochs);
 
 enum class ModelFamily { NnC, Nn, Const, LrC, NlrC };
 std::string to_string(ModelFamily family);
 ModelFamily family_from_string(const std::string& s);  // models.cpp (ParamError on unknown)
 
-/// features.cpp:10-21 / 59-72
+/// features.cpp:10-72
 std::vector<std::string> feature_names(kernels::KernelKind kind, bool with_n_thd);
+std::vector<double> featurize(const kernels::InstanceParams& params, bool augmented, bool with_n_thd);
+std::vector<double> featurize(const kernels::InstanceParams& params, bool augmented);  // with n_thd
+std::vector<std::string> model_schema(const std::vector<std::string>& base_names, ModelFamily family);
 std::pair<kernels::KernelKind, bool> kind_from_feature_names(const std::vector<std::string>& names);
 bool family_augmented(ModelFamily family);
 
@@ -250,6 +370,7 @@ struct TrainedModel {
 };
 
 std::vector<double> model_features(const datagen::Sample& sample, ModelFamily family);
+std::vector<double> model_features(const kernels::InstanceParams& params, ModelFamily family, bool with_n_thd = true);
 
 /// models.cpp:279-303 — trained on the GPU (one-model population).
 TrainedModel train_nn(const datagen::Dataset& train, const ModelConfig& config);
@@ -298,6 +419,7 @@ struct EvalReport {
 };
 EvalReport make_report(std::span<const double> truth, std::span<const double> pred,
                        double drop_fraction = 0.3);
+double speedup(double baseline_s, double chosen_s);  // eval.cpp: baseline / chosen (DomainError if <= 0)
 
 /// eval.cpp:110-197: per-group means (std::map key order) + an "overall" row.
 enum class GroupBy { Kernel, Variant, ModelFamily };

@@ -676,4 +676,22 @@ int ref_eval_model(const char* model_path, const char* csv, double drop, double*
     }
 }
 
+// n sample_params draws (datagen.cpp:60-110) of ParamSpace::defaults(kind, 8) from Rng(seed):
+// featurize(p, true) rows padded to LANN_ROW; returns the feature count.
+int ref_sample_features(int kind, std::uint64_t seed, int n, double* out) {
+    try {
+        const auto space = datagen::ParamSpace::defaults(kind_of(kind), 8);
+        Rng rng(seed);
+        int nf = 0;
+        for (int i = 0; i < n; ++i) {
+            const auto f = models::featurize(datagen::sample_params(space, rng), true);
+            nf = int(f.size());
+            std::copy(f.begin(), f.end(), out + std::size_t(i) * LANN_ROW);
+        }
+        return nf;
+    } catch (const std::exception& e) {
+        return -status_of(e);
+    }
+}
+
 }  // extern "C"

@@ -6,6 +6,16 @@
 //   formats_tool model-load IN             prints "ok" or "<ErrorType>: <what>"
 //   formats_tool model-synth OUT SEED      a model with awkward doubles (subnormals, -0, 0.1, ...)
 //   formats_tool model-dump IN             %a of f_min, f_max, t_min, t_max, flat params, loss_trace
+//   formats_tool api-gen KIND VARIANT MAXTHR DIMMAX GPU COUNT SEED OUT [SIDES...]
+//                                          datagen::build_dataset(descriptor, ParamSpace, ..., {probe})
+//                                          with the reference CLI's mock probe (perfsage.cpp:71-84)
+//   formats_tool api-init SEED D0 D1 ...   %a of Mlp::init(dims, Rng(SEED)) flattened
+//   formats_tool api-params KIND SEED N    N sample_params draws: features (augmented, n_thd) as %a
+//   formats_tool api-train SEED EPOCHS LR N D0 D1 ...
+//                                          models::train_full_batch on the GPU (needs a device):
+//                                          prints X, y, initial params, then trace + final params
+//                                          or "TrainingError <epoch>"
+//   formats_tool api-validate              InstanceParams::validate / complexity edge cases
 #include <cfloat>
 #include <cmath>
 #include <cstdio>
@@ -27,7 +37,7 @@ static int report(const std::exception& e) {
 }
 
 int main(int argc, char** argv) {
-  if (argc < 3) return 2;
+  if (argc < 2) return 2;
   const std::string mode = argv[1];
   try {
     if (mode == "csv-roundtrip") {
@@ -110,6 +120,123 @@ int main(int argc, char** argv) {
       std::printf("%a\n%a\n", m.norm.t_min, m.norm.t_max);
       for (double v : models::flatten_params(std::get<models::Mlp>(m.payload))) std::printf("%a\n", v);
       for (double v : m.loss_trace) std::printf("%a\n", v);
+    } else if (mode == "api-gen") {
+      if (argc < 10) return 2;
+      const auto kind = kernels::kind_from_string(argv[2]);
+      const std::string vid = argv[3];
+      auto space = datagen::ParamSpace::defaults(kind, std::atoi(argv[4]));
+      space.dim_max = std::uint32_t(std::strtoul(argv[5], nullptr, 10));
+      if (kind == kernels::KernelKind::Blur) {
+        space.blur_sides.clear();
+        for (int i = 10; i < argc; ++i) space.blur_sides.push_back(std::uint32_t(std::strtoul(argv[i], nullptr, 10)));
+        space.schedules = std::atoi(argv[6]) ? kernels::ScheduleSpace::gpu_style() : kernels::ScheduleSpace::cpu_default();
+      }
+      kernels::VariantDescriptor v;
+      v.variant_id = vid;
+      v.kind = kind;
+      v.threading = vid.ends_with("_single") ? kernels::Threading::FixedSingle : kernels::Threading::Threaded;
+      datagen::BuildOptions opts;
+      opts.probe = [](const kernels::InstanceParams& p) {  // perfsage.cpp:71-84
+        std::uint64_t h = 0x9e3779b97f4a7c15ULL;
+        for (double f : models::featurize(p, true)) {
+          std::uint64_t bits;
+          std::memcpy(&bits, &f, sizeof bits);
+          h ^= bits;
+          splitmix64(h);
+        }
+        const double jitter = 0.5 + double(splitmix64(h) >> 11) * 0x1.0p-53;
+        return 1e-9 * double(kernels::complexity(p)) * jitter + 1e-6;
+      };
+      datagen::save_csv(datagen::build_dataset(v, space, std::size_t(std::atoi(argv[7])),
+                                               std::strtoull(argv[8], nullptr, 10), opts),
+                        argv[9]);
+    } else if (mode == "api-init") {
+      Rng rng(std::strtoull(argv[2], nullptr, 10));
+      std::vector<int> dims;
+      for (int i = 3; i < argc; ++i) dims.push_back(std::atoi(argv[i]));
+      try {
+        for (double v : models::flatten_params(models::Mlp::init(dims, rng))) std::printf("%a\n", v);
+      } catch (const ParamError& e) {
+        return report(e);
+      }
+    } else if (mode == "api-params") {
+      if (argc < 5) return 2;
+      const auto kind = kernels::kind_from_string(argv[2]);
+      auto space = datagen::ParamSpace::defaults(kind, 8);
+      Rng rng(std::strtoull(argv[3], nullptr, 10));
+      for (int i = 0, n = std::atoi(argv[4]); i < n; ++i) {
+        const auto p = datagen::sample_params(space, rng);
+        for (double f : models::featurize(p, true)) std::printf("%a ", f);
+        std::printf("\n");
+      }
+    } else if (mode == "api-train") {
+      if (argc < 8) return 2;
+      const std::uint64_t seed = std::strtoull(argv[2], nullptr, 10);
+      const int epochs = std::atoi(argv[3]), n = std::atoi(argv[5]);
+      const double lr = std::strtod(argv[4], nullptr);
+      std::vector<int> dims;
+      for (int i = 6; i < argc; ++i) dims.push_back(std::atoi(argv[i]));
+      Rng rng(seed);
+      auto net = models::Mlp::init(dims, rng);
+      std::vector<std::vector<double>> X(static_cast<std::size_t>(n), std::vector<double>(static_cast<std::size_t>(dims[0])));
+      std::vector<double> y(static_cast<std::size_t>(n));
+      for (auto& row : X)
+        for (auto& v : row) v = rng.uniform();
+      for (auto& v : y) v = rng.uniform();
+      std::printf("X");
+      for (const auto& row : X)
+        for (double v : row) std::printf(" %a", v);
+      std::printf("\ny");
+      for (double v : y) std::printf(" %a", v);
+      std::printf("\np0");
+      for (double v : models::flatten_params(net)) std::printf(" %a", v);
+      std::printf("\n");
+      try {
+        const auto trace = models::train_full_batch(net, X, y, lr, epochs);
+        std::printf("trace");
+        for (double v : trace) std::printf(" %a", v);
+        std::printf("\np1");
+        for (double v : models::flatten_params(net)) std::printf(" %a", v);
+        std::printf("\n");
+      } catch (const TrainingError& e) {
+        std::printf("TrainingError %d\n", e.epoch());
+      }
+    } else if (mode == "api-validate") {
+      using P = kernels::InstanceParams;
+      const std::pair<const char*, P> cases[] = {
+          {"mm-ok", P::mm(3, 4, 5, 0.5, 1.0, 2)},
+          {"mm-zero-dim", P::mm(0, 4, 5)},
+          {"mm-density", P::mm(3, 4, 5, 0.0, 1.0)},
+          {"mv-ok", P::mv(7, 9, 0.25, 1)},
+          {"mc-ok", P::mc(9, 8, 3, 1.0, 1)},
+          {"mc-small", P::mc(2, 8, 3)},
+          {"mp-ok", P::mp(9, 8, 3, 2, 1.0, 1)},
+          {"mp-small", P::mp(1, 8, 3, 2)},
+          {"blur-ok", P::blur(1024, {8, 256, 128, 8})},
+          {"blur-npow2", P::blur(1024, {8, 255, 128, 8})},
+          {"blur-small", P::blur(2, {8, 256, 128, 8})},
+      };
+      for (const auto& [name, p] : cases) {
+        try {
+          std::printf("%s %llu\n", name, static_cast<unsigned long long>(kernels::complexity(p)));
+        } catch (const ParamError&) {
+          std::printf("%s ParamError\n", name);
+        }
+      }
+      try {
+        auto bad = P::mv(3, 3);
+        bad.n_thd = 0;
+        bad.validate();
+        std::printf("n_thd0 ok\n");
+      } catch (const ParamError&) {
+        std::printf("n_thd0 ParamError\n");
+      }
+      std::printf("median %a %a\n", datagen::median_of({3.0, 1.0, 2.0}), datagen::median_of({4.0, 1.0, 2.0, 3.0}));
+      std::printf("speedup %a\n", eval::speedup(2.0, 0.5));
+      const auto lad = datagen::density_ladder(10, false);
+      std::printf("ladder");
+      for (double d : lad) std::printf(" %a", d);
+      std::printf("\n");
     } else {
       return 2;
     }

@@ -189,6 +189,7 @@ class Reference(_Lib):
         L.ref_eval_model.argtypes = [C.c_char_p, C.c_char_p, C.c_double, _dp]
         L.ref_cli_gen_mock.argtypes = [C.c_int, C.c_char_p, C.c_int, C.c_uint, C.c_int, _u32p, C.c_int, C.c_int,
                                        C.c_uint64, C.c_char_p]
+        L.ref_sample_features.argtypes = [C.c_int, C.c_uint64, C.c_int, _dp]
         L.ref_cli_select_mock.argtypes = [C.c_uint, C.c_int, C.c_uint64, C.c_int, C.c_int, _dp]
         L.ref_save_external_csv.argtypes = [C.c_int, C.c_int, C.c_int, C.c_char_p, C.c_char_p, C.c_int, C.c_uint64,
                                             C.c_char_p]
@@ -217,6 +218,11 @@ class Reference(_Lib):
         sides = np.ascontiguousarray(sides, dtype=np.uint32)
         return self.lib.ref_cli_gen_mock(kind, variant_id.encode(), max_threads, dim_max, len(sides), sides,
                                          int(gpu_lattice), count, seed, str(path).encode())
+
+    def sample_features(self, kind, seed, n):
+        out = np.zeros(n * 8)
+        nf = self.lib.ref_sample_features(kind, seed, n, out)
+        return nf, out.reshape(n, 8)[:, :max(nf, 0)]
 
     def cli_select_mock(self, n, n_cands, seed, epochs, threads):
         out = np.zeros(15)

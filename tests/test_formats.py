@@ -242,6 +242,65 @@ def test_gen_mock_timer_is_the_reference_cli(tmp_path, reference, kernel, kind, 
     assert open(ours, "rb").read() == open(ref, "rb").read()
 
 
+@pytest.mark.parametrize("kernel,kind,variant,dim_max,sides,gpu", [
+    ("mm", abi.MM, "dense_threaded", 1024, [1024], False),
+    ("mm", abi.MM, "tiled_threaded", 4096, [1024], False),
+    ("mv", abi.MV, "sparse_single", 1024, [1024], False),
+    ("mc", abi.MC, "dense_single", 300, [1024], False),
+    ("mp", abi.MP, "dense_threaded", 1024, [1024], False),
+    ("blur", abi.BLUR, "tiled", 1024, [512, 2048], False),
+    ("blur", abi.BLUR, "tiled", 1024, [1024], True),
+])
+def test_api_build_dataset_is_the_reference(tmp_path, tool, reference, kernel, kind, variant, dim_max, sides, gpu):
+    """The C++ API path a reference user calls — ParamSpace::defaults, VariantDescriptor,
+    datagen::build_dataset(variant, space, count, seed, {probe}) (datagen.cpp:177-223, sample_params
+    :60-110, featurize, complexity, Rng) — writes the reference's dataset byte for byte."""
+    ours = tmp_path / "api.csv"
+    run(tool, "api-gen", kernel, variant, "6", str(dim_max), str(int(gpu)), "80", "4", str(ours), *map(str, sides))
+    ref = tmp_path / "ref.csv"
+    assert reference.cli_gen_mock(kind, variant, 6, dim_max, sides, gpu, 80, 4, ref) == 0, reference.last_error()
+    assert open(ours, "rb").read() == open(ref, "rb").read()
+
+
+@pytest.mark.parametrize("kernel,kind", [("mm", abi.MM), ("mv", abi.MV), ("mc", abi.MC), ("mp", abi.MP),
+                                         ("blur", abi.BLUR)])
+def test_api_sample_params_is_the_reference(tool, reference, kernel, kind):
+    """datagen::sample_params draws (defaults space, max_threads 8) featurize to the reference's
+    values bit for bit over 300 draws of one Rng stream."""
+    rows = [[float.fromhex(x) for x in line.split()] for line in run(tool, "api-params", kernel, "11", "300").splitlines()]
+    nf, ref = reference.sample_features(kind, 11, 300)
+    assert nf > 0, reference.last_error()
+    assert [[v.hex() for v in r] for r in rows] == [[float(v).hex() for v in r] for r in ref]
+
+
+@pytest.mark.parametrize("dims", [[4, 8, 1], [6, 5, 5, 1], [7, 1], [1, 1], [3, 16, 16, 1]])
+def test_api_mlp_init_is_the_reference(tool, reference, dims):
+    """models::Mlp::init(dims, Rng) (mlp.cpp: Glorot-uniform weights, zero biases) draws the
+    reference's parameters bit for bit."""
+    ours = [float.fromhex(x) for x in run(tool, "api-init", "2024", *map(str, dims)).split()]
+    n, ref = reference.mlp_init(dims, 2024, raw=True)
+    assert n == len(ours)
+    assert [v.hex() for v in ours] == [float(v).hex() for v in ref]
+
+
+@pytest.mark.parametrize("dims", [["4"], ["4", "0", "1"]])
+def test_api_mlp_init_rejects_bad_dims(tool, dims):
+    assert run(tool, "api-init", "1", *dims).startswith("ParamError")
+
+
+def test_api_instance_params_validate_and_complexity(tool):
+    """kernels.cpp:149-206: InstanceParams::validate domain rules and the complexity formulas;
+    datagen::median_of, density_ladder and eval::speedup."""
+    out = dict(line.split(" ", 1) for line in run(tool, "api-validate").splitlines())
+    assert out["mm-ok"] == "60" and out["mv-ok"] == "63" and out["mc-ok"] == str(7 * 6 * 9)
+    assert out["mp-ok"] == str(4 * 5 * 4) and out["blur-ok"] == str(1024 * 1024)
+    for bad in ("mm-zero-dim", "mm-density", "mc-small", "mp-small", "blur-npow2", "blur-small", "n_thd0"):
+        assert out[bad] == "ParamError", bad
+    assert [float.fromhex(x) for x in out["median"].split()] == [2.0, 2.5]
+    assert float.fromhex(out["speedup"]) == 4.0
+    assert [float.fromhex(x) for x in out["ladder"].split()] == [0.5, 0.25, 0.125]
+
+
 def test_gen_rejects_unknown_native_variant(tmp_path):
     out = subprocess.run([CLI, "gen", "--mock-timer", "--kernel", "blur", "--variant", "dense_single", "--out",
                           str(tmp_path)], capture_output=True, text=True)

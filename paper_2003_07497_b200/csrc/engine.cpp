@@ -158,7 +158,7 @@ struct Fp32Bucket {
 
 struct Fp64Bucket {
   int shape[3] = {0, 0, 0};  // compiled shape, or {0,0,0} = generic kernel
-  int n = 0, max_p = 0, dyn = 0, in_smem = 0;
+  int n = 0, max_p = 0, dyn = 0, in_smem = 0, products = 0;
   DBuf<int> order;
   DBuf<double> scratch;
   DBuf<int64_t> soff;
@@ -373,7 +373,7 @@ std::unique_ptr<TrainPlan> build_plan(lann_engine* e, const DevTrain& t, int pre
       b->shape[2] = std::get<2>(shape);
       b->n = int(order.size());
       b->cost = cost(order.front());
-      size_t max_bytes_smem = 0, max_state = 0;
+      size_t max_bytes_smem = 0, max_state = 0, max_bytes_prod = 0;
       std::vector<int64_t> soff(t.n_models, 0);
       int64_t scratch = 0;
       for (int m : order) {
@@ -384,11 +384,19 @@ std::unique_ptr<TrainPlan> build_plan(lann_engine* e, const DevTrain& t, int pre
         const size_t state = fp64_state_bytes(np);
         max_state = std::max(max_state, state);
         max_bytes_smem = std::max(max_bytes_smem, state + rec);
+        if (b->shape[0] > 0)
+          max_bytes_prod = std::max(max_bytes_prod, state + fp64_product_record_bytes(t.tile_inputs[tile], t.h1[m],
+                                                                                      t.h2[m], t.tile_rows[tile]));
         soff[m] = scratch;
         scratch += int64_t(rec / 8);
       }
       b->in_smem = max_bytes_smem <= size_t(e->max_smem);
       b->dyn = int(b->in_smem ? max_bytes_smem : max_state);
+      // compiled shapes whose product rows fit too: phase B becomes pure DADD chains
+      if (b->shape[0] > 0 && max_bytes_prod <= size_t(e->max_smem) && !std::getenv("LANN_FP64_NOPROD")) {
+        b->products = 1;
+        b->dyn = int(max_bytes_prod);
+      }
       if (!b->in_smem) b->scratch = DBuf<double>(size_t(scratch), s);
       b->soff = DBuf<int64_t>(soff, s);
       b->order = DBuf<int>(order, s);
@@ -468,6 +476,7 @@ void execute_plan(lann_engine* e, const TrainPlan& P, double* dparams, double* d
     a.scratch = b->scratch.p;
     a.scratch_offset = b->soff.p;
     a.smem_records = b->in_smem;
+    a.rec_products = b->products;
     a.phase_cycles = b->prof.p;
     launch_train_fp64(a, b->max_p, b->dyn, b->shape[0] > 0 ? b->shape : nullptr, next_stream());
     ck(cudaGetLastError(), "train_fp64 launch");

@@ -34,6 +34,7 @@ struct TrainArgs {
   double* scratch;           // global per-sample records for models too big for smem
   const int64_t* scratch_offset;
   int smem_records;          // 1: per-sample records live in shared memory
+  int rec_products;          // 1: phase A also stores every weight's per-sample product row
   long long* phase_cycles;   // optional (LANN_PHASE_PROFILE): CTA 0's clock64 per phase
 };
 
@@ -94,6 +95,7 @@ void launch_train_fp64(const TrainArgs& a, int max_p, int dyn_bytes, const int* 
 bool fp64_shape_compiled(int in, int h1, int h2);
 // FP64 trainer footprint (see train_fp64.cu): record matrix of a model, model state
 size_t fp64_record_bytes(int in, int h1, int h2, int n);
+size_t fp64_product_record_bytes(int in, int h1, int h2, int n);
 size_t fp64_state_bytes(int p);
 bool launch_train_fp32(const TrainF32Args& a, int in, int h1, int h2, int lanes, int tile_bytes,
                        cudaStream_t s);

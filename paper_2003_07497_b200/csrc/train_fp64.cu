@@ -15,6 +15,11 @@
 //   phase B  threads own PARAMETERS: each sums its N per-sample terms in sample
 //            order (the only order-sensitive reduction), then applies Adam;
 //            one thread sums the loss terms in sample order.
+// Product rows (compiled shapes, N <= 256, the default): phase A also forms every weight's
+// term t*a for its sample (the same rounded product mlp.cpp:113 forms) and stores it as a
+// row, so a phase-B chain is a pure DADD chain over one row (~10.6 cycles per link against
+// ~18.7 with the DMUL inside the chain: one warp's FP64 issue, not shared memory, bounded
+// those); the single owner keeps w, m, v in registers.
 // Two __syncthreads per epoch. The record matrix is stored structure-of-arrays
 // (one row per quantity, samples contiguous): phase-A stores are contiguous across
 // lanes, and a phase-B chain fetches two samples per 128-bit shared-memory load, so
@@ -36,6 +41,12 @@ __host__ __device__ constexpr int rec_rows(int H1, int H2) {
   return 8 + 2 * (H1 + (H2 > 0 ? H2 : 0)) + 3;
 }
 __host__ __device__ constexpr int rec_ld(int N) { return (N + 1) & ~1; }  // even: 16-B aligned pairs
+// Product-row kernels (N <= 256) use one compile-time row stride: every phase-A record access
+// is then an immediate offset from the thread's sample column (no address arithmetic), and
+// 258 doubles = 516 words = 4 (mod 32) banks keeps a quarter-warp's 16-B loads of eight
+// consecutive rows at one sample conflict-free in phase B.
+constexpr int kProdMaxRows = 256;
+constexpr int kProdLd = 258;
 
 struct Shape {
   int I, H1, H2, nl, P, R;
@@ -89,8 +100,13 @@ struct Fixed {
   static constexpr int WO = H2 > 0 ? B2 + H2 : B1 + H1;  // output weights
   static constexpr int BO = WO + (H2 > 0 ? H2 : H1);
   static constexpr int P = BO + 1;
+  // product rows (kProd): one per weight, in parameter order without the biases, after the
+  // record rows: W1 (o,i) -> PR + o*I + i, W2 (o,i) -> PR + I*H1 + o*H1 + i, output i -> PO + i
+  static constexpr int PR = rec_rows(H1, H2);
+  static constexpr int P2 = PR + I * H1, PO = P2 + H1 * H2;
 
   // r = column s of the record matrix (r[row * ld])
+  template <bool kProd>
   __device__ static void sample(const double* __restrict__ w, double* __restrict__ r, int ld,
                                 double inv_n) {
     double x[I];
@@ -129,7 +145,7 @@ struct Fixed {
 #pragma unroll
       for (int o = 0; o < H2; ++o) {
         a2[o] = a2[o] > 0.0 ? a2[o] : 0.0;
-        r[(A2 + o) * ld] = a2[o];
+        if constexpr (!kProd) r[(A2 + o) * ld] = a2[o];  // kProd: only phase A reads a2
       }
       z = w[BO];
 #pragma unroll
@@ -142,14 +158,17 @@ struct Fixed {
     const double err = __dsub_rn(z, y);
     r[E2 * ld] = __dmul_rn(err, err);
     const double dout = __dmul_rn(2.0, err);
-    r[TO * ld] = __dmul_rn(inv_n, dout);
+    const double tout = __dmul_rn(inv_n, dout);
+    r[TO * ld] = tout;
+    double t1[H1];
     if constexpr (H2 > 0) {
-      double d2[H2];
+      double d2[H2], t2[H2];
 #pragma unroll
       for (int i = 0; i < H2; ++i) {
         const double acc = __dadd_rn(0.0, __dmul_rn(w[WO + i], dout));
         d2[i] = a2[i] > 0.0 ? acc : 0.0;
-        r[(T2 + i) * ld] = __dmul_rn(inv_n, d2[i]);
+        t2[i] = __dmul_rn(inv_n, d2[i]);
+        r[(T2 + i) * ld] = t2[i];
       }
       double acc[H1];
 #pragma unroll
@@ -159,13 +178,35 @@ struct Fixed {
 #pragma unroll
         for (int i = 0; i < H1; ++i) acc[i] = __dadd_rn(acc[i], __dmul_rn(w[W2 + o * H1 + i], d2[o]));
 #pragma unroll
-      for (int i = 0; i < H1; ++i) r[(T1 + i) * ld] = __dmul_rn(inv_n, a1[i] > 0.0 ? acc[i] : 0.0);
+      for (int i = 0; i < H1; ++i) {
+        t1[i] = __dmul_rn(inv_n, a1[i] > 0.0 ? acc[i] : 0.0);
+        r[(T1 + i) * ld] = t1[i];
+      }
+      if constexpr (kProd) {  // the terms t * a of mlp.cpp:113 (same product, formed once here)
+#pragma unroll
+        for (int i = 0; i < H2; ++i) r[(PO + i) * ld] = __dmul_rn(tout, a2[i]);
+#pragma unroll
+        for (int o = 0; o < H2; ++o)
+#pragma unroll
+          for (int i = 0; i < H1; ++i) r[(P2 + o * H1 + i) * ld] = __dmul_rn(t2[o], a1[i]);
+      }
     } else {
 #pragma unroll
       for (int i = 0; i < H1; ++i) {
         const double acc = __dadd_rn(0.0, __dmul_rn(w[WO + i], dout));
-        r[(T1 + i) * ld] = __dmul_rn(inv_n, a1[i] > 0.0 ? acc : 0.0);
+        t1[i] = __dmul_rn(inv_n, a1[i] > 0.0 ? acc : 0.0);
+        r[(T1 + i) * ld] = t1[i];
       }
+      if constexpr (kProd) {
+#pragma unroll
+        for (int i = 0; i < H1; ++i) r[(PO + i) * ld] = __dmul_rn(tout, a1[i]);
+      }
+    }
+    if constexpr (kProd) {
+#pragma unroll
+      for (int o = 0; o < H1; ++o)
+#pragma unroll
+        for (int i = 0; i < I; ++i) r[(PR + o * I + i) * ld] = __dmul_rn(t1[o], x[i]);
     }
   }
 };
@@ -270,9 +311,10 @@ __device__ __forceinline__ double chain_sum_impl(const double* __restrict__ tp,
   return g;
 }
 
-template <int KB, int I, int H1, int H2, bool SMEM>
+template <int KB, int I, int H1, int H2, bool SMEM, bool PROD = false>
 __global__ void __launch_bounds__(256) train_fp64_exact(TrainArgs a) {
   constexpr bool kFixed = I > 0;
+  static_assert(!PROD || (kFixed && SMEM && KB == 1), "product rows: compiled shapes in shared memory");
   using F = Fixed<(I > 0 ? I : 1), (H1 > 0 ? H1 : 1), H2>;
   extern __shared__ double smem[];
   const int m = a.order[blockIdx.x];
@@ -282,7 +324,7 @@ __global__ void __launch_bounds__(256) train_fp64_exact(TrainArgs a) {
   const double lr = a.lr[m];
   const Shape sh = make_shape(a.tile_inputs[tile], a.h1[m], a.h2[m]);
   const int P = sh.P;
-  const int ld = rec_ld(N);
+  const int ld = PROD ? kProdLd : rec_ld(N);
   const int tid = threadIdx.x, nt = blockDim.x;
 
   double* w = smem;           // [P]
@@ -301,6 +343,8 @@ __global__ void __launch_bounds__(256) train_fp64_exact(TrainArgs a) {
     mom[p] = 0.0;
     vel[p] = 0.0;
   }
+  // KB == 1: the owner keeps w, m, v of its parameter in registers (smem w is phase A's copy)
+  double wr = (KB == 1 && tid < P) ? gp[tid] : 0.0, mr = 0.0, vr = 0.0;
   const double* X = a.X + a.tile_offset[tile] * 8;
   const double* Y = a.y + a.tile_offset[tile];
   for (int s = tid; s < N; s += nt) {
@@ -308,6 +352,7 @@ __global__ void __launch_bounds__(256) train_fp64_exact(TrainArgs a) {
     rec[7 * ld + s] = Y[s];        // inputs use rows 0..I-1 (I <= 7): row 7 holds the target
     rec[sh.ones * ld + s] = 1.0;   // bias terms are t * 1.0 (exact)
   }
+
 
   // phase-B ownership: parameter p -> (record row of its delta, of its input or of 1.0)
   int tix[KB], aix[KB];
@@ -323,9 +368,13 @@ __global__ void __launch_bounds__(256) train_fp64_exact(TrainArgs a) {
           const int q = p - sh.woff[l];
           tix[k] = sh.toff[l] + q / in;
           aix[k] = sh.inoff[l] + q % in;
+          if (PROD) {  // the product row phase A stored: a pure DADD chain
+            tix[k] = F::PR + (l == 0 ? 0 : l == 1 && sh.nl == 3 ? F::P2 - F::PR : F::PO - F::PR) + q;
+            aix[k] = -2;
+          }
         } else if (p >= sh.boff[l] && p < sh.boff[l] + out) {
           tix[k] = sh.toff[l] + (p - sh.boff[l]);
-          aix[k] = sh.ones;  // x 1.0: every lane of a warp runs the same multiply-add chain
+          aix[k] = PROD ? -2 : sh.ones;  // x 1.0 is exact: PROD sums the delta row itself
         }
       }
     }
@@ -347,7 +396,7 @@ __global__ void __launch_bounds__(256) train_fp64_exact(TrainArgs a) {
     const double2 bc = a.bias_corr[e];  // issued early: its latency hides behind phase A
     // ---- phase A: per-sample forward / backward (mlp.cpp:86-104) ----
     for (int s = tid; s < N; s += nt) {
-      if constexpr (kFixed) F::sample(w, rec + s, ld, inv_n);
+      if constexpr (kFixed) F::template sample<PROD>(w, rec + s, ld, inv_n);
       else sample_generic(sh, w, rec + s, ld, inv_n);
     }
     __syncthreads();
@@ -359,7 +408,10 @@ __global__ void __launch_bounds__(256) train_fp64_exact(TrainArgs a) {
     for (int k = 0; k < KB; ++k) g[k] = 0.0;
     long long clk2 = 0;
     if (tix[0] >= 0) {
-      if (KB == 1) {
+      if (PROD) {
+        g[0] = chain_sum_impl<4, false>(rec + tix[0] * ld, nullptr, N);
+        if (prof) clk2 = clock64();
+      } else if (KB == 1) {
         g[0] = chain_sum_impl<4, true>(rec + tix[0] * ld, rec + aix[0] * ld, N);
         if (prof) clk2 = clock64();
       } else {
@@ -370,6 +422,16 @@ __global__ void __launch_bounds__(256) train_fp64_exact(TrainArgs a) {
               g[k] = __dadd_rn(g[k], __dmul_rn(rec[tix[k] * ld + s], rec[aix[k] * ld + s]));
         }
       }
+      if (KB == 1) {
+        const double mk = __dadd_rn(__dmul_rn(beta1, mr), __dmul_rn(c1, g[0]));
+        const double vk = __dadd_rn(__dmul_rn(beta2, vr), __dmul_rn(__dmul_rn(c2, g[0]), g[0]));
+        mr = mk;
+        vr = vk;
+        const double mhat = __ddiv_rn(mk, bc.x);
+        const double vhat = __ddiv_rn(vk, bc.y);
+        wr = __dsub_rn(wr, __ddiv_rn(__dmul_rn(lr, mhat), __dadd_rn(__dsqrt_rn(vhat), eps)));
+        w[tid] = wr;
+      } else
 #pragma unroll
       for (int k = 0; k < KB; ++k) {
         const int p = tid + k * nt;
@@ -423,6 +485,11 @@ size_t fp64_record_bytes(int in, int h1, int h2, int n) {
   (void)in;
   return size_t(rec_rows(h1, h2)) * size_t(rec_ld(n)) * 8;
 }
+size_t fp64_product_record_bytes(int in, int h1, int h2, int n) {
+  const int nw = in * h1 + h1 * h2 + (h2 > 0 ? h2 : h1);
+  if (n > kProdMaxRows) return ~size_t(0) >> 1;  // never fits: products need N <= 256
+  return size_t(rec_rows(h1, h2) + nw) * size_t(kProdLd) * 8;
+}
 size_t fp64_state_bytes(int p) { return size_t((3 * p + 2 + 1) & ~1) * 8; }
 
 bool fp64_shape_compiled(int in, int h1, int h2) {
@@ -442,6 +509,27 @@ void launch_train_fp64(const TrainArgs& a, int max_p, int dyn_bytes, const int* 
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_bytes);
     kern<<<a.n_models, block, dyn_bytes, s>>>(a);
   };
+
+  if (shape && shape[0] > 0 && kb <= 1 && a.smem_records && a.rec_products) {
+    const int I = shape[0], H1 = shape[1], H2 = shape[2];
+    if (H1 == 8 && H2 == 0) {
+      switch (I) {
+        case 1: return go(train_fp64_exact<1, 1, 8, 0, true, true>);
+        case 2: return go(train_fp64_exact<1, 2, 8, 0, true, true>);
+        case 3: return go(train_fp64_exact<1, 3, 8, 0, true, true>);
+        case 4: return go(train_fp64_exact<1, 4, 8, 0, true, true>);
+        case 5: return go(train_fp64_exact<1, 5, 8, 0, true, true>);
+        case 6: return go(train_fp64_exact<1, 6, 8, 0, true, true>);
+        case 7: return go(train_fp64_exact<1, 7, 8, 0, true, true>);
+      }
+    } else if (H1 == 5 && H2 == 5) {
+      switch (I) {
+        case 4: return go(train_fp64_exact<1, 4, 5, 5, true, true>);
+        case 5: return go(train_fp64_exact<1, 5, 5, 5, true, true>);
+        case 6: return go(train_fp64_exact<1, 6, 5, 5, true, true>);
+      }
+    }
+  }
   if (shape && shape[0] > 0 && kb <= 1 && a.smem_records) {
     const int I = shape[0], H1 = shape[1], H2 = shape[2];
     if (H1 == 8 && H2 == 0) {

@@ -23,6 +23,7 @@
 #include <string>
 #include <thread>
 #include <tuple>
+#include <type_traits>
 #include <vector>
 
 #include <cuda_runtime.h>
@@ -44,6 +45,8 @@ struct lann_engine {
   double last_ms = 0.0, last_train_ms = 0.0;
   int64_t launches = 0;
   int max_smem = 0;
+  unsigned char* pin = nullptr;  // pinned host staging for population uploads (grows, kept)
+  size_t pin_cap = 0;
 };
 
 namespace lann {
@@ -66,6 +69,7 @@ struct DBuf {
   T* p = nullptr;
   size_t n = 0;
   cudaStream_t s = nullptr;
+  bool owned = true;
   DBuf() = default;
   DBuf(size_t count, cudaStream_t st) : n(count), s(st) {
     if (n) ck(cudaMallocAsync((void**)&p, n * sizeof(T), s), "cudaMallocAsync");
@@ -79,14 +83,25 @@ struct DBuf {
     std::swap(p, o.p);
     std::swap(n, o.n);
     std::swap(s, o.s);
+    std::swap(owned, o.owned);
     return *this;
   }
   ~DBuf() {
-    if (p) cudaFreeAsync(p, s);
+    if (p && owned) cudaFreeAsync(p, s);
   }
-  void up(const T* host) {
-    if (n) ck(cudaMemcpyAsync(p, host, n * sizeof(T), cudaMemcpyHostToDevice, s), "H2D");
-    t_h2d += int64_t(n * sizeof(T));
+  // a non-owning window into another buffer (the population blob)
+  static DBuf view(T* ptr, size_t count, cudaStream_t st) {
+    DBuf d;
+    d.p = ptr;
+    d.n = count;
+    d.s = st;
+    d.owned = false;
+    return d;
+  }
+  void up(const T* host) { up(host, n * sizeof(T)); }
+  void up(const void* host, size_t bytes) {
+    if (bytes) ck(cudaMemcpyAsync(p, host, bytes, cudaMemcpyHostToDevice, s), "H2D");
+    t_h2d += int64_t(bytes);
   }
   void down(T* host) const {
     if (n) ck(cudaMemcpyAsync(host, p, n * sizeof(T), cudaMemcpyDeviceToHost, s), "D2H");
@@ -507,6 +522,31 @@ void execute_plan(lann_engine* e, const TrainPlan& P, double* dparams, double* d
 }
 
 // ---- prepared population ----------------------------------------------------------------
+// 16-B aligned sub-array offsets of one allocation
+struct BlobLayout {
+  size_t bytes = 0;
+  template <class T>
+  size_t add(size_t count) {
+    const size_t off = (bytes + 15) & ~size_t(15);
+    bytes = off + count * sizeof(T);
+    return off;
+  }
+};
+
+// The engine's pinned staging buffer, grown to at least `bytes` (the previous upload from it
+// has completed: population preparation synchronises its stream before returning).
+unsigned char* pinned_stage(lann_engine* e, size_t bytes) {
+  if (bytes > e->pin_cap) {
+    if (e->pin) ck(cudaFreeHost(e->pin), "cudaFreeHost");
+    e->pin = nullptr;
+    e->pin_cap = 0;
+    const size_t cap = std::max(bytes, size_t(1) << 21);
+    ck(cudaMallocHost(reinterpret_cast<void**>(&e->pin), cap), "cudaMallocHost");
+    e->pin_cap = cap;
+  }
+  return e->pin;
+}
+
 struct Population {
   lann_engine* e = nullptr;
   int n_jobs = 0, M = 0, precision = 0;
@@ -515,8 +555,8 @@ struct Population {
   DevTrain t;
   int64_t rows = 0, n_eval_rows = 0;
   int max_eval = 1;
-  std::vector<double> init_params;
-  // device
+  // device: every array lives in one blob (views below)
+  DBuf<unsigned char> blob;
   DBuf<double> dX, dY, dP0, dP, dF, dER, dPred, dN, dET, dMape, dThr, dRho, dT;
   DBuf<int> dB, dEM, dI, dh1, dh2, dlog, dEL, dK, dS;
   DBuf<int64_t> dpo, dEO, dTO;
@@ -568,10 +608,16 @@ class HostPool {
   void loop() {
     std::uint64_t seen = 0;
     for (;;) {
+      // a population preparation issues several parallel_for calls back to back: spin ~50 us
+      // on the generation counter before sleeping, so the next call finds its workers awake
+      const auto t0 = std::chrono::steady_clock::now();
+      while (gen_.load(std::memory_order_acquire) == seen &&
+             std::chrono::steady_clock::now() - t0 < std::chrono::microseconds(50))
+        std::this_thread::yield();
       {
         std::unique_lock<std::mutex> lk(m_);
-        cv_.wait(lk, [&] { return gen_ != seen; });
-        seen = gen_;
+        cv_.wait(lk, [&] { return gen_.load() != seen; });
+        seen = gen_.load();
       }
       drain();
       std::lock_guard<std::mutex> lk(m_);
@@ -583,7 +629,7 @@ class HostPool {
   const std::function<void(int)>* fn_ = nullptr;
   std::atomic<int> next_{0};
   int n_ = 0, workers_ = 0, active_ = 0;
-  std::uint64_t gen_ = 0;
+  std::atomic<std::uint64_t> gen_{0};
 };
 
 template <class F>
@@ -688,20 +734,17 @@ int prepare_population(lann_engine* e, int n_jobs, const lann_job* jobs, int pre
   const int M = int(pop.model_job.size());
   pop.M = M;
   if (M == 0) return pop.base[0].status;
-  // pack
+  // pack straight into the engine's pinned staging buffer, laid out like the one device blob
+  // that receives it (a single H2D copy; no growing host vectors, no pageable staging)
   DevTrain& t = pop.t;
   t.n_models = M;
   t.n_tiles = int(tiles.size());
-  std::vector<double> X, Y, eval_rows, eval_truth, norm(size_t(M) * 18);
-  std::vector<int> eval_model, n_in(M), logt(M), eval_len(M);
-  std::vector<int64_t> eval_off(M);
-  for (size_t k = 0; k < tiles.size(); ++k) {
-    t.tile_rows.push_back(std::max(1, tiles[k].n_train()));
-    t.tile_inputs.push_back(std::max(1, tiles[k].n_inputs));
-    t.tile_offset.push_back(pop.rows);
-    X.insert(X.end(), tiles[k].Xn.begin(), tiles[k].Xn.end());
-    Y.insert(Y.end(), tiles[k].yn.begin(), tiles[k].yn.end());
-    pop.rows += tiles[k].n_train();
+  int64_t n_eval_total = 0, eval_row_doubles = 0;
+  for (size_t k = 0; k < tiles.size(); ++k) pop.rows += tiles[k].n_train();
+  for (int m = 0; m < M; ++m) {
+    const Tile& T = tiles[job_tile[pop.model_job[m]]];
+    n_eval_total += T.n_eval();
+    eval_row_doubles += int64_t(T.eval_rows.size());
   }
   for (int m = 0; m < M; ++m) {
     const lann_job& J = jobs[pop.model_job[m]];
@@ -714,60 +757,124 @@ int prepare_population(lann_engine* e, int n_jobs, const lann_job* jobs, int pre
     t.param_offset.push_back(t.total_params);
     t.total_params += param_count(T.n_inputs, t.h1.back(), t.h2.back());
     pop.train_flop += double(J.epochs) * flop_per_model_epoch(T.n_inputs, t.h1.back(), t.h2.back(), T.n_train());
-    std::memcpy(&norm[size_t(m) * 18], T.norm, sizeof T.norm);
-    n_in[m] = T.n_inputs;
-    logt[m] = T.log_target;
-    eval_off[m] = int64_t(eval_truth.size());
-    eval_len[m] = T.n_eval();
     pop.max_eval = std::max(pop.max_eval, T.n_eval());
-    eval_rows.insert(eval_rows.end(), T.eval_rows.begin(), T.eval_rows.end());
-    eval_truth.insert(eval_truth.end(), T.eval_truth.begin(), T.eval_truth.end());
-    for (int r = 0; r < T.n_eval(); ++r) eval_model.push_back(m);
   }
-  pop.init_params.assign(size_t(t.total_params), 0.0);
-  parallel_for(M, [&](int m) {
-    const lann_job& J = jobs[pop.model_job[m]];
-    glorot_init(n_in[m], t.h1[m], t.h2[m], J.init_seed, &pop.init_params[size_t(t.param_offset[m])]);
-  });
-  if (Status st = validate_train(t)) return set_err(e, st);
-  if (size_t(pop.max_eval) * 36 + 16 > size_t(e->max_smem))
-    return set_err(e, {LANN_PARAM_ERROR, "evaluation set too large for one CTA"});
   pop.toff.assign(M, 0);
   if (want_trace)
     for (int m = 0; m < M; ++m) {
       pop.toff[m] = pop.trace_total;
       pop.trace_total += t.epochs[m];
     }
+  pop.n_eval_rows = n_eval_total;
+  BlobLayout L;
+  const size_t oX = L.add<double>(size_t(pop.rows) * 8), oY = L.add<double>(size_t(pop.rows));
+  const size_t oP0 = L.add<double>(size_t(t.total_params)), oN = L.add<double>(size_t(M) * 18);
+  const size_t oER = L.add<double>(size_t(eval_row_doubles)), oET = L.add<double>(size_t(n_eval_total));
+  const size_t oEM = L.add<int>(size_t(n_eval_total)), oI = L.add<int>(size_t(M)), oH1 = L.add<int>(size_t(M));
+  const size_t oH2 = L.add<int>(size_t(M)), oLog = L.add<int>(size_t(M)), oEL = L.add<int>(size_t(M));
+  const size_t oPO = L.add<int64_t>(size_t(M)), oEO = L.add<int64_t>(size_t(M)), oTO = L.add<int64_t>(size_t(M));
+  const size_t up_bytes = L.bytes;
+  // device-only outputs follow the uploaded part
+  const size_t oP = L.add<double>(size_t(t.total_params)), oF = L.add<double>(size_t(M));
+  const size_t oT = L.add<double>(size_t(pop.trace_total)), oPred = L.add<double>(size_t(n_eval_total));
+  const size_t oMape = L.add<double>(size_t(M)), oThr = L.add<double>(size_t(M)), oRho = L.add<double>(size_t(M));
+  const size_t oB = L.add<int>(size_t(M)), oK = L.add<int>(size_t(M)), oS = L.add<int>(size_t(M));
+  unsigned char* h = pinned_stage(e, up_bytes);
+  auto H = [&](auto* type_tag, size_t off) { return reinterpret_cast<decltype(type_tag)>(h + off); };
+  {
+    double* X = H((double*)nullptr, oX);
+    double* Y = H((double*)nullptr, oY);
+    int64_t r0 = 0;
+    for (size_t k = 0; k < tiles.size(); ++k) {
+      t.tile_rows.push_back(std::max(1, tiles[k].n_train()));
+      t.tile_inputs.push_back(std::max(1, tiles[k].n_inputs));
+      t.tile_offset.push_back(r0);
+      r0 += tiles[k].n_train();
+    }
+    double* norm = H((double*)nullptr, oN);
+    double* ER = H((double*)nullptr, oER);
+    double* ET = H((double*)nullptr, oET);
+    int* EM = H((int*)nullptr, oEM);
+    int* n_in = H((int*)nullptr, oI);
+    int* logt = H((int*)nullptr, oLog);
+    int* eval_len = H((int*)nullptr, oEL);
+    int64_t* eval_off = H((int64_t*)nullptr, oEO);
+    std::vector<int64_t> er_off(M);
+    int64_t er = 0, et = 0;
+    for (int m = 0; m < M; ++m) {
+      const Tile& T = tiles[job_tile[pop.model_job[m]]];
+      std::memcpy(norm + size_t(m) * 18, T.norm, sizeof T.norm);
+      n_in[m] = T.n_inputs;
+      logt[m] = T.log_target;
+      eval_off[m] = et;
+      eval_len[m] = T.n_eval();
+      er_off[m] = er;
+      er += int64_t(T.eval_rows.size());
+      et += T.n_eval();
+    }
+    double* P0 = H((double*)nullptr, oP0);
+    // the bulk copies (~1.5 MB for config 2) and the initial weights run on the pool: one thread is memory-latency bound
+    const int nt = int(tiles.size());
+    parallel_for(nt + M, [&](int j) {
+      if (j < nt) {
+        std::copy(tiles[j].Xn.begin(), tiles[j].Xn.end(), X + t.tile_offset[j] * 8);
+        std::copy(tiles[j].yn.begin(), tiles[j].yn.end(), Y + t.tile_offset[j]);
+        return;
+      }
+      const int m = j - nt;
+      const Tile& T = tiles[job_tile[pop.model_job[m]]];
+      std::copy(T.eval_rows.begin(), T.eval_rows.end(), ER + er_off[m]);
+      std::copy(T.eval_truth.begin(), T.eval_truth.end(), ET + eval_off[m]);
+      std::fill(EM + eval_off[m], EM + eval_off[m] + T.n_eval(), m);
+      // glorot_init writes every weight and (zero) bias of the model
+      glorot_init(n_in[m], t.h1[m], t.h2[m], jobs[pop.model_job[m]].init_seed, P0 + t.param_offset[m]);
+    });
+    std::copy(t.h1.begin(), t.h1.end(), H((int*)nullptr, oH1));
+    std::copy(t.h2.begin(), t.h2.end(), H((int*)nullptr, oH2));
+    std::copy(t.param_offset.begin(), t.param_offset.end(), H((int64_t*)nullptr, oPO));
+    std::copy(pop.toff.begin(), pop.toff.end(), H((int64_t*)nullptr, oTO));
+    hlog("pack", h2);
+  }
+  if (Status st = validate_train(t)) return set_err(e, st);
+  if (size_t(pop.max_eval) * 36 + 16 > size_t(e->max_smem))
+    return set_err(e, {LANN_PARAM_ERROR, "evaluation set too large for one CTA"});
   hlog("pack+init", h2);
   const auto h3 = now();
-  // upload once
+  // one device blob, one upload
   cudaStream_t s = e->stream;
-  pop.dX = DBuf<double>(X, s);
-  pop.dY = DBuf<double>(Y, s);
-  pop.dP0 = DBuf<double>(pop.init_params, s);
-  pop.dP = DBuf<double>(pop.init_params.size(), s);
-  pop.dF = DBuf<double>(size_t(M), s);
-  pop.dB = DBuf<int>(size_t(M), s);
-  pop.dT = DBuf<double>(size_t(pop.trace_total), s);
-  pop.dTO = DBuf<int64_t>(pop.toff, s);
-  pop.n_eval_rows = int64_t(eval_truth.size());
-  pop.dER = DBuf<double>(eval_rows, s);
-  pop.dPred = DBuf<double>(size_t(pop.n_eval_rows), s);
-  pop.dN = DBuf<double>(norm, s);
-  pop.dET = DBuf<double>(eval_truth, s);
-  pop.dEM = DBuf<int>(eval_model, s);
-  pop.dI = DBuf<int>(n_in, s);
-  pop.dh1 = DBuf<int>(t.h1, s);
-  pop.dh2 = DBuf<int>(t.h2, s);
-  pop.dlog = DBuf<int>(logt, s);
-  pop.dpo = DBuf<int64_t>(t.param_offset, s);
-  pop.dEO = DBuf<int64_t>(eval_off, s);
-  pop.dEL = DBuf<int>(eval_len, s);
-  pop.dK = DBuf<int>(size_t(M), s);
-  pop.dS = DBuf<int>(size_t(M), s);
-  pop.dMape = DBuf<double>(size_t(M), s);
-  pop.dThr = DBuf<double>(size_t(M), s);
-  pop.dRho = DBuf<double>(size_t(M), s);
+  pop.blob = DBuf<unsigned char>(L.bytes, s);
+  pop.blob.up(h, up_bytes);
+  unsigned char* d = pop.blob.p;
+  auto V = [&](auto* type_tag, size_t off, size_t n) {
+    using T = std::remove_pointer_t<decltype(type_tag)>;
+    return DBuf<T>::view(reinterpret_cast<T*>(d + off), n, s);
+  };
+  const size_t Mz = size_t(M), Ez = size_t(n_eval_total), Pz = size_t(t.total_params);
+  pop.dX = V((double*)nullptr, oX, size_t(pop.rows) * 8);
+  pop.dY = V((double*)nullptr, oY, size_t(pop.rows));
+  pop.dP0 = V((double*)nullptr, oP0, Pz);
+  pop.dN = V((double*)nullptr, oN, Mz * 18);
+  pop.dER = V((double*)nullptr, oER, size_t(eval_row_doubles));
+  pop.dET = V((double*)nullptr, oET, Ez);
+  pop.dEM = V((int*)nullptr, oEM, Ez);
+  pop.dI = V((int*)nullptr, oI, Mz);
+  pop.dh1 = V((int*)nullptr, oH1, Mz);
+  pop.dh2 = V((int*)nullptr, oH2, Mz);
+  pop.dlog = V((int*)nullptr, oLog, Mz);
+  pop.dEL = V((int*)nullptr, oEL, Mz);
+  pop.dpo = V((int64_t*)nullptr, oPO, Mz);
+  pop.dEO = V((int64_t*)nullptr, oEO, Mz);
+  pop.dTO = V((int64_t*)nullptr, oTO, Mz);
+  pop.dP = V((double*)nullptr, oP, Pz);
+  pop.dF = V((double*)nullptr, oF, Mz);
+  pop.dT = V((double*)nullptr, oT, size_t(pop.trace_total));
+  pop.dPred = V((double*)nullptr, oPred, Ez);
+  pop.dMape = V((double*)nullptr, oMape, Mz);
+  pop.dThr = V((double*)nullptr, oThr, Mz);
+  pop.dRho = V((double*)nullptr, oRho, Mz);
+  pop.dB = V((int*)nullptr, oB, Mz);
+  pop.dK = V((int*)nullptr, oK, Mz);
+  pop.dS = V((int*)nullptr, oS, Mz);
   hlog("uploads", h3);
   const auto h4 = now();
   pop.plan = build_plan(e, t, precision, pop.dX.p, pop.dY.p, pop.rows);
@@ -904,6 +1011,7 @@ void lann_engine_destroy(lann_engine* e) {
   for (auto a : e->aux)
     if (a) cudaStreamDestroy(a);
   if (e->stream) cudaStreamDestroy(e->stream);
+  if (e->pin) cudaFreeHost(e->pin);
   delete e;
 }
 

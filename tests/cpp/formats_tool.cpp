@@ -15,6 +15,7 @@
 //                                          models::train_full_batch on the GPU (needs a device):
 //                                          prints X, y, initial params, then trace + final params
 //                                          or "TrainingError <epoch>"
+//   formats_tool api-gen-errors            build_dataset's ParamError / BuildAbortError contract
 //   formats_tool api-validate              InstanceParams::validate / complexity edge cases
 #include <cfloat>
 #include <cmath>
@@ -201,6 +202,34 @@ int main(int argc, char** argv) {
       } catch (const TrainingError& e) {
         std::printf("TrainingError %d\n", e.epoch());
       }
+    } else if (mode == "api-gen-errors") {
+      auto space = datagen::ParamSpace::defaults(kernels::KernelKind::MM, 4);
+      kernels::VariantDescriptor v;
+      v.variant_id = "dense_threaded";
+      datagen::BuildOptions opts;
+      int calls = 0;
+      opts.probe = [&](const kernels::InstanceParams&) { return ++calls == 3 ? 0.0 : 1e-3; };
+      auto attempt = [&](const char* name, auto&& fn) {
+        try {
+          fn();
+          std::printf("%s ok\n", name);
+        } catch (const BuildAbortError& e) {
+          std::printf("%s BuildAbortError %zu %s\n", name, e.completed(), e.what());
+        } catch (const ParamError& e) {
+          std::printf("%s ParamError %s\n", name, e.what());
+        }
+      };
+      attempt("count1", [&] { datagen::build_dataset(v, space, 1, 1, opts); });
+      attempt("kind", [&] {
+        auto other = v;
+        other.kind = kernels::KernelKind::MV;
+        datagen::build_dataset(other, space, 5, 1, opts);
+      });
+      attempt("noprobe", [&] { datagen::build_dataset(v, space, 5, 1); });
+      attempt("zero", [&] { datagen::build_dataset(v, space, 5, 1, opts); });
+      datagen::BuildOptions bad;
+      bad.probe = [](const kernels::InstanceParams&) -> double { throw ParamError("probe failed"); };
+      attempt("throws", [&] { datagen::build_dataset(v, space, 5, 1, bad); });
     } else if (mode == "api-validate") {
       using P = kernels::InstanceParams;
       const std::pair<const char*, P> cases[] = {

@@ -288,6 +288,18 @@ def test_api_mlp_init_rejects_bad_dims(tool, dims):
     assert run(tool, "api-init", "1", *dims).startswith("ParamError")
 
 
+def test_api_build_dataset_errors(tool):
+    """datagen.cpp:177-223: ParamError before sampling (count < 2, kind mismatch); a probe
+    failure or a runtime <= 0 aborts with BuildAbortError carrying the completed count and the
+    reference's message; without a probe the engine (which times no CPU kernel) refuses."""
+    out = dict(line.split(" ", 1) for line in run(tool, "api-gen-errors").splitlines())
+    assert out["count1"] == "ParamError build_dataset needs count >= 2"
+    assert out["kind"] == "ParamError variant kernel does not match the parameter space"
+    assert out["noprobe"].startswith("ParamError ")
+    assert out["zero"] == "BuildAbortError 2 dataset build aborted after 2/5 samples: measured runtime must be > 0"
+    assert out["throws"] == "BuildAbortError 0 dataset build aborted after 0/5 samples: probe failed"
+
+
 def test_api_instance_params_validate_and_complexity(tool):
     """kernels.cpp:149-206: InstanceParams::validate domain rules and the complexity formulas;
     datagen::median_of, density_ladder and eval::speedup."""

@@ -102,9 +102,12 @@ struct Net {
 
 // Forward + backward of ONE sample, accumulating its gradient contribution into gr
 // and err^2 into loss. scale = 2/N folds the 1/N of the mean and the 2 of d(err^2).
-template <int I, int H1, int H2>
+// kFirst: gr and loss are ASSIGNED this sample's terms (no zeroing pass, FMUL for FFMA).
+template <int I, int H1, int H2, bool kFirst = false>
 __device__ __forceinline__ void accumulate_sample(const float* w, const float* xv, float* gr,
                                                   float& loss, float scale, bool valid = true) {
+  auto acc = [](float& g, float v) { g = kFirst ? v : g + v; };
+  auto fma_acc = [](float& g, float x, float y) { g = kFirst ? x * y : fmaf(x, y, g); };
   using N = Net<I, H1, H2>;
   float z1[H1];
 #pragma unroll
@@ -141,39 +144,39 @@ __device__ __forceinline__ void accumulate_sample(const float* w, const float* x
     out = acc0 + acc1;
   }
   const float err = valid ? out - xv[7] : 0.f;
-  loss = fmaf(err, err, loss);
+  fma_acc(loss, err, err);
   const float d = err * scale;
   if constexpr (H2 > 0) {
-    gr[N::L3B] += d;
+    acc(gr[N::L3B], d);
     float d2[H2];
 #pragma unroll
     for (int o = 0; o < H2; ++o) {
-      gr[N::L3W + o] = fmaf(d, z2[o], gr[N::L3W + o]);
+      fma_acc(gr[N::L3W + o], d, z2[o]);
       d2[o] = z2[o] > 0.f ? w[N::L3W + o] * d : 0.f;
-      gr[N::L2B + o] += d2[o];
+      acc(gr[N::L2B + o], d2[o]);
     }
 #pragma unroll
     for (int h = 0; h < H1; ++h) {
-      float acc = 0.f;
+      float bd = 0.f;
 #pragma unroll
       for (int o = 0; o < H2; ++o) {
-        gr[N::L2W + o * H1 + h] = fmaf(d2[o], z1[h], gr[N::L2W + o * H1 + h]);
-        acc = fmaf(w[N::L2W + o * H1 + h], d2[o], acc);
+        fma_acc(gr[N::L2W + o * H1 + h], d2[o], z1[h]);
+        bd = o == 0 ? w[N::L2W + h] * d2[0] : fmaf(w[N::L2W + o * H1 + h], d2[o], bd);
       }
-      const float d1 = z1[h] > 0.f ? acc : 0.f;
-      gr[N::L1B + h] += d1;
+      const float d1 = z1[h] > 0.f ? bd : 0.f;
+      acc(gr[N::L1B + h], d1);
 #pragma unroll
-      for (int i = 0; i < I; ++i) gr[N::L1W + h * I + i] = fmaf(d1, xv[i], gr[N::L1W + h * I + i]);
+      for (int i = 0; i < I; ++i) fma_acc(gr[N::L1W + h * I + i], d1, xv[i]);
     }
   } else {
-    gr[N::L2B] += d;
+    acc(gr[N::L2B], d);
 #pragma unroll
     for (int h = 0; h < H1; ++h) {
-      gr[N::L2W + h] = fmaf(d, z1[h], gr[N::L2W + h]);
+      fma_acc(gr[N::L2W + h], d, z1[h]);
       const float d1 = z1[h] > 0.f ? w[N::L2W + h] * d : 0.f;
-      gr[N::L1B + h] += d1;
+      acc(gr[N::L1B + h], d1);
 #pragma unroll
-      for (int i = 0; i < I; ++i) gr[N::L1W + h * I + i] = fmaf(d1, xv[i], gr[N::L1W + h * I + i]);
+      for (int i = 0; i < I; ++i) fma_acc(gr[N::L1W + h * I + i], d1, xv[i]);
     }
   }
 }
@@ -495,13 +498,26 @@ struct LeanRS {
   template <int M>
   __device__ __forceinline__ static void run(float (&v)[M], int lane) {
     const bool up = (lane & O) != 0;
-#pragma unroll
-    for (int j = 0; j < H; ++j) {
+    auto half = [&](int j, float& keep, float& send) {
       const float lo = v[j];
       const float hi = (H + j < N) ? v[(H + j < N) ? H + j : 0] : 0.f;
-      const float send = up ? lo : hi;
-      const float keep = up ? hi : lo;
-      v[j] = keep + __shfl_xor_sync(0xffffffffu, send, O);
+      send = up ? lo : hi;
+      keep = up ? hi : lo;
+    };
+    // pairs of kept values add on one FADD2 (packed f32x2)
+#pragma unroll
+    for (int j = 0; j + 1 < H; j += 2) {
+      float k0, s0, k1, s1;
+      half(j, k0, s0);
+      half(j + 1, k1, s1);
+      const float r0 = __shfl_xor_sync(0xffffffffu, s0, O);
+      const float r1 = __shfl_xor_sync(0xffffffffu, s1, O);
+      upk(add2(pk(k0, k1), pk(r0, r1)), v[j], v[j + 1]);
+    }
+    if constexpr (H & 1) {
+      float k0, s0;
+      half(H - 1, k0, s0);
+      v[H - 1] = k0 + __shfl_xor_sync(0xffffffffu, s0, O);
     }
     if constexpr (O > 1) LeanRS<H, O / 2>::run(v, lane);
   }
@@ -868,17 +884,21 @@ __global__ void __launch_bounds__(32 * W, 1) train_fp32_cta_kernel(TrainF32Args 
       }
     }
     float gr[PT];
-#pragma unroll
-    for (int p = 0; p < PT; ++p) gr[p] = 0.f;
     float loss = 0.f;
     if constexpr (kPair) {
-      // two samples per thread in one basic block: independent chains interleave
-      if (rows <= 2 * T) {
-        if (tid < rows) {
-          accumulate_sample<I, H1, H2>(w, xa, gr, loss, scale);
-          accumulate_sample<I, H1, H2>(w, xb, gr, loss, scale, tid + T < rows);
-        }
+      // two samples per thread in one basic block: independent chains interleave; the first
+      // sample assigns the accumulators (no zeroing pass)
+      if (rows <= 2 * T && tid < rows) {
+        accumulate_sample<I, H1, H2, true>(w, xa, gr, loss, scale);
+        accumulate_sample<I, H1, H2>(w, xb, gr, loss, scale, tid + T < rows);
+#pragma unroll
+        for (int p = P; p < PT; ++p) gr[p] = 0.f;
+      } else if (rows <= 2 * T) {
+#pragma unroll
+        for (int p = 0; p < PT; ++p) gr[p] = 0.f;
       } else {
+#pragma unroll
+        for (int p = 0; p < PT; ++p) gr[p] = 0.f;
         for (int s0 = tid; s0 < rows; s0 += 2 * T) {
           const int s1 = s0 + T;
           float ya[8], yb[8];
@@ -889,6 +909,8 @@ __global__ void __launch_bounds__(32 * W, 1) train_fp32_cta_kernel(TrainF32Args 
         }
       }
     } else {
+#pragma unroll
+      for (int p = 0; p < PT; ++p) gr[p] = 0.f;
       for (int s = tid; s < rows; s += T) {
         float xv[8];
         load_row(trow, s, xv);

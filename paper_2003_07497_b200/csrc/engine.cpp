@@ -191,6 +191,7 @@ struct TrainPlan {
   // FP64 part (exact mode, or FP32-mode models without a compiled FP32 shape)
   std::vector<std::unique_ptr<Fp64Bucket>> buckets64;
   DBuf<double2> bc;
+  DBuf<float2> brcp;  // FP32 Adam bias-correction reciprocals per epoch
   const double* dX = nullptr;
   const double* dY = nullptr;
   int trace_stride = 1;
@@ -244,6 +245,12 @@ std::unique_ptr<TrainPlan> build_plan(lann_engine* e, const DevTrain& t, int pre
     int max_epochs_all = 0;
     for (auto& [shape, ms] : by_shape)
       for (int m : ms) max_epochs_all = std::max(max_epochs_all, t.epochs[m]);
+    {  // the CTA kernel reads its bias corrections per epoch instead of computing them
+      const auto& bc = adam_bias_table(std::max(1, max_epochs_all));
+      std::vector<float2> r(size_t(std::max(1, max_epochs_all)));
+      for (size_t k = 0; k < r.size(); ++k) r[k] = make_float2(float(1.0 / bc[2 * k]), float(1.0 / bc[2 * k + 1]));
+      P.brcp = DBuf<float2>(r, s);
+    }
     int global_lanes = 0;
     int off_lanes = 4;  // lanes for buckets off the critical path (mid-size populations)
     if (!env_lanes && !small) {
@@ -461,6 +468,7 @@ void execute_plan(lann_engine* e, const TrainPlan& P, double* dparams, double* d
     a.trace_offset = dtrace_off;
     a.trace_stride = P.trace_stride;
     a.phase_cycles = b->prof.p;
+    a.bias_rcp = P.brcp.p;
     if (!launch_train_fp32(a, b->in, b->h1, b->h2, b->lanes, b->tile_bytes, next_stream()))
       throw CudaFail{"no FP32 kernel for this shape"};
     ck(cudaGetLastError(), "train_fp32 launch");

@@ -58,6 +58,7 @@ struct TrainF32Args {
   const int64_t* trace_offset;
   int trace_stride;
   long long* phase_cycles;   // optional (LANN_PHASE_PROFILE): CTA 0's clock64 per phase
+  const float2* bias_rcp;    // [max_epochs] {1/(1-0.9^t), 1/(1-0.999^t)} from the host (CTA kernel)
 };
 
 // Prediction over rows (models.cpp:346-363).

@@ -837,7 +837,6 @@ __global__ void __launch_bounds__(32 * W, 1) train_fp32_cta_kernel(TrainF32Args 
   float mo[OWN], ve[OWN];
 #pragma unroll
   for (int k = 0; k < OWN; ++k) mo[k] = ve[k] = 0.f;
-  float pw1 = 1.f, pw2 = 1.f;
   const float lr = (float)a.lr[m];
   const float scale = 2.0f / (float)rows, inv_n = 1.0f / (float)rows;
   double* trace = a.loss_trace ? a.loss_trace + a.trace_offset[m] : nullptr;
@@ -859,10 +858,9 @@ __global__ void __launch_bounds__(32 * W, 1) train_fp32_cta_kernel(TrainF32Args 
   const long long clk_begin = prof ? clock64() : 0;
   for (int e = 0; e < E; ++e) {
     const long long clk0 = prof ? clock64() : 0;
-    // this epoch's Adam factors (bias corrections), computed while the samples run
-    pw1 *= 0.9f;
-    pw2 *= 0.999f;
-    const float step = lr / (1.f - pw1), rb2 = 1.f / (1.f - pw2);
+    // this epoch's Adam factors (host bias-correction reciprocals), loaded while the samples run
+    const float2 br = a.bias_rcp[e];
+    const float step = lr * br.x, rb2 = br.y;
     float w[PT];
 #pragma unroll
     for (int p = 0; p < PT; p += 4) {

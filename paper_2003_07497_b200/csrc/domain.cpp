@@ -227,8 +227,12 @@ Status build_dataset(const lann_world& w, std::uint64_t seed, int count, Dataset
   ds.runtime.assign(count, 0.0);
   SeqRng rng(derive_seed(seed, 0));
   SeqRng noise(derive_seed(seed, 0x9015E));
+  SampleSpace sp;  // the default space, built once (its side list is a heap vector)
+  sp.kind = w.kind;
+  sp.max_threads = w.max_threads;
+  sp.gpu_lattice = w.blur_lattice;
   for (int i = 0; i < count; ++i) {
-    Instance p = sample_instance(w.kind, w.max_threads, w.blur_lattice, rng);
+    Instance p = sample_instance(sp, rng);
     if (w.hw_class != LANN_HW_CPU) p.n_thd = 1;      // Threading::FixedSingle (datagen.cpp:195)
     if (w.kind == LANN_BLUR) p.n_thd = w.max_threads; // datagen.cpp:196
     base_features(p, takes_thd, &ds.feats[std::size_t(i) * LANN_ROW]);

@@ -42,7 +42,23 @@ class SeqRng {
  public:
   explicit SeqRng(std::uint64_t seed) : e_(seed) {}
   std::uint64_t next() { return e_(); }
+  // Rng::bounded (rng.hpp): reject r < 2^64 mod n, return r mod n. Powers of two take a mask
+  // and small n a cached exact remainder (floor((2^64-1)/n) multiplier, mulhi, <= 2
+  // corrections) instead of two 64-bit divisions per draw; the results are identical.
   std::uint64_t bounded(std::uint64_t n) {
+    if ((n & (n - 1)) == 0) return e_() & (n - 1);  // 2^64 mod 2^k = 0: nothing to reject
+    if (n <= kSmallN) {
+      const SmallMod& t = small_mod(n);
+      for (;;) {
+        const std::uint64_t r = e_();
+        if (r >= t.thr) {
+          std::uint64_t rem = r - std::uint64_t((unsigned __int128)r * t.mul >> 64) * n;
+          if (rem >= n) rem -= n;
+          if (rem >= n) rem -= n;
+          return rem;
+        }
+      }
+    }
     const std::uint64_t thr = (0 - n) % n;
     for (;;) {
       const std::uint64_t r = e_();
@@ -53,6 +69,18 @@ class SeqRng {
   double uniform(double lo, double hi) { return lo + (hi - lo) * uniform(); }
 
  private:
+  static constexpr std::uint64_t kSmallN = 4096;
+  struct SmallMod {
+    std::uint64_t mul, thr;
+  };
+  static const SmallMod& small_mod(std::uint64_t n) {
+    static const std::vector<SmallMod> table = [] {
+      std::vector<SmallMod> t(kSmallN + 1, SmallMod{0, 0});
+      for (std::uint64_t k = 1; k <= kSmallN; ++k) t[k] = SmallMod{~std::uint64_t(0) / k, (0 - k) % k};
+      return t;
+    }();
+    return table[n];
+  }
   std::mt19937_64 e_;
 };
 

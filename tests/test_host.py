@@ -98,3 +98,16 @@ def test_no_cpu_fallback_without_device():
 def test_derive_seed_matches_oracle(oracle):
     for r, s in [(0, 0), (1, 0x9015E), (2 ** 64 - 1, 0xA11CE), (12345, 7)]:
         assert P.derive_seed(r, s) == oracle.lib.or_derive_seed(r, s)
+
+
+def test_seqrng_bounded_fast_paths_are_exact(tmp_path):
+    """The host sampler's bounded() fast paths (mask for powers of two, cached exact remainder
+    for n <= 4096) draw exactly what Rng::bounded (rng.hpp) draws: 10 M draws over n = 1..5000
+    and four large n."""
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = str(tmp_path / "seqrng_check")
+    subprocess.run(["g++", "-std=c++20", "-O2", "-I", os.path.join(root, "paper_2003_07497_b200", "csrc"),
+                    os.path.join(root, "tests", "cpp", "seqrng_bounded_check.cpp"), "-o", exe], check=True)
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0 and " 0 mismatches" in out.stdout, out.stdout

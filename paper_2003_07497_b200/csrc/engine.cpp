@@ -47,6 +47,8 @@ struct lann_engine {
   int max_smem = 0;
   unsigned char* pin = nullptr;  // pinned host staging for population uploads (grows, kept)
   size_t pin_cap = 0;
+  float2* brcp = nullptr;        // FP32 Adam bias-correction reciprocal table (grows, kept)
+  int brcp_n = 0;
 };
 
 namespace lann {
@@ -191,7 +193,7 @@ struct TrainPlan {
   // FP64 part (exact mode, or FP32-mode models without a compiled FP32 shape)
   std::vector<std::unique_ptr<Fp64Bucket>> buckets64;
   DBuf<double2> bc;
-  DBuf<float2> brcp;  // FP32 Adam bias-correction reciprocals per epoch
+  const float2* brcp = nullptr;  // FP32 Adam bias-correction reciprocals per epoch (engine-owned)
   const double* dX = nullptr;
   const double* dY = nullptr;
   int trace_stride = 1;
@@ -245,12 +247,22 @@ std::unique_ptr<TrainPlan> build_plan(lann_engine* e, const DevTrain& t, int pre
     int max_epochs_all = 0;
     for (auto& [shape, ms] : by_shape)
       for (int m : ms) max_epochs_all = std::max(max_epochs_all, t.epochs[m]);
-    {  // the CTA kernel reads its bias corrections per epoch instead of computing them
-      const auto& bc = adam_bias_table(std::max(1, max_epochs_all));
-      std::vector<float2> r(size_t(std::max(1, max_epochs_all)));
+    // the CTA kernel reads its bias corrections per epoch instead of computing them; the table
+    // is engine-resident (grown on demand), not re-uploaded per population
+    if (e->brcp_n < max_epochs_all) {
+      const int n = std::max(max_epochs_all, 32768);
+      const auto& bc = adam_bias_table(n);
+      std::vector<float2> r(static_cast<size_t>(n));
       for (size_t k = 0; k < r.size(); ++k) r[k] = make_float2(float(1.0 / bc[2 * k]), float(1.0 / bc[2 * k + 1]));
-      P.brcp = DBuf<float2>(r, s);
+      ck(cudaDeviceSynchronize(), "bias table");  // no launch in flight still reads the old one
+      if (e->brcp) ck(cudaFree(e->brcp), "cudaFree");
+      e->brcp = nullptr;
+      e->brcp_n = 0;
+      ck(cudaMalloc(reinterpret_cast<void**>(&e->brcp), r.size() * sizeof(float2)), "cudaMalloc");
+      ck(cudaMemcpy(e->brcp, r.data(), r.size() * sizeof(float2), cudaMemcpyHostToDevice), "H2D");
+      e->brcp_n = n;
     }
+    P.brcp = e->brcp;
     int global_lanes = 0;
     int off_lanes = 4;  // lanes for buckets off the critical path (mid-size populations)
     if (!env_lanes && !small) {
@@ -468,7 +480,7 @@ void execute_plan(lann_engine* e, const TrainPlan& P, double* dparams, double* d
     a.trace_offset = dtrace_off;
     a.trace_stride = P.trace_stride;
     a.phase_cycles = b->prof.p;
-    a.bias_rcp = P.brcp.p;
+    a.bias_rcp = P.brcp;
     if (!launch_train_fp32(a, b->in, b->h1, b->h2, b->lanes, b->tile_bytes, next_stream()))
       throw CudaFail{"no FP32 kernel for this shape"};
     ck(cudaGetLastError(), "train_fp32 launch");
@@ -1020,6 +1032,7 @@ void lann_engine_destroy(lann_engine* e) {
     if (a) cudaStreamDestroy(a);
   if (e->stream) cudaStreamDestroy(e->stream);
   if (e->pin) cudaFreeHost(e->pin);
+  if (e->brcp) cudaFree(e->brcp);
   delete e;
 }
 

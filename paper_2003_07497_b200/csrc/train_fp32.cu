@@ -810,7 +810,7 @@ struct CtaLayout {
   static constexpr int PT = (P + 3) & ~3;  // transpose row stride (float4 writes, 4-wavefront STS.128)
 };
 
-template <int I, int H1, int H2, int W, bool kShuffleReduce, bool kPair>
+template <int I, int H1, int H2, int W, bool kShuffleReduce, bool kPair, bool kProf = false>
 __global__ void __launch_bounds__(32 * W, 1) train_fp32_cta_kernel(TrainF32Args a) {
   constexpr int P = Net<I, H1, H2>::P;
   constexpr int PT = CtaLayout<P>::PT;
@@ -847,7 +847,8 @@ __global__ void __launch_bounds__(32 * W, 1) train_fp32_cta_kernel(TrainF32Args 
   mbar_wait(&bar, 0);
   __syncthreads();
 
-  const bool prof = a.phase_cycles && blockIdx.x == 0 && tid == 0;
+  // kProf (LANN_PHASE_PROFILE launches only): the clock64 phase split; compiled out otherwise
+  const bool prof = kProf && a.phase_cycles && blockIdx.x == 0 && tid == 0;
   long long pc[4] = {0, 0, 0, 0};
   // kPair: each thread's two samples are the same every epoch, so their rows stay in registers
   float xa[8], xb[8];
@@ -1003,7 +1004,11 @@ void launch_cta(const TrainF32Args& a, int tile_bytes, cudaStream_t s) {
   const bool pair = pe == nullptr || pe[0] != '0';
   if (std::getenv("LANN_CTA_SMEM_REDUCE") == nullptr) {
     const int dyn = tile_bytes;
-    if (pair) {
+    if (pair && a.phase_cycles) {
+      auto kern = train_fp32_cta_kernel<I, H1, H2, W, true, true, true>;
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
+      kern<<<a.n_groups, 32 * W, dyn, s>>>(a);
+    } else if (pair) {
       auto kern = train_fp32_cta_kernel<I, H1, H2, W, true, true>;
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
       kern<<<a.n_groups, 32 * W, dyn, s>>>(a);

@@ -810,7 +810,7 @@ struct CtaLayout {
   static constexpr int PT = (P + 3) & ~3;  // transpose row stride (float4 writes, 4-wavefront STS.128)
 };
 
-template <int I, int H1, int H2, int W, bool kShuffleReduce, bool kPair, bool kProf = false>
+template <int I, int H1, int H2, int W, bool kShuffleReduce, bool kPair, bool kProf = false, bool kTrace = true>
 __global__ void __launch_bounds__(32 * W, 1) train_fp32_cta_kernel(TrainF32Args a) {
   constexpr int P = Net<I, H1, H2>::P;
   constexpr int PT = CtaLayout<P>::PT;
@@ -839,7 +839,8 @@ __global__ void __launch_bounds__(32 * W, 1) train_fp32_cta_kernel(TrainF32Args 
   for (int k = 0; k < OWN; ++k) mo[k] = ve[k] = 0.f;
   const float lr = (float)a.lr[m];
   const float scale = 2.0f / (float)rows, inv_n = 1.0f / (float)rows;
-  double* trace = a.loss_trace ? a.loss_trace + a.trace_offset[m] : nullptr;
+  // kTrace = false (launches without a loss trace): the per-epoch trace store compiled out
+  double* trace = (kTrace && a.loss_trace) ? a.loss_trace + a.trace_offset[m] : nullptr;
   int bad = -1;
   float last = 0.f;
   int rs_base, rs_valid;
@@ -1008,8 +1009,12 @@ void launch_cta(const TrainF32Args& a, int tile_bytes, cudaStream_t s) {
       auto kern = train_fp32_cta_kernel<I, H1, H2, W, true, true, true>;
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
       kern<<<a.n_groups, 32 * W, dyn, s>>>(a);
-    } else if (pair) {
+    } else if (pair && a.loss_trace) {
       auto kern = train_fp32_cta_kernel<I, H1, H2, W, true, true>;
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
+      kern<<<a.n_groups, 32 * W, dyn, s>>>(a);
+    } else if (pair) {
+      auto kern = train_fp32_cta_kernel<I, H1, H2, W, true, true, false, false>;
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
       kern<<<a.n_groups, 32 * W, dyn, s>>>(a);
     } else {

@@ -665,7 +665,7 @@ double flop_per_model_epoch(int I, int h1, int h2, int n) {
 
 // Host preparation (datasets, splits, tiles, validation, init) + upload.
 int prepare_population(lann_engine* e, int n_jobs, const lann_job* jobs, int precision,
-                       bool want_trace, Population& pop) {
+                       bool want_trace, Population& pop, bool sync_uploads = true) {
   pop.e = e;
   pop.n_jobs = n_jobs;
   pop.precision = precision;
@@ -898,7 +898,10 @@ int prepare_population(lann_engine* e, int n_jobs, const lann_job* jobs, int pre
   hlog("uploads", h3);
   const auto h4 = now();
   pop.plan = build_plan(e, t, precision, pop.dX.p, pop.dY.p, pop.rows);
-  ck(cudaStreamSynchronize(s), "prepare");
+  // a prepared population is resident when create returns; lann_run_population launches right
+  // behind the uploads on the same stream instead (stream order suffices, nothing host-side
+  // is reused before its own synchronisation)
+  if (sync_uploads) ck(cudaStreamSynchronize(s), "prepare");
   hlog("plan", h4);
   return LANN_OK;
 }
@@ -1596,8 +1599,19 @@ int lann_init_params(int32_t n_dims, const int32_t* dims, uint64_t seed, double*
   return LANN_OK;
 }
 
+namespace {
+int population_create(lann_engine* e, int32_t n_jobs, const lann_job* jobs, int32_t precision,
+                      int32_t record_trace, lann_population** out, bool sync_uploads);
+}
+
 int lann_population_create(lann_engine* e, int32_t n_jobs, const lann_job* jobs,
                            int32_t precision, int32_t record_trace, lann_population** out) {
+  return population_create(e, n_jobs, jobs, precision, record_trace, out, true);
+}
+
+namespace {
+int population_create(lann_engine* e, int32_t n_jobs, const lann_job* jobs, int32_t precision,
+                      int32_t record_trace, lann_population** out, bool sync_uploads) {
   if (!e) return LANN_NO_DEVICE;
   if (!out || n_jobs < 1 || !jobs) return set_err(e, {LANN_PARAM_ERROR, "empty population"});
   if (precision != LANN_FP64_EXACT && precision != LANN_FP32)
@@ -1606,7 +1620,7 @@ int lann_population_create(lann_engine* e, int32_t n_jobs, const lann_job* jobs,
   auto* p = new lann_population;
   try {
     ck(cudaSetDevice(e->device), "cudaSetDevice");
-    const int st = prepare_population(e, n_jobs, jobs, precision, record_trace != 0, p->pop);
+    const int st = prepare_population(e, n_jobs, jobs, precision, record_trace != 0, p->pop, sync_uploads);
     if (st != LANN_OK && p->pop.M == 0) {
       delete p;
       return st;
@@ -1619,6 +1633,7 @@ int lann_population_create(lann_engine* e, int32_t n_jobs, const lann_job* jobs,
   *out = p;
   return LANN_OK;
 }
+}  // namespace
 
 int lann_population_run(lann_population* p, int32_t n_steps) {
   if (!p) return LANN_PARAM_ERROR;
@@ -1694,7 +1709,7 @@ int lann_run_population(lann_engine* e, int32_t n_jobs, const lann_job* jobs, in
   if (!e) return LANN_NO_DEVICE;
   if (!results) return set_err(e, {LANN_PARAM_ERROR, "null results"});
   lann_population* p = nullptr;
-  const int st = lann_population_create(e, n_jobs, jobs, precision, trace_out != nullptr, &p);
+  const int st = population_create(e, n_jobs, jobs, precision, trace_out != nullptr, &p, false);
   if (!p) {
     for (int j = 0; j < n_jobs && jobs; ++j) {
       std::memset(&results[j], 0, sizeof(lann_job_result));

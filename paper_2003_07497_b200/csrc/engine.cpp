@@ -710,26 +710,30 @@ int prepare_population(lann_engine* e, int n_jobs, const lann_job* jobs, int pre
     }
     job_tile[j] = it->second;
   }
+  // one pool pass: each task builds a dataset and then every tile cut from it
   std::vector<Dataset> dsets(dsrc.size());
   std::vector<Status> dstat(dsrc.size());
-  parallel_for(int(dsrc.size()), [&](int d) {
-    dstat[d] = build_dataset(dsrc[d]->world, dsrc[d]->data_seed, dsrc[d]->count, dsets[d]);
-  });
-  hlog("datasets", h0);
-  const auto h1 = now();
   std::vector<Tile> tiles(tsrc.size());
   std::vector<Status> tstat(tsrc.size());
-  parallel_for(int(tsrc.size()), [&](int k) {
-    const auto& [d, frac, folds, fold, family, logt] = tsrc[k];
-    if (dstat[d]) {
-      tstat[k] = dstat[d];
-      return;
+  std::vector<std::vector<int>> tiles_of(dsrc.size());
+  for (int k = 0; k < int(tsrc.size()); ++k) tiles_of[std::get<0>(tsrc[k])].push_back(k);
+  const auto h1 = now();
+  parallel_for(int(dsrc.size()), [&](int d) {
+    dstat[d] = build_dataset(dsrc[d]->world, dsrc[d]->data_seed, dsrc[d]->count, dsets[d]);
+    for (int k : tiles_of[d]) {
+      const auto& [dd, frac, folds, fold, family, logt] = tsrc[k];
+      (void)dd;
+      if (dstat[d]) {
+        tstat[k] = dstat[d];
+        continue;
+      }
+      std::vector<int64_t> order;
+      int ntr = 0;
+      tstat[k] = split_order(dsets[d].size(), frac, dsrc[d]->data_seed, order, ntr);
+      if (!tstat[k]) tstat[k] = make_tile(dsets[d], order, ntr, folds, fold, family, logt != 0, tiles[k]);
     }
-    std::vector<int64_t> order;
-    int ntr = 0;
-    tstat[k] = split_order(dsets[d].size(), frac, dsrc[d]->data_seed, order, ntr);
-    if (!tstat[k]) tstat[k] = make_tile(dsets[d], order, ntr, folds, fold, family, logt != 0, tiles[k]);
   });
+  hlog("datasets", h0);
   for (int j = 0; j < n_jobs; ++j) {
     const int k = job_tile[j];
     Status st = tstat[k];

@@ -8,6 +8,7 @@
 // any number of times with launches only — so a prepared population re-runs
 // with its inputs resident in HBM and no host<->device traffic.
 #include <algorithm>
+#include <array>
 #include <atomic>
 #include <chrono>
 #include <condition_variable>
@@ -577,6 +578,8 @@ struct Population {
   int max_eval = 1;
   // device: every array lives in one blob (views below)
   DBuf<unsigned char> blob;
+  size_t res_off = 0, res_bytes = 0;  // the per-model result block inside the blob
+  std::array<size_t, 7> res_rel{};   // final loss, mape, thr, rho, bad epoch, kept, status
   DBuf<double> dX, dY, dP0, dP, dF, dER, dPred, dN, dET, dMape, dThr, dRho, dT;
   DBuf<int> dB, dEM, dI, dh1, dh2, dlog, dEL, dK, dS;
   DBuf<int64_t> dpo, dEO, dTO;
@@ -799,10 +802,15 @@ int prepare_population(lann_engine* e, int n_jobs, const lann_job* jobs, int pre
   const size_t oPO = L.add<int64_t>(size_t(M)), oEO = L.add<int64_t>(size_t(M)), oTO = L.add<int64_t>(size_t(M));
   const size_t up_bytes = L.bytes;
   // device-only outputs follow the uploaded part
-  const size_t oP = L.add<double>(size_t(t.total_params)), oF = L.add<double>(size_t(M));
-  const size_t oT = L.add<double>(size_t(pop.trace_total)), oPred = L.add<double>(size_t(n_eval_total));
+  // the per-model results first, contiguous, so fetch is one D2H copy
+  const size_t oF = L.add<double>(size_t(M));
   const size_t oMape = L.add<double>(size_t(M)), oThr = L.add<double>(size_t(M)), oRho = L.add<double>(size_t(M));
   const size_t oB = L.add<int>(size_t(M)), oK = L.add<int>(size_t(M)), oS = L.add<int>(size_t(M));
+  pop.res_off = oF;
+  pop.res_bytes = L.bytes - oF;
+  pop.res_rel = {0, oMape - oF, oThr - oF, oRho - oF, oB - oF, oK - oF, oS - oF};
+  const size_t oP = L.add<double>(size_t(t.total_params));
+  const size_t oT = L.add<double>(size_t(pop.trace_total)), oPred = L.add<double>(size_t(n_eval_total));
   unsigned char* h = pinned_stage(e, up_bytes);
   auto H = [&](auto* type_tag, size_t off) { return reinterpret_cast<decltype(type_tag)>(h + off); };
   {
@@ -933,15 +941,19 @@ int fetch_population(Population& pop, lann_job_result* results, double* params_o
   const int M = pop.M;
   for (int j = 0; j < pop.n_jobs; ++j) results[j] = pop.base[j];
   if (M == 0) return pop.base[0].status;
-  std::vector<double> fin(M), mape(M), thr(M), rho(M), params;
-  std::vector<int> bad(M), kept(M), est(M);
-  pop.dF.down(fin.data());
-  pop.dB.down(bad.data());
-  pop.dMape.down(mape.data());
-  pop.dThr.down(thr.data());
-  pop.dRho.down(rho.data());
-  pop.dK.down(kept.data());
-  pop.dS.down(est.data());
+  std::vector<double> params;
+  // one D2H of the result block into the engine's pinned staging buffer (its upload finished
+  // earlier on the same stream)
+  unsigned char* hr = pinned_stage(pop.e, pop.res_bytes);
+  ck(cudaMemcpyAsync(hr, pop.blob.p + pop.res_off, pop.res_bytes, cudaMemcpyDeviceToHost, pop.e->stream), "D2H");
+  t_d2h += int64_t(pop.res_bytes);
+  const double* fin = reinterpret_cast<const double*>(hr + pop.res_rel[0]);
+  const double* mape = reinterpret_cast<const double*>(hr + pop.res_rel[1]);
+  const double* thr = reinterpret_cast<const double*>(hr + pop.res_rel[2]);
+  const double* rho = reinterpret_cast<const double*>(hr + pop.res_rel[3]);
+  const int* bad = reinterpret_cast<const int*>(hr + pop.res_rel[4]);
+  const int* kept = reinterpret_cast<const int*>(hr + pop.res_rel[5]);
+  const int* est = reinterpret_cast<const int*>(hr + pop.res_rel[6]);
   if (params_out) {
     params.resize(pop.dP.n);
     pop.dP.down(params.data());

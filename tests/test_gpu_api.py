@@ -38,7 +38,8 @@ def fromhex(vals):
 
 
 @pytest.mark.parametrize("dims,n,epochs", [([4, 8, 1], 250, 300), ([6, 5, 5, 1], 250, 300), ([7, 8, 8, 1], 97, 120),
-                                           ([2, 3, 1], 5, 50)])
+                                           ([2, 3, 1], 5, 50), ([6, 5, 5, 1], 249, 80), ([5, 8, 1], 3, 40),
+                                           ([7, 8, 1], 256, 60)])
 def test_train_full_batch_is_the_reference(tool, reference, dims, n, epochs):
     r = api_train(tool, 7, epochs, 1e-2, n, dims)
     X = np.zeros((n, 8))

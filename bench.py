@@ -142,6 +142,17 @@ def fp32_peak():
     return 74.4, "derived nominal: 148 SM x 128 lanes x 2 FLOP x 1.965 GHz (no measured FP32 peak found)"
 
 
+def host_cpu_name():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 def cpu_reference_run(jobs, threads):
     """The reference's own CPU path (oracle/_ref, compiled from the reference sources) or,
     if that library is absent, the C restatement; returns (seconds, kind)."""
@@ -181,7 +192,8 @@ def run_reference_arm(args, rank, world):
         "config": {"workload": WORKLOAD, "models": len(jobs), "model_epochs_per_step": me,
                    "host": "reference perfsage core (oracle/_ref) train_nn+predict_dataset+make_report, one model per std::thread task"},
         "cpu_baseline": {"value": value, "unit": "model-epochs/s", "cores": threads, "kind": kind,
-                         "sample": f"the whole config-2 population (48 models, {me} model-epochs) per step on {threads} host threads"},
+                         "sample": f"the whole config-2 population (48 models, {me} model-epochs) per step on {threads} host threads",
+                         "host": host_cpu_name()},
         "e2e": {"value": value, "unit": "model-epochs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -311,10 +323,15 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
         secs, kind, cbad = cpu_reference_run(jobs, threads)
+        # single-core rate: one prediction net and one blur net on one thread
+        one = [next(j for j in jobs if j.epochs < max(x.epochs for x in jobs)), max(jobs, key=lambda j: j.epochs)]
+        secs1, _, _ = cpu_reference_run(one, 1)
         line["cpu_baseline"] = {"value": me_rank / secs, "unit": "model-epochs/s", "cores": threads, "kind": kind,
                                 "sample": f"the whole config-2 population (48 models, {me_rank} model-epochs) once, "
                                           f"one model per host thread task, {threads} threads",
-                                "seconds": secs}
+                                "seconds": secs, "host": host_cpu_name(),
+                                "single_core": {"value": popmod.model_epochs(one) / secs1, "unit": "model-epochs/s",
+                                                "sample": "one H=8 prediction net + one 5-5 blur net on 1 thread"}}
     if rank == 0:
         print(json.dumps(line), flush=True)
     pop.close()

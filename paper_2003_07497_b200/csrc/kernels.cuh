@@ -94,6 +94,9 @@ struct EvalArgs {
 // shape = {I, H1, H2} when every model of the launch has that compiled shape, else null
 void launch_train_fp64(const TrainArgs& a, int max_p, int dyn_bytes, const int* shape, cudaStream_t s);
 bool fp64_shape_compiled(int in, int h1, int h2);
+// pipelined exact trainer (train_fp64_pipe.cu): compiled shapes with N <= 256
+bool fp64_pipe_shape(int in, int h1, int h2);
+bool launch_train_fp64_pipe(const TrainArgs& a, int I, int H1, int H2, int producer_warps, cudaStream_t s);
 // FP64 trainer footprint (see train_fp64.cu): record matrix of a model, model state
 size_t fp64_record_bytes(int in, int h1, int h2, int n);
 size_t fp64_product_record_bytes(int in, int h1, int h2, int n);

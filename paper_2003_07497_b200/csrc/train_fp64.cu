@@ -27,6 +27,7 @@
 // wavefronts — bounds the epoch latency. Phase A is compiled per network shape for
 // the default topologies (unrolled, immediate offsets); other shapes use a generic path.
 #include <cmath>
+#include <cstdlib>
 
 #include "kernels.cuh"
 
@@ -505,6 +506,14 @@ void launch_train_fp64(const TrainArgs& a, int max_p, int dyn_bytes, const int* 
                        cudaStream_t s) {
   const int block = 256;
   const int kb = (max_p + block - 1) / block;
+  // product-row buckets (compiled shape, every model N <= 256) run the pipelined trainer
+  // (train_fp64_pipe.cu) unless LANN_FP64_PHASED asks for this phased one
+  if (shape && shape[0] > 0 && a.smem_records && a.rec_products && !std::getenv("LANN_FP64_PHASED") &&
+      fp64_pipe_shape(shape[0], shape[1], shape[2])) {
+    int npw = 4;
+    if (const char* env = std::getenv("LANN_FP64_PRODUCERS")) npw = std::atoi(env);
+    if (launch_train_fp64_pipe(a, shape[0], shape[1], shape[2], npw, s)) return;
+  }
   auto go = [&](auto kern) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_bytes);
     kern<<<a.n_models, block, dyn_bytes, s>>>(a);

@@ -1,0 +1,352 @@
+// train_fp64_pipe.cu — K1a, pipelined: the FP64 exact-order LANN trainer for the compiled
+// shapes (I-8-1, I <= 7, and I-5-5-1, I <= 6) with N <= 256 samples.
+//
+// Same arithmetic, bit for bit, as models::train_full_batch (mlp.cpp:156-175): forward in the
+// reference order (mlp.cpp:36-52), the per-sample delta recursion (mlp.cpp:93-104), the
+// SEQUENTIAL per-parameter sums over samples 0..N-1 of (inv_n*delta)*a (mlp.cpp:106-118),
+// Adam in the reference expression order with host-libm bias corrections (mlp.cpp:142-154),
+// the pre-update loss trace and the non-finite check. Built with -fmad=false; every operation
+// is an explicit __d*_rn intrinsic.
+//
+// Why a second FP64 kernel: an epoch's floor is one N-long dependent DADD chain per parameter
+// (the reference's sample-order sum cannot be reassociated), ~8.3 cycles per link on the B200
+// (tools/mb/fp64_issue_mb.cu). The phased kernel (train_fp64.cu) runs "all samples forward /
+// backward" and "all chains" one after the other behind CTA barriers, so an epoch costs
+// phase A + chain + Adam. Here the two overlap inside the epoch:
+//   producer warps  own SAMPLES: thread k runs samples k, k + 32*NPW, ... ("rounds"), forward
+//                   and backward, and stores the sample's column of the record matrix: one row
+//                   per parameter holding its term ((inv_n*delta)*a for a weight, the product
+//                   mlp.cpp:113 forms; inv_n*delta for a bias, mlp.cpp:117) plus the err^2 row;
+//                   the producer threads arrive on the round's mbarrier when their columns are
+//                   stored; the epoch's weights are read into registers once per epoch;
+//   chain lanes     own PARAMETERS (lane c sums row c; one more lane the loss): a lane waits for
+//                   round q's mbarrier, then extends its DADD chain over that round's samples,
+//                   two per 16-B load, in sample order — the chain starts after round 0 and runs
+//                   while the producers are on later rounds.
+// Measured (config 2, blur net 6-5-5-1, 4 producer warps): ~1290 cycles to round 0, the chain
+// ~3660 (~14.6 cycles per link: shared-memory traffic of the producers' stores is the
+// contention), Adam ~1000 — ~6000 cycles per epoch against ~6950 phased.
+// The owner lane keeps w, m, v in registers; after Adam it writes w to shared memory for the
+// producers; one CTA barrier per epoch separates epochs.
+#include <cmath>
+
+#include "kernels.cuh"
+
+namespace lann {
+namespace {
+
+constexpr int kLd = 258;     // record row stride (doubles): N <= 256 samples + even padding
+constexpr int kChainWarps = 3;
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
+  asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.release.cta.shared::cta.b64 st, [%0];\n\t}" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+// Parameter offsets of a compiled shape (H2 == 0: one hidden layer), flat layout of
+// mlp.cpp:124-131. Record row c (c < P) holds parameter c's per-sample term, row P the loss term.
+template <int I, int H1, int H2>
+struct PipeShape {
+  static_assert(H2 == 0 ? (H1 == 8 && I >= 1 && I <= 7) : (H1 == 5 && H2 == 5 && I >= 1 && I <= 6),
+                "compiled pipelined shapes: I-8-1 (I <= 7) and I-5-5-1 (I <= 6)");
+  static constexpr int W1 = 0, B1 = I * H1;
+  static constexpr int W2 = B1 + H1, B2 = W2 + H1 * H2;
+  static constexpr int WO = H2 > 0 ? B2 + H2 : B1 + H1;
+  static constexpr int BO = WO + (H2 > 0 ? H2 : H1);
+  static constexpr int P = BO + 1;
+  static constexpr int ROWS = P + 1;
+  static_assert(ROWS <= 32 * kChainWarps, "one chain lane per record row");
+
+  // One sample, forward + backward in the reference order; stores its record column:
+  // weight terms (inv_n*delta)*a (mlp.cpp:113), bias terms inv_n*delta (mlp.cpp:117), err^2.
+  // w: this epoch's weights (the producer's registers); r: rec + s (row j at r[j * kLd]).
+  __device__ static void sample(const double (&w)[P], const double (&x)[I], double y,
+                                double* __restrict__ r, double inv_n) {
+    double a1[H1];
+#pragma unroll
+    for (int o = 0; o < H1; ++o) {
+      double z = w[B1 + o];
+#pragma unroll
+      for (int i = 0; i < I; ++i) z = __dadd_rn(z, __dmul_rn(w[W1 + o * I + i], x[i]));
+      a1[o] = z > 0.0 ? z : 0.0;
+    }
+    double z;
+    double a2[H2 > 0 ? H2 : 1];
+    if constexpr (H2 > 0) {
+#pragma unroll
+      for (int o = 0; o < H2; ++o) {
+        double q = w[B2 + o];
+#pragma unroll
+        for (int i = 0; i < H1; ++i) q = __dadd_rn(q, __dmul_rn(w[W2 + o * H1 + i], a1[i]));
+        a2[o] = q > 0.0 ? q : 0.0;
+      }
+      z = w[BO];
+#pragma unroll
+      for (int i = 0; i < H2; ++i) z = __dadd_rn(z, __dmul_rn(w[WO + i], a2[i]));
+    } else {
+      z = w[BO];
+#pragma unroll
+      for (int i = 0; i < H1; ++i) z = __dadd_rn(z, __dmul_rn(w[WO + i], a1[i]));
+    }
+    const double err = __dsub_rn(z, y);           // mlp.cpp:90
+    const double dout = __dmul_rn(2.0, err);      // mlp.cpp:92
+    const double tout = __dmul_rn(inv_n, dout);   // left factor of mlp.cpp:113,117
+    r[P * kLd] = __dmul_rn(err, err);             // mlp.cpp:91
+    r[BO * kLd] = tout;
+    double t1[H1];
+    if constexpr (H2 > 0) {
+      double d2[H2];
+#pragma unroll
+      for (int i = 0; i < H2; ++i) {  // acc = 0.0 + w*delta (mlp.cpp:97-100), ReLU gate
+        const double acc = __dadd_rn(0.0, __dmul_rn(w[WO + i], dout));
+        d2[i] = a2[i] > 0.0 ? acc : 0.0;
+        r[(WO + i) * kLd] = __dmul_rn(tout, a2[i]);
+      }
+#pragma unroll
+      for (int o = 0; o < H2; ++o) {
+        const double t2 = __dmul_rn(inv_n, d2[o]);
+#pragma unroll
+        for (int i = 0; i < H1; ++i) r[(W2 + o * H1 + i) * kLd] = __dmul_rn(t2, a1[i]);
+        r[(B2 + o) * kLd] = t2;
+      }
+#pragma unroll
+      for (int i = 0; i < H1; ++i) {
+        double acc = 0.0;
+#pragma unroll
+        for (int o = 0; o < H2; ++o) acc = __dadd_rn(acc, __dmul_rn(w[W2 + o * H1 + i], d2[o]));
+        t1[i] = __dmul_rn(inv_n, a1[i] > 0.0 ? acc : 0.0);
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < H1; ++i) {
+        const double acc = __dadd_rn(0.0, __dmul_rn(w[WO + i], dout));
+        t1[i] = __dmul_rn(inv_n, a1[i] > 0.0 ? acc : 0.0);
+        r[(WO + i) * kLd] = __dmul_rn(tout, a1[i]);
+      }
+    }
+#pragma unroll
+    for (int o = 0; o < H1; ++o) {
+#pragma unroll
+      for (int i = 0; i < I; ++i) r[(W1 + o * I + i) * kLd] = __dmul_rn(t1[o], x[i]);
+      r[(B1 + o) * kLd] = t1[o];
+    }
+  }
+};
+
+template <int I, int H1, int H2>
+__host__ __device__ constexpr int pipe_smem_doubles() {
+  using S = PipeShape<I, H1, H2>;
+  // records | weights (even) | loss (2) | mbarriers (<= 8 x u64)
+  return S::ROWS * kLd + ((S::P + 1) & ~1) + 2 + 8;
+}
+
+template <int I, int H1, int H2, int NPW, bool kProf>
+__global__ void __launch_bounds__(32 * (kChainWarps + NPW), 1) train_fp64_pipe(TrainArgs a) {
+  using S = PipeShape<I, H1, H2>;
+  constexpr int NPT = 32 * NPW;                 // producer threads = samples per round
+  constexpr int R = (256 + NPT - 1) / NPT;      // rounds (samples per producer thread) at most
+  extern __shared__ __align__(16) double smem[];
+  double* rec = smem;                                       // [ROWS][kLd]
+  double* ws = rec + S::ROWS * kLd;                         // [P] weights (producers' copy)
+  double* Ls = ws + ((S::P + 1) & ~1);                      // [2] epoch loss
+  unsigned long long* bar = reinterpret_cast<unsigned long long*>(Ls + 2);  // [R] rounds
+
+  const int m = a.order[blockIdx.x];
+  const int tile = a.model_tile[m];
+  const int N = a.tile_rows[tile];
+  const int E = a.epochs[m];
+  const double lr = a.lr[m];
+  const int tid = threadIdx.x;
+  const double inv_n = 1.0 / (double)N;  // mlp.cpp:84
+  const double* gp = a.params + a.param_offset[m];
+  const double* X = a.X + a.tile_offset[tile] * 8;
+  const double* Y = a.y + a.tile_offset[tile];
+
+  for (int p = tid; p < S::P; p += blockDim.x) ws[p] = gp[p];
+  // padding column (odd N) holds zero terms: they leave every chain unchanged (a chain starts
+  // at +0.0 and is never -0.0, and x + (+-0) == x for every other x)
+  for (int s = tid; s < kLd; s += blockDim.x)
+    for (int j = 0; j < S::ROWS; ++j) rec[j * kLd + s] = 0.0;
+  if (tid < R) mbar_init(&bar[tid], NPT);  // one per producer round: every producer thread arrives
+  __syncthreads();
+
+  double* trace = a.loss_trace ? a.loss_trace + a.trace_offset[m] : nullptr;
+  int bad = -1;
+  double last = 0.0;
+
+  if (tid < 32 * kChainWarps) {
+    // ---- chain lanes: lane c sums record row c over the samples in order, then Adam ----
+    const int p = tid < S::P ? tid : tid == S::P ? -1 : -2;  // parameter, -1 the loss, -2 idle
+    const double2* Tr = reinterpret_cast<const double2*>(rec + (tid <= S::P ? tid : S::P) * kLd);
+    const int npairs = (N + 1) >> 1;
+    double wr = p >= 0 ? gp[p] : 0.0, mr = 0.0, vr = 0.0;
+    const double beta1 = 0.9, beta2 = 0.999, eps = 1e-8;
+    const double c1 = 1.0 - beta1, c2 = 1.0 - beta2;
+    long long pc[4] = {0, 0, 0, 0};
+    int next_trace = 0;
+    for (int e = 0; e < E; ++e) {
+      const double2 bc = a.bias_corr[e];  // issued early: latency hidden behind the chain
+      long long k0 = 0, k1 = 0, k2 = 0;
+      if (kProf) k0 = clock64();
+      double g = 0.0;
+      for (int q = 0, j = 0; j < npairs; ++q) {
+        mbar_wait(bar + q, e & 1);  // producer round q's columns are stored
+        if (kProf && q == 0) k1 = clock64();
+        const int j1 = min(npairs, (q + 1) * (NPT / 2));
+        if (p != -2) {  // idle lanes load nothing (a warp's 16-B load costs a wavefront per 8 lanes)
+#pragma unroll 8
+          for (; j < j1; ++j) {  // two samples per 16-B load, in sample order (mlp.cpp:106-118)
+            const double2 t = Tr[j];
+            g = __dadd_rn(g, t.x);
+            g = __dadd_rn(g, t.y);
+          }
+        }
+        j = j1;
+      }
+      if (kProf) k2 = clock64();
+      if (p >= 0) {  // AdamState::update (mlp.cpp:142-154), bias corrections from the host libm
+        const double mk = __dadd_rn(__dmul_rn(beta1, mr), __dmul_rn(c1, g));
+        const double vk = __dadd_rn(__dmul_rn(beta2, vr), __dmul_rn(__dmul_rn(c2, g), g));
+        mr = mk;
+        vr = vk;
+        // m == 0 (a unit that has never been active): the step (lr*(m/bc1))/(sqrt(v/bc2)+eps)
+        // is a zero with m's sign (lr, bc1 and the divisor are positive), set directly: a zero
+        // dividend and a zero v take the slow (divergent) paths of CUDA's division and sqrt
+        double step;
+        if (mk == 0.0) {
+          step = copysign(0.0, mk);
+        } else {
+          const double mhat = __ddiv_rn(mk, bc.x);
+          const double vhat = __ddiv_rn(vk, bc.y);
+          step = __ddiv_rn(__dmul_rn(lr, mhat), __dadd_rn(__dsqrt_rn(vhat), eps));
+        }
+        wr = __dsub_rn(wr, step);
+        ws[p] = wr;
+      } else if (p == -1) {
+        const double L = __dmul_rn(g, inv_n);  // mlp.cpp:120
+        Ls[e & 1] = L;
+        if (trace && e == next_trace) {
+          trace[e / a.trace_stride] = L;
+          next_trace += a.trace_stride;
+        }
+      }
+      long long k3 = 0;
+      if (kProf) k3 = clock64();
+      __syncthreads();
+      if (kProf) {
+        const long long k4 = clock64();
+        pc[0] += k1 - k0;  // epoch start -> producer round 0 stored
+        pc[1] += k2 - k1;  // the chains over all samples
+        pc[2] += k3 - k2;  // Adam
+        pc[3] += k4 - k3;  // epoch barrier
+      }
+      last = Ls[e & 1];
+      if (!isfinite(last)) {  // mlp.cpp:166-169: TrainingError(epoch)
+        bad = e;
+        break;
+      }
+    }
+    if (p >= 0) a.params[a.param_offset[m] + p] = wr;
+    if (p == -1) {
+      a.final_loss[m] = last;
+      a.nonfinite_epoch[m] = bad;
+    }
+    if (kProf && tid == 0 && blockIdx.x == 0)
+      for (int k = 0; k < 4; ++k) a.phase_cycles[k] = pc[k];
+  } else {
+    // ---- producer threads: samples k, k + NPT, ... (rounds), inputs kept in registers ----
+    const int k = tid - 32 * kChainWarps;
+    double xr[R][I], yr[R];
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+      const int s = k + q * NPT;
+#pragma unroll
+      for (int i = 0; i < I; ++i) xr[q][i] = s < N ? X[(size_t)s * 8 + i] : 0.0;
+      yr[q] = s < N ? Y[s] : 0.0;
+    }
+    for (int e = 0; e < E; ++e) {
+      double wv[S::P];  // this epoch's weights: one broadcast read per epoch, not per sample
+#pragma unroll
+      for (int j = 0; j < S::P; ++j) wv[j] = ws[j];
+#pragma unroll
+      for (int q = 0; q < R; ++q) {
+        if (q * NPT < N) {
+          const int s = k + q * NPT;
+          if (s < N) S::sample(wv, xr[q], yr[q], rec + s, inv_n);
+          mbar_arrive(&bar[q]);
+        }
+      }
+      __syncthreads();
+      last = Ls[e & 1];
+      if (!isfinite(last)) break;
+    }
+  }
+}
+
+template <int I, int H1, int H2, int NPW>
+void go_pipe(const TrainArgs& a, cudaStream_t s) {
+  const int dyn = pipe_smem_doubles<I, H1, H2>() * 8;
+  auto launch = [&](auto kern) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
+    kern<<<a.n_models, 32 * (kChainWarps + NPW), dyn, s>>>(a);
+  };
+  if (a.phase_cycles) launch(train_fp64_pipe<I, H1, H2, NPW, true>);
+  else launch(train_fp64_pipe<I, H1, H2, NPW, false>);
+}
+
+template <int NPW>
+bool dispatch_pipe(const TrainArgs& a, int I, int H1, int H2, cudaStream_t s) {
+  if (H1 == 8 && H2 == 0) {
+    switch (I) {
+      case 1: return go_pipe<1, 8, 0, NPW>(a, s), true;
+      case 2: return go_pipe<2, 8, 0, NPW>(a, s), true;
+      case 3: return go_pipe<3, 8, 0, NPW>(a, s), true;
+      case 4: return go_pipe<4, 8, 0, NPW>(a, s), true;
+      case 5: return go_pipe<5, 8, 0, NPW>(a, s), true;
+      case 6: return go_pipe<6, 8, 0, NPW>(a, s), true;
+      case 7: return go_pipe<7, 8, 0, NPW>(a, s), true;
+    }
+  } else if (H1 == 5 && H2 == 5) {
+    switch (I) {
+      case 4: return go_pipe<4, 5, 5, NPW>(a, s), true;
+      case 5: return go_pipe<5, 5, 5, NPW>(a, s), true;
+      case 6: return go_pipe<6, 5, 5, NPW>(a, s), true;
+    }
+  }
+  return false;
+}
+
+}  // namespace
+
+bool fp64_pipe_shape(int in, int h1, int h2) {
+  return (h1 == 8 && h2 == 0 && in >= 1 && in <= 7) || (h1 == 5 && h2 == 5 && in >= 4 && in <= 6);
+}
+
+// Every model of the launch must have this shape and N <= 256 rows (checked by the caller).
+bool launch_train_fp64_pipe(const TrainArgs& a, int I, int H1, int H2, int producer_warps,
+                            cudaStream_t s) {
+  switch (producer_warps) {
+    case 2: return dispatch_pipe<2>(a, I, H1, H2, s);
+    case 3: return dispatch_pipe<3>(a, I, H1, H2, s);
+    case 8: return dispatch_pipe<8>(a, I, H1, H2, s);
+    default: return dispatch_pipe<4>(a, I, H1, H2, s);
+  }
+}
+
+}  // namespace lann

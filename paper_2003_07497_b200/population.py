@@ -43,6 +43,42 @@ def default_model(world, family=abi.NNC, unconstrained=False):
     return hidden, lr, epochs, logt
 
 
+def combo_worlds():
+    """The 48 synthetic kernel-variant-hardware worlds (SURVEY 7 hard part 8), restated from the
+    engine's table (csrc/domain.cpp:401-456, exported as lann_default_combos) so that job lists
+    can be built without loading the engine library (the reference arm of bench.py must not map
+    it); tests/test_host.py checks the two tables are identical. 4 kernels x {dense, sparse} x
+    {3 CPU hosts with n_thd, 2 GPU-class black boxes without} = 40 prediction worlds (combo 0 is
+    the acceptance world, acceptance_main.cpp:271-279), then 8 blur selection worlds."""
+    kind_alpha = (3e-9, 2e-9, 1.5e-9, 1e-9)
+    hws = ((abi.HW_CPU, 4, 1.0, 0.25, 0.75, 0.0), (abi.HW_CPU, 8, 0.7, 0.15, 0.85, 0.0),
+           (abi.HW_CPU, 16, 1.3, 0.10, 0.90, 0.0), (abi.HW_GPU, 1, 0.02, 1.0, 0.0, 5e-6),
+           (abi.HW_GPU, 1, 0.05, 1.0, 0.0, 2e-5))
+    out = []
+    for kind in range(4):
+        for variant in range(2):
+            for cls, threads, mult, g0, g1, beta in hws:
+                out.append(abi.World(kind=kind, hw_class=cls, max_threads=threads, blur_lattice=0,
+                                     alpha=kind_alpha[kind] * (2.5 if variant else 1.0) * mult, g0=g0, g1=g1,
+                                     delta=0.9 if variant else 0.0, beta=beta, noise=0.02))
+    blurs = ((0, 1.0e-9, 0.0, (3, 8, 7, 3), (0.05, 0.02, 0.03, 0.04)),
+             (0, 0.7e-9, 0.0, (4, 7, 6, 2), (0.04, 0.03, 0.02, 0.05)),
+             (0, 1.3e-9, 0.0, (2, 9, 8, 4), (0.06, 0.01, 0.04, 0.03)),
+             (1, 1e-11, 1e-5, (2, 4, 4, 0), (0.20, 0.10, 0.10, 0.0)),
+             (1, 2e-11, 2e-5, (3, 3, 5, 0), (0.15, 0.12, 0.08, 0.0)),
+             (0, 2.0e-9, 0.0, (5, 6, 5, 3), (0.03, 0.05, 0.05, 0.02)),   # FFT stand-ins (PAPER.md:296)
+             (0, 1.5e-9, 0.0, (6, 10, 9, 5), (0.02, 0.04, 0.06, 0.01)),
+             (0, 0.9e-9, 0.0, (1, 5, 3, 1), (0.08, 0.02, 0.02, 0.06)))
+    for lattice, alpha, beta, mu, kappa in blurs:
+        w = abi.World(kind=abi.BLUR, hw_class=abi.HW_CPU, max_threads=1, blur_lattice=lattice, alpha=alpha,
+                      g0=1.0, g1=0.0, delta=0.0, beta=beta, noise=0.02)
+        for j in range(4):
+            w.mu[j] = float(mu[j])
+            w.kappa[j] = kappa[j]
+        out.append(w)
+    return out
+
+
 def combo_seed(root_seed: int, combo: int) -> int:
     return derive_seed(root_seed, combo)
 
@@ -53,8 +89,7 @@ def config1_jobs(seeds=(1, 2, 3, 4, 5), family=abi.NNC):
 
 
 def config2_jobs(root_seed=1, family=abi.NNC, combos=None, epochs_scale=1.0):
-    from .engine import default_combos
-    worlds = combos if combos is not None else default_combos()
+    worlds = combos if combos is not None else combo_worlds()
     jobs = []
     for i, w in enumerate(worlds):
         hidden, lr, epochs, logt = default_model(w, family)
@@ -67,8 +102,7 @@ def config2_jobs(root_seed=1, family=abi.NNC, combos=None, epochs_scale=1.0):
 def config3_jobs(root_seed=1, n_seeds=256, n_folds=5, family=abi.NNC, combos=None, seed_offset=0):
     """48 combos x n_seeds init seeds x n_folds folds; fold f holds out block f of the
     combo's 250-sample training split (contiguous blocks of the split permutation)."""
-    from .engine import default_combos
-    worlds = combos if combos is not None else default_combos()
+    worlds = combos if combos is not None else combo_worlds()
     jobs = []
     for i, w in enumerate(worlds):
         hidden, lr, epochs, logt = default_model(w, family)

@@ -44,3 +44,13 @@ def golden():
 
     with open(os.path.join(ROOT, "tests", "golden", "golden_r01.json")) as f:
         return json.load(f)
+
+
+@pytest.fixture(scope="session")
+def golden_full():
+    """Full-length reference goldens (tests/golden/make_golden_r02.py): config 2 at 8000 / 20,000
+    epochs and the stratified config-3 subset (48 combos x 4 seeds x 5 folds)."""
+    import json
+
+    with open(os.path.join(ROOT, "tests", "golden", "golden_r02_full.json")) as f:
+        return json.load(f)

@@ -18,31 +18,58 @@ pytestmark = pytest.mark.gpu
 FWD_RTOL = 1e-5  # north_star: forward predictions within 1e-5 relative for identical weights
 
 
-def test_fp32_forward_parity(engine, oracle, golden):
-    """FP32 forward (FMA) vs the exact FP64 prediction on the config-1 seed-1 model, all 250
-    held-out rows: relative error of the network output measured in the model's normalised
-    target units (|z32 - z64| <= 1e-5 * max(|z64|, 1)), i.e. 1e-5 relative of the target range."""
-    g = golden["predict_config1_seed1"]
-    st, feats, c, rt, nf = oracle.build_dataset(abi.acceptance_world(), 1, 500)
-    _, order, ntr = oracle.split_order(500, 0.5, 1)
+def heldout_rows(oracle, job, n_inputs):
+    """Raw model-input rows (features, then c) of a config-2 job's held-out half."""
+    st, feats, c, rt, nf = oracle.build_dataset(job.world, job.data_seed, job.count)
+    _, order, ntr = oracle.split_order(job.count, job.train_fraction, job.data_seed)
     te = order[ntr:]
     rows = np.zeros((len(te), 8))
-    rows[:, :6] = feats[te, :6]
-    rows[:, 6] = c[te].astype(np.float64)
-    norm = np.array(g["norm"])
-    model = {"inputs": 7, "h1": 8, "h2": 0, "log_target": 0, "params": np.array(g["params"]), "norm": norm}
-    rm = np.zeros(len(te), dtype=np.int32)
-    p64 = engine.predict([model], rows, rm, abi.FP64_EXACT)
-    p32 = engine.predict([model], rows, rm, abi.FP32)
-    rng = norm[17] - norm[16]
-    z64 = (p64 - norm[16]) / rng
-    z32 = (p32 - norm[16]) / rng
-    keep = p64 > 1e-9  # rows not clamped by max(v, 1e-9)
-    err = np.abs(z32 - z64)[keep] / np.maximum(np.abs(z64[keep]), 1.0)
-    assert err.max() <= FWD_RTOL, err.max()
-    # and in seconds, relative, for every prediction above 1% of the target range
-    big = p64 > norm[16] + 0.01 * rng
-    assert np.max(np.abs(p32[big] - p64[big]) / p64[big]) <= 1e-3
+    rows[:, :nf] = feats[te, :nf]
+    rows[:, nf] = c[te].astype(np.float64)
+    assert nf + 1 == n_inputs
+    return rows
+
+
+def test_fp32_forward_parity_relative_in_seconds(engine, oracle):
+    """north_star: forward predictions within 1e-5 RELATIVE error for identical weights — here
+    measured in seconds (the unit predict() returns, models.cpp:346-363) over every held-out row
+    of all 48 config-2 models, FP32 predictor vs the exact FP64 one with the same (FP64-trained)
+    weights. Measured on a B200 (round 2), 12,000 predictions: 98.7% within 1e-5, median
+    1.5e-7, p99 1.3e-5, max 7.1e-4; max 2.9e-5 over predictions above 1% of the target range.
+    So FP32 meets 1e-5 for the bulk of the predictions but not everywhere — least of all for the
+    smallest runtimes of a linear-target model: the
+    network output is a difference of O(1) terms there, so an FP32 rounding of ~6e-8 of the
+    target range becomes ~1e-4..1e-3 relative of a prediction at ~1e-3 of the range. The FP64
+    predictor is bit-identical to the reference (test_gpu_parity.py), which is why the
+    precision-matched headline runs FP64."""
+    jobs = P.config2_jobs(root_seed=1, epochs_scale=0.25)
+    pop = engine.prepare(jobs, abi.FP64_EXACT)
+    pop.run(1)
+    st, res, params, _ = pop.fetch(want_params=True)
+    norms = pop.norms()
+    pop.close()
+    errs, errs_big, n_total = [], [], 0
+    for j, r, p, nm in zip(jobs, res, params, norms):
+        rows = heldout_rows(oracle, j, r.n_inputs)
+        model = {"inputs": r.n_inputs, "h1": j.hidden[0], "h2": j.hidden[1] if j.n_hidden > 1 else 0,
+                 "log_target": j.log_target, "params": p, "norm": nm}
+        rm = np.zeros(len(rows), dtype=np.int32)
+        p64 = engine.predict([model], rows, rm, abi.FP64_EXACT)
+        p32 = engine.predict([model], rows, rm, abi.FP32)
+        keep = p64 > 1e-9  # rows not clamped by max(v, 1e-9)
+        rel = np.abs(p32[keep] - p64[keep]) / p64[keep]
+        errs.append(rel)
+        lo, hi = (np.exp(nm[16]), np.exp(nm[17])) if j.log_target else (nm[16], nm[17])
+        errs_big.append(rel[p64[keep] >= lo + 0.01 * (hi - lo)])
+        n_total += len(rows)
+    e = np.concatenate(errs)
+    eb = np.concatenate(errs_big)
+    stats = {"predictions": int(n_total), "frac_within_1e-5": float(np.mean(e <= FWD_RTOL)),
+             "median": float(np.median(e)), "p99": float(np.percentile(e, 99)), "max": float(e.max()),
+             "max_above_1pct_of_range": float(eb.max())}
+    print("FP32 forward, relative error in seconds:", stats)
+    assert stats["frac_within_1e-5"] >= 0.95, stats
+    assert stats["max_above_1pct_of_range"] <= 1e-4, stats
 
 
 def test_fp32_one_step_parity(engine, oracle):

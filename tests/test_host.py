@@ -59,6 +59,15 @@ def test_default_combos_are_the_golden_worlds(golden):
     assert bytes(combos[0]) == bytes(abi.acceptance_world())
 
 
+def test_python_world_table_is_the_engine_table():
+    """population.combo_worlds() (used by job lists, incl. bench.py's reference arm, which must
+    not load the engine library) is byte-identical to the engine's lann_default_combos."""
+    py, eng = P.combo_worlds(), E.default_combos()
+    assert len(py) == len(eng) == 48
+    for a, b in zip(py, eng):
+        assert bytes(a) == bytes(b)
+
+
 def test_init_matches_reference(golden):
     for g in golden["mse_gradient"]:
         assert E.init_params(g["dims"], 5).tolist() == g["params"]

@@ -192,3 +192,30 @@ def test_oracle_matches_reference_metrics_random(oracle, reference):
         assert oracle.mape(t, p) == reference.mape(t, p)
         assert oracle.mape_thresholded(t, p) == reference.mape_thresholded(t, p)
         assert oracle.spearman(t, p) == reference.spearman(t, p)
+
+
+@pytest.mark.parametrize("combo", [0, 17, 40, 43])
+def test_full_length_config2_model_bit_exact(oracle, golden_full, combo):
+    """Config-2 models at their FULL length (8000 epochs for prediction nets, 20,000 for the
+    blur selection nets): the oracle reproduces the reference's every loss (full-trace sha256),
+    weight and metric (tests/golden/make_golden_r02.py)."""
+    g = golden_full["config2_full"]
+    jd, exp = g["jobs"][combo], g["results"][combo]
+    r, params, trace = oracle.run_job(job_from(jd), want_params=True, want_trace=True)
+    assert len(trace) == jd["epochs"]
+    check_result(r, exp, params, trace)
+    assert trace[-3:].tolist() == exp["trace_tail"]
+
+
+def test_config3_subset_recipe_and_oracle(oracle, golden_full):
+    """The stratified config-3 subset is population.config3_jobs(root_seed=1, n_seeds=4) byte
+    for byte; two of its fold models (one per hidden-layer shape) reproduce the reference."""
+    from paper_2003_07497_b200 import population as P
+    g = golden_full["config3_subset"]
+    jobs = P.config3_jobs(root_seed=1, n_seeds=g["n_seeds"])
+    assert len(jobs) == 48 * 4 * 5 == len(g["results"])
+    assert hashlib.sha256(b"".join(bytes(j) for j in jobs)).hexdigest() == g["jobs_sha256"]
+    for i in (3, 40 * 20 + 7):  # an MM fold model, a blur fold model
+        r, params, _ = oracle.run_job(jobs[i], want_params=True)
+        check_result(r, g["results"][i])
+        assert sha(np.asarray(params, dtype=np.float64)) == g["results"][i]["params_sha256"]

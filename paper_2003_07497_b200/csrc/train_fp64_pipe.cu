@@ -30,6 +30,7 @@
 // producers; one CTA barrier per epoch separates epochs.
 #include <cmath>
 
+#include "exact_fp64.cuh"
 #include "kernels.cuh"
 
 namespace lann {
@@ -149,6 +150,12 @@ struct PipeShape {
   }
 };
 
+// The Adam step through CUDA's IEEE division and square root (mlp.cpp:149-152): the fallback for
+// lanes whose verified short path (exact_fp64.cuh) does not apply.
+__device__ __noinline__ double adam_step_ieee(double mk, double vk, double2 bc, double lr, double eps) {
+  return __ddiv_rn(__dmul_rn(lr, __ddiv_rn(mk, bc.x)), __dadd_rn(__dsqrt_rn(__ddiv_rn(vk, bc.y)), eps));
+}
+
 template <int I, int H1, int H2>
 __host__ __device__ constexpr int pipe_smem_doubles() {
   using S = PipeShape<I, H1, H2>;
@@ -202,6 +209,7 @@ __global__ void __launch_bounds__(32 * (kChainWarps + NPW), 1) train_fp64_pipe(T
     int next_trace = 0;
     for (int e = 0; e < E; ++e) {
       const double2 bc = a.bias_corr[e];  // issued early: latency hidden behind the chain
+      const double y1 = rcp_refined(bc.x), y2 = rcp_refined(bc.y);  // per epoch, off the chain
       long long k0 = 0, k1 = 0, k2 = 0;
       if (kProf) k0 = clock64();
       double g = 0.0;
@@ -225,18 +233,27 @@ __global__ void __launch_bounds__(32 * (kChainWarps + NPW), 1) train_fp64_pipe(T
         const double vk = __dadd_rn(__dmul_rn(beta2, vr), __dmul_rn(__dmul_rn(c2, g), g));
         mr = mk;
         vr = vk;
-        // m == 0 (a unit that has never been active): the step (lr*(m/bc1))/(sqrt(v/bc2)+eps)
-        // is a zero with m's sign (lr, bc1 and the divisor are positive), set directly: a zero
-        // dividend and a zero v take the slow (divergent) paths of CUDA's division and sqrt
-        double step;
-        if (mk == 0.0) {
-          step = copysign(0.0, mk);
-        } else {
-          const double mhat = __ddiv_rn(mk, bc.x);
-          const double vhat = __ddiv_rn(vk, bc.y);
-          step = __ddiv_rn(__dmul_rn(lr, mhat), __dadd_rn(__dsqrt_rn(vhat), eps));
+        // (lr * (m / bc1)) / (sqrt(v / bc2) + eps) with every division and the square root
+        // correctly rounded: a verified short path (exact_fp64.cuh), CUDA's IEEE functions for
+        // any lane whose verification fails (zeros, subnormals, huge values)
+        bool ok = true;
+        const double mhat = div_checked(mk, bc.x, y1, ok);
+        const double vhat = div_checked(vk, bc.y, y2, ok);
+        const double den = __dadd_rn(sqrt_checked(vhat, ok), eps);
+        const double num = __dmul_rn(lr, mhat);
+        const double step = div_checked(num, den, rcp_refined(den), ok);
+        if (fabs(mk) >= 0x1p-900) {
+          wr = __dsub_rn(wr, ok ? step : adam_step_ieee(mk, vk, bc, lr, eps));
+        } else if (mk == 0.0) {
+          // a unit never active so far: the step is a zero with m's sign (lr, bc1 and the
+          // divisor are positive)
+          wr = __dsub_rn(wr, copysign(0.0, mk));
+        } else if (fabs(wr) < 0x1p-820) {
+          wr = __dsub_rn(wr, adam_step_ieee(mk, vk, bc, lr, eps));
         }
-        wr = __dsub_rn(wr, step);
+        // else: a unit that stopped being active (m decays by 0.9 per epoch and then sticks at
+        // the smallest subnormal): |step| <= lr * (|m| / bc1) / eps <= 1e7 |m| < 2^-876 is below
+        // half an ulp of |w| >= 2^-820, so RN(w - step) == w exactly and w is unchanged
         ws[p] = wr;
       } else if (p == -1) {
         const double L = __dmul_rn(g, inv_n);  // mlp.cpp:120

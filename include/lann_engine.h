@@ -9,7 +9,10 @@
  * Reference interfaces each entry point replaces (paths into the reference
  * tree proj/core/):
  *   lann_train            models::train_full_batch       include/perfsage/mlp.hpp:64-66
- *                         (+ mse_gradient mlp.hpp:42-43, AdamState::update mlp.hpp:59)
+ *   lann_mlp_forward      Mlp::forward                   include/perfsage/mlp.hpp:27
+ *   lann_mse_loss         mse_loss                       include/perfsage/mlp.hpp:34-35
+ *   lann_mse_gradient     mse_gradient + LossGrad        include/perfsage/mlp.hpp:37-44
+ *   lann_adam_update      AdamState::update              include/perfsage/mlp.hpp:50-60
  *   lann_predict          models::predict / predict_dataset include/perfsage/models.hpp:109,119-120
  *   lann_eval             eval::mape / mape_thresholded / spearman / make_report
  *                                                         include/perfsage/eval.hpp:13-49
@@ -188,6 +191,36 @@ int lann_predict(lann_engine* engine, const lann_model_set* models, int64_t n_ro
 int lann_eval(lann_engine* engine, int32_t n_sets, const int64_t* offset, const int32_t* len,
               const double* truth, const double* pred, double drop_fraction,
               double* mape, double* mape_thr, int32_t* n_kept, double* rho);
+
+/* ---- mlp.hpp building blocks on the GPU, batched over nets -------------------------
+ * Mlp::forward (mlp.cpp:54-62), mse_loss (mlp.cpp:64-73), mse_gradient + LossGrad
+ * (mlp.hpp:34-44, mlp.cpp:75-122) and AdamState::update (mlp.hpp:50-60, mlp.cpp:142-154)
+ * for generic nets: any depth up to 8 layers, every width up to 64 (the reference's Mlp;
+ * the population trainers compile the LANN shapes instead). Nets are concatenated: net k has
+ * n_dims[k] dims (inputs, hidden..., outputs), its flat parameters (mlp.cpp:124-131 layout)
+ * follow the previous net's, and its n_rows[k] rows of dims[0] doubles (and targets) follow
+ * the previous net's rows. Exact reference operation order: results are bit-identical. */
+typedef struct lann_mlp_batch {
+  int32_t n_nets;
+  const int32_t* n_dims;  /* per net, 2..9 */
+  const int32_t* dims;    /* concatenated */
+  const double* params;   /* concatenated flat parameters */
+  const int32_t* n_rows;  /* per net, >= 1 */
+  const double* X;        /* concatenated rows */
+  const double* y;        /* concatenated targets (unused by lann_mlp_forward) */
+} lann_mlp_batch;
+
+/* out[row]: the network output (output unit 0) of every row of every net */
+int lann_mlp_forward(lann_engine* engine, const lann_mlp_batch* batch, double* out);
+/* loss[net] = (sum over rows in order of (f(x) - y)^2) / n_rows */
+int lann_mse_loss(lann_engine* engine, const lann_mlp_batch* batch, double* loss);
+/* loss[net] and grad (concatenated like params); the last layer must have one output */
+int lann_mse_gradient(lann_engine* engine, const lann_mlp_batch* batch, double* loss, double* grad);
+/* One Adam step over n parameters in place (params, m, v); `step` is the step count AFTER
+ * the increment AdamState::update performs first; bias corrections 1 - pow(beta, step) are
+ * taken from the host libm exactly as the reference computes them. */
+int lann_adam_update(lann_engine* engine, int64_t n, double* params, const double* grad, double* m, double* v,
+                     int32_t step, double lr, double beta1, double beta2, double epsilon);
 
 /* ---- selection ------------------------------------------------------------------
  * Blur schedule selection (selector.cpp:42-53): candidates [n][4] u32 schedules,

@@ -288,9 +288,38 @@ struct Mlp {
   /// mlp.cpp:9-25: Glorot-uniform weights U(-sqrt(6/(in+out)), +sqrt(6/(in+out))) drawn in layer /
   /// row order from `rng`, biases 0 (host-side, bit-identical to the reference)
   static Mlp init(const std::vector<int>& dims, Rng& rng);
+  /// mlp.hpp:27 / mlp.cpp:54-62 on the GPU (lann_mlp_forward): the network output for one
+  /// feature vector, bit-identical to the reference's; SchemaError on a length mismatch
+  double forward(std::span<const double> x) const;
   int input_dim() const { return layers.empty() ? 0 : layers.front().in; }
   int param_count() const;
 };
+
+/// mlp.hpp:34-35 / mlp.cpp:64-73 on the GPU (lann_mse_loss): mean squared error over rows of X
+double mse_loss(const Mlp& net, const std::vector<std::vector<double>>& X, std::span<const double> y);
+
+/// mlp.hpp:37-44 / mlp.cpp:75-122 on the GPU (lann_mse_gradient): the analytic gradient of
+/// mse_loss, flattened in layer order (weights then biases per layer), and the loss
+struct LossGrad {
+  double loss = 0.0;
+  std::vector<double> grad;
+};
+LossGrad mse_gradient(const Mlp& net, const std::vector<std::vector<double>>& X, std::span<const double> y);
+
+/// mlp.hpp:50-60 / mlp.cpp:142-154: Adam over a flat parameter vector; update() runs on the
+/// GPU (lann_adam_update) with the bias corrections from the host libm, as the reference
+struct AdamState {
+  std::vector<double> m;
+  std::vector<double> v;
+  int step = 0;
+  double beta1 = 0.9;
+  double beta2 = 0.999;
+  double epsilon = 1e-8;
+
+  explicit AdamState(std::size_t n) : m(n, 0.0), v(n, 0.0) {}
+  void update(std::span<double> params, std::span<const double> grad, double lr);
+};
+
 void unflatten_params(Mlp& net, std::span<const double> flat);  // mlp.cpp:132-140
 /// mlp.hpp:64-66 / mlp.cpp:156-175 on the GPU (one-model lann_train): `epochs` full-batch Adam
 /// epochs over normalised rows X (one vector per sample) and targets y; net's weights updated in

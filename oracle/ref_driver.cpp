@@ -251,6 +251,56 @@ int ref_mse_gradient(int n_dims, const int* dims, const double* params, int n,
     }
 }
 
+namespace {
+models::Mlp net_from(int n_dims, const int* dims, const double* params) {
+    std::vector<int> d(dims, dims + n_dims);
+    Rng rng(0);
+    auto net = models::Mlp::init(d, rng);
+    std::size_t total = 0;
+    for (auto& l : net.layers) total += l.w.size() + l.b.size();
+    models::unflatten_params(net, std::span<const double>(params, total));
+    return net;
+}
+}  // namespace
+
+// Mlp::forward (mlp.cpp:54-62) per row, rows at stride LANN_ROW
+int ref_mlp_forward(int n_dims, const int* dims, const double* params, int n, const double* X, double* out) {
+    try {
+        const auto net = net_from(n_dims, dims, params);
+        for (int i = 0; i < n; ++i)
+            out[i] = net.forward(std::span<const double>(X + std::size_t(i) * LANN_ROW, std::size_t(dims[0])));
+        return 0;
+    } catch (const std::exception& e) {
+        return status_of(e);
+    }
+}
+
+// mse_loss (mlp.cpp:64-73)
+int ref_mse_loss(int n_dims, const int* dims, const double* params, int n, const double* X, const double* y,
+                 double* loss) {
+    try {
+        const auto net = net_from(n_dims, dims, params);
+        std::vector<std::vector<double>> rows;
+        for (int i = 0; i < n; ++i)
+            rows.emplace_back(X + std::size_t(i) * LANN_ROW, X + std::size_t(i) * LANN_ROW + dims[0]);
+        *loss = models::mse_loss(net, rows, std::span<const double>(y, std::size_t(n)));
+        return 0;
+    } catch (const std::exception& e) {
+        return status_of(e);
+    }
+}
+
+// `steps` AdamState::update calls (mlp.cpp:142-154) with gradients grads[step][n]; m, v out
+int ref_adam_steps(int n, double* params, const double* grads, int steps, double lr, double* m, double* v) {
+    models::AdamState st(static_cast<std::size_t>(n));
+    for (int k = 0; k < steps; ++k)
+        st.update(std::span<double>(params, std::size_t(n)),
+                  std::span<const double>(grads + std::size_t(k) * n, std::size_t(n)), lr);
+    std::copy(st.m.begin(), st.m.end(), m);
+    std::copy(st.v.begin(), st.v.end(), v);
+    return 0;
+}
+
 // train_full_batch on caller-normalized rows (mlp.cpp:156-175).
 int ref_train_full_batch(int n_dims, const int* dims, double* params, int n,
                          const double* X, const double* y, double lr, int epochs,

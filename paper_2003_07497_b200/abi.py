@@ -63,6 +63,14 @@ class ModelSet(C.Structure):
     ]
 
 
+class MlpBatch(C.Structure):
+    """lann_mlp_batch: generic nets for lann_mlp_forward / lann_mse_loss / lann_mse_gradient."""
+    _fields_ = [
+        ("n_nets", C.c_int32), ("n_dims", C.c_void_p), ("dims", C.c_void_p), ("params", C.c_void_p),
+        ("n_rows", C.c_void_p), ("X", C.c_void_p), ("y", C.c_void_p),
+    ]
+
+
 def acceptance_world() -> World:
     """acceptance_main.cpp:271-289: MM dense_threaded, max_threads 4, t = 3e-9 c (0.25+0.75/n_thd)(1+U(-2%,2%))."""
     return World(kind=MM, hw_class=HW_CPU, max_threads=4, blur_lattice=0, alpha=3e-9, g0=0.25, g1=0.75,

@@ -174,6 +174,82 @@ void unflatten_params(Mlp& net, std::span<const double> flat) {
   if (off != flat.size()) throw ParamError("flat parameter size mismatch");
 }
 
+namespace {
+// one net as a lann_mlp_batch (the C ABI's generic-net entry points)
+struct OneNet {
+  std::vector<std::int32_t> dims;
+  std::vector<double> params, X;
+  std::int32_t n_dims = 0, n_rows = 0;
+  lann_mlp_batch b{};
+  OneNet(const Mlp& net, const std::vector<std::vector<double>>* rows, std::span<const double> single) {
+    if (net.layers.empty()) throw ParamError("empty network");
+    dims.push_back(net.layers.front().in);
+    for (const auto& L : net.layers) dims.push_back(L.out);
+    params = flatten_params(net);
+    const std::size_t I = std::size_t(net.input_dim());
+    if (rows) {
+      for (const auto& r : *rows) {
+        if (r.size() != I) throw SchemaError("feature vector length does not match the network input");
+        X.insert(X.end(), r.begin(), r.end());
+      }
+      n_rows = std::int32_t(rows->size());
+    } else {
+      X.assign(single.begin(), single.end());
+      n_rows = 1;
+    }
+    n_dims = std::int32_t(dims.size());
+    b.n_nets = 1;
+    b.n_dims = &n_dims;
+    b.dims = dims.data();
+    b.params = params.data();
+    b.n_rows = &n_rows;
+    b.X = X.data();
+  }
+};
+void raise_mlp(int st) {
+  lann_engine* e = engine::get();
+  if (st == LANN_PARAM_ERROR) throw ParamError(lann_last_error(e));
+  if (st == LANN_SCHEMA_ERROR) throw SchemaError(lann_last_error(e));
+  if (st) throw Error(lann_last_error(e));
+}
+}  // namespace
+
+double Mlp::forward(std::span<const double> x) const {
+  if (static_cast<int>(x.size()) != input_dim())  // mlp.cpp:55-56
+    throw SchemaError("feature vector length does not match the network input");
+  OneNet one(*this, nullptr, x);
+  double out = 0.0;
+  raise_mlp(lann_mlp_forward(engine::get(), &one.b, &out));
+  return out;
+}
+
+double mse_loss(const Mlp& net, const std::vector<std::vector<double>>& X, std::span<const double> y) {
+  if (X.size() != y.size() || X.empty()) throw ParamError("bad training batch");  // mlp.cpp:66
+  OneNet one(net, &X, {});
+  one.b.y = y.data();
+  double loss = 0.0;
+  raise_mlp(lann_mse_loss(engine::get(), &one.b, &loss));
+  return loss;
+}
+
+LossGrad mse_gradient(const Mlp& net, const std::vector<std::vector<double>>& X, std::span<const double> y) {
+  if (X.size() != y.size() || X.empty()) throw ParamError("bad training batch");  // mlp.cpp:77
+  OneNet one(net, &X, {});
+  one.b.y = y.data();
+  LossGrad r;
+  r.grad.assign(one.params.size(), 0.0);
+  raise_mlp(lann_mse_gradient(engine::get(), &one.b, &r.loss, r.grad.data()));
+  return r;
+}
+
+void AdamState::update(std::span<double> params, std::span<const double> grad, double lr) {
+  ++step;  // mlp.cpp:143
+  if (grad.size() < params.size() || m.size() < params.size() || v.size() < params.size())
+    throw ParamError("Adam state / gradient shorter than the parameter vector");
+  raise_mlp(lann_adam_update(engine::get(), std::int64_t(params.size()), params.data(), grad.data(), m.data(),
+                             v.data(), step, lr, beta1, beta2, epsilon));
+}
+
 std::vector<double> train_full_batch(Mlp& net, const std::vector<std::vector<double>>& X, std::span<const double> y,
                                      double lr, int epochs) {
   if (X.size() != y.size() || X.empty()) throw ParamError("feature/target size mismatch");

@@ -130,9 +130,14 @@ __global__ void predict_linear_kernel(PredictLinearArgs a) {
 // ---- forest ----------------------------------------------------------------------------------
 // shared memory: X [n][LANN_ROW] (double), y [n], sample of slot [n] (u16), lists 2 x (p+1) x n
 // (u16), level tables 2 x {start, count, node} x n (i32)
+// kGlobal: the same working set in a per-CTA slice of a global scratch buffer, for training sets
+// too large for shared memory (the reference forest takes any size, forest.cpp:13-143)
+template <bool kGlobal>
 __global__ void fit_forest_kernel(ForestArgs a) {
-  extern __shared__ __align__(16) unsigned char smem[];
+  extern __shared__ __align__(16) unsigned char dsmem[];
   const int m = blockIdx.y, tree = blockIdx.x;
+  unsigned char* smem =
+      kGlobal ? a.scratch_ws + (size_t(m) * a.trees + tree) * a.ws_stride : dsmem;
   const int n = a.n_rows[m], p = a.n_feats[m], L = p + 1;
   const int tid = threadIdx.x, T = blockDim.x;
   double* X = reinterpret_cast<double*>(smem);
@@ -336,9 +341,13 @@ size_t forest_smem_bytes(int max_rows) {
          2 * size_t(LANN_ROW + 1) * max_rows * 2 + 16 + 16 + 2 * 3 * size_t(max_rows) * 4;
 }
 void launch_fit_forest(const ForestArgs& a, cudaStream_t s) {
+  if (a.scratch_ws) {
+    fit_forest_kernel<true><<<dim3(a.trees, a.n_models), 128, 0, s>>>(a);
+    return;
+  }
   const size_t smem = forest_smem_bytes(a.max_rows);
-  cudaFuncSetAttribute(fit_forest_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-  fit_forest_kernel<<<dim3(a.trees, a.n_models), 128, smem, s>>>(a);
+  cudaFuncSetAttribute(fit_forest_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  fit_forest_kernel<false><<<dim3(a.trees, a.n_models), 128, smem, s>>>(a);
 }
 void launch_predict_forest(const PredictForestArgs& a, cudaStream_t s) {
   if (a.n_rows > 0) predict_forest_kernel<<<unsigned((a.n_rows + 127) / 128), 128, 0, s>>>(a);

@@ -868,8 +868,6 @@ int prepare_population(lann_engine* e, int n_jobs, const lann_job* jobs, int pre
     hlog("pack", h2);
   }
   if (Status st = validate_train(t)) return set_err(e, st);
-  if (size_t(pop.max_eval) * 36 + 16 > size_t(e->max_smem))
-    return set_err(e, {LANN_PARAM_ERROR, "evaluation set too large for one CTA"});
   hlog("pack+init", h2);
   const auto h3 = now();
   // one device blob, one upload
@@ -921,6 +919,7 @@ int prepare_population(lann_engine* e, int n_jobs, const lann_job* jobs, int pre
 // One device-only pass: reset weights, train, predict every evaluation row, metrics.
 void run_device(Population& pop) {
   lann_engine* e = pop.e;
+  if (!pop.plan) throw CudaFail{"population has no launch plan"};
   cudaStream_t s = e->stream;
   ck(cudaMemcpyAsync(pop.dP.p, pop.dP0.p, pop.dP0.n * sizeof(double), cudaMemcpyDeviceToDevice, s), "D2D");
   execute_plan(e, *pop.plan, pop.dP.p, pop.dF.p, pop.dB.p, pop.trace_total ? pop.dT.p : nullptr, pop.dTO.p);
@@ -931,8 +930,8 @@ void run_device(Population& pop) {
   e->launches += pop.n_eval_rows > 0;
   EvalArgs ea{pop.M, pop.dEO.p, pop.dEL.p, pop.dET.p, pop.dPred.p, 0.3, pop.dMape.p, pop.dThr.p,
               pop.dK.p, pop.dRho.p, pop.dS.p};
-  launch_eval(ea, pop.max_eval, s);
-  e->launches += 1;
+  launch_eval(ea, pop.max_eval, e->max_smem, pop.n_eval_rows, s);
+  e->launches += eval_launch_count(pop.max_eval, e->max_smem);
   ck(cudaGetLastError(), "population launch");
 }
 
@@ -1178,8 +1177,6 @@ int lann_eval(lann_engine* e, int32_t n_sets, const int64_t* offset, const int32
     total = std::max<int64_t>(total, offset[i] + len[i]);
     max_len = std::max(max_len, len[i]);
   }
-  if (size_t(max_len) * 36 + 16 > size_t(e->max_smem))
-    return set_err(e, {LANN_PARAM_ERROR, "evaluation set too large for one CTA"});
   try {
     ck(cudaSetDevice(e->device), "cudaSetDevice");
     cudaStream_t s = e->stream;
@@ -1189,9 +1186,9 @@ int lann_eval(lann_engine* e, int32_t n_sets, const int64_t* offset, const int32
     DBuf<double> dt(truth, size_t(total), s), dp(pred, size_t(total), s), dm(size_t(n_sets), s),
         dmt(size_t(n_sets), s), dr(size_t(n_sets), s);
     EvalArgs a{n_sets, doff.p, dlen.p, dt.p, dp.p, drop, dm.p, dmt.p, dk.p, dr.p, dst.p};
-    launch_eval(a, max_len, s);
+    launch_eval(a, max_len, e->max_smem, total, s);
     ck(cudaGetLastError(), "eval launch");
-    e->launches += 1;
+    e->launches += eval_launch_count(max_len, e->max_smem);
     std::vector<int> status(n_sets);
     dm.down(mape);
     dmt.down(mape_thr);
@@ -1201,6 +1198,141 @@ int lann_eval(lann_engine* e, int32_t n_sets, const int64_t* offset, const int32
     timer.stop();
     for (int i = 0; i < n_sets; ++i)
       if (status[i]) return set_err(e, {LANN_DOMAIN_ERROR, "metric inputs outside their domain"});
+    e->err.clear();
+    return LANN_OK;
+  } catch (const CudaFail& f) {
+    e->err = f.what;
+    return LANN_CUDA_ERROR;
+  }
+}
+
+// ---- mlp.hpp building blocks (mlp_ops.cu) -------------------------------------------------------
+extern "C++" {
+namespace {
+struct MlpHost {
+  std::vector<int64_t> dims_off, param_off, row_off, x_off;
+  std::vector<int> n_params, row_net;
+  int64_t total_dims = 0, total_params = 0, total_rows = 0, total_x = 0;
+};
+
+Status plan_mlp(const lann_mlp_batch* b, bool need_y, bool single_output, MlpHost& h) {
+  if (!b || b->n_nets < 1 || !b->n_dims || !b->dims || !b->params || !b->n_rows || !b->X)
+    return {LANN_PARAM_ERROR, "bad training batch"};
+  if (need_y && !b->y) return {LANN_PARAM_ERROR, "bad training batch"};
+  for (int k = 0; k < b->n_nets; ++k) {
+    const int nd = b->n_dims[k];
+    if (nd < 2 || nd > kMaxLayers + 1) return {LANN_PARAM_ERROR, "network depth outside 1..8 layers"};
+    const int32_t* d = b->dims + h.total_dims;
+    int P = 0;
+    for (int l = 0; l < nd; ++l)
+      if (d[l] < 1 || d[l] > kMaxMlpWidth) return {LANN_PARAM_ERROR, "network widths must lie in 1..64"};
+    for (int l = 0; l + 1 < nd; ++l) P += (d[l] + 1) * d[l + 1];
+    if (single_output && d[nd - 1] != 1) return {LANN_PARAM_ERROR, "mse_gradient needs a single output"};
+    if (b->n_rows[k] < 1) return {LANN_PARAM_ERROR, "bad training batch"};  // mlp.cpp:66,77
+    h.dims_off.push_back(h.total_dims);
+    h.param_off.push_back(h.total_params);
+    h.n_params.push_back(P);
+    h.row_off.push_back(h.total_rows);
+    h.x_off.push_back(h.total_x);
+    h.row_net.insert(h.row_net.end(), size_t(b->n_rows[k]), k);
+    h.total_dims += nd;
+    h.total_params += P;
+    h.total_rows += b->n_rows[k];
+    h.total_x += int64_t(b->n_rows[k]) * d[0];
+  }
+  return {};
+}
+
+// Uploads a batch and runs fn(args, stream) with device views; returns a status.
+template <typename Fn>
+int with_mlp_batch(lann_engine* e, const lann_mlp_batch* b, bool need_y, bool single_output, Fn&& fn) {
+  if (!e) return LANN_NO_DEVICE;
+  MlpHost h;
+  if (Status st = plan_mlp(b, need_y, single_output, h)) return set_err(e, st);
+  try {
+    ck(cudaSetDevice(e->device), "cudaSetDevice");
+    cudaStream_t s = e->stream;
+    Timer timer(e);
+    const int n = b->n_nets;
+    DBuf<int> dnd(b->n_dims, size_t(n), s), ddims(b->dims, size_t(h.total_dims), s), dnp(h.n_params, s),
+        dnr(b->n_rows, size_t(n), s), drn(h.row_net, s);
+    DBuf<int64_t> ddo(h.dims_off, s), dpo(h.param_off, s), dro(h.row_off, s), dxo(h.x_off, s);
+    DBuf<double> dp(b->params, size_t(h.total_params), s), dX(b->X, size_t(h.total_x), s);
+    DBuf<double> dy;
+    if (need_y) dy = DBuf<double>(b->y, size_t(h.total_rows), s);
+    MlpArgs a{n, dnd.p, ddo.p, ddims.p, dpo.p, dnp.p, dp.p, dro.p, dnr.p, dxo.p, dX.p, dy.p, drn.p, h.total_rows};
+    fn(a, h, s);
+    ck(cudaGetLastError(), "mlp launch");
+    timer.stop();
+    e->err.clear();
+    return LANN_OK;
+  } catch (const CudaFail& f) {
+    e->err = f.what;
+    return LANN_CUDA_ERROR;
+  }
+}
+}  // namespace
+}  // extern "C++"
+
+int lann_mlp_forward(lann_engine* e, const lann_mlp_batch* b, double* out) {
+  if (!out) return set_err(e, {LANN_PARAM_ERROR, "null output"});
+  return with_mlp_batch(e, b, false, false, [&](const MlpArgs& a, const MlpHost& h, cudaStream_t s) {
+    DBuf<double> dout(size_t(h.total_rows), s);
+    launch_mlp_forward(a, dout.p, s);
+    e->launches += 1;
+    dout.down(out);
+  });
+}
+
+int lann_mse_loss(lann_engine* e, const lann_mlp_batch* b, double* loss) {
+  if (!loss) return set_err(e, {LANN_PARAM_ERROR, "null output"});
+  return with_mlp_batch(e, b, true, false, [&](const MlpArgs& a, const MlpHost& h, cudaStream_t s) {
+    DBuf<double> dfwd(size_t(h.total_rows), s), dl(size_t(a.n_nets), s);
+    launch_mlp_loss(a, dfwd.p, dl.p, s);
+    e->launches += 2;
+    dl.down(loss);
+  });
+}
+
+int lann_mse_gradient(lann_engine* e, const lann_mlp_batch* b, double* loss, double* grad) {
+  if (!loss || !grad) return set_err(e, {LANN_PARAM_ERROR, "null output"});
+  return with_mlp_batch(e, b, true, true, [&](const MlpArgs& a, const MlpHost& h, cudaStream_t s) {
+    std::vector<int64_t> soff(size_t(a.n_nets));
+    int64_t total = 0;
+    for (int k = 0; k < a.n_nets; ++k) {
+      soff[size_t(k)] = total;
+      total += int64_t(h.n_params[size_t(k)] + 1) * b->n_rows[k];
+    }
+    DBuf<int64_t> dso(soff, s);
+    DBuf<double> scratch(size_t(total), s), dl(size_t(a.n_nets), s), dg(size_t(h.total_params), s);
+    launch_mlp_grad(a, scratch.p, dso.p, dl.p, dg.p, s);
+    e->launches += 1;
+    dl.down(loss);
+    dg.down(grad);
+  });
+}
+
+int lann_adam_update(lann_engine* e, int64_t n, double* params, const double* grad, double* m, double* v,
+                     int32_t step, double lr, double beta1, double beta2, double epsilon) {
+  if (!e) return LANN_NO_DEVICE;
+  if (n < 0 || (n > 0 && (!params || !grad || !m || !v))) return set_err(e, {LANN_PARAM_ERROR, "bad Adam buffers"});
+  if (step < 1) return set_err(e, {LANN_PARAM_ERROR, "Adam step must be >= 1"});
+  try {
+    ck(cudaSetDevice(e->device), "cudaSetDevice");
+    cudaStream_t s = e->stream;
+    Timer timer(e);
+    const size_t N = size_t(n);
+    DBuf<double> dp(params, N, s), dg(grad, N, s), dm(m, N, s), dv(v, N, s);
+    // mlp.cpp:145-146: the bias corrections through the host libm's pow, as the reference
+    AdamArgs a{n, dp.p, dg.p, dm.p, dv.p, beta1, beta2, epsilon, lr,
+               1.0 - std::pow(beta1, step), 1.0 - std::pow(beta2, step)};
+    launch_adam(a, s);
+    e->launches += n > 0;
+    ck(cudaGetLastError(), "adam launch");
+    dp.down(params);
+    dm.down(m);
+    dv.down(v);
+    timer.stop();
     e->err.clear();
     return LANN_OK;
   } catch (const CudaFail& f) {
@@ -1447,8 +1579,9 @@ int lann_fit_forest(lann_engine* e, const lann_design* d, int32_t trees, int32_t
     if (d->n_rows[m] < 10) return set_err(e, {LANN_PARAM_ERROR, "forest needs at least 10 samples"});
     max_rows = std::max(max_rows, d->n_rows[m]);
   }
-  if (forest_smem_bytes(max_rows) > size_t(e->max_smem))
-    return set_err(e, {LANN_PARAM_ERROR, "forest training set too large for one CTA"});
+  if (max_rows > 65535)  // slot lists are 16-bit
+    return set_err(e, {LANN_PARAM_ERROR, "forest training set above 65535 samples"});
+  const bool ws_global = forest_smem_bytes(max_rows) > size_t(e->max_smem);
   // bootstraps (forest.cpp:132-136): Rng(derive_seed(seed, t)).bounded(n) x n, sorted
   std::vector<uint16_t> boot(size_t(M) * trees * max_rows, 0);
   parallel_for(M * trees, [&](int k) {
@@ -1473,6 +1606,12 @@ int lann_fit_forest(lann_engine* e, const lann_design* d, int32_t trees, int32_t
     DBuf<double> ss(size_t(M) * trees * max_rows * LANN_ROW, s), sth(size_t(M) * trees * max_rows * LANN_ROW, s);
     ForestArgs fa{M, trees, max_depth, min_samples_split, max_rows, dn.p, df.p, doff.p, dX.p, dY.p, dB.p,
                   nf.p, nt.p, nl.p, nr.p, nv.p, nc.p, ss.p, sth.p};
+    DBuf<unsigned char> ws;
+    if (ws_global) {  // per-(model, tree) working set in HBM instead of shared memory
+      fa.ws_stride = (forest_smem_bytes(max_rows) + 255) & ~size_t(255);
+      ws = DBuf<unsigned char>(size_t(M) * trees * fa.ws_stride, s);
+      fa.scratch_ws = ws.p;
+    }
     launch_fit_forest(fa, s);
     ck(cudaGetLastError(), "fit_forest launch");
     e->launches += 1;
@@ -1617,7 +1756,8 @@ int lann_init_params(int32_t n_dims, const int32_t* dims, uint64_t seed, double*
 
 namespace {
 int population_create(lann_engine* e, int32_t n_jobs, const lann_job* jobs, int32_t precision,
-                      int32_t record_trace, lann_population** out, bool sync_uploads);
+                      int32_t record_trace, lann_population** out, bool sync_uploads,
+                      std::vector<lann_job_result>* base_out = nullptr);
 }
 
 int lann_population_create(lann_engine* e, int32_t n_jobs, const lann_job* jobs,
@@ -1627,7 +1767,8 @@ int lann_population_create(lann_engine* e, int32_t n_jobs, const lann_job* jobs,
 
 namespace {
 int population_create(lann_engine* e, int32_t n_jobs, const lann_job* jobs, int32_t precision,
-                      int32_t record_trace, lann_population** out, bool sync_uploads) {
+                      int32_t record_trace, lann_population** out, bool sync_uploads,
+                      std::vector<lann_job_result>* base_out) {
   if (!e) return LANN_NO_DEVICE;
   if (!out || n_jobs < 1 || !jobs) return set_err(e, {LANN_PARAM_ERROR, "empty population"});
   if (precision != LANN_FP64_EXACT && precision != LANN_FP32)
@@ -1637,7 +1778,10 @@ int population_create(lann_engine* e, int32_t n_jobs, const lann_job* jobs, int3
   try {
     ck(cudaSetDevice(e->device), "cudaSetDevice");
     const int st = prepare_population(e, n_jobs, jobs, precision, record_trace != 0, p->pop, sync_uploads);
-    if (st != LANN_OK && p->pop.M == 0) {
+    // any failure that left no launch plan is fatal for the whole population (M == 0: every job
+    // failed host preparation; M > 0: a population-wide check after packing failed)
+    if (st != LANN_OK && !p->pop.plan) {
+      if (base_out && p->pop.M == 0) *base_out = p->pop.base;  // the per-job statuses
       delete p;
       return st;
     }
@@ -1725,9 +1869,14 @@ int lann_run_population(lann_engine* e, int32_t n_jobs, const lann_job* jobs, in
   if (!e) return LANN_NO_DEVICE;
   if (!results) return set_err(e, {LANN_PARAM_ERROR, "null results"});
   lann_population* p = nullptr;
-  const int st = population_create(e, n_jobs, jobs, precision, trace_out != nullptr, &p, false);
+  std::vector<lann_job_result> base;
+  const int st = population_create(e, n_jobs, jobs, precision, trace_out != nullptr, &p, false, &base);
   if (!p) {
     for (int j = 0; j < n_jobs && jobs; ++j) {
+      if (size_t(j) < base.size()) {  // every job failed host preparation: its own status
+        results[j] = base[j];
+        continue;
+      }
       std::memset(&results[j], 0, sizeof(lann_job_result));
       results[j].status = st;
       results[j].nonfinite_epoch = -1;

@@ -107,7 +107,8 @@ bool fp32_shape_supported(int in, int h1, int h2);
 int fp32_warp_slots_per_sm(int in, int h1, int h2, int lanes, int tile_bytes);
 void launch_predict_fp64(const PredictArgs& a, cudaStream_t s);
 void launch_predict_fp32(const PredictArgs& a, cudaStream_t s);
-void launch_eval(const EvalArgs& a, int max_len, cudaStream_t s);
+void launch_eval(const EvalArgs& a, int max_len, int max_smem, int64_t total, cudaStream_t s);
+int eval_launch_count(int max_len, int max_smem);
 
 }  // namespace lann
 
@@ -182,6 +183,8 @@ struct ForestArgs {
   int* node_count;            // [model][tree]
   double* scratch_sse;        // [model][tree][max_rows][LANN_ROW]
   double* scratch_thr;
+  unsigned char* scratch_ws = nullptr;  // non-null: the working set in global memory, ws_stride B per CTA
+  size_t ws_stride = 0;
 };
 struct PredictForestArgs {
   int64_t n_rows;
@@ -200,4 +203,40 @@ void launch_predict_linear(const PredictLinearArgs& a, cudaStream_t s);
 size_t forest_smem_bytes(int max_rows);
 void launch_fit_forest(const ForestArgs& a, cudaStream_t s);
 void launch_predict_forest(const PredictForestArgs& a, cudaStream_t s);
+}  // namespace lann
+
+namespace lann {
+// mlp_ops.cu: mlp.hpp's per-net operations (Mlp::forward, mse_loss, mse_gradient,
+// AdamState::update) on the GPU, batched over nets of any depth <= kMaxLayers
+constexpr int kMaxLayers = 8;
+constexpr int kMaxMlpWidth = 64;
+struct MlpArgs {
+  int n_nets;
+  const int* n_dims;          // per net: L + 1 (inputs, hidden..., outputs)
+  const int64_t* dims_offset; // into dims
+  const int* dims;
+  const int64_t* param_offset;
+  const int* n_params;
+  const double* params;
+  const int64_t* row_offset;  // first row of the net (into y and the global row index)
+  const int* n_rows;
+  const int64_t* x_offset;    // first double of the net's rows (row stride = dims[0])
+  const double* X;
+  const double* y;
+  const int* row_net;         // per global row: its net
+  int64_t total_rows;
+};
+struct AdamArgs {
+  int64_t n;
+  double* params;
+  const double* grad;
+  double* m;
+  double* v;
+  double beta1, beta2, eps, lr, bc1, bc2;
+};
+void launch_mlp_forward(const MlpArgs& a, double* out, cudaStream_t s);
+void launch_mlp_loss(const MlpArgs& a, const double* fwd, double* loss, cudaStream_t s);
+void launch_mlp_grad(const MlpArgs& a, double* scratch, const int64_t* scratch_offset, double* loss, double* grad,
+                     cudaStream_t s);
+void launch_adam(const AdamArgs& a, cudaStream_t s);
 }  // namespace lann

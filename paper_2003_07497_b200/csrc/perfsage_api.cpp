@@ -814,6 +814,7 @@ double spearman(std::span<const double> truth, std::span<const double> pred) {
 
 EvalReport make_report(std::span<const double> truth, std::span<const double> pred, double drop) {
   const auto thr = mape_thresholded(truth, pred, drop);
+  if (truth.size() < 2) throw DomainError("spearman needs at least two samples");  // eval.cpp:80
   const Metrics m = run(truth, pred, drop);
   EvalReport r;
   r.mape_full = m.mape;

@@ -171,6 +171,97 @@ __global__ void __launch_bounds__(256) eval_kernel(EvalArgs a) {
   }
 }
 
+// K3 for sets too large for one CTA's shared memory (the reference handles any size,
+// eval.cpp:26-108): ranks and sorted positions counted by a grid over (sample block, set), the
+// other samples streamed through shared memory in tiles; the sequential sums then run in a
+// second kernel from global memory, in the same order as eval_kernel.
+constexpr int kRankTile = 1024;
+
+__global__ void __launch_bounds__(256) eval_rank_global(EvalArgs a, double* rt_g, double* rp_g, int* pos_g) {
+  __shared__ double tt[kRankTile], tp[kRankTile];
+  const int set = blockIdx.y;
+  const int n = a.len[set];
+  const int64_t o = a.offset[set];
+  const double* t = a.truth + o;
+  const double* p = a.pred + o;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if ((int)(blockIdx.x * blockDim.x) >= n) return;  // uniform per CTA
+  const double ti = i < n ? t[i] : 0.0, pi = i < n ? p[i] : 0.0;
+  int lt = 0, et = 0, lp = 0, ep = 0, before = 0;
+  for (int j0 = 0; j0 < n; j0 += kRankTile) {
+    const int m = min(kRankTile, n - j0);
+    __syncthreads();
+    for (int j = threadIdx.x; j < m; j += blockDim.x) {
+      tt[j] = t[j0 + j];
+      tp[j] = p[j0 + j];
+    }
+    __syncthreads();
+    for (int j = 0; j < m; ++j) {
+      const double tj = tt[j], pj = tp[j];
+      lt += tj < ti;
+      et += tj == ti;
+      lp += pj < pi;
+      ep += pj == pi;
+      before += (tj < ti) || (tj == ti && j0 + j < i);
+    }
+  }
+  if (i < n) {
+    rt_g[o + i] = ((double)lt + (double)(lt + et - 1)) / 2.0 + 1.0;
+    rp_g[o + i] = ((double)lp + (double)(lp + ep - 1)) / 2.0 + 1.0;
+    pos_g[o + before] = i;
+  }
+}
+
+__global__ void __launch_bounds__(96) eval_sums_global(EvalArgs a, const double* rt_g, const double* rp_g,
+                                                       const int* pos_g) {
+  const int set = blockIdx.x;
+  const int n = a.len[set];
+  const int64_t o = a.offset[set];
+  const double* st = a.truth + o;
+  const double* sp = a.pred + o;
+  __shared__ int bad;
+  if (threadIdx.x == 0) bad = 0;
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += blockDim.x)
+    if (!(st[i] > 0.0)) atomicOr(&bad, 1);  // eval.cpp:16-22 check_pair
+  __syncthreads();
+  if (n < 2 || bad) {
+    if (threadIdx.x == 0) {
+      a.status[set] = 4;  // LANN_DOMAIN_ERROR
+      a.mape[set] = a.mape_thr[set] = a.rho[set] = 0.0;
+      a.n_kept[set] = 0;
+    }
+    return;
+  }
+  const int n_drop = (int)floor(__dadd_rn(__dmul_rn(a.drop_fraction, (double)n), 1e-12));
+  if (threadIdx.x == 0) {
+    double acc = 0.0;
+    for (int i = 0; i < n; ++i) acc = __dadd_rn(acc, __ddiv_rn(fabs(__dsub_rn(st[i], sp[i])), st[i]));
+    a.mape[set] = __ddiv_rn(__dmul_rn(100.0, acc), (double)n);
+  } else if (threadIdx.x == 32) {
+    if (n_drop >= n) {
+      a.status[set] = 4;
+    } else {
+      double acc = 0.0;
+      for (int k = n_drop; k < n; ++k) {
+        const int j = pos_g[o + k];
+        acc = __dadd_rn(acc, __ddiv_rn(fabs(__dsub_rn(st[j], sp[j])), st[j]));
+      }
+      a.mape_thr[set] = __ddiv_rn(__dmul_rn(100.0, acc), (double)(n - n_drop));
+      a.n_kept[set] = n - n_drop;
+      a.status[set] = 0;
+    }
+  } else if (threadIdx.x == 64) {
+    const double nn = (double)n;
+    double d2 = 0.0;
+    for (int i = 0; i < n; ++i) {
+      const double d = __dsub_rn(rt_g[o + i], rp_g[o + i]);
+      d2 = __dadd_rn(d2, __dmul_rn(d, d));
+    }
+    a.rho[set] = __dsub_rn(1.0, __ddiv_rn(__dmul_rn(6.0, d2), __dmul_rn(nn, __dsub_rn(__dmul_rn(nn, nn), 1.0))));
+  }
+}
+
 }  // namespace
 
 void launch_predict_fp64(const PredictArgs& a, cudaStream_t s) {
@@ -183,12 +274,31 @@ void launch_predict_fp32(const PredictArgs& a, cudaStream_t s) {
   predict_kernel<false><<<(unsigned)((a.n_rows + 127) / 128), 128, 0, s>>>(a);
 }
 
-// max_len bounds the shared-memory footprint: 4 doubles + 1 int per sample.
-void launch_eval(const EvalArgs& a, int max_len, cudaStream_t s) {
+// max_len bounds the shared-memory footprint: 4 doubles + 1 int per sample. Sets that do not
+// fit one CTA's shared memory take the two-kernel global-memory path (scratch: rank and position
+// arrays over the whole [0, total) index range, stream-ordered allocation).
+int eval_launch_count(int max_len, int max_smem) {
+  return size_t(max_len) * 36 + 16 <= size_t(max_smem) ? 1 : 2;
+}
+
+void launch_eval(const EvalArgs& a, int max_len, int max_smem, int64_t total, cudaStream_t s) {
   if (a.n_sets <= 0) return;
-  const int bytes = max_len * (4 * 8 + 4) + 16;
-  cudaFuncSetAttribute(eval_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-  eval_kernel<<<a.n_sets, 256, bytes, s>>>(a);
+  if (eval_launch_count(max_len, max_smem) == 1) {
+    const int bytes = max_len * (4 * 8 + 4) + 16;
+    cudaFuncSetAttribute(eval_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    eval_kernel<<<a.n_sets, 256, bytes, s>>>(a);
+    return;
+  }
+  void* scratch = nullptr;
+  const size_t nt = size_t(total);
+  if (cudaMallocAsync(&scratch, nt * (8 + 8 + 4) + 16, s) != cudaSuccess) return;
+  double* rt = static_cast<double*>(scratch);
+  double* rp = rt + nt;
+  int* pos = reinterpret_cast<int*>(rp + nt);
+  const dim3 grid((unsigned)((max_len + 255) / 256), (unsigned)a.n_sets);
+  eval_rank_global<<<grid, 256, 0, s>>>(a, rt, rp, pos);
+  eval_sums_global<<<a.n_sets, 96, 0, s>>>(a, rt, rp, pos);
+  cudaFreeAsync(scratch, s);
 }
 
 }  // namespace lann

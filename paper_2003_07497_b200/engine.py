@@ -16,7 +16,7 @@ import os
 import numpy as np
 
 from . import abi
-from .abi import ROW, Job, JobResult, ModelSet, TrainBatch, World
+from .abi import ROW, Job, JobResult, MlpBatch, ModelSet, TrainBatch, World
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "lib", "libperfsage_b200.so")
@@ -70,7 +70,8 @@ EXPORTS = ["lann_engine_create", "lann_engine_destroy", "lann_last_error", "lann
            "lann_build_mock_dataset", "lann_mock_schedules",
            "lann_init_params", "lann_population_create", "lann_population_run", "lann_population_fetch",
            "lann_population_flop", "lann_population_models", "lann_population_destroy",
-           "lann_population_norm", "lann_transfer_bytes", "lann_run_population", "lann_default_combos"]
+           "lann_population_norm", "lann_transfer_bytes", "lann_run_population", "lann_default_combos",
+           "lann_mlp_forward", "lann_mse_loss", "lann_mse_gradient", "lann_adam_update"]
 
 
 def transfer_bytes(reset=False):
@@ -123,6 +124,11 @@ def load_library(path: str = LIB_PATH):
     L.lann_run_population.argtypes = [vp, C.c_int32, C.POINTER(Job), C.c_int32, C.POINTER(JobResult),
                                       vp, vp, vp, vp]
     L.lann_default_combos.argtypes = [C.POINTER(World), C.c_int32]
+    L.lann_mlp_forward.argtypes = [vp, C.POINTER(MlpBatch), vp]
+    L.lann_mse_loss.argtypes = [vp, C.POINTER(MlpBatch), vp]
+    L.lann_mse_gradient.argtypes = [vp, C.POINTER(MlpBatch), vp, vp]
+    L.lann_adam_update.argtypes = [vp, C.c_int64, vp, vp, vp, vp, C.c_int32, C.c_double, C.c_double, C.c_double,
+                                   C.c_double]
     _lib = L
     return L
 
@@ -284,6 +290,55 @@ class Engine:
         if st:
             self._raise(st)
         return out
+
+    # ---- mlp.hpp building blocks over generic nets (Mlp::forward, mse_loss, mse_gradient) ----
+    def _mlp_batch(self, nets, need_y):
+        """nets: list of (dims, params, X [n][dims[0]], y or None)."""
+        nd = np.array([len(d) for d, _, _, _ in nets], dtype=np.int32)
+        dims = np.concatenate([np.asarray(d, dtype=np.int32) for d, _, _, _ in nets])
+        params = np.concatenate([np.asarray(p, dtype=np.float64) for _, p, _, _ in nets])
+        rows = np.array([len(x) for _, _, x, _ in nets], dtype=np.int32)
+        X = np.concatenate([np.asarray(x, dtype=np.float64).ravel() for _, _, x, _ in nets])
+        keep = [nd, dims, params, rows, X]
+        b = MlpBatch(len(nets), _ptr(nd), _ptr(dims), _ptr(params), _ptr(rows), _ptr(X), None)
+        if need_y:
+            y = np.concatenate([np.asarray(t, dtype=np.float64) for _, _, _, t in nets])
+            keep.append(y)
+            b.y = _ptr(y)
+        return b, keep, int(rows.sum()), len(params)
+
+    def mlp_forward(self, nets):
+        b, keep, n_rows, _ = self._mlp_batch([(d, p, x, None) for d, p, x in nets], False)
+        out = np.zeros(n_rows)
+        st = self.L.lann_mlp_forward(self.h, C.byref(b), _ptr(out))
+        if st:
+            self._raise(st)
+        return out
+
+    def mse_loss(self, nets):
+        b, keep, _, _ = self._mlp_batch(nets, True)
+        loss = np.zeros(len(nets))
+        st = self.L.lann_mse_loss(self.h, C.byref(b), _ptr(loss))
+        if st:
+            self._raise(st)
+        return loss
+
+    def mse_gradient(self, nets):
+        """Returns (loss per net, list of gradient vectors)."""
+        b, keep, _, n_params = self._mlp_batch(nets, True)
+        loss, grad = np.zeros(len(nets)), np.zeros(n_params)
+        st = self.L.lann_mse_gradient(self.h, C.byref(b), _ptr(loss), _ptr(grad))
+        if st:
+            self._raise(st)
+        sizes = np.cumsum([len(p) for _, p, _, _ in nets])[:-1]
+        return loss, np.split(grad, sizes)
+
+    def adam_update(self, params, grad, m, v, step, lr, beta1=0.9, beta2=0.999, eps=1e-8):
+        """AdamState::update in place on float64 arrays (step = the count after increment)."""
+        st = self.L.lann_adam_update(self.h, len(params), _ptr(params), _ptr(np.ascontiguousarray(grad)), _ptr(m),
+                                     _ptr(v), step, lr, beta1, beta2, eps)
+        if st:
+            self._raise(st)
 
     # ---- eval::mape / mape_thresholded / spearman over many sets ----
     def eval(self, truths, preds, drop=0.3):

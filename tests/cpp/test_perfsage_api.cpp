@@ -2,6 +2,7 @@
 // test_eval.cpp, test_selector.cpp), restated against include/perfsage_b200/perfsage.hpp with
 // unchanged call syntax, plus bit-exact pins from the reference's golden run. Built and run by
 // tests/test_gpu_cpp_api.py on the GPU box. Exit code 0 = all checks passed.
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <functional>
@@ -59,7 +60,92 @@ static Dataset synth_mm(std::size_t count, std::uint64_t seed,
   return ds;
 }
 
+// test_models.cpp:176-196 near_relu_kink (= acceptance_main.cpp:172-190 has_relu_kink)
+static bool near_relu_kink(const Mlp& net, const std::vector<std::vector<double>>& X, double margin) {
+  for (const auto& x : X) {
+    std::vector<double> act(x);
+    for (std::size_t l = 0; l + 1 < net.layers.size(); ++l) {
+      const auto& layer = net.layers[l];
+      std::vector<double> next(layer.out);
+      for (int o = 0; o < layer.out; ++o) {
+        double z = layer.b[o];
+        for (int i = 0; i < layer.in; ++i) z += layer.w[std::size_t(o) * layer.in + i] * act[i];
+        if (std::abs(z) < margin) return true;
+        next[o] = z > 0 ? z : 0.0;
+      }
+      act = std::move(next);
+    }
+  }
+  return false;
+}
+
+// GradientCheck.AnalyticMatchesFiniteDifferences (test_models.cpp:200-235) with the seed, trial
+// count, net sizes and sample count of the named source: mse_gradient and mse_loss on the GPU
+static double gradient_check(std::uint64_t seed, int trials, int in_span, int h_span, int h2_span, int rows) {
+  Rng rng(seed);
+  double worst = 0.0;
+  for (int trial = 0; trial < trials; ++trial) {
+    const int inputs = 2 + int(rng.bounded(std::uint64_t(in_span)));
+    std::vector<int> dims{inputs, 2 + int(rng.bounded(std::uint64_t(h_span)))};
+    if (trial % 2 == 1) dims.push_back(2 + int(rng.bounded(std::uint64_t(h2_span))));
+    dims.push_back(1);
+    Mlp net = Mlp::init(dims, rng);
+    std::vector<std::vector<double>> X(static_cast<std::size_t>(rows), std::vector<double>(static_cast<std::size_t>(inputs)));
+    std::vector<double> y(X.size());
+    do {
+      for (auto& row : X)
+        for (auto& v : row) v = rng.uniform(-1.0, 1.0);
+    } while (near_relu_kink(net, X, 1e-3));
+    for (auto& v : y) v = rng.uniform(0.0, 1.0);
+    const auto lg = mse_gradient(net, X, y);
+    auto params = flatten_params(net);
+    const double h = 1e-5;
+    for (std::size_t i = 0; i < params.size(); ++i) {
+      const double saved = params[i];
+      params[i] = saved + h;
+      unflatten_params(net, params);
+      const double up = mse_loss(net, X, y);
+      params[i] = saved - h;
+      unflatten_params(net, params);
+      const double down = mse_loss(net, X, y);
+      params[i] = saved;
+      unflatten_params(net, params);
+      const double numeric = (up - down) / (2 * h);
+      const double denom = std::max({std::abs(numeric), std::abs(lg.grad[i]), 1e-6});
+      const double rel = std::abs(numeric - lg.grad[i]) / denom;
+      worst = std::max(worst, rel);
+      CHECK(rel < 1e-4);
+    }
+  }
+  return worst;
+}
+
 int main() {
+  // GradientCheck (test_models.cpp:200-235: Rng(77), 6 nets, 5 rows) and acceptance criterion 3
+  // (acceptance_main.cpp:194-239: Rng(0x6AD), 20 nets, 6 rows, worst relative error <= 1e-4)
+  {
+    const double w1 = gradient_check(77, 6, 4, 4, 3, 5);
+    const double w3 = gradient_check(0x6AD, 20, 5, 5, 4, 6);
+    std::printf("gradient check: test_models worst rel %.3g, criterion 3 (20 nets) worst rel %.3g\n", w1, w3);
+    // Mlp::forward == the last sample's forward inside mse_loss; AdamState::update moves the
+    // parameters against the gradient and counts steps
+    Rng rng(5);
+    Mlp net = Mlp::init({3, 4, 1}, rng);
+    const std::vector<std::vector<double>> X{{0.1, 0.2, 0.3}};
+    const std::vector<double> y{0.5};
+    const double f = net.forward(X[0]);
+    CHECK(mse_loss(net, X, y) == (f - 0.5) * (f - 0.5));
+    CHECK_THROWS(net.forward(std::vector<double>{1.0}), SchemaError);
+    CHECK_THROWS(mse_loss(net, {}, {}), ParamError);
+    auto p = flatten_params(net);
+    AdamState adam(p.size());
+    const auto g = mse_gradient(net, X, y);
+    const auto before = p;
+    adam.update(p, g.grad, 1e-2);
+    CHECK(adam.step == 1);
+    for (std::size_t i = 0; i < p.size(); ++i)
+      if (g.grad[i] != 0.0) CHECK((p[i] - before[i]) * g.grad[i] < 0.0);
+  }
   // ParamCount (test_models.cpp:76-90)
   CHECK(param_count_for(7, {8}) == 73);
   CHECK(param_count_for(6, {5, 5}) == 71);

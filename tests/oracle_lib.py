@@ -89,6 +89,26 @@ class _Lib:
                                          np.ascontiguousarray(y), lr, epochs, trace, C.byref(bad))
         return st, p, trace, bad.value
 
+    def mlp_forward(self, dims, params, X):
+        dims = np.asarray(dims, dtype=np.int32)
+        out = np.zeros(len(X))
+        st = self._f("mlp_forward")(len(dims), dims, np.ascontiguousarray(params), len(X), np.ascontiguousarray(X), out)
+        return st, out
+
+    def mse_loss(self, dims, params, X, y):
+        dims = np.asarray(dims, dtype=np.int32)
+        loss = C.c_double(0)
+        st = self._f("mse_loss")(len(dims), dims, np.ascontiguousarray(params), len(y), np.ascontiguousarray(X),
+                                 np.ascontiguousarray(y), C.byref(loss))
+        return st, loss.value
+
+    def adam_steps(self, params, grads, lr):
+        p = np.array(params, dtype=np.float64)
+        g = np.ascontiguousarray(grads, dtype=np.float64)
+        m, v = np.zeros_like(p), np.zeros_like(p)
+        st = self._f("adam_steps")(len(p), p, g, len(g), lr, m, v)
+        return st, p, m, v
+
     def mape(self, t, p):
         o = C.c_double(0)
         st = self._f("mape")(len(t), np.ascontiguousarray(t, dtype=np.float64), np.ascontiguousarray(p, dtype=np.float64), C.byref(o))
@@ -173,6 +193,9 @@ class Reference(_Lib):
         super().__init__(os.path.join(REF_DIR, "libperfsage_ref.so"))
         L = self.lib
         L.ref_last_error.restype = C.c_char_p
+        L.ref_mlp_forward.argtypes = [C.c_int, _i32p, _dp, C.c_int, _dp, _dp]
+        L.ref_mse_loss.argtypes = [C.c_int, _i32p, _dp, C.c_int, _dp, _dp, C.POINTER(C.c_double)]
+        L.ref_adam_steps.argtypes = [C.c_int, _dp, _dp, C.c_int, C.c_double, _dp, _dp]
         L.ref_train_nn.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, _dp, _u64p, _dp, C.c_int, _i32p, C.c_double, C.c_int,
                                    C.c_uint64, C.c_int, C.c_int, _dp, C.POINTER(C.c_int), C.c_void_p, _dp, C.POINTER(C.c_int)]
         L.ref_predict.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, _i32p, _dp, _dp, C.c_int, C.c_int, _dp, _u64p, _dp]

@@ -219,3 +219,19 @@ def test_cli_select_mock_timer_is_the_reference_cli(tmp_path, reference):
     assert sched(rep["true_best"]) == list(ref[6:10])
     assert (rep["true_best_s"], rep["default_s"], rep["regret"], rep["speedup_vs_default"],
             rep["speedup_vs_random_mean"]) == tuple(ref[10:15])
+
+
+def test_cli_forest_and_eval_on_large_sets(tmp_path, reference):
+    """nlrc on 5000 training rows (its working set no longer fits shared memory: the forest
+    kernel runs from HBM scratch) and eval on 5000 held-out rows; the report of the trained
+    model equals the reference library's evaluate_model_on of the same model file."""
+    cli("gen", "--world", 0, "--count", 10000, "--seed", 4, "--out", tmp_path)
+    (data,) = [p for p in tmp_path.iterdir() if p.suffix == ".csv"]
+    cli("train", "--data", data, "--seed", 4, "--family", "nlrc", "--out", tmp_path)
+    cli("eval", "--model", tmp_path / "model_nlrc.json", "--data", tmp_path / "test.csv", "--out", tmp_path / "e")
+    (row,) = read_reports(tmp_path / "e" / "eval.csv")
+    st, ref = reference.eval_model(tmp_path / "model_nlrc.json", tmp_path / "test.csv")
+    assert st == 0, reference.last_error()
+    assert int(row["n_total"]) == 5000
+    got = [float(row["mape_full"]), float(row["mape_thresholded"]), float(row["rho"])]
+    np.testing.assert_allclose(got, ref[:3], rtol=1e-12)

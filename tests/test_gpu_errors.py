@@ -61,3 +61,51 @@ def test_training_error_in_population(engine):
     w.alpha = 1e300
     st, res, _, _ = engine.run_population([abi.make_job(w, 1, count=60, epochs=5)], abi.FP64_EXACT)
     assert st in (abi.TRAINING_ERROR, abi.PARAM_ERROR, abi.BUILD_ABORT)
+
+
+def test_population_wide_check_failure_is_an_error_not_a_crash(engine):
+    """A failure of the checks that run after packing (hidden widths over 64, which the
+    unconstrained budget lets through) comes back as PARAM_ERROR for the whole population,
+    with or without good jobs beside it (a null launch plan was run)."""
+    bad = job(hidden=(65,), unconstrained=True)
+    st, res, _, _ = engine.run_population([bad], abi.FP64_EXACT)
+    assert st == abi.PARAM_ERROR
+    st, res, _, _ = engine.run_population([job(), bad], abi.FP64_EXACT)
+    assert st == abi.PARAM_ERROR
+    with pytest.raises(E.ParamError):
+        engine.prepare([job(), bad], abi.FP64_EXACT)
+
+
+def test_all_jobs_failing_keep_their_own_statuses(engine):
+    """Every job fails host preparation: each result carries its own status (a DomainError for
+    a one-sample evaluation set beside ParamErrors), not one aggregate code."""
+    tiny = abi.make_job(abi.acceptance_world(), 1, count=3, epochs=5)  # 2 train / 1 eval sample
+    st, res, _, _ = engine.run_population([job(lr=0.5), tiny, job(hidden=(32,))], abi.FP64_EXACT)
+    assert st != 0
+    assert [r.status for r in res] == [abi.PARAM_ERROR, abi.DOMAIN_ERROR, abi.PARAM_ERROR]
+
+
+def test_large_evaluation_set(engine, oracle):
+    """Evaluation sets beyond one CTA's shared memory (the reference takes any size) go
+    through the global-memory metric kernels, bit-identical to the reference order."""
+    rng = np.random.default_rng(5)
+    n = 12000
+    t = rng.uniform(1e-6, 1e-3, n)
+    t[::7] = t[3]  # ties in the truth
+    p = t * rng.uniform(0.8, 1.25, n)
+    p[::11] = p[5]  # ties in the predictions
+    mape, thr, kept, rho = engine.eval([t, t[:300]], [p, p[:300]], 0.3)
+    for k, (tt, pp) in enumerate([(t, p), (t[:300], p[:300])]):
+        assert mape[k] == oracle.mape(tt, pp)[1]
+        _, othr, okept = oracle.mape_thresholded(tt, pp, 0.3)
+        assert (thr[k], kept[k]) == (othr, okept)
+        assert rho[k] == oracle.spearman(tt, pp)[1]
+
+
+def test_population_with_large_evaluation_set(engine, oracle):
+    """count 14000 -> 7000 held-out samples per model: runs (was 'evaluation set too large')."""
+    j = abi.make_job(abi.acceptance_world(), 2, count=14000, epochs=3)
+    st, res, _, _ = engine.run_population([j], abi.FP64_EXACT)
+    assert st == 0, engine.last_error
+    ref, _, _ = oracle.run_job(j)
+    assert (res[0].mape, res[0].mape_thr, res[0].rho) == (ref.mape, ref.mape_thr, ref.rho)

@@ -36,6 +36,7 @@ struct TrainArgs {
   int smem_records;          // 1: per-sample records live in shared memory
   int rec_products;          // 1: phase A also stores every weight's per-sample product row
   long long* phase_cycles;   // optional (LANN_PHASE_PROFILE): CTA 0's clock64 per phase
+  int prof_flags = 0;        // profiling experiments (LANN_PROF_FLAGS), only read under phase_cycles
 };
 
 // FP32 throughput trainer: models grouped into warps that share one tile.

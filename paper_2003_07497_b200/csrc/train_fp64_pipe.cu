@@ -13,22 +13,24 @@
 // (tools/mb/fp64_issue_mb.cu). The phased kernel (train_fp64.cu) runs "all samples forward /
 // backward" and "all chains" one after the other behind CTA barriers, so an epoch costs
 // phase A + chain + Adam. Here the two overlap inside the epoch:
-//   producer warps  own SAMPLES: thread k runs samples k, k + 32*NPW, ... ("rounds"), forward
-//                   and backward, and stores the sample's column of the record matrix: one row
-//                   per parameter holding its term ((inv_n*delta)*a for a weight, the product
-//                   mlp.cpp:113 forms; inv_n*delta for a bias, mlp.cpp:117) plus the err^2 row;
-//                   the producer threads arrive on the round's mbarrier when their columns are
+//   producer warps  own BLOCKS of 32 samples (warp w: blocks w, w + NPW, ...; lane k sample
+//                   32 b + k), forward and backward, and store each sample's column of the record
+//                   matrix: one row per parameter holding its term ((inv_n*delta)*a for a weight,
+//                   the product mlp.cpp:113 forms; inv_n*delta for a bias, mlp.cpp:117) plus the
+//                   err^2 row; the warp arrives on the block's mbarrier when its columns are
 //                   stored; the epoch's weights are read into registers once per epoch;
 //   chain lanes     own PARAMETERS (lane c sums row c; one more lane the loss): a lane waits for
-//                   round q's mbarrier, then extends its DADD chain over that round's samples,
-//                   two per 16-B load, in sample order — the chain starts after round 0 and runs
-//                   while the producers are on later rounds.
-// Measured (config 2, blur net 6-5-5-1, 4 producer warps): ~1290 cycles to round 0, the chain
-// ~3660 (~14.6 cycles per link: shared-memory traffic of the producers' stores is the
-// contention), Adam ~1000 — ~6000 cycles per epoch against ~6950 phased.
+//                   producer round 0 (NPW blocks), then extends its DADD chain over the blocks in
+//                   sample order, two samples per 16-B load; inside a round the NEXT block's 16
+//                   loads are issued before the current block's 32 links, so shared-memory
+//                   latency stays off the chain; the next round is waited for (blocking) only
+//                   after the last block of the current one. The chain starts after round 0 and
+//                   runs while the producers are on round 1.
 // The owner lane keeps w, m, v in registers; after Adam it writes w to shared memory for the
-// producers; one CTA barrier per epoch separates epochs.
+// producers; one CTA barrier per epoch separates epochs. Warps 0-2 (chains) and the producer
+// warps that follow share the four SM sub-partitions so block 0's warp runs alone on one.
 #include <cmath>
+#include <cstdlib>
 
 #include "exact_fp64.cuh"
 #include "kernels.cuh"
@@ -38,9 +40,18 @@ namespace {
 
 constexpr int kLd = 258;     // record row stride (doubles): N <= 256 samples + even padding
 constexpr int kChainWarps = 3;
+constexpr int kBlk = 32;     // samples per producer block (one warp's columns)
+constexpr int kPairs = kBlk / 2;
+constexpr int kMaxBlk = 8;   // N <= 256
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
   return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+// clock read that stays between the surrounding memory operations (profiling instantiation only)
+__device__ __forceinline__ long long clk() {
+  long long t;
+  asm volatile("mov.u64 %0, %%clock64;" : "=l"(t)::"memory");
+  return t;
 }
 __device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
@@ -110,12 +121,17 @@ struct PipeShape {
     const double tout = __dmul_rn(inv_n, dout);   // left factor of mlp.cpp:113,117
     r[P * kLd] = __dmul_rn(err, err);             // mlp.cpp:91
     r[BO * kLd] = tout;
+    // The reference's delta sums start at 0.0 (mlp.cpp:97-100: acc = 0.0; acc += w*delta); here
+    // they start at the first product. The two differ only in the sign of a zero (0.0 + -0.0 is
+    // +0.0), and a delta reaches the outputs only through record terms inv_n*delta*a summed into
+    // chains that start at +0.0 and never hold -0.0, where +0.0 and -0.0 terms are both no-ops
+    // (the ReLU gates test activations, not deltas): every weight, loss and metric is unchanged.
     double t1[H1];
     if constexpr (H2 > 0) {
       double d2[H2];
 #pragma unroll
-      for (int i = 0; i < H2; ++i) {  // acc = 0.0 + w*delta (mlp.cpp:97-100), ReLU gate
-        const double acc = __dadd_rn(0.0, __dmul_rn(w[WO + i], dout));
+      for (int i = 0; i < H2; ++i) {  // w*delta (mlp.cpp:97-100), ReLU gate
+        const double acc = __dmul_rn(w[WO + i], dout);
         d2[i] = a2[i] > 0.0 ? acc : 0.0;
         r[(WO + i) * kLd] = __dmul_rn(tout, a2[i]);
       }
@@ -128,15 +144,15 @@ struct PipeShape {
       }
 #pragma unroll
       for (int i = 0; i < H1; ++i) {
-        double acc = 0.0;
+        double acc = __dmul_rn(w[W2 + i], d2[0]);
 #pragma unroll
-        for (int o = 0; o < H2; ++o) acc = __dadd_rn(acc, __dmul_rn(w[W2 + o * H1 + i], d2[o]));
+        for (int o = 1; o < H2; ++o) acc = __dadd_rn(acc, __dmul_rn(w[W2 + o * H1 + i], d2[o]));
         t1[i] = __dmul_rn(inv_n, a1[i] > 0.0 ? acc : 0.0);
       }
     } else {
 #pragma unroll
       for (int i = 0; i < H1; ++i) {
-        const double acc = __dadd_rn(0.0, __dmul_rn(w[WO + i], dout));
+        const double acc = __dmul_rn(w[WO + i], dout);
         t1[i] = __dmul_rn(inv_n, a1[i] > 0.0 ? acc : 0.0);
         r[(WO + i) * kLd] = __dmul_rn(tout, a1[i]);
       }
@@ -166,17 +182,17 @@ __host__ __device__ constexpr int pipe_smem_doubles() {
 template <int I, int H1, int H2, int NPW, bool kProf>
 __global__ void __launch_bounds__(32 * (kChainWarps + NPW), 1) train_fp64_pipe(TrainArgs a) {
   using S = PipeShape<I, H1, H2>;
-  constexpr int NPT = 32 * NPW;                 // producer threads = samples per round
-  constexpr int R = (256 + NPT - 1) / NPT;      // rounds (samples per producer thread) at most
+  constexpr int R = (kMaxBlk + NPW - 1) / NPW;  // blocks per producer warp at most
   extern __shared__ __align__(16) double smem[];
   double* rec = smem;                                       // [ROWS][kLd]
   double* ws = rec + S::ROWS * kLd;                         // [P] weights (producers' copy)
   double* Ls = ws + ((S::P + 1) & ~1);                      // [2] epoch loss
-  unsigned long long* bar = reinterpret_cast<unsigned long long*>(Ls + 2);  // [R] rounds
+  unsigned long long* bar = reinterpret_cast<unsigned long long*>(Ls + 2);  // [nb] blocks
 
   const int m = a.order[blockIdx.x];
   const int tile = a.model_tile[m];
   const int N = a.tile_rows[tile];
+  const int nb = (N + kBlk - 1) / kBlk;
   const int E = a.epochs[m];
   const double lr = a.lr[m];
   const int tid = threadIdx.x;
@@ -186,11 +202,11 @@ __global__ void __launch_bounds__(32 * (kChainWarps + NPW), 1) train_fp64_pipe(T
   const double* Y = a.y + a.tile_offset[tile];
 
   for (int p = tid; p < S::P; p += blockDim.x) ws[p] = gp[p];
-  // padding column (odd N) holds zero terms: they leave every chain unchanged (a chain starts
-  // at +0.0 and is never -0.0, and x + (+-0) == x for every other x)
+  // padding columns (N up to the block end) hold zero terms: they leave every chain unchanged (a
+  // chain starts at +0.0 and is never -0.0, and x + (+-0) == x for every other x)
   for (int s = tid; s < kLd; s += blockDim.x)
     for (int j = 0; j < S::ROWS; ++j) rec[j * kLd + s] = 0.0;
-  if (tid < R) mbar_init(&bar[tid], NPT);  // one per producer round: every producer thread arrives
+  if (tid * NPW < nb) mbar_init(&bar[tid], 32 * NPW);  // one per producer round: every producer thread arrives
   __syncthreads();
 
   double* trace = a.loss_trace ? a.loss_trace + a.trace_offset[m] : nullptr;
@@ -201,33 +217,60 @@ __global__ void __launch_bounds__(32 * (kChainWarps + NPW), 1) train_fp64_pipe(T
     // ---- chain lanes: lane c sums record row c over the samples in order, then Adam ----
     const int p = tid < S::P ? tid : tid == S::P ? -1 : -2;  // parameter, -1 the loss, -2 idle
     const double2* Tr = reinterpret_cast<const double2*>(rec + (tid <= S::P ? tid : S::P) * kLd);
-    const int npairs = (N + 1) >> 1;
     double wr = p >= 0 ? gp[p] : 0.0, mr = 0.0, vr = 0.0;
     const double beta1 = 0.9, beta2 = 0.999, eps = 1e-8;
     const double c1 = 1.0 - beta1, c2 = 1.0 - beta2;
     long long pc[4] = {0, 0, 0, 0};
+    long long k0 = kProf ? clk() : 0;  // epoch start: the previous epoch's barrier exit
     int next_trace = 0;
+    double2 A[kPairs], B[kPairs];
     for (int e = 0; e < E; ++e) {
+      const unsigned ph = e & 1;
       const double2 bc = a.bias_corr[e];  // issued early: latency hidden behind the chain
       const double y1 = rcp_refined(bc.x), y2 = rcp_refined(bc.y);  // per epoch, off the chain
-      long long k0 = 0, k1 = 0, k2 = 0;
-      if (kProf) k0 = clock64();
+      long long k1 = 0, k2 = 0;
       double g = 0.0;
-      for (int q = 0, j = 0; j < npairs; ++q) {
-        mbar_wait(bar + q, e & 1);  // producer round q's columns are stored
-        if (kProf && q == 0) k1 = clock64();
-        const int j1 = min(npairs, (q + 1) * (NPT / 2));
-        if (p != -2) {  // idle lanes load nothing (a warp's 16-B load costs a wavefront per 8 lanes)
-#pragma unroll 8
-          for (; j < j1; ++j) {  // two samples per 16-B load, in sample order (mlp.cpp:106-118)
-            const double2 t = Tr[j];
-            g = __dadd_rn(g, t.x);
-            g = __dadd_rn(g, t.y);
+      // idle lanes read the loss row with lane S::P (same address: a broadcast, no extra
+      // wavefront), so the loads need no branch
+      auto load = [&](double2(&dst)[kPairs], int b) {
+#pragma unroll
+        for (int j = 0; j < kPairs; ++j) dst[j] = Tr[b * kPairs + j];
+      };
+      auto links = [&](const double2(&cur)[kPairs]) {  // 32 links in sample order (mlp.cpp:106-118)
+#pragma unroll
+        for (int j = 0; j < kPairs; ++j) {
+          g = __dadd_rn(g, cur[j].x);
+          g = __dadd_rn(g, cur[j].y);
+        }
+      };
+      // One blocking wait per producer ROUND (NPW blocks of 32 samples); inside a round, block
+      // b + 1's 16 loads are issued before block b's 32 links (same basic block, no branch: the
+      // block index is clamped instead), so shared-memory latency stays off the chain. Only the
+      // first block of the next round waits for its barrier after the current block's links.
+      // (A non-blocking barrier test ahead of unconditional loads is unsafe: the loads are not
+      // ordered after the test unless they depend on its result.)
+      mbar_wait(bar, ph);  // round 0's columns are stored
+      if (kProf && (a.prof_flags & 1)) mbar_wait(bar + (nb - 1) / NPW, ph);  // experiment: chain after every round
+      if (kProf) k1 = clk();
+      load(A, 0);
+#pragma unroll
+      for (int b = 0; b < kMaxBlk; ++b) {
+        if (b < nb) {
+          double2(&cur)[kPairs] = (b & 1) ? B : A;
+          double2(&nxt)[kPairs] = (b & 1) ? A : B;
+          if ((b + 1) % NPW != 0) {  // next block in this (complete) round
+            load(nxt, b + 1 < nb ? b + 1 : b);
+            links(cur);
+          } else {
+            links(cur);
+            if (b + 1 < nb) {
+              mbar_wait(bar + (b + 1) / NPW, ph);
+              load(nxt, b + 1);
+            }
           }
         }
-        j = j1;
       }
-      if (kProf) k2 = clock64();
+      if (kProf) k2 = clk();
       if (p >= 0) {  // AdamState::update (mlp.cpp:142-154), bias corrections from the host libm
         const double mk = __dadd_rn(__dmul_rn(beta1, mr), __dmul_rn(c1, g));
         const double vk = __dadd_rn(__dmul_rn(beta2, vr), __dmul_rn(__dmul_rn(c2, g), g));
@@ -264,14 +307,15 @@ __global__ void __launch_bounds__(32 * (kChainWarps + NPW), 1) train_fp64_pipe(T
         }
       }
       long long k3 = 0;
-      if (kProf) k3 = clock64();
+      if (kProf) k3 = clk();
       __syncthreads();
       if (kProf) {
-        const long long k4 = clock64();
-        pc[0] += k1 - k0;  // epoch start -> producer round 0 stored
+        const long long k4 = clk();
+        pc[0] += k1 - k0;  // epoch start -> producer block 0 stored
         pc[1] += k2 - k1;  // the chains over all samples
         pc[2] += k3 - k2;  // Adam
         pc[3] += k4 - k3;  // epoch barrier
+        k0 = k4;
       }
       last = Ls[e & 1];
       if (!isfinite(last)) {  // mlp.cpp:166-169: TrainingError(epoch)
@@ -287,12 +331,12 @@ __global__ void __launch_bounds__(32 * (kChainWarps + NPW), 1) train_fp64_pipe(T
     if (kProf && tid == 0 && blockIdx.x == 0)
       for (int k = 0; k < 4; ++k) a.phase_cycles[k] = pc[k];
   } else {
-    // ---- producer threads: samples k, k + NPT, ... (rounds), inputs kept in registers ----
-    const int k = tid - 32 * kChainWarps;
+    // ---- producer warps: blocks w, w + NPW, ... ; inputs kept in registers ----
+    const int w = (tid >> 5) - kChainWarps, k = tid & 31;
     double xr[R][I], yr[R];
 #pragma unroll
     for (int q = 0; q < R; ++q) {
-      const int s = k + q * NPT;
+      const int s = (w + q * NPW) * kBlk + k;
 #pragma unroll
       for (int i = 0; i < I; ++i) xr[q][i] = s < N ? X[(size_t)s * 8 + i] : 0.0;
       yr[q] = s < N ? Y[s] : 0.0;
@@ -303,10 +347,10 @@ __global__ void __launch_bounds__(32 * (kChainWarps + NPW), 1) train_fp64_pipe(T
       for (int j = 0; j < S::P; ++j) wv[j] = ws[j];
 #pragma unroll
       for (int q = 0; q < R; ++q) {
-        if (q * NPT < N) {
-          const int s = k + q * NPT;
+        if (q * NPW < nb) {  // a round with at least one block
+          const int s = (w + q * NPW) * kBlk + k;
           if (s < N) S::sample(wv, xr[q], yr[q], rec + s, inv_n);
-          mbar_arrive(&bar[q]);
+          mbar_arrive(&bar[q]);  // every producer thread arrives on its round's barrier
         }
       }
       __syncthreads();
@@ -323,7 +367,12 @@ void go_pipe(const TrainArgs& a, cudaStream_t s) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
     kern<<<a.n_models, 32 * (kChainWarps + NPW), dyn, s>>>(a);
   };
-  if (a.phase_cycles) launch(train_fp64_pipe<I, H1, H2, NPW, true>);
+  if (a.phase_cycles) {
+    TrainArgs b = a;
+    if (const char* f = std::getenv("LANN_PROF_FLAGS")) b.prof_flags = std::atoi(f);
+    cudaFuncSetAttribute(train_fp64_pipe<I, H1, H2, NPW, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
+    train_fp64_pipe<I, H1, H2, NPW, true><<<b.n_models, 32 * (kChainWarps + NPW), dyn, s>>>(b);
+  }
   else launch(train_fp64_pipe<I, H1, H2, NPW, false>);
 }
 

@@ -354,6 +354,33 @@ void lann_population_destroy(lann_population* pop);
  * only). Writes up to cap entries, returns the count. */
 int lann_default_combos(lann_world* out, int32_t cap);
 
+/* ---- multi-GPU populations ("multiple models may be trained concurrently",
+ * SPEC.md:327) ---------------------------------------------------------------------------
+ * A group owns one engine per listed device. lann_group_run_population cuts the job list into
+ * contiguous, cost-balanced shards (cost = epochs x train rows x parameters, so a combination's
+ * seeds and folds stay together and share their tile), runs every shard through
+ * lann_run_population on its own device from its own host thread, and writes the results (and
+ * optional weights / loss traces, offsets as in lann_run_population) into the caller's arrays in
+ * job order. Shards exchange nothing: no device-to-device traffic, no collective, no NCCL. A
+ * device may be listed more than once (its shards then share it). FP64-exact results do not
+ * depend on the sharding. */
+typedef struct lann_group lann_group;
+int lann_group_create(int32_t n_devices, const int32_t* devices, lann_group** out);
+void lann_group_destroy(lann_group* group);
+const char* lann_group_last_error(const lann_group* group);
+int32_t lann_group_size(const lann_group* group);
+/* the shard cut for n_jobs jobs over n_shards devices (host only, no device needed):
+ * bounds[0] = 0 <= bounds[1] <= ... <= bounds[n_shards] = n_jobs */
+int lann_shard_bounds(int32_t n_shards, int32_t n_jobs, const lann_job* jobs, int32_t* bounds);
+int lann_group_shard_bounds(const lann_group* group, int32_t n_jobs, const lann_job* jobs, int32_t* bounds);
+int lann_group_run_population(lann_group* group, int32_t n_jobs, const lann_job* jobs, int32_t precision,
+                              lann_job_result* results, double* params_out, const int64_t* params_offset,
+                              double* trace_out, const int64_t* trace_offset);
+/* device time of the last run: the maximum over the group's devices (their shards run
+ * concurrently), and the wall time of the whole call */
+double lann_group_last_device_ms(const lann_group* group);
+double lann_group_last_wall_ms(const lann_group* group);
+
 #ifdef __cplusplus
 }
 #endif

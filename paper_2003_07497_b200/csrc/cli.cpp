@@ -17,7 +17,8 @@
 //   select   blur schedules: train on measured samples, GPU argmin over the candidates,
 //            regret / speedups (selection.json, schedules.csv)
 //   sweep    the 48-combination population x seeds x k folds (config 3 / config 5) through
-//            the prepared-population engine -> sweep.csv + per-combination summary
+//            the engine, sharded over --devices (one engine + host thread per GPU, contiguous
+//            cost-balanced shards, no collective) -> sweep.csv + per-combination summary
 //   select-variants  config 4: counter-generated candidate shapes scored by V variant models,
 //            argmin per candidate -> variant histogram (variants.csv)
 // Every run appends {command, argv, seed, timestamp, inputs, outputs} to <out>/manifest.json
@@ -649,29 +650,43 @@ int cmd_sweep(const Args& a) {
           meta.push_back({i, f, s, k});
         }
     }
-  lann_engine* e = nullptr;
-  if (lann_engine_create(int(a.integer("device", 0)), &e) != LANN_OK)
-    throw Error("no CUDA device: the LANN engine has no CPU fallback");
-  const auto t0 = std::chrono::steady_clock::now();
-  lann_population* pop = nullptr;
-  int st = lann_population_create(e, int(jobs.size()), jobs.data(), precision, 0, &pop);
-  if (st) {
-    const std::string msg = lann_last_error(e);
-    lann_engine_destroy(e);
-    throw ParamError("population setup failed: " + msg);
+  // one engine per device (--devices 0,1,... or a range 0-7; default --device, 0): contiguous
+  // cost-balanced shards, one host thread per device, results gathered in job order, no NCCL
+  std::vector<std::int32_t> devices;
+  if (a.has("devices")) {
+    const std::string d = a.get("devices", "0");
+    if (const auto dash = d.find('-'); dash != std::string::npos && d.find(',') == std::string::npos) {
+      const int lo = std::stoi(d.substr(0, dash)), hi = std::stoi(d.substr(dash + 1));
+      if (lo < 0 || hi < lo) throw ParamError("--devices range must be lo-hi with 0 <= lo <= hi");
+      for (int i = lo; i <= hi; ++i) devices.push_back(i);
+    } else {
+      for (int v : parse_ints(d)) devices.push_back(v);
+    }
+  } else {
+    devices.push_back(std::int32_t(a.integer("device", 0)));
   }
-  const auto t1 = std::chrono::steady_clock::now();
-  st = lann_population_run(pop, 1);
-  const double dev_ms = lann_last_device_ms(e);
+  lann_group* group = nullptr;
+  if (lann_group_create(std::int32_t(devices.size()), devices.data(), &group) != LANN_OK)
+    throw Error("no CUDA device: the LANN engine has no CPU fallback");
+  std::vector<std::int32_t> bounds(devices.size() + 1);
+  lann_group_shard_bounds(group, std::int32_t(jobs.size()), jobs.data(), bounds.data());
+  const auto t0 = std::chrono::steady_clock::now();
   std::vector<lann_job_result> res(jobs.size());
-  if (!st) st = lann_population_fetch(pop, res.data(), nullptr, nullptr, nullptr, nullptr);
+  const int st = lann_group_run_population(group, std::int32_t(jobs.size()), jobs.data(), precision, res.data(),
+                                           nullptr, nullptr, nullptr, nullptr);
   const auto t2 = std::chrono::steady_clock::now();
-  const double flop = lann_population_flop(pop);
-  const std::string err = st ? lann_last_error(e) : "";
-  lann_population_destroy(pop);
-  lann_engine_destroy(e);
+  const double dev_ms = lann_group_last_device_ms(group);
+  double flop = 0.0;  // algorithmic FLOP of the trainers
+  for (std::size_t m = 0; m < jobs.size(); ++m)
+    if (res[m].status == LANN_OK) {
+      const auto& j = jobs[m];
+      const int I = res[m].n_inputs, h1 = j.hidden[0], h2 = j.n_hidden > 1 ? j.hidden[1] : 0;
+      const double fs = h2 > 0 ? 4.0 * I * h1 + 6.0 * h1 * h2 + 6.0 * h2 + h1 + 5 : 4.0 * I * h1 + 6.0 * h1 + 5;
+      flop += double(j.epochs) * (res[m].n_train * fs + 14.0 * res[m].n_params);
+    }
+  const std::string err = st ? lann_group_last_error(group) : "";
+  lann_group_destroy(group);
   if (st) throw Error("population run failed: " + err);
-
   const fs::path out = a.get("out", "perfsage_out");
   fs::create_directories(out);
   const fs::path csv = out / "sweep.csv";
@@ -706,11 +721,17 @@ int cmd_sweep(const Args& a) {
               << med << "\n";
     std::cout.unsetf(std::ios::fixed);
   }
-  const double prep_s = std::chrono::duration<double>(t1 - t0).count();
   const double all_s = std::chrono::duration<double>(t2 - t0).count();
-  std::cout << jobs.size() << " models, " << model_epochs << " model-epochs: device " << dev_ms << " ms ("
-            << double(model_epochs) / (dev_ms / 1e3) << " model-epochs/s, " << flop / (dev_ms / 1e3) / 1e12
-            << " TFLOP/s algorithmic), host prepare " << prep_s << " s, end to end " << all_s << " s\n";
+  std::cout << jobs.size() << " models, " << model_epochs << " model-epochs on " << devices.size()
+            << " device(s): device " << dev_ms << " ms (max over devices; " << double(model_epochs) / (dev_ms / 1e3)
+            << " model-epochs/s, " << flop / (dev_ms / 1e3) / 1e12 << " TFLOP/s algorithmic), end to end " << all_s
+            << " s\n";
+  if (devices.size() > 1) {
+    std::cout << "shards (jobs per device):";
+    for (std::size_t d = 0; d < devices.size(); ++d)
+      std::cout << ' ' << devices[d] << ':' << bounds[d + 1] - bounds[d];
+    std::cout << "\n";
+  }
   record_run(out, a, root, {}, {csv.string()});
   return 0;
 }

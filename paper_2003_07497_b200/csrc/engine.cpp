@@ -1897,3 +1897,130 @@ int lann_default_combos(lann_world* out, int32_t cap) {
 }
 
 }  // extern "C"
+
+// ---- multi-GPU populations: one engine and one host thread per device ---------------------------
+struct lann_group {
+  std::vector<lann_engine*> engines;
+  std::string err;
+  double last_device_ms = 0.0, last_wall_ms = 0.0;
+};
+
+namespace {
+// the sharding cost of a job: epochs x train rows x parameters (paper_2003_07497_b200/sharding.py)
+double job_cost(const lann_job& j) {
+  int n_train = int(std::llround(double(j.count) * j.train_fraction));
+  if (j.n_folds >= 2) n_train -= n_train / j.n_folds;
+  static const int base[5] = {5, 3, 4, 5, 5};  // features per kind without n_thd and c
+  const int k = j.world.kind >= 0 && j.world.kind < 5 ? j.world.kind : 0;
+  const int I = base[k] + (j.world.hw_class == LANN_HW_CPU && j.world.kind != LANN_BLUR ? 1 : 0) +
+                (j.family == LANN_NNC ? 1 : 0);
+  const int h1 = std::max(1, j.hidden[0]), h2 = j.n_hidden > 1 ? std::max(1, j.hidden[1]) : 0;
+  const double p = h2 ? double((I + 1) * h1 + (h1 + 1) * h2 + h2 + 1) : double((I + 1) * h1 + h1 + 1);
+  return double(j.epochs) * double(std::max(0, n_train)) * p;
+}
+
+void shard_bounds(int n_jobs, const lann_job* jobs, int world, int32_t* b) {
+  double total = 0.0;
+  for (int i = 0; i < n_jobs; ++i) total += job_cost(jobs[i]);
+  int r = 1, nb = 1;
+  b[0] = 0;
+  double acc = 0.0;
+  for (int i = 0; i < n_jobs; ++i) {
+    acc += job_cost(jobs[i]);
+    while (r < world && acc >= total * r / world) {
+      b[nb++] = i + 1;
+      ++r;
+    }
+  }
+  while (nb < world) b[nb++] = n_jobs;
+  b[world] = n_jobs;
+}
+}  // namespace
+
+int lann_group_create(int32_t n_devices, const int32_t* devices, lann_group** out) {
+  if (!out || n_devices < 1 || !devices) return LANN_PARAM_ERROR;
+  *out = nullptr;
+  auto* g = new lann_group;
+  for (int i = 0; i < n_devices; ++i) {
+    lann_engine* e = nullptr;
+    const int st = lann_engine_create(devices[i], &e);
+    if (st) {
+      for (lann_engine* x : g->engines) lann_engine_destroy(x);
+      delete g;
+      return st;
+    }
+    g->engines.push_back(e);
+  }
+  *out = g;
+  return LANN_OK;
+}
+
+void lann_group_destroy(lann_group* g) {
+  if (!g) return;
+  for (lann_engine* e : g->engines) lann_engine_destroy(e);
+  delete g;
+}
+
+const char* lann_group_last_error(const lann_group* g) { return g ? g->err.c_str() : "no group"; }
+int32_t lann_group_size(const lann_group* g) { return g ? int32_t(g->engines.size()) : 0; }
+double lann_group_last_device_ms(const lann_group* g) { return g ? g->last_device_ms : 0.0; }
+double lann_group_last_wall_ms(const lann_group* g) { return g ? g->last_wall_ms : 0.0; }
+
+int lann_shard_bounds(int32_t n_shards, int32_t n_jobs, const lann_job* jobs, int32_t* bounds) {
+  if (n_shards < 1 || !bounds || n_jobs < 0 || (n_jobs > 0 && !jobs)) return LANN_PARAM_ERROR;
+  shard_bounds(n_jobs, jobs, n_shards, bounds);
+  return LANN_OK;
+}
+
+int lann_group_shard_bounds(const lann_group* g, int32_t n_jobs, const lann_job* jobs, int32_t* bounds) {
+  if (!g || !bounds || n_jobs < 0 || (n_jobs > 0 && !jobs)) return LANN_PARAM_ERROR;
+  shard_bounds(n_jobs, jobs, int(g->engines.size()), bounds);
+  return LANN_OK;
+}
+
+int lann_group_run_population(lann_group* g, int32_t n_jobs, const lann_job* jobs, int32_t precision,
+                              lann_job_result* results, double* params_out, const int64_t* params_offset,
+                              double* trace_out, const int64_t* trace_offset) {
+  if (!g) return LANN_NO_DEVICE;
+  if (!results || !jobs || n_jobs < 1) {
+    g->err = "empty population";
+    return LANN_PARAM_ERROR;
+  }
+  const int W = int(g->engines.size());
+  std::vector<int32_t> b(size_t(W) + 1);
+  shard_bounds(n_jobs, jobs, W, b.data());
+  std::vector<int> st(size_t(W), LANN_OK);
+  std::vector<double> dev_ms(size_t(W), 0.0);
+  std::vector<int64_t> h2d(size_t(W), 0), d2h(size_t(W), 0);
+  const auto t0 = std::chrono::steady_clock::now();
+  auto work = [&](int w) {
+    const int lo = b[size_t(w)], n = b[size_t(w) + 1] - lo;
+    if (n <= 0) return;
+    lann_transfer_bytes(nullptr, nullptr, 1);
+    // offsets are absolute indices into the caller's arrays: pass them shifted, the bases as is
+    st[size_t(w)] = lann_run_population(g->engines[size_t(w)], n, jobs + lo, precision, results + lo, params_out,
+                                        params_offset ? params_offset + lo : nullptr, trace_out,
+                                        trace_offset ? trace_offset + lo : nullptr);
+    dev_ms[size_t(w)] = lann_last_device_ms(g->engines[size_t(w)]);
+    lann_transfer_bytes(&h2d[size_t(w)], &d2h[size_t(w)], 1);
+  };
+  std::vector<std::thread> threads;
+  for (int w = 1; w < W; ++w) threads.emplace_back(work, w);
+  work(0);
+  for (auto& t : threads) t.join();
+  g->last_wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  g->last_device_ms = *std::max_element(dev_ms.begin(), dev_ms.end());
+  for (int w = 0; w < W; ++w) {  // the caller's thread accounts for every shard's copies
+    t_h2d += h2d[size_t(w)];
+    t_d2h += d2h[size_t(w)];
+  }
+  g->err.clear();
+  int rc = LANN_OK;
+  for (int w = 0; w < W; ++w)
+    if (st[size_t(w)] != LANN_OK && rc == LANN_OK) {
+      rc = st[size_t(w)];
+      g->err = std::string("device ") + std::to_string(g->engines[size_t(w)]->device) + ": " +
+               lann_last_error(g->engines[size_t(w)]);
+    }
+  return rc;
+}

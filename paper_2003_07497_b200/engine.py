@@ -71,7 +71,10 @@ EXPORTS = ["lann_engine_create", "lann_engine_destroy", "lann_last_error", "lann
            "lann_init_params", "lann_population_create", "lann_population_run", "lann_population_fetch",
            "lann_population_flop", "lann_population_models", "lann_population_destroy",
            "lann_population_norm", "lann_transfer_bytes", "lann_run_population", "lann_default_combos",
-           "lann_mlp_forward", "lann_mse_loss", "lann_mse_gradient", "lann_adam_update"]
+           "lann_mlp_forward", "lann_mse_loss", "lann_mse_gradient", "lann_adam_update",
+           "lann_group_create", "lann_group_destroy", "lann_group_last_error", "lann_group_size",
+           "lann_shard_bounds", "lann_group_shard_bounds", "lann_group_run_population",
+           "lann_group_last_device_ms", "lann_group_last_wall_ms"]
 
 
 def transfer_bytes(reset=False):
@@ -129,6 +132,19 @@ def load_library(path: str = LIB_PATH):
     L.lann_mse_gradient.argtypes = [vp, C.POINTER(MlpBatch), vp, vp]
     L.lann_adam_update.argtypes = [vp, C.c_int64, vp, vp, vp, vp, C.c_int32, C.c_double, C.c_double, C.c_double,
                                    C.c_double]
+    L.lann_group_create.argtypes = [C.c_int32, vp, C.POINTER(vp)]
+    L.lann_group_destroy.argtypes = [vp]
+    L.lann_group_last_error.argtypes = [vp]
+    L.lann_group_last_error.restype = C.c_char_p
+    L.lann_group_size.argtypes = [vp]
+    L.lann_shard_bounds.argtypes = [C.c_int32, C.c_int32, C.POINTER(Job), vp]
+    L.lann_group_shard_bounds.argtypes = [vp, C.c_int32, C.POINTER(Job), vp]
+    L.lann_group_run_population.argtypes = [vp, C.c_int32, C.POINTER(Job), C.c_int32, C.POINTER(JobResult),
+                                            vp, vp, vp, vp]
+    L.lann_group_last_device_ms.argtypes = [vp]
+    L.lann_group_last_device_ms.restype = C.c_double
+    L.lann_group_last_wall_ms.argtypes = [vp]
+    L.lann_group_last_wall_ms.restype = C.c_double
     _lib = L
     return L
 
@@ -471,3 +487,75 @@ def _model_set(models, precision):
     ms = ModelSet(n_models=M, precision=precision, n_inputs=_ptr(I), h1=_ptr(h1), h2=_ptr(h2), log_target=_ptr(lt),
                   param_offset=_ptr(poff), params=_ptr(params), total_params=len(params), norm=_ptr(norm))
     return ms, (I, h1, h2, lt, poff, params, norm)
+
+
+def shard_bounds(jobs, n_shards: int):
+    """lann_shard_bounds: the engine's contiguous cost-balanced cut of a job list (host only)."""
+    L = load_library()
+    n = len(jobs)
+    arr = (Job * max(n, 1))(*jobs)
+    b = np.zeros(n_shards + 1, dtype=np.int32)
+    st = L.lann_shard_bounds(n_shards, n, arr, _ptr(b))
+    if st:
+        raise ParamError(f"lann_shard_bounds status {st}")
+    return [int(x) for x in b]
+
+
+class Group:
+    """lann_group_*: one engine and one host thread per listed device; a population is cut into
+    contiguous cost-balanced shards that run concurrently and are gathered in job order on the
+    host (no device-to-device traffic, no NCCL)."""
+
+    def __init__(self, devices):
+        self.L = load_library()
+        devs = np.asarray(list(devices), dtype=np.int32)
+        self.h = C.c_void_p()
+        st = self.L.lann_group_create(len(devs), _ptr(devs), C.byref(self.h))
+        if st:
+            raise _ERR.get(st, Error)(f"lann_group_create status {st}")
+        self.devices = [int(d) for d in devs]
+
+    def close(self):
+        if self.h:
+            self.L.lann_group_destroy(self.h)
+            self.h = C.c_void_p()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    @property
+    def last_error(self) -> str:
+        return self.L.lann_group_last_error(self.h).decode()
+
+    @property
+    def last_device_ms(self) -> float:
+        return self.L.lann_group_last_device_ms(self.h)
+
+    @property
+    def last_wall_ms(self) -> float:
+        return self.L.lann_group_last_wall_ms(self.h)
+
+    def shard_bounds(self, jobs):
+        n = len(jobs)
+        arr = (Job * n)(*jobs)
+        b = np.zeros(len(self.devices) + 1, dtype=np.int32)
+        self.L.lann_group_shard_bounds(self.h, n, arr, _ptr(b))
+        return [int(x) for x in b]
+
+    def run_population(self, jobs, precision=abi.FP64_EXACT, want_params=False):
+        """Returns (status, results, params list or None)."""
+        n = len(jobs)
+        arr = (Job * n)(*jobs)
+        res = (JobResult * n)()
+        params = off = None
+        if want_params:  # 2048 slots per model, as Engine.run_population
+            params = np.zeros(n * 2048)
+            off = np.arange(n, dtype=np.int64) * 2048
+        st = self.L.lann_group_run_population(self.h, n, arr, precision, res, _ptr(params), _ptr(off), None, None)
+        plist = None
+        if want_params:
+            plist = [params[off[k]: off[k] + res[k].n_params].copy() for k in range(n)]
+        return st, list(res), plist

@@ -82,3 +82,17 @@ def test_weak_scaling_populations_are_distinct():
     assert [j.data_seed for j in a] != [j.data_seed for j in b]
     assert [bytes(j.world) for j in a] == [bytes(j.world) for j in b]
     assert all(j.world.kind == abi.BLUR for j in a[40:])
+
+
+def test_engine_shard_bounds_match_the_python_rule():
+    """lann_shard_bounds (the C++ cut behind lann_group_run_population and `perfsage sweep
+    --devices`) == sharding.shard_bounds on the config-2 / config-3 / config-5 job lists."""
+    from paper_2003_07497_b200 import engine as E
+
+    lists = [P.config2_jobs(root_seed=1), P.config3_jobs(root_seed=1, n_seeds=4),
+             P.config3_jobs(root_seed=1, n_seeds=2, family=abi.NN) + P.config3_jobs(root_seed=1, n_seeds=2)]
+    for jobs in lists:
+        for w in (1, 2, 3, 4, 8):
+            b = E.shard_bounds(jobs, w)
+            assert b == sharding.shard_bounds(jobs, w)
+            assert b[0] == 0 and b[-1] == len(jobs) and all(x <= y for x, y in zip(b, b[1:]))

@@ -113,7 +113,9 @@ typedef struct lann_job_result {
   double final_loss;       /* loss_trace.back() */
   double mape, mape_thr, rho; /* on the evaluation part */
   int32_t n_kept;
-  int32_t pad_;
+  int32_t precision_run;   /* lann_precision the trainer actually ran (-1: not trained): LANN_FP32 requests for
+                              shapes without an FP32 kernel (or tiles over 96 KB) run in
+                              LANN_FP64_EXACT and say so here */
 } lann_job_result;
 
 /* ---- engine ---------------------------------------------------------------- */
@@ -239,6 +241,22 @@ int lann_select_variants(lann_engine* engine, const lann_model_set* models,
                          const int32_t* with_n_thd, int32_t kind, int32_t max_threads,
                          uint64_t seed, int64_t first, int64_t n_cands,
                          int32_t* out_idx, double* out_score);
+
+/* lann_select_variants with compact, streamed outputs: out_idx[i] (uint8) and out_score[i]
+ * (float: the FP32 scorer's own precision; FP64-exact models round their score once) for
+ * candidate first + i, and hist[v] = number of candidates whose argmin is model v. Any of the
+ * three outputs may be NULL (hist alone moves M counters, not per-candidate data). The range is
+ * scored in chunks whose device-to-host copies overlap the next chunk's scoring; outputs in
+ * pinned host memory (lann_host_alloc) are written by DMA directly, pageable ones through the
+ * engine's pinned staging buffer. At most 255 models. */
+int lann_select_variants_compact(lann_engine* engine, const lann_model_set* models, const int32_t* with_n_thd,
+                                 int32_t kind, int32_t max_threads, uint64_t seed, int64_t first, int64_t n_cands,
+                                 uint8_t* out_idx, float* out_score, int64_t* hist);
+
+/* Pinned (page-locked) host memory for engine outputs: device-to-host copies into it run at
+ * full link bandwidth and overlap compute. */
+int lann_host_alloc(size_t bytes, void** out);
+void lann_host_free(void* ptr);
 
 /* ---- synthetic data (datagen::build_dataset + split, datagen.cpp:177-248) ----
  * feats [count][LANN_ROW] base features (no c), c [count], runtime [count];

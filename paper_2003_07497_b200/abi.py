@@ -38,7 +38,7 @@ class JobResult(C.Structure):
     _fields_ = [
         ("status", C.c_int32), ("nonfinite_epoch", C.c_int32), ("n_inputs", C.c_int32), ("n_params", C.c_int32),
         ("n_train", C.c_int32), ("n_eval", C.c_int32), ("final_loss", C.c_double), ("mape", C.c_double),
-        ("mape_thr", C.c_double), ("rho", C.c_double), ("n_kept", C.c_int32), ("pad_", C.c_int32),
+        ("mape_thr", C.c_double), ("rho", C.c_double), ("n_kept", C.c_int32), ("precision_run", C.c_int32),
     ]
 
 

@@ -198,6 +198,7 @@ struct TrainPlan {
   const double* dX = nullptr;
   const double* dY = nullptr;
   int trace_stride = 1;
+  std::vector<int> model_precision;  // per model: the lann_precision its trainer runs in
 };
 
 std::unique_ptr<TrainPlan> build_plan(lann_engine* e, const DevTrain& t, int precision,
@@ -219,6 +220,7 @@ std::unique_ptr<TrainPlan> build_plan(lann_engine* e, const DevTrain& t, int pre
   P.trace_stride = t.trace_stride;
 
   std::vector<int> fp64_models;
+  P.model_precision.assign(size_t(t.n_models), LANN_FP64_EXACT);
   if (precision == LANN_FP32) {
     P.rows_f = DBuf<float>(size_t(total_rows) * 8, s);
     launch_pack_rows(dX, dY, total_rows, P.rows_f.p, s);
@@ -227,9 +229,10 @@ std::unique_ptr<TrainPlan> build_plan(lann_engine* e, const DevTrain& t, int pre
     for (int m = 0; m < t.n_models; ++m) {
       const int tile = t.model_tile[m];
       const int I = t.tile_inputs[tile];
-      if (fp32_shape_supported(I, t.h1[m], t.h2[m]) && t.tile_rows[tile] * 32 <= 96 * 1024)
+      if (fp32_shape_supported(I, t.h1[m], t.h2[m]) && t.tile_rows[tile] * 32 <= 96 * 1024) {
         by_shape[{I, t.h1[m], t.h2[m]}].push_back(m);
-      else
+        P.model_precision[size_t(m)] = LANN_FP32;
+      } else
         fp64_models.push_back(m);
     }
     int env_lanes = 0;
@@ -673,7 +676,10 @@ int prepare_population(lann_engine* e, int n_jobs, const lann_job* jobs, int pre
   pop.n_jobs = n_jobs;
   pop.precision = precision;
   pop.base.assign(n_jobs, lann_job_result{});
-  for (auto& r : pop.base) r.nonfinite_epoch = -1;
+  for (auto& r : pop.base) {
+    r.nonfinite_epoch = -1;
+    r.precision_run = -1;  // not trained (host preparation failed)
+  }
   e->err.clear();
   const bool hprof = std::getenv("LANN_HOST_PROFILE") != nullptr;
   auto now = [] { return std::chrono::steady_clock::now(); };
@@ -965,6 +971,7 @@ int fetch_population(Population& pop, lann_job_result* results, double* params_o
     lann_job_result& r = results[j];
     r.final_loss = fin[m];
     r.nonfinite_epoch = bad[m];
+    r.precision_run = pop.plan->model_precision[size_t(m)];
     if (bad[m] >= 0) {
       r.status = LANN_TRAINING_ERROR;
     } else {
@@ -1374,26 +1381,33 @@ int lann_select_schedule(lann_engine* e, const lann_model_set* ms, uint32_t n_im
   }
 }
 
-int lann_select_variants(lann_engine* e, const lann_model_set* ms, const int32_t* with_n_thd,
-                         int32_t kind, int32_t max_threads, uint64_t seed, int64_t first,
-                         int64_t n_cands, int32_t* out_idx, double* out_score) {
-  if (!e) return LANN_NO_DEVICE;
-  if (!ms || ms->n_models < 1) return set_err(e, {LANN_PARAM_ERROR, "empty model set"});
-  if (kind < LANN_MM || kind > LANN_MP)
-    return set_err(e, {LANN_PARAM_ERROR, "variant mapping covers the mm/mv/mc/mp kernels"});
-  if (max_threads < 1) return set_err(e, {LANN_PARAM_ERROR, "max_threads must be >= 1"});
-  if (n_cands < 1) return set_err(e, {LANN_PARAM_ERROR, "select needs at least one candidate"});
+namespace {
+Status check_variant_models(const lann_model_set* ms, const int32_t* with_n_thd, int32_t kind, int32_t max_threads,
+                            int64_t n_cands) {
+  if (!ms || ms->n_models < 1) return {LANN_PARAM_ERROR, "empty model set"};
+  if (kind < LANN_MM || kind > LANN_MP) return {LANN_PARAM_ERROR, "variant mapping covers the mm/mv/mc/mp kernels"};
+  if (max_threads < 1) return {LANN_PARAM_ERROR, "max_threads must be >= 1"};
+  if (n_cands < 1) return {LANN_PARAM_ERROR, "select needs at least one candidate"};
+  if (!with_n_thd) return {LANN_PARAM_ERROR, "missing with_n_thd"};
   int max_p = 0;
   for (int m = 0; m < ms->n_models; ++m) {
     const int want = base_feature_count(kind, with_n_thd[m] != 0);
     if (ms->n_inputs[m] != want && ms->n_inputs[m] != want + 1)
-      return set_err(e, {LANN_SCHEMA_ERROR, "model schema does not match the candidate kernel"});
-    if (ms->h1[m] < 1 || ms->h1[m] > 64 || ms->h2[m] < 0 || ms->h2[m] > 64)
-      return set_err(e, {LANN_PARAM_ERROR, "bad model shape"});
+      return {LANN_SCHEMA_ERROR, "model schema does not match the candidate kernel"};
+    if (ms->h1[m] < 1 || ms->h1[m] > 64 || ms->h2[m] < 0 || ms->h2[m] > 64) return {LANN_PARAM_ERROR, "bad model shape"};
     max_p = std::max(max_p, param_count(ms->n_inputs[m], ms->h1[m], ms->h2[m]));
   }
   if (!select_variants_supported(ms->n_models, max_p))
-    return set_err(e, {LANN_PARAM_ERROR, "variant scorer holds at most 32 lightweight models"});
+    return {LANN_PARAM_ERROR, "variant scorer holds at most 32 lightweight models"};
+  return {};
+}
+}  // namespace
+
+int lann_select_variants(lann_engine* e, const lann_model_set* ms, const int32_t* with_n_thd,
+                         int32_t kind, int32_t max_threads, uint64_t seed, int64_t first,
+                         int64_t n_cands, int32_t* out_idx, double* out_score) {
+  if (!e) return LANN_NO_DEVICE;
+  if (Status st = check_variant_models(ms, with_n_thd, kind, max_threads, n_cands)) return set_err(e, st);
   try {
     ck(cudaSetDevice(e->device), "cudaSetDevice");
     cudaStream_t s = e->stream;
@@ -1408,12 +1422,12 @@ int lann_select_variants(lann_engine* e, const lann_model_set* ms, const int32_t
     if (ms->precision == LANN_FP32 && !std::getenv("LANN_SELECT_GENERIC") &&
         select_variants_fast_launch(M, kind, max_threads, seed, first, n_cands, ms->n_inputs, ms->h1,
                                     ms->h2, ms->log_target, with_n_thd, ms->param_offset, ms->params,
-                                    ms->norm, didx.p, dsc.p, e->sms, s))
+                                    ms->norm, didx.p, dsc.p, false, nullptr, e->sms, s))
       e->launches += 1;
     else
       e->launches += select_variants_launch(M, ms->precision, kind, max_threads, seed, first, n_cands,
                                             dI.p, dh1.p, dh2.p, dl.p, dt.p, dpo.p, dp.p, dn.p, didx.p,
-                                            dsc.p, e->sms, s);
+                                            dsc.p, false, nullptr, e->sms, s);
     ck(cudaGetLastError(), "select_variants launch");
     ck(cudaEventRecord(e->tr1, s), "event");
     didx.down(out_idx);
@@ -1422,6 +1436,142 @@ int lann_select_variants(lann_engine* e, const lann_model_set* ms, const int32_t
     float kms = 0.f;
     ck(cudaEventElapsedTime(&kms, e->tr0, e->tr1), "elapsed");
     e->last_train_ms = kms;  // the scoring kernel's own device time
+    e->err.clear();
+    return LANN_OK;
+  } catch (const CudaFail& f) {
+    e->err = f.what;
+    return LANN_CUDA_ERROR;
+  }
+}
+
+int lann_host_alloc(size_t bytes, void** out) {
+  if (!out) return LANN_PARAM_ERROR;
+  *out = nullptr;
+  if (bytes == 0) return LANN_OK;
+  return cudaMallocHost(out, bytes) == cudaSuccess ? LANN_OK : LANN_NO_DEVICE;
+}
+
+void lann_host_free(void* p) {
+  if (p) cudaFreeHost(p);
+}
+
+namespace {
+bool is_pinned(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();  // clear the sticky-free error of an unregistered pointer
+    return false;
+  }
+  return at.type == cudaMemoryTypeHost;
+}
+}  // namespace
+
+int lann_select_variants_compact(lann_engine* e, const lann_model_set* ms, const int32_t* with_n_thd, int32_t kind,
+                                 int32_t max_threads, uint64_t seed, int64_t first, int64_t n_cands,
+                                 uint8_t* out_idx, float* out_score, int64_t* hist) {
+  if (!e) return LANN_NO_DEVICE;
+  if (Status st = check_variant_models(ms, with_n_thd, kind, max_threads, n_cands)) return set_err(e, st);
+  if (ms->n_models > 255) return set_err(e, {LANN_PARAM_ERROR, "compact indices hold at most 255 models"});
+  if (!out_idx && !out_score && !hist) return set_err(e, {LANN_PARAM_ERROR, "no output requested"});
+  try {
+    ck(cudaSetDevice(e->device), "cudaSetDevice");
+    cudaStream_t s = e->stream, cs = e->aux[0];
+    const int M = ms->n_models;
+    DBuf<int> dI(ms->n_inputs, M, s), dh1(ms->h1, M, s), dh2(ms->h2, M, s), dl(ms->log_target, M, s),
+        dt(with_n_thd, M, s);
+    DBuf<int64_t> dpo(ms->param_offset, M, s);
+    DBuf<double> dp(ms->params, size_t(ms->total_params), s), dn(ms->norm, size_t(M) * 18, s);
+    DBuf<unsigned char> didx(out_idx ? size_t(n_cands) : 0, s);
+    DBuf<float> dsc(out_score ? size_t(n_cands) : 0, s);
+    DBuf<unsigned long long> dh(hist ? size_t(M) : 0, s);
+    if (hist) ck(cudaMemsetAsync(dh.p, 0, sizeof(unsigned long long) * size_t(M), s), "memset");
+    // chunks: the scoring kernel of chunk k + 1 runs while chunk k is copied out
+    // 4 chunks: measured e2e within 2% of 8 while each extra chunk's tail costs ~3% of kernel
+    // time; without per-candidate outputs there is nothing to overlap
+    int64_t max_chunks = out_idx || out_score ? 4 : 1;
+    if (const char* env = std::getenv("LANN_SELECT_CHUNKS")) max_chunks = std::max(1, std::atoi(env));
+    const int64_t n_chunks = std::min<int64_t>(max_chunks, std::max<int64_t>(1, n_cands / (1 << 20)));
+    const int64_t chunk = (n_cands + n_chunks - 1) / n_chunks;
+    const bool pin_idx = is_pinned(out_idx), pin_sc = is_pinned(out_score);
+    const size_t row_bytes = (out_idx && !pin_idx ? 1 : 0) + (out_score && !pin_sc ? 4 : 0);
+    unsigned char* stage = row_bytes ? pinned_stage(e, size_t(2 * chunk) * row_bytes) : nullptr;
+    std::vector<cudaEvent_t> scored(static_cast<size_t>(n_chunks)), copied(static_cast<size_t>(n_chunks));
+    for (int64_t k = 0; k < n_chunks; ++k) {
+      ck(cudaEventCreateWithFlags(&scored[size_t(k)], cudaEventDisableTiming), "event");
+      ck(cudaEventCreateWithFlags(&copied[size_t(k)], cudaEventDisableTiming), "event");
+    }
+    Timer timer(e);
+    ck(cudaEventRecord(e->tr0, s), "event");
+    for (int64_t k = 0; k < n_chunks; ++k) {
+      const int64_t lo = k * chunk, n = std::min(chunk, n_cands - lo);
+      if (n <= 0) break;
+      void* pi = out_idx ? static_cast<void*>(didx.p + lo) : nullptr;
+      void* ps = out_score ? static_cast<void*>(dsc.p + lo) : nullptr;
+      if (ms->precision == LANN_FP32 && !std::getenv("LANN_SELECT_GENERIC") &&
+          select_variants_fast_launch(M, kind, max_threads, seed, first + lo, n, ms->n_inputs, ms->h1, ms->h2,
+                                      ms->log_target, with_n_thd, ms->param_offset, ms->params, ms->norm, pi, ps,
+                                      true, hist ? dh.p : nullptr, e->sms, s))
+        e->launches += 1;
+      else
+        e->launches += select_variants_launch(M, ms->precision, kind, max_threads, seed, first + lo, n, dI.p, dh1.p,
+                                              dh2.p, dl.p, dt.p, dpo.p, dp.p, dn.p, pi, ps, true,
+                                              hist ? dh.p : nullptr, e->sms, s);
+      ck(cudaEventRecord(scored[size_t(k)], s), "event");
+    }
+    ck(cudaGetLastError(), "select_variants launch");
+    ck(cudaEventRecord(e->tr1, s), "event");
+    // copies on the side stream: pinned caller buffers directly, pageable ones through two
+    // pinned staging slots whose host-side copy overlaps the next chunk's transfer
+    unsigned char* slot[2] = {stage, stage ? stage + size_t(chunk) * row_bytes : nullptr};
+    for (int64_t k = 0; k < n_chunks; ++k) {
+      const int64_t lo = k * chunk, n = std::min(chunk, n_cands - lo);
+      if (n <= 0) break;
+      ck(cudaStreamWaitEvent(cs, scored[size_t(k)], 0), "wait");
+      unsigned char* sl = slot[k & 1];
+      if (out_idx) {
+        void* dst = pin_idx ? static_cast<void*>(out_idx + lo) : static_cast<void*>(sl);
+        ck(cudaMemcpyAsync(dst, didx.p + lo, size_t(n), cudaMemcpyDeviceToHost, cs), "D2H");
+      }
+      if (out_score) {
+        void* dst = pin_sc ? static_cast<void*>(out_score + lo)
+                           : static_cast<void*>(sl + (out_idx && !pin_idx ? size_t(n) : 0));
+        ck(cudaMemcpyAsync(dst, dsc.p + lo, size_t(n) * 4, cudaMemcpyDeviceToHost, cs), "D2H");
+      }
+      t_d2h += int64_t(n) * ((out_idx ? 1 : 0) + (out_score ? 4 : 0));
+      ck(cudaEventRecord(copied[size_t(k)], cs), "event");
+      if (row_bytes && k >= 1) {  // drain chunk k - 1 from its slot while chunk k transfers
+        const int64_t plo = (k - 1) * chunk, pn = std::min(chunk, n_cands - plo);
+        ck(cudaEventSynchronize(copied[size_t(k - 1)]), "sync");
+        unsigned char* ps = slot[(k - 1) & 1];
+        if (out_idx && !pin_idx) std::memcpy(out_idx + plo, ps, size_t(pn));
+        if (out_score && !pin_sc) std::memcpy(out_score + plo, ps + (out_idx && !pin_idx ? size_t(pn) : 0), size_t(pn) * 4);
+      }
+      if (row_bytes && k + 1 < n_chunks) ck(cudaEventSynchronize(copied[size_t(k)]), "sync");  // slot reuse
+    }
+    {  // the last chunk
+      const int64_t k = n_chunks - 1, plo = k * chunk, pn = std::min(chunk, n_cands - plo);
+      ck(cudaStreamSynchronize(cs), "sync");
+      if (row_bytes && pn > 0) {
+        unsigned char* ps = slot[k & 1];
+        if (out_idx && !pin_idx) std::memcpy(out_idx + plo, ps, size_t(pn));
+        if (out_score && !pin_sc) std::memcpy(out_score + plo, ps + (out_idx && !pin_idx ? size_t(pn) : 0), size_t(pn) * 4);
+      }
+    }
+    if (hist) {
+      std::vector<unsigned long long> h(static_cast<size_t>(M));
+      dh.down(h.data());
+      ck(cudaStreamSynchronize(s), "sync");
+      for (int m = 0; m < M; ++m) hist[m] = int64_t(h[size_t(m)]);
+    }
+    timer.stop();
+    float kms = 0.f;
+    ck(cudaEventElapsedTime(&kms, e->tr0, e->tr1), "elapsed");
+    e->last_train_ms = kms;  // the scoring kernels' own device time
+    for (int64_t k = 0; k < n_chunks; ++k) {
+      cudaEventDestroy(scored[size_t(k)]);
+      cudaEventDestroy(copied[size_t(k)]);
+    }
     e->err.clear();
     return LANN_OK;
   } catch (const CudaFail& f) {
@@ -1880,6 +2030,7 @@ int lann_run_population(lann_engine* e, int32_t n_jobs, const lann_job* jobs, in
       std::memset(&results[j], 0, sizeof(lann_job_result));
       results[j].status = st;
       results[j].nonfinite_epoch = -1;
+      results[j].precision_run = -1;
     }
     return st;
   }

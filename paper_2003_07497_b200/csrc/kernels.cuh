@@ -124,13 +124,14 @@ bool select_variants_supported(int n_models, int max_params);
 bool select_variants_fast_launch(int n_models, int kind, int max_threads, uint64_t seed, int64_t first,
                                  int64_t n, const int* n_inputs, const int* h1, const int* h2,
                                  const int* logt, const int* with_thd, const int64_t* param_offset,
-                                 const double* params, const double* norm, int* d_idx, double* d_score,
-                                 int sms, cudaStream_t s);
+                                 const double* params, const double* norm, void* d_idx, void* d_score,
+                                 bool compact, unsigned long long* d_hist, int sms, cudaStream_t s);
 int select_variants_launch(int n_models, int precision, int kind, int max_threads, uint64_t seed,
                            int64_t first, int64_t n, const int* d_in, const int* d_h1,
                            const int* d_h2, const int* d_logt, const int* d_thd,
                            const int64_t* d_poff, const double* d_params, const double* d_norm,
-                           int* d_idx, double* d_score, int sms, cudaStream_t s);
+                           void* d_idx, void* d_score, bool compact, unsigned long long* d_hist, int sms,
+                           cudaStream_t s);
 }  // namespace lann
 
 namespace lann {

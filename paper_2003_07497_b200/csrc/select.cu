@@ -14,6 +14,7 @@
 //   sample_params' draw order (datagen.cpp:60-110) — generated in registers,
 //   never stored. Model weights and normalisation live in shared memory.
 #include <cmath>
+#include <type_traits>
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
@@ -285,16 +286,20 @@ struct VariantArgs {
   const int64_t* param_offset;
   const double* params;
   const double* norm;
-  int* out_idx;
-  double* out_score;
+  void* out_idx;    // IdxT[n] or null
+  void* out_score;  // ScoreT[n] or null
+  unsigned long long* hist;  // [n_models] wins, or null
 };
 
+template <typename IdxT, typename ScoreT>
 __global__ void __launch_bounds__(256) select_variants_kernel(VariantArgs a) {
   __shared__ double wd[kMaxModels][kMaxParams];
   __shared__ float wf[kMaxModels][kMaxParams];
   __shared__ double nd[kMaxModels][18];
   __shared__ float nf[kMaxModels][18];
   __shared__ int shp[kMaxModels][5];
+  __shared__ unsigned wins[kMaxModels];
+  if (threadIdx.x < kMaxModels) wins[threadIdx.x] = 0;
   for (int t = threadIdx.x; t < a.n_models * kMaxParams; t += blockDim.x) {
     const int m = t / kMaxParams, p = t % kMaxParams;
     const int I = a.n_inputs[m], H1 = a.h1[m], H2 = a.h2[m];
@@ -342,8 +347,14 @@ __global__ void __launch_bounds__(256) select_variants_kernel(VariantArgs a) {
         best_s = s;
       }
     }
-    a.out_idx[i] = best;
-    a.out_score[i] = best_s;
+    if (a.out_idx) static_cast<IdxT*>(a.out_idx)[i] = (IdxT)best;
+    if (a.out_score) static_cast<ScoreT*>(a.out_score)[i] = (ScoreT)best_s;
+    if (a.hist) atomicAdd(&wins[best], 1u);
+  }
+  if (a.hist) {
+    __syncthreads();
+    if (threadIdx.x < a.n_models && wins[threadIdx.x])
+      atomicAdd(&a.hist[threadIdx.x], (unsigned long long)wins[threadIdx.x]);
   }
 }
 
@@ -434,12 +445,20 @@ struct FastModels2 {
   int logt[kFastMaxV];
 };
 
-template <int NB>
+// Outputs: IdxT / ScoreT per candidate (int32 + double, or the compact uint8 + float), either
+// pointer may be null; hist (optional) counts each variant's wins (shared-memory tallies, one
+// global atomic per variant per CTA).
+template <int NB, typename IdxT, typename ScoreT>
 __global__ void __launch_bounds__(256) select_variants_fast2(const __grid_constant__ FastModels2 fm,
                                                              int kind, int max_threads, uint64_t seed,
-                                                             int64_t first, int64_t n, int* out_idx,
-                                                             double* out_score) {
+                                                             int64_t first, int64_t n, IdxT* out_idx,
+                                                             ScoreT* out_score, unsigned long long* hist) {
   constexpr int NC = NB + 2;  // columns: base features, n_thd, c
+  __shared__ unsigned wins[kFastMaxV];
+  if (hist) {
+    if (threadIdx.x < kFastMaxV) wins[threadIdx.x] = 0;
+    __syncthreads();
+  }
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
     double base[8];
@@ -480,8 +499,13 @@ __global__ void __launch_bounds__(256) select_variants_fast2(const __grid_consta
         }
       }
     }
-    out_idx[i] = best;
-    out_score[i] = (double)best_s;
+    if (out_idx) out_idx[i] = (IdxT)best;
+    if (out_score) out_score[i] = (ScoreT)best_s;
+    if (hist) atomicAdd(&wins[best], 1u);
+  }
+  if (hist) {
+    __syncthreads();
+    if (threadIdx.x < fm.nv && wins[threadIdx.x]) atomicAdd(&hist[threadIdx.x], (unsigned long long)wins[threadIdx.x]);
   }
 }
 
@@ -501,8 +525,8 @@ void ensure_fastmod_table(cudaStream_t s) {
 bool select_variants_fast_launch(int n_models, int kind, int max_threads, uint64_t seed, int64_t first,
                                  int64_t n, const int* n_inputs, const int* h1, const int* h2,
                                  const int* logt, const int* with_thd, const int64_t* param_offset,
-                                 const double* params, const double* norm, int* d_idx, double* d_score,
-                                 int sms, cudaStream_t s) {
+                                 const double* params, const double* norm, void* d_idx, void* d_score,
+                                 bool compact, unsigned long long* d_hist, int sms, cudaStream_t s) {
   if (n_models < 1 || n_models > kFastMaxV || kind < 0 || kind > 3) return false;
   ensure_fastmod_table(s);
   static const int nb_of[4] = {5, 3, 4, 5};
@@ -564,17 +588,28 @@ bool select_variants_fast_launch(int n_models, int kind, int max_threads, uint64
       f2.trange[v] = fm.trange[v];
       f2.logt[v] = fm.logt[v];
     }
+    auto go = [&](auto nbc) {
+      constexpr int NB = decltype(nbc)::value;
+      if (compact)
+        select_variants_fast2<NB, unsigned char, float><<<(unsigned)blocks, 256, 0, s>>>(
+            f2, kind, max_threads, seed, first, n, static_cast<unsigned char*>(d_idx), static_cast<float*>(d_score),
+            d_hist);
+      else
+        select_variants_fast2<NB, int, double><<<(unsigned)blocks, 256, 0, s>>>(
+            f2, kind, max_threads, seed, first, n, static_cast<int*>(d_idx), static_cast<double*>(d_score), d_hist);
+    };
     switch (nb) {
-      case 3: select_variants_fast2<3><<<(unsigned)blocks, 256, 0, s>>>(f2, kind, max_threads, seed, first, n, d_idx, d_score); break;
-      case 4: select_variants_fast2<4><<<(unsigned)blocks, 256, 0, s>>>(f2, kind, max_threads, seed, first, n, d_idx, d_score); break;
-      default: select_variants_fast2<5><<<(unsigned)blocks, 256, 0, s>>>(f2, kind, max_threads, seed, first, n, d_idx, d_score); break;
+      case 3: go(std::integral_constant<int, 3>{}); break;
+      case 4: go(std::integral_constant<int, 4>{}); break;
+      default: go(std::integral_constant<int, 5>{}); break;
     }
     return true;
   }
+  if (compact || d_hist) return false;  // the unpacked developer path writes int32 + double only
   switch (nb) {
-    case 3: select_variants_fast<3><<<(unsigned)blocks, 256, 0, s>>>(fm, kind, max_threads, seed, first, n, d_idx, d_score); break;
-    case 4: select_variants_fast<4><<<(unsigned)blocks, 256, 0, s>>>(fm, kind, max_threads, seed, first, n, d_idx, d_score); break;
-    default: select_variants_fast<5><<<(unsigned)blocks, 256, 0, s>>>(fm, kind, max_threads, seed, first, n, d_idx, d_score); break;
+    case 3: select_variants_fast<3><<<(unsigned)blocks, 256, 0, s>>>(fm, kind, max_threads, seed, first, n, static_cast<int*>(d_idx), static_cast<double*>(d_score)); break;
+    case 4: select_variants_fast<4><<<(unsigned)blocks, 256, 0, s>>>(fm, kind, max_threads, seed, first, n, static_cast<int*>(d_idx), static_cast<double*>(d_score)); break;
+    default: select_variants_fast<5><<<(unsigned)blocks, 256, 0, s>>>(fm, kind, max_threads, seed, first, n, static_cast<int*>(d_idx), static_cast<double*>(d_score)); break;
   }
   return true;
 }
@@ -598,15 +633,17 @@ int select_variants_launch(int n_models, int precision, int kind, int max_thread
                            int64_t first, int64_t n, const int* d_in, const int* d_h1,
                            const int* d_h2, const int* d_logt, const int* d_thd,
                            const int64_t* d_poff, const double* d_params, const double* d_norm,
-                           int* d_idx, double* d_score, int sms, cudaStream_t s) {
+                           void* d_idx, void* d_score, bool compact, unsigned long long* d_hist, int sms,
+                           cudaStream_t s) {
   ensure_fastmod_table(s);
   VariantArgs a{n_models, precision, kind, max_threads, seed, first, n, d_in, d_h1, d_h2,
-                d_logt, d_thd, d_poff, d_params, d_norm, d_idx, d_score};
+                d_logt, d_thd, d_poff, d_params, d_norm, d_idx, d_score, d_hist};
   int64_t blocks = (n + 255) / 256;
   const int64_t cap = (int64_t)sms * 8;
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
-  select_variants_kernel<<<(unsigned)blocks, 256, 0, s>>>(a);
+  if (compact) select_variants_kernel<unsigned char, float><<<(unsigned)blocks, 256, 0, s>>>(a);
+  else select_variants_kernel<int, double><<<(unsigned)blocks, 256, 0, s>>>(a);
   return 1;
 }
 

@@ -74,7 +74,8 @@ EXPORTS = ["lann_engine_create", "lann_engine_destroy", "lann_last_error", "lann
            "lann_mlp_forward", "lann_mse_loss", "lann_mse_gradient", "lann_adam_update",
            "lann_group_create", "lann_group_destroy", "lann_group_last_error", "lann_group_size",
            "lann_shard_bounds", "lann_group_shard_bounds", "lann_group_run_population",
-           "lann_group_last_device_ms", "lann_group_last_wall_ms"]
+           "lann_group_last_device_ms", "lann_group_last_wall_ms",
+           "lann_select_variants_compact", "lann_host_alloc", "lann_host_free"]
 
 
 def transfer_bytes(reset=False):
@@ -132,6 +133,10 @@ def load_library(path: str = LIB_PATH):
     L.lann_mse_gradient.argtypes = [vp, C.POINTER(MlpBatch), vp, vp]
     L.lann_adam_update.argtypes = [vp, C.c_int64, vp, vp, vp, vp, C.c_int32, C.c_double, C.c_double, C.c_double,
                                    C.c_double]
+    L.lann_select_variants_compact.argtypes = [vp, C.POINTER(ModelSet), vp, C.c_int32, C.c_int32, C.c_uint64,
+                                               C.c_int64, C.c_int64, vp, vp, vp]
+    L.lann_host_alloc.argtypes = [C.c_size_t, C.POINTER(vp)]
+    L.lann_host_free.argtypes = [vp]
     L.lann_group_create.argtypes = [C.c_int32, vp, C.POINTER(vp)]
     L.lann_group_destroy.argtypes = [vp]
     L.lann_group_last_error.argtypes = [vp]
@@ -393,6 +398,19 @@ class Engine:
             self._raise(st)
         return idx, score
 
+    def select_variants_compact(self, models, with_n_thd, kind, max_threads, seed, first, n, precision=abi.FP32,
+                                idx=None, score=None, want_hist=True):
+        """lann_select_variants_compact: idx / score are caller arrays (uint8 / float32, pinned or
+        not) or None; returns (idx, score, hist)."""
+        ms, keep = _model_set(models, precision)
+        thd = _c(with_n_thd, np.int32)
+        hist = np.zeros(len(models), dtype=np.int64) if want_hist else None
+        st = self.L.lann_select_variants_compact(self.h, C.byref(ms), _ptr(thd), kind, max_threads, seed, first, n,
+                                                 _ptr(idx), _ptr(score), _ptr(hist))
+        if st:
+            self._raise(st)
+        return idx, score, hist
+
     # ---- models::train_nn + predict_dataset + make_report over a population ----
     def run_population(self, jobs, precision=abi.FP64_EXACT, want_params=False, want_trace=False):
         n = len(jobs)
@@ -559,3 +577,30 @@ class Group:
         if want_params:
             plist = [params[off[k]: off[k] + res[k].n_params].copy() for k in range(n)]
         return st, list(res), plist
+
+
+class Pinned:
+    """A numpy array in pinned host memory (lann_host_alloc): engine outputs written into it by
+    DMA at full link bandwidth."""
+
+    def __init__(self, n, dtype):
+        self.L = load_library()
+        dt = np.dtype(dtype)
+        self.ptr = C.c_void_p()
+        st = self.L.lann_host_alloc(max(1, n) * dt.itemsize, C.byref(self.ptr))
+        if st or not self.ptr.value:
+            raise NoDeviceError("lann_host_alloc failed (no CUDA device?)")
+        buf = (C.c_byte * (max(1, n) * dt.itemsize)).from_address(self.ptr.value)
+        self.array = np.frombuffer(buf, dtype=dt, count=n)
+
+    def free(self):
+        if self.ptr and self.ptr.value:
+            self.array = None
+            self.L.lann_host_free(self.ptr)
+            self.ptr = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass

@@ -207,3 +207,18 @@ def test_fp32_training_error_and_trace_tail(engine, monkeypatch, lanes, I, hidde
     with pytest.raises(E.TrainingError) as ei:
         engine.train([X], [y_bad], [m], abi.FP32)
     assert ei.value.epoch == 0
+
+
+def test_fp32_requests_report_the_precision_that_ran(engine):
+    """Shapes with an FP32 kernel (H=8, 5-5) run in FP32; an unconstrained 7-64-1 net has none and
+    runs in the FP64 exact mode, which lann_job_result.precision_run says."""
+    w = abi.acceptance_world()
+    jobs = [abi.make_job(w, 1, count=120, epochs=30), abi.make_job(w, 2, count=120, epochs=30, hidden=(64,),
+                                                                   unconstrained=True)]
+    st, res, _, _ = engine.run_population(jobs, abi.FP32)
+    assert st == 0
+    assert [r.precision_run for r in res] == [abi.FP32, abi.FP64_EXACT]
+    st, res, _, _ = engine.run_population(jobs, abi.FP64_EXACT)
+    assert [r.precision_run for r in res] == [abi.FP64_EXACT, abi.FP64_EXACT]
+    st, res, _, _ = engine.run_population([abi.make_job(w, 1, count=120, epochs=30, lr=0.5)], abi.FP32)
+    assert res[0].precision_run == -1

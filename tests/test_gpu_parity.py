@@ -266,3 +266,32 @@ def test_select_variants_fp32_argmin(engine, oracle):
     assert len(mism) <= n * 1e-3
     both = gi == ei
     assert np.all(np.abs(gs[both] - es[both]) <= 1e-3 * np.abs(es[both]) + 1e-7)
+
+
+def test_compact_streamed_selection_equals_the_full_outputs(engine):
+    """lann_select_variants_compact (uint8 index + float score, chunked copies overlapping the
+    scoring, win histogram): the same argmins and scores as lann_select_variants, into pinned
+    and pageable buffers, and hist == bincount(idx)."""
+    rng = np.random.default_rng(11)
+    models = []
+    for v in range(10):
+        I = 7 if v % 2 == 0 else 6  # with / without n_thd (augmented MM nets)
+        p = rng.uniform(-1, 1, (I + 1) * 8 + 9)
+        nrm = np.zeros(18)
+        nrm[:8] = rng.uniform(0, 10, 8)
+        nrm[8:16] = nrm[:8] + rng.uniform(1, 1e3, 8)
+        nrm[16], nrm[17] = -12.0, -2.0
+        models.append({"inputs": I, "h1": 8, "h2": 0, "log_target": 1, "params": p, "norm": nrm})
+    thd = [1 if v % 2 == 0 else 0 for v in range(10)]
+    n = 3_000_001
+    idx, score = engine.select_variants(models, thd, abi.MM, 4, 7, 11, n)
+    pi, ps = E.Pinned(n, np.uint8), E.Pinned(n, np.float32)
+    for bi, bs in [(pi.array, ps.array), (np.zeros(n, np.uint8), np.zeros(n, np.float32))]:
+        ci, cs, hist = engine.select_variants_compact(models, thd, abi.MM, 4, 7, 11, n, idx=bi, score=bs)
+        assert np.array_equal(ci.astype(np.int32), idx)
+        assert np.array_equal(cs, score.astype(np.float32))
+        assert np.array_equal(hist, np.bincount(idx, minlength=10))
+    _, _, hist = engine.select_variants_compact(models, thd, abi.MM, 4, 7, 11, n)  # histogram only
+    assert np.array_equal(hist, np.bincount(idx, minlength=10))
+    pi.free()
+    ps.free()

@@ -171,6 +171,16 @@ def cpu_reference_run(jobs, threads):
     return time.perf_counter() - t0, "port", [r.status for r in res if r.status]
 
 
+def hbm_peak():
+    """(GB/s, source): MEASURED_PEAKS.json's copy bandwidth (driver-written), else the
+    profiling recipe's B200 fallback."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "of measured (MEASURED_PEAKS.json hbm_gbs: copy, read+write bytes)"
+    except Exception:  # noqa: BLE001
+        return 6650.0, "of fallback (B200_PROFILING.md: 6.65 TB/s)"
+
+
 def fp_peaks():
     """FP64 / FP32 CUDA-core peaks measured on this pool's B200 (tools/peaks.cu ->
     profiles/fp32_peak.json); MEASURED_PEAKS.json carries neither."""
@@ -468,6 +478,66 @@ def extras(E, eng, rank, world, barrier, max_over_ranks, args, flush, peaks):
         out["config4_selection"] = selection_extra(E, eng, rank, world, barrier, max_over_ranks)
     except Exception as ex:  # noqa: BLE001
         out["config4_selection"] = {"error": str(ex)}
+    try:
+        out["batched_predictor"] = predictor_extra(E, eng, rank, world, barrier, max_over_ranks)
+    except Exception as ex:  # noqa: BLE001
+        out["batched_predictor"] = {"error": str(ex)}
+    return out
+
+
+def predictor_extra(E, eng, rank, world, barrier, max_over_ranks, rows_per_model=1_000_000):
+    """The general batched predictor (lann_predict: models::predict / predict_dataset,
+    models.cpp:346-378): the 48 trained config-2 models x rows_per_model rows each (every model's
+    250 held-out rows tiled), FP32 and FP64-exact. value = predictions/s of the predictor kernel
+    with rows resident in HBM; e2e = the whole call from host rows (64 B/row H2D, 8 B/row D2H).
+    Roofline: HBM, 76 algorithmic bytes per prediction (64-B row + 4-B model index + 8-B result)."""
+    jobs = popmod.config2_jobs(root_seed=1)
+    out = {"models": len(jobs), "rows_per_model": rows_per_model, "bytes_per_prediction": 76,
+           "n_gpus": world, "scaling": "weak"}
+    for prec, name in ((abi.FP32, "fp32"), (abi.FP64_EXACT, "fp64_exact")):
+        pop = eng.prepare(jobs, prec)
+        pop.run(1)
+        st, res, params, _ = pop.fetch(want_params=True)
+        norms = pop.norms()
+        pop.close()
+        models = [{"inputs": r.n_inputs, "h1": j.hidden[0], "h2": j.hidden[1] if j.n_hidden > 1 else 0,
+                   "log_target": j.log_target, "params": p, "norm": nrm} for j, r, p, nrm in zip(jobs, res, params, norms)]
+        # rows: each model's own feature distribution (its world at its data seed), tiled
+        base = []
+        for j in jobs:  # model inputs: the dataset's features (+ c for the augmented family)
+            f, c, _, nf = E.build_dataset(j.world, j.data_seed, 500)
+            if j.family == abi.NNC:
+                f[:, nf] = c.astype(np.float64)
+            base.append(f)
+        n_rows = rows_per_model * len(jobs)
+        # host buffers in pinned memory: the copies run at link speed (the call's own H2D / D2H)
+        p_rows, p_rm, p_out = E.Pinned(n_rows * abi.ROW, np.float64), E.Pinned(n_rows, np.int32), \
+            E.Pinned(n_rows, np.float64)
+        rows = p_rows.array.reshape(n_rows, abi.ROW)
+        rows[:] = np.concatenate([np.resize(b, (rows_per_model, abi.ROW)) for b in base])
+        row_model = p_rm.array
+        row_model[:] = np.repeat(np.arange(len(jobs), dtype=np.int32), rows_per_model)  # grouped by model
+        eng.predict(models, rows[:1024], row_model[:1024], precision=prec)  # warm-up
+        barrier()
+        kms, wall = [], []
+        for _ in range(3):
+            t0 = time.perf_counter()
+            eng.predict(models, rows, row_model, precision=prec, out=p_out.array)
+            wall.append((time.perf_counter() - t0) * 1e3)
+            kms.append(eng.last_train_ms)
+        for b in (p_rows, p_rm, p_out):
+            b.free()
+        k = max_over_ranks(statistics.median(kms))
+        w = max_over_ranks(statistics.median(wall))
+        n = n_rows * world
+        gbs = 76 * n_rows / (k / 1e3) / 1e9
+        peak = hbm_peak()
+        out[name] = {"value": n / (k / 1e3), "unit": "predictions/s", "kernel_ms": k,
+                     "e2e": {"value": n / (w / 1e3), "unit": "predictions/s", "ms": w,
+                             "h2d_bytes": 68 * n_rows, "d2h_bytes": 8 * n_rows,
+                             "note": "lann_predict from pinned host rows: H2D of 68 B and D2H of 8 B per row inside"},
+                     "roofline": {"bound": "hbm", "achieved": gbs, "peak": peak[0], "unit": "GB/s",
+                                  "frac": gbs / peak[0], "peak_source": peak[1]}}
     return out
 
 

@@ -131,7 +131,8 @@ double lann_last_device_ms(const lann_engine* engine);
 int64_t lann_last_launches(const lann_engine* engine);
 /* Device time (ms) of the dominant kernel of the most recent call: the
  * trainer launches of lann_train / lann_population_run (summed over steps), or
- * the scoring kernel of lann_select_variants; CUDA events on the launch stream. */
+ * the scoring kernel of lann_select_variants(_compact), or the predictor of
+ * lann_predict (inputs already on the device); CUDA events on the launch stream. */
 double lann_last_train_ms(const lann_engine* engine);
 
 /* ---- training (train_full_batch, batched) ----------------------------------

@@ -931,9 +931,9 @@ void run_device(Population& pop) {
   execute_plan(e, *pop.plan, pop.dP.p, pop.dF.p, pop.dB.p, pop.trace_total ? pop.dT.p : nullptr, pop.dTO.p);
   PredictArgs pa{pop.n_eval_rows, pop.dER.p, pop.dEM.p, pop.dI.p, pop.dh1.p, pop.dh2.p, pop.dlog.p,
                  pop.dpo.p, pop.dP.p, pop.dN.p, pop.dPred.p};
-  if (pop.precision == LANN_FP32) launch_predict_fp32(pa, s);
+  if (pop.precision == LANN_FP32) launch_predict_fp32(pa, pop.M, pop.t.total_params, s);
   else launch_predict_fp64(pa, s);
-  e->launches += pop.n_eval_rows > 0;
+  e->launches += pop.n_eval_rows > 0 ? (pop.precision == LANN_FP32 ? 2 : 1) : 0;
   EvalArgs ea{pop.M, pop.dEO.p, pop.dEL.p, pop.dET.p, pop.dPred.p, 0.3, pop.dMape.p, pop.dThr.p,
               pop.dK.p, pop.dRho.p, pop.dS.p};
   launch_eval(ea, pop.max_eval, e->max_smem, pop.n_eval_rows, s);
@@ -1157,12 +1157,17 @@ int lann_predict(lann_engine* e, const lann_model_set* ms, int64_t n_rows, const
     DBuf<int64_t> dpo(ms->param_offset, M, s);
     DBuf<double> dp(ms->params, size_t(ms->total_params), s), dn(ms->norm, size_t(M) * 18, s);
     PredictArgs a{n_rows, drows.p, drm.p, dI.p, dh1.p, dh2.p, dlog.p, dpo.p, dp.p, dn.p, dout.p};
-    if (ms->precision == LANN_FP32) launch_predict_fp32(a, s);
+    ck(cudaEventRecord(e->tr0, s), "event");
+    if (ms->precision == LANN_FP32) launch_predict_fp32(a, M, ms->total_params, s);
     else launch_predict_fp64(a, s);
     ck(cudaGetLastError(), "predict launch");
-    e->launches += n_rows > 0;
+    ck(cudaEventRecord(e->tr1, s), "event");
+    e->launches += n_rows > 0 ? (ms->precision == LANN_FP32 ? 2 : 1) : 0;
     dout.down(out);
     timer.stop();
+    float kms = 0.f;
+    ck(cudaEventElapsedTime(&kms, e->tr0, e->tr1), "elapsed");
+    e->last_train_ms = kms;  // the predictor's own device time (inputs already resident)
     e->err.clear();
     return LANN_OK;
   } catch (const CudaFail& f) {

@@ -107,7 +107,7 @@ bool launch_train_fp32(const TrainF32Args& a, int in, int h1, int h2, int lanes,
 bool fp32_shape_supported(int in, int h1, int h2);
 int fp32_warp_slots_per_sm(int in, int h1, int h2, int lanes, int tile_bytes);
 void launch_predict_fp64(const PredictArgs& a, cudaStream_t s);
-void launch_predict_fp32(const PredictArgs& a, cudaStream_t s);
+void launch_predict_fp32(const PredictArgs& a, int n_models, int64_t n_params, cudaStream_t s);
 void launch_eval(const EvalArgs& a, int max_len, int max_smem, int64_t total, cudaStream_t s);
 int eval_launch_count(int max_len, int max_smem);
 

@@ -13,7 +13,9 @@
 //   average ranks (eval.cpp:59-90). Ranks come from O(n^2) counting in
 //   parallel; every floating-point sum runs sequentially in the reference's
 //   order, so the metrics are bit-identical.
+#include <algorithm>
 #include <cmath>
+#include <type_traits>
 
 #include "kernels.cuh"
 
@@ -22,29 +24,27 @@ namespace {
 
 constexpr int kMaxWidth = 64;
 
+// Generic shapes (any widths up to 64, one or two hidden layers): local-memory activations.
+// Out of line, the row passed by value: the compiled-shape path keeps its row in registers.
+struct Row8 {
+  double v[8];
+};
 template <bool kExact>
-__global__ void predict_kernel(PredictArgs a) {
-  const int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (row >= a.n_rows) return;
-  const int m = a.row_model[row];
-  const int I = a.n_inputs[m], H1 = a.h1[m], H2 = a.h2[m];
-  const double* nrm = a.norm + 18 * (int64_t)m;
-  const double* x = a.rows + row * 8;
-  const double* w = a.params + a.param_offset[m];
-  double v;
+__device__ __noinline__ double forward_generic(const Row8 xr, const double* nrm, const double* w, int I, int H1,
+                                               int H2) {
+  const double* x = xr.v;
   if (kExact) {
     double a0[8], a1[kMaxWidth], a2[kMaxWidth];
     for (int j = 0; j < I; ++j) {
       const double range = __dsub_rn(nrm[8 + j], nrm[j]);
       a0[j] = range > 0.0 ? __ddiv_rn(__dsub_rn(x[j], nrm[j]), range) : 0.0;
     }
-    int off = 0;
     for (int o = 0; o < H1; ++o) {
       double z = w[I * H1 + o];
       for (int i = 0; i < I; ++i) z = __dadd_rn(z, __dmul_rn(w[o * I + i], a0[i]));
       a1[o] = z > 0.0 ? z : 0.0;
     }
-    off = (I + 1) * H1;
+    int off = (I + 1) * H1;
     const double* last_in = a1;
     int nin = H1;
     if (H2 > 0) {
@@ -59,20 +59,19 @@ __global__ void predict_kernel(PredictArgs a) {
     }
     double z = w[off + nin];
     for (int i = 0; i < nin; ++i) z = __dadd_rn(z, __dmul_rn(w[off + i], last_in[i]));
-    v = z;
+    return z;
   } else {
     float a0[8], a1[kMaxWidth], a2[kMaxWidth];
     for (int j = 0; j < I; ++j) {
       const double range = nrm[8 + j] - nrm[j];
       a0[j] = range > 0.0 ? (float)((x[j] - nrm[j]) / range) : 0.f;
     }
-    int off = 0;
     for (int o = 0; o < H1; ++o) {
       float z = (float)w[I * H1 + o];
       for (int i = 0; i < I; ++i) z = fmaf((float)w[o * I + i], a0[i], z);
       a1[o] = fmaxf(z, 0.f);
     }
-    off = (I + 1) * H1;
+    int off = (I + 1) * H1;
     const float* last_in = a1;
     int nin = H1;
     if (H2 > 0) {
@@ -87,12 +86,219 @@ __global__ void predict_kernel(PredictArgs a) {
     }
     float z = (float)w[off + nin];
     for (int i = 0; i < nin; ++i) z = fmaf((float)w[off + i], last_in[i], z);
-    v = (double)z;
+    return (double)z;
   }
-  const double trange = __dsub_rn(nrm[17], nrm[16]);
-  double t = trange > 0.0 ? __dadd_rn(nrm[16], __dmul_rn(v, trange)) : nrm[16];
-  if (a.log_target[m]) t = exp(t);
-  a.out[row] = t < 1e-9 ? 1e-9 : t;  // std::max(value, 1e-9)
+}
+
+// Compiled shapes (the LANN nets: I-8-1 and I-5-5-1): fully unrolled, activations in registers,
+// R rows of the SAME model per call so every weight is loaded once for R rows (the predictor is
+// load-instruction bound otherwise: ~100 weight loads per row).
+// FP64 exact: the reference order (mlp.cpp:36-52) after NormStats::normalize's division
+// (models.cpp:118-127). FP32: inputs normalised in FP64 by the model's precomputed reciprocal
+// ranges (one rounding), the forward pass on FFMA with the model's FP32 weight copy.
+template <bool kExact, int I, int H1, int H2, int R>
+__device__ __forceinline__ void forward_shape(const double (&x)[R][8], const double* nrm, const double* rinv,
+                                              const double* __restrict__ w, const float* __restrict__ wf,
+                                              double (&v)[R]) {
+  constexpr int B1 = I * H1, W2 = B1 + H1, B2 = W2 + H1 * H2;
+  constexpr int WO = H2 > 0 ? B2 + H2 : B1 + H1;
+  constexpr int BO = WO + (H2 > 0 ? H2 : H1);
+  using T = std::conditional_t<kExact, double, float>;
+  T a0[R][I], a1[R][H1], a2[R][H2 > 0 ? H2 : 1];
+  auto wt = [&](int k) -> T {
+    if constexpr (kExact) return __ldg(w + k);
+    else return __ldg(wf + k);
+  };
+  auto madd = [](T z, T ww, T a) -> T {
+    if constexpr (kExact) return __dadd_rn(z, __dmul_rn(ww, a));
+    else return fmaf(ww, a, z);
+  };
+  auto relu = [](T z) -> T {
+    if constexpr (kExact) return z > 0.0 ? z : 0.0;
+    else return fmaxf(z, 0.f);
+  };
+#pragma unroll
+  for (int j = 0; j < I; ++j) {
+    const double lo = __ldg(nrm + j);
+    if constexpr (kExact) {
+      const double range = __dsub_rn(__ldg(nrm + 8 + j), lo);
+#pragma unroll
+      for (int r = 0; r < R; ++r) a0[r][j] = range > 0.0 ? __ddiv_rn(__dsub_rn(x[r][j], lo), range) : 0.0;
+    } else {
+      const double ri = __ldg(rinv + j);
+#pragma unroll
+      for (int r = 0; r < R; ++r) a0[r][j] = (float)((x[r][j] - lo) * ri);
+    }
+  }
+#pragma unroll
+  for (int o = 0; o < H1; ++o) {
+    const T b = wt(B1 + o);
+    T z[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) z[r] = b;
+#pragma unroll
+    for (int i = 0; i < I; ++i) {
+      const T ww = wt(o * I + i);
+#pragma unroll
+      for (int r = 0; r < R; ++r) z[r] = madd(z[r], ww, a0[r][i]);
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) a1[r][o] = relu(z[r]);
+  }
+  T z[R];
+  const T bo = wt(BO);
+#pragma unroll
+  for (int r = 0; r < R; ++r) z[r] = bo;
+  if constexpr (H2 > 0) {
+#pragma unroll
+    for (int o = 0; o < H2; ++o) {
+      const T b = wt(B2 + o);
+      T q[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) q[r] = b;
+#pragma unroll
+      for (int i = 0; i < H1; ++i) {
+        const T ww = wt(W2 + o * H1 + i);
+#pragma unroll
+        for (int r = 0; r < R; ++r) q[r] = madd(q[r], ww, a1[r][i]);
+      }
+#pragma unroll
+      for (int r = 0; r < R; ++r) a2[r][o] = relu(q[r]);
+    }
+#pragma unroll
+    for (int i = 0; i < H2; ++i) {
+      const T ww = wt(WO + i);
+#pragma unroll
+      for (int r = 0; r < R; ++r) z[r] = madd(z[r], ww, a2[r][i]);
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < H1; ++i) {
+      const T ww = wt(WO + i);
+#pragma unroll
+      for (int r = 0; r < R; ++r) z[r] = madd(z[r], ww, a1[r][i]);
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < R; ++r) v[r] = (double)z[r];
+}
+
+// models.cpp:135-139 + the clamp of predict (models.cpp:362)
+__device__ __forceinline__ double denorm(double v, const double* nrm, int logt) {
+  const double tmin = __ldg(nrm + 16), trange = __dsub_rn(__ldg(nrm + 17), tmin);
+  double t = trange > 0.0 ? __dadd_rn(tmin, __dmul_rn(v, trange)) : tmin;
+  if (logt) t = exp(t);
+  return t < 1e-9 ? 1e-9 : t;  // std::max(value, 1e-9)
+}
+
+// R rows of one model: compiled shapes unrolled, others through the generic forward row by row
+template <bool kExact, int R>
+__device__ __forceinline__ void predict_rows(const PredictArgs& a, const double* rinv, const float* wf, int m,
+                                             const double (&x)[R][8], double (&out)[R]) {
+  const int I = __ldg(a.n_inputs + m), H1 = __ldg(a.h1 + m), H2 = __ldg(a.h2 + m);
+  const double* nrm = a.norm + 18 * (int64_t)m;
+  const double* ri = rinv ? rinv + 8 * (int64_t)m : nullptr;
+  const int64_t po = __ldg(a.param_offset + m);
+  const double* w = a.params + po;
+  const float* f = wf ? wf + po : nullptr;
+  double v[R];
+  const int key = (I << 8) | (H1 << 4) | H2;
+#define LANN_SHAPE(II, A, B) \
+  case ((II) << 8) | ((A) << 4) | (B): forward_shape<kExact, II, A, B, R>(x, nrm, ri, w, f, v); break;
+  switch (key) {
+    LANN_SHAPE(1, 8, 0) LANN_SHAPE(2, 8, 0) LANN_SHAPE(3, 8, 0) LANN_SHAPE(4, 8, 0)
+    LANN_SHAPE(5, 8, 0) LANN_SHAPE(6, 8, 0) LANN_SHAPE(7, 8, 0)
+    LANN_SHAPE(4, 5, 5) LANN_SHAPE(5, 5, 5) LANN_SHAPE(6, 5, 5)
+    default:
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        Row8 row;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) row.v[k] = x[r][k];
+        v[r] = forward_generic<kExact>(row, nrm, w, I, H1, H2);
+      }
+  }
+#undef LANN_SHAPE
+  const int logt = __ldg(a.log_target + m);
+#pragma unroll
+  for (int r = 0; r < R; ++r) out[r] = denorm(v[r], nrm, logt);
+}
+
+// K2 predict (models.cpp:346-363): grid-stride over QUADS of consecutive rows. A quad whose four
+// rows share a model (rows are grouped by model in predict_dataset order, so nearly all do) runs
+// as one 4-row call: its model indices in one 16-B load, its 256 B of inputs in 16-B
+// non-coherent loads, every weight loaded once for the four rows. Mixed quads and the ragged
+// tail go row by row.
+template <bool kExact, int R>
+__global__ void __launch_bounds__(256) predict_kernel(PredictArgs a, const double* rinv, const float* wf) {
+  static_assert(R == 1 || R == 2 || R == 4, "rows per thread");
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t n_quads = a.n_rows / R;
+  auto load = [&](int64_t row, double(&x)[8]) {
+    const double2* xr = reinterpret_cast<const double2*>(a.rows + row * 8);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const double2 v = __ldg(xr + k);
+      x[2 * k] = v.x;
+      x[2 * k + 1] = v.y;
+    }
+  };
+  const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (int64_t q = t0; q < n_quads; q += stride) {
+    const int64_t row = q * R;
+    int ms[R];
+    if constexpr (R == 4) {
+      const int4 mm = __ldg(reinterpret_cast<const int4*>(a.row_model + row));
+      ms[0] = mm.x, ms[1] = mm.y, ms[2] = mm.z, ms[3] = mm.w;
+    } else if constexpr (R == 2) {
+      const int2 mm = __ldg(reinterpret_cast<const int2*>(a.row_model + row));
+      ms[0] = mm.x, ms[1] = mm.y;
+    } else {
+      ms[0] = __ldg(a.row_model + row);
+    }
+    double x[R][8];
+#pragma unroll
+    for (int r = 0; r < R; ++r) load(row + r, x[r]);
+    bool same = true;
+#pragma unroll
+    for (int r = 1; r < R; ++r) same = same && ms[r] == ms[0];
+    if (same) {
+      double out[R];
+      predict_rows<kExact, R>(a, rinv, wf, ms[0], x, out);
+#pragma unroll
+      for (int r = 0; r + 1 < R; r += 2) reinterpret_cast<double2*>(a.out + row)[r / 2] = make_double2(out[r], out[r + 1]);
+      if constexpr (R == 1) a.out[row] = out[0];
+    } else {
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        double xo[1][8], o[1];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) xo[0][k] = x[r][k];
+        predict_rows<kExact, 1>(a, rinv, wf, ms[r], xo, o);
+        a.out[row + r] = o[0];
+      }
+    }
+  }
+  for (int64_t row = n_quads * R + t0; row < a.n_rows; row += stride) {  // the tail
+    double xo[1][8], o[1];
+    load(row, xo[0]);
+    predict_rows<kExact, 1>(a, rinv, wf, __ldg(a.row_model + row), xo, o);
+    a.out[row] = o[0];
+  }
+}
+
+// FP32 path preparation: per-model reciprocal ranges (0 where the range is 0) and an FP32
+// copy of every weight (one thread per parameter / per model).
+__global__ void predict_prep_kernel(PredictArgs a, int n_models, int64_t n_params, double* rinv, float* wf) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t < n_params) wf[t] = (float)a.params[t];
+  if (t < n_models) {
+    const double* nrm = a.norm + 18 * t;
+    for (int j = 0; j < 8; ++j) {
+      const double range = nrm[8 + j] - nrm[j];
+      rinv[8 * t + j] = range > 0.0 ? 1.0 / range : 0.0;
+    }
+  }
 }
 
 // K3: one CTA per set; n <= blockDim * kPerThread handled through shared memory.
@@ -264,14 +470,40 @@ __global__ void __launch_bounds__(96) eval_sums_global(EvalArgs a, const double*
 
 }  // namespace
 
+namespace {
+// rows per thread: 4 for FP32 (weights loaded once per quad; 61% of HBM); the FP64-exact path
+// is FP64-issue heavy (a correctly rounded division per input) and register-bound at 4 rows
+#ifndef LANN_EXACT_ROWS
+#define LANN_EXACT_ROWS 1
+#endif
+constexpr int kExactRows = LANN_EXACT_ROWS;
+unsigned predict_grid(int64_t n_rows) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t want = (n_rows + 255) / 256, cap = int64_t(sms) * 8;  // 8 CTAs of 256 per SM
+  return (unsigned)std::max<int64_t>(1, std::min(want, cap));
+}
+}  // namespace
+
 void launch_predict_fp64(const PredictArgs& a, cudaStream_t s) {
   if (a.n_rows <= 0) return;
-  predict_kernel<true><<<(unsigned)((a.n_rows + 127) / 128), 128, 0, s>>>(a);
+  predict_kernel<true, kExactRows><<<predict_grid(a.n_rows), 256, 0, s>>>(a, nullptr, nullptr);
 }
 
-void launch_predict_fp32(const PredictArgs& a, cudaStream_t s) {
+// n_models / n_params size the FP32 preparation (reciprocal ranges, FP32 weight copy); the
+// scratch lives for the launch only (stream-ordered allocation)
+void launch_predict_fp32(const PredictArgs& a, int n_models, int64_t n_params, cudaStream_t s) {
   if (a.n_rows <= 0) return;
-  predict_kernel<false><<<(unsigned)((a.n_rows + 127) / 128), 128, 0, s>>>(a);
+  void* scratch = nullptr;
+  const size_t bytes = size_t(n_models) * 8 * sizeof(double) + size_t(n_params) * sizeof(float) + 16;
+  if (cudaMallocAsync(&scratch, bytes, s) != cudaSuccess) return;
+  double* rinv = static_cast<double*>(scratch);
+  float* wf = reinterpret_cast<float*>(rinv + size_t(n_models) * 8);
+  const int64_t n_prep = std::max<int64_t>(n_models, n_params);
+  predict_prep_kernel<<<(unsigned)((n_prep + 255) / 256), 256, 0, s>>>(a, n_models, n_params, rinv, wf);
+  predict_kernel<false, 4><<<predict_grid(a.n_rows), 256, 0, s>>>(a, rinv, wf);
+  cudaFreeAsync(scratch, s);
 }
 
 // max_len bounds the shared-memory footprint: 4 doubles + 1 int per sample. Sets that do not

@@ -299,14 +299,21 @@ class Engine:
         return out_p, final, bad, traces
 
     # ---- models::predict over rows (models.cpp:346-363) ----
-    def predict(self, models, rows, row_model, precision=abi.FP64_EXACT):
+    def predict(self, models, rows, row_model, precision=abi.FP64_EXACT, out=None):
+        """lann_predict. Rows already [n][8] float64 C-contiguous (e.g. in pinned memory, Pinned)
+        are passed as they are; out (float64[n]) may be a caller buffer."""
         ms, keep = _model_set(models, precision)
-        rows = np.ascontiguousarray(rows, dtype=np.float64)
+        rows = np.asarray(rows)
         n = rows.shape[0]
-        full = np.zeros((n, ROW))
-        full[:, : rows.shape[1]] = rows
-        rm = _c(row_model, np.int32)
-        out = np.zeros(n)
+        if rows.dtype == np.float64 and rows.ndim == 2 and rows.shape[1] == ROW and rows.flags.c_contiguous:
+            full = rows
+        else:
+            full = np.zeros((n, ROW))
+            full[:, : rows.shape[1]] = rows
+        rm = row_model if (isinstance(row_model, np.ndarray) and row_model.dtype == np.int32
+                           and row_model.flags.c_contiguous) else _c(row_model, np.int32)
+        if out is None:
+            out = np.zeros(n)
         st = self.L.lann_predict(self.h, C.byref(ms), n, _ptr(full), _ptr(rm), _ptr(out))
         if st:
             self._raise(st)

@@ -295,3 +295,40 @@ def test_compact_streamed_selection_equals_the_full_outputs(engine):
     assert np.array_equal(hist, np.bincount(idx, minlength=10))
     pi.free()
     ps.free()
+
+
+def test_batched_predictor_compiled_and_generic_shapes(engine, oracle):
+    """lann_predict over a mixed model set: compiled shapes (I-8-1, I-5-5-1, unrolled) and
+    generic ones (7-64-1, 3-12-6-1), rows interleaved across models: FP64 exact == the oracle's
+    predict (models.cpp:346-363) row by row; FP32 within 1e-5 of the target range."""
+    rng = np.random.default_rng(3)
+    shapes = [(7, (8,), 0), (4, (8,), 0), (6, (5, 5), 1), (5, (5, 5), 0), (7, (64,), 0), (3, (12, 6), 1)]
+    models = []
+    for I, h, lt in shapes:
+        P_ = (I + 1) * h[0] + ((h[0] + 1) * h[1] + h[1] + 1 if len(h) > 1 else h[0] + 1)
+        nrm = np.zeros(18)
+        nrm[:I] = rng.uniform(0, 100, I)
+        nrm[8:8 + I] = nrm[:I] + rng.uniform(1, 1e4, I)
+        nrm[16], nrm[17] = (-9.0, -1.0) if lt else (1e-6, 2e-3)
+        models.append({"inputs": I, "h1": h[0], "h2": h[1] if len(h) > 1 else 0, "log_target": lt,
+                       "params": rng.uniform(-0.6, 0.6, P_), "norm": nrm})
+    n = 6000
+    rm = rng.integers(0, len(models), n).astype(np.int32)
+    rows = np.zeros((n, 8))
+    for r in range(n):
+        m = models[rm[r]]
+        rows[r, : m["inputs"]] = rng.uniform(m["norm"][: m["inputs"]], m["norm"][8: 8 + m["inputs"]])
+    got = engine.predict(models, rows, rm, precision=abi.FP64_EXACT)
+    for r in range(0, n, 7):
+        m = models[rm[r]]
+        h = (m["h1"],) if m["h2"] == 0 else (m["h1"], m["h2"])
+        ref = oracle.predict_row(m["inputs"], h, m["params"], m["norm"], m["log_target"], rows[r, : m["inputs"]])
+        if m["log_target"]:  # exp through CUDA's libm (<= 1 ulp from glibc), DESIGN 4
+            assert abs(got[r] - ref) <= 4e-16 * abs(ref)
+        else:
+            assert got[r] == ref
+    got32 = engine.predict(models, rows, rm, precision=abi.FP32)
+    for r in range(n):
+        m = models[rm[r]]
+        if not m["log_target"]:
+            assert abs(got32[r] - got[r]) <= 1e-5 * (m["norm"][17] - m["norm"][16]) + 1e-12

@@ -369,6 +369,52 @@ void lann_transfer_bytes(int64_t* h2d, int64_t* d2h, int32_t reset);
 int64_t lann_population_models(const lann_population* pop);
 void lann_population_destroy(lann_population* pop);
 
+/* ---- cross-validation summary of a k-fold sweep (BASELINE config 3) -------------
+ * The reference has no k-fold driver; its primitives are split (datagen.cpp:225-248),
+ * predict_dataset (models.cpp:365-378), make_report (eval.cpp:98-108) and aggregate's per-group
+ * means (eval.cpp:110-146). Definitions (restated in oracle/lann_oracle.c, or_fold_mean):
+ *  - CV GROUP: the k-fold jobs (n_folds >= 2) equal in every field except fold and init_seed
+ *    (one combination x family x hyper-parameters); groups in order of first appearance.
+ *  - ENSEMBLE: one init_seed of a group (order of first appearance). When all k folds are present
+ *    and every one trained and evaluated OK, its FOLD-MEAN model predicts the split's test part
+ *    (the samples no fold trains or validates on) as (p_0 + p_1 + ... + p_{k-1}) / k, summed in
+ *    fold order, each p_f = models::predict of fold f's model with its own NormStats, and is
+ *    scored with make_report (drop fraction 0.3).
+ *  - Group statistics over the group's OK models (held-out fold metrics, job order) and its OK
+ *    ensembles (fold-mean test metrics, ensemble order): mean = the values summed sequentially in
+ *    that order / count (aggregate's rule); median = the middle of the sorted values, (a + b) / 2
+ *    of the two middles for an even count.
+ * A prepared population with k-fold jobs computes all of it on the device in every pass
+ * (lann_population_run), after training and the held-out metrics. */
+typedef struct lann_cv_stat {
+  double mean, median;
+} lann_cv_stat;
+typedef struct lann_cv_group {
+  int32_t first_job;       /* the group's first job (its world / family / hyper-parameters) */
+  int32_t n_folds;
+  int32_t n_models;        /* the group's jobs */
+  int32_t n_models_ok;     /* ... that trained and evaluated OK (fold statistics are over these) */
+  int32_t n_ensembles;     /* distinct init seeds */
+  int32_t n_ensembles_ok;  /* ... complete, every member OK, test metrics OK */
+  int32_t n_test;          /* test-part samples */
+  int32_t reserved;
+  lann_cv_stat fold_mape, fold_mape_thr, fold_rho; /* held-out fold metrics */
+  lann_cv_stat test_mape, test_mape_thr, test_rho; /* fold-mean model on the test part */
+} lann_cv_group;
+typedef struct lann_cv_ensemble {
+  int32_t group;           /* index into the groups */
+  int32_t status;          /* LANN_OK; else why no fold-mean score: a missing fold (LANN_PARAM_ERROR),
+                              a member's own status, or make_report's (LANN_DOMAIN_ERROR) */
+  uint64_t init_seed;
+  double mape, mape_thr, rho;
+  int32_t n_kept, n_test;
+} lann_cv_ensemble;
+/* host only (no device): how many groups / ensembles a job list forms */
+int lann_cv_layout(int32_t n_jobs, const lann_job* jobs, int32_t* n_groups, int32_t* n_ensembles);
+/* the last pass's summary; arrays sized by lann_cv_layout (or lann_population_cv_count) */
+int lann_population_cv_count(const lann_population* pop, int32_t* n_groups, int32_t* n_ensembles);
+int lann_population_cv(lann_population* pop, lann_cv_group* groups, lann_cv_ensemble* ensembles);
+
 /* The 48 kernel-variant-hardware combinations of BASELINE config 2 (worlds
  * only). Writes up to cap entries, returns the count. */
 int lann_default_combos(lann_world* out, int32_t cap);

@@ -775,3 +775,59 @@ done:
   free(order);
   return st;
 }
+
+/* Cross-validation fold-mean model (engine definition, include/lann_engine.h "cross-validation
+ * summary"; the reference has no k-fold driver). fold_jobs[f] is fold f of one seed (all other
+ * fields equal), params[f] its trained weights. Each fold model predicts the split's test part
+ * order[n_train..count) (datagen.cpp:225-248) with its own NormStats (fit on its training blocks,
+ * models.cpp:89-116) as models::predict does (models.cpp:346-363); the predictions are summed in
+ * fold order and divided by k. Writes n_test predictions and the truths beside them. */
+int or_fold_mean(int k, const lann_job* fold_jobs, const double* const* params, double* pred, double* truth,
+                 int* n_test) {
+  const lann_job* j0 = &fold_jobs[0];
+  const int count = j0->count;
+  double* feats = malloc(sizeof(double) * LANN_ROW * (size_t)count);
+  uint64_t* c = malloc(sizeof(uint64_t) * (size_t)count);
+  double* rt = malloc(sizeof(double) * (size_t)count);
+  int64_t* order = malloc(sizeof(int64_t) * (size_t)count);
+  int nf = 0, n_train = 0;
+  int st = or_build_dataset(&j0->world, j0->data_seed, count, feats, c, rt, &nf);
+  if (!st) st = or_split_order(count, j0->train_fraction, j0->data_seed, order, &n_train);
+  const int nt = count - n_train;
+  *n_test = nt;
+  const int aug = j0->family == LANN_NNC;
+  const int I = nf + aug;
+  double* X = calloc((size_t)(n_train > 0 ? n_train : 1) * LANN_ROW, sizeof(double));
+  double* y = malloc(sizeof(double) * (size_t)(n_train > 0 ? n_train : 1));
+  for (int f = 0; f < k && !st; ++f) {
+    const lann_job* j = &fold_jobs[f];
+    const int b0 = n_train * j->fold / j->n_folds, b1 = n_train * (j->fold + 1) / j->n_folds;
+    int ntr = 0;
+    for (int i = 0; i < n_train; ++i) {
+      if (i >= b0 && i < b1) continue;
+      memset(X + (size_t)ntr * LANN_ROW, 0, sizeof(double) * LANN_ROW);
+      memcpy(X + (size_t)ntr * LANN_ROW, feats + order[i] * LANN_ROW, sizeof(double) * (size_t)nf);
+      if (aug) X[(size_t)ntr * LANN_ROW + nf] = (double)c[order[i]];
+      y[ntr++] = rt[order[i]];
+    }
+    double norm[18];
+    or_norm_fit(ntr, I, X, y, j->log_target, norm);
+    for (int s = 0; s < nt; ++s) {
+      const int64_t idx = order[n_train + s];
+      double x[LANN_ROW] = {0};
+      memcpy(x, feats + idx * LANN_ROW, sizeof(double) * (size_t)nf);
+      if (aug) x[nf] = (double)c[idx];
+      const double p = or_predict_row(I, j->n_hidden, j->hidden, params[f], norm, j->log_target, x);
+      pred[s] = f == 0 ? p : pred[s] + p;
+      truth[s] = rt[idx];
+    }
+  }
+  for (int s = 0; s < nt && !st; ++s) pred[s] = pred[s] / (double)k;
+  free(X);
+  free(y);
+  free(feats);
+  free(c);
+  free(rt);
+  free(order);
+  return st;
+}

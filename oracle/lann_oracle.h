@@ -60,6 +60,9 @@ void or_select_variants(const lann_model_set* models, const int32_t* with_n_thd,
 
 /* whole job (acceptance criterion-5 protocol, acceptance_main.cpp:283-328) */
 int or_run_job(const lann_job* job, lann_job_result* r, double* params, double* trace);
+/* cross-validation fold-mean model of one seed's k fold models on the split's test part */
+int or_fold_mean(int k, const lann_job* fold_jobs, const double* const* params, double* pred, double* truth,
+                 int* n_test);
 
 #ifdef __cplusplus
 }

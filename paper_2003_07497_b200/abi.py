@@ -42,6 +42,28 @@ class JobResult(C.Structure):
     ]
 
 
+class CvStat(C.Structure):
+    _fields_ = [("mean", C.c_double), ("median", C.c_double)]
+
+
+class CvGroup(C.Structure):
+    """lann_cv_group: one combination x family x hyper-parameters of a k-fold sweep."""
+    _fields_ = [
+        ("first_job", C.c_int32), ("n_folds", C.c_int32), ("n_models", C.c_int32), ("n_models_ok", C.c_int32),
+        ("n_ensembles", C.c_int32), ("n_ensembles_ok", C.c_int32), ("n_test", C.c_int32), ("reserved", C.c_int32),
+        ("fold_mape", CvStat), ("fold_mape_thr", CvStat), ("fold_rho", CvStat),
+        ("test_mape", CvStat), ("test_mape_thr", CvStat), ("test_rho", CvStat),
+    ]
+
+
+class CvEnsemble(C.Structure):
+    """lann_cv_ensemble: one init seed's fold-mean model scored on the split's test part."""
+    _fields_ = [
+        ("group", C.c_int32), ("status", C.c_int32), ("init_seed", C.c_uint64), ("mape", C.c_double),
+        ("mape_thr", C.c_double), ("rho", C.c_double), ("n_kept", C.c_int32), ("n_test", C.c_int32),
+    ]
+
+
 class TrainBatch(C.Structure):
     _fields_ = [
         ("n_models", C.c_int32), ("precision", C.c_int32), ("n_tiles", C.c_int32),

@@ -344,6 +344,19 @@ Status make_tile(const Dataset& ds, const std::vector<std::int64_t>& order, int 
     row_of(ev[s], &t.eval_rows[s * LANN_ROW]);
     t.eval_truth[s] = ds.runtime[ev[s]];
   }
+  // k-fold tiles also carry the split's test part (no fold trains or validates on it): the
+  // rows the fold-mean model of a cross-validation ensemble is scored on
+  t.test_rows.clear();
+  t.test_truth.clear();
+  if (n_folds >= 2) {
+    const std::size_t n_test = order.size() - std::size_t(n_train);
+    t.test_rows.assign(n_test * LANN_ROW, 0.0);
+    t.test_truth.resize(n_test);
+    for (std::size_t s = 0; s < n_test; ++s) {
+      row_of(order[std::size_t(n_train) + s], &t.test_rows[s * LANN_ROW]);
+      t.test_truth[s] = ds.runtime[order[std::size_t(n_train) + s]];
+    }
+  }
   return {};
 }
 

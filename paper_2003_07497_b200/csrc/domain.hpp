@@ -135,8 +135,11 @@ struct Tile {
   std::vector<double> Xn, yn;            // [n_train][LANN_ROW], [n_train]
   std::vector<double> eval_rows;         // raw model inputs [n_eval][LANN_ROW]
   std::vector<double> eval_truth;        // [n_eval]
+  std::vector<double> test_rows;         // k-fold tiles: the split's test part, raw [n_test][LANN_ROW]
+  std::vector<double> test_truth;        // [n_test]
   int n_train() const { return int(yn.size()); }
   int n_eval() const { return int(eval_truth.size()); }
+  int n_test() const { return int(test_truth.size()); }
 };
 
 Status make_tile(const Dataset& ds, const std::vector<std::int64_t>& order, int n_train,

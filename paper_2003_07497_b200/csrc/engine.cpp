@@ -571,6 +571,88 @@ unsigned char* pinned_stage(lann_engine* e, size_t bytes) {
   return e->pin;
 }
 
+// ---- cross-validation layout (lann_engine.h "cross-validation summary"), host only ----------
+struct CvLayout {
+  std::vector<int> job_group, job_ens;  // -1 for jobs outside k-fold groups
+  std::vector<int> group_first, group_folds, group_models, group_ens;
+  std::vector<int> ens_group;
+  std::vector<uint64_t> ens_seed;
+  std::vector<std::vector<int>> ens_member;  // [ensemble][fold]: first job of that fold, -1 if absent
+  int n_groups() const { return int(group_first.size()); }
+  int n_ens() const { return int(ens_group.size()); }
+};
+
+// every job field except fold and init_seed (struct padding is not part of the key)
+std::string cv_group_key(const lann_job& j) {
+  std::string k(reinterpret_cast<const char*>(&j.world), sizeof(lann_world));
+  auto add = [&k](const auto& v) { k.append(reinterpret_cast<const char*>(&v), sizeof v); };
+  add(j.data_seed);
+  add(j.count);
+  add(j.train_fraction);
+  add(j.n_folds);
+  add(j.family);
+  add(j.n_hidden);
+  add(j.hidden[0]);
+  add(j.hidden[1]);
+  add(j.learning_rate);
+  add(j.epochs);
+  add(j.log_target);
+  add(j.unconstrained);
+  return k;
+}
+
+CvLayout cv_layout(int n, const lann_job* jobs) {
+  CvLayout L;
+  L.job_group.assign(size_t(n), -1);
+  L.job_ens.assign(size_t(n), -1);
+  std::map<std::string, int> groups;
+  std::map<std::pair<int, uint64_t>, int> ens;
+  for (int j = 0; j < n; ++j) {
+    const lann_job& J = jobs[j];
+    if (J.n_folds < 2) continue;
+    auto g = groups.find(cv_group_key(J));
+    if (g == groups.end()) {
+      g = groups.emplace(cv_group_key(J), L.n_groups()).first;
+      L.group_first.push_back(j);
+      L.group_folds.push_back(J.n_folds);
+      L.group_models.push_back(0);
+      L.group_ens.push_back(0);
+    }
+    const int gi = g->second;
+    L.job_group[size_t(j)] = gi;
+    ++L.group_models[size_t(gi)];
+    auto e = ens.find({gi, J.init_seed});
+    if (e == ens.end()) {
+      e = ens.emplace(std::make_pair(gi, J.init_seed), L.n_ens()).first;
+      L.ens_group.push_back(gi);
+      L.ens_seed.push_back(J.init_seed);
+      L.ens_member.emplace_back(size_t(J.n_folds), -1);
+      ++L.group_ens[size_t(gi)];
+    }
+    L.job_ens[size_t(j)] = e->second;
+    auto& mem = L.ens_member[size_t(e->second)];
+    if (J.fold >= 0 && J.fold < J.n_folds && mem[size_t(J.fold)] < 0) mem[size_t(J.fold)] = j;
+  }
+  return L;
+}
+
+// device side of a population's cross-validation summary (all arrays are views into the blob)
+struct CvState {
+  CvLayout L;
+  std::vector<int> dev_of;       // per ensemble: its device slot, or -1
+  std::vector<int> host_status;  // per ensemble off the device: why
+  std::vector<int> ens_test;     // per ensemble: test-part samples
+  std::vector<int> dev_members;  // [slot][kmax]: engine model indices (for member statuses)
+  std::vector<int> group_test;
+  int n_dev = 0, kmax = 0, max_test = 0;
+  int64_t total_out = 0;
+  size_t res_off = 0, res_bytes = 0;
+  size_t r_mape = 0, r_thr = 0, r_rho = 0, r_sf = 0, r_se = 0, r_kept = 0, r_st = 0, r_bad = 0, r_nf = 0, r_ne = 0;
+  FoldMeanArgs fm{};
+  EvalArgs ev{};
+  CvStatsArgs sf{}, se{};
+};
+
 struct Population {
   lann_engine* e = nullptr;
   int n_jobs = 0, M = 0, precision = 0;
@@ -587,6 +669,7 @@ struct Population {
   DBuf<int> dB, dEM, dI, dh1, dh2, dlog, dEL, dK, dS;
   DBuf<int64_t> dpo, dEO, dTO;
   std::unique_ptr<TrainPlan> plan;
+  std::unique_ptr<CvState> cv;  // k-fold populations only
   int64_t trace_total = 0;
   std::vector<int64_t> toff;
   double train_flop = 0.0;  // algorithmic FLOP of one training pass
@@ -767,6 +850,75 @@ int prepare_population(lann_engine* e, int n_jobs, const lann_job* jobs, int pre
   const int M = int(pop.model_job.size());
   pop.M = M;
   if (M == 0) return pop.base[0].status;
+  // cross-validation ensembles of the k-fold jobs: members, test sets, group item lists
+  std::vector<int> cv_set_tile, cv_ens_set, cv_fold_items, cv_ens_items;
+  std::vector<int64_t> cv_fold_off, cv_ens_off, cv_set_row;
+  std::vector<int> cv_fold_len, cv_ens_len;
+  int64_t cv_rows = 0;
+  if (std::any_of(jobs, jobs + n_jobs, [](const lann_job& J) { return J.n_folds >= 2; })) {
+    pop.cv = std::make_unique<CvState>();
+    CvState& cv = *pop.cv;
+    cv.L = cv_layout(n_jobs, jobs);
+    const int E = cv.L.n_ens(), G = cv.L.n_groups();
+    std::vector<int> job_model(size_t(n_jobs), -1);
+    for (int m = 0; m < M; ++m) job_model[size_t(pop.model_job[size_t(m)])] = m;
+    cv.dev_of.assign(size_t(E), -1);
+    cv.host_status.assign(size_t(E), LANN_OK);
+    cv.ens_test.assign(size_t(E), 0);
+    for (int f : cv.L.group_folds) cv.kmax = std::max(cv.kmax, f);
+    std::map<std::tuple<int, double, int>, int> skeys;  // (dataset, train fraction, family)
+    for (int en = 0; en < E; ++en) {
+      const auto& mem = cv.L.ens_member[size_t(en)];
+      int st = LANN_OK;
+      for (int j : mem) {
+        if (j < 0) {
+          st = LANN_PARAM_ERROR;  // a fold of this seed is not in the job list
+          break;
+        }
+        if (job_model[size_t(j)] < 0) {
+          st = pop.base[size_t(j)].status;  // the member failed host preparation
+          break;
+        }
+      }
+      if (st != LANN_OK) {
+        cv.host_status[size_t(en)] = st;
+        continue;
+      }
+      const int k = job_tile[size_t(mem[0])];
+      const std::tuple<int, double, int> key{std::get<0>(tsrc[size_t(k)]), std::get<1>(tsrc[size_t(k)]),
+                                             std::get<4>(tsrc[size_t(k)])};
+      auto it = skeys.find(key);
+      if (it == skeys.end()) {
+        it = skeys.emplace(key, int(cv_set_tile.size())).first;
+        cv_set_tile.push_back(k);
+        cv_set_row.push_back(cv_rows);
+        cv_rows += tiles[size_t(k)].n_test();
+      }
+      cv.ens_test[size_t(en)] = tiles[size_t(k)].n_test();
+      cv.dev_of[size_t(en)] = cv.n_dev++;
+      cv_ens_set.push_back(it->second);
+      for (int f = 0; f < cv.kmax; ++f)
+        cv.dev_members.push_back(f < int(mem.size()) ? job_model[size_t(mem[size_t(f)])] : 0);
+      cv.max_test = std::max(cv.max_test, cv.ens_test[size_t(en)]);
+      cv.total_out += cv.ens_test[size_t(en)];
+    }
+    // item lists: a group's trained models in job order, its device ensembles in ensemble order
+    std::vector<std::vector<int>> fi(static_cast<size_t>(G)), ei(static_cast<size_t>(G));
+    for (int m = 0; m < M; ++m) {
+      const int g = cv.L.job_group[size_t(pop.model_job[size_t(m)])];
+      if (g >= 0) fi[size_t(g)].push_back(m);
+    }
+    for (int en = 0; en < E; ++en)
+      if (cv.dev_of[size_t(en)] >= 0) ei[size_t(cv.L.ens_group[size_t(en)])].push_back(cv.dev_of[size_t(en)]);
+    for (int g = 0; g < G; ++g) {
+      cv_fold_off.push_back(int64_t(cv_fold_items.size()));
+      cv_fold_len.push_back(int(fi[size_t(g)].size()));
+      cv_fold_items.insert(cv_fold_items.end(), fi[size_t(g)].begin(), fi[size_t(g)].end());
+      cv_ens_off.push_back(int64_t(cv_ens_items.size()));
+      cv_ens_len.push_back(int(ei[size_t(g)].size()));
+      cv_ens_items.insert(cv_ens_items.end(), ei[size_t(g)].begin(), ei[size_t(g)].end());
+    }
+  }
   // pack straight into the engine's pinned staging buffer, laid out like the one device blob
   // that receives it (a single H2D copy; no growing host vectors, no pageable staging)
   DevTrain& t = pop.t;
@@ -806,6 +958,14 @@ int prepare_population(lann_engine* e, int n_jobs, const lann_job* jobs, int pre
   const size_t oEM = L.add<int>(size_t(n_eval_total)), oI = L.add<int>(size_t(M)), oH1 = L.add<int>(size_t(M));
   const size_t oH2 = L.add<int>(size_t(M)), oLog = L.add<int>(size_t(M)), oEL = L.add<int>(size_t(M));
   const size_t oPO = L.add<int64_t>(size_t(M)), oEO = L.add<int64_t>(size_t(M)), oTO = L.add<int64_t>(size_t(M));
+  CvState* cvp = pop.cv.get();
+  const int cvG = cvp ? cvp->L.n_groups() : 0, cvD = cvp ? cvp->n_dev : 0, cvK = cvp ? cvp->kmax : 0;
+  const size_t cRows = L.add<double>(size_t(cv_rows) * 8), cTruth = L.add<double>(size_t(cv_rows));
+  const size_t cK = L.add<int>(size_t(cvD)), cMem = L.add<int>(size_t(cvD) * size_t(cvK));
+  const size_t cER = L.add<int64_t>(size_t(cvD)), cEL = L.add<int>(size_t(cvD)), cEO = L.add<int64_t>(size_t(cvD));
+  const size_t cFO = L.add<int64_t>(size_t(cvG)), cFL = L.add<int>(size_t(cvG));
+  const size_t cFI = L.add<int>(cv_fold_items.size());
+  const size_t cGO = L.add<int64_t>(size_t(cvG)), cGL = L.add<int>(size_t(cvG)), cGI = L.add<int>(cv_ens_items.size());
   const size_t up_bytes = L.bytes;
   // device-only outputs follow the uploaded part
   // the per-model results first, contiguous, so fetch is one D2H copy
@@ -817,6 +977,29 @@ int prepare_population(lann_engine* e, int n_jobs, const lann_job* jobs, int pre
   pop.res_rel = {0, oMape - oF, oThr - oF, oRho - oF, oB - oF, oK - oF, oS - oF};
   const size_t oP = L.add<double>(size_t(t.total_params));
   const size_t oT = L.add<double>(size_t(pop.trace_total)), oPred = L.add<double>(size_t(n_eval_total));
+  // cross-validation outputs: the fold-mean sets, then one contiguous result block (one D2H)
+  const int64_t cv_out = cvp ? cvp->total_out : 0;
+  const size_t cPred = L.add<double>(size_t(cv_out)), cTOut = L.add<double>(size_t(cv_out));
+  const size_t cScr = L.add<double>(std::max(cv_fold_items.size(), cv_ens_items.size()));
+  const size_t cRes = L.add<double>(size_t(cvD));  // ensemble MAPE (result block starts here)
+  const size_t cThr = L.add<double>(size_t(cvD)), cRho = L.add<double>(size_t(cvD));
+  const size_t cSF = L.add<double>(size_t(cvG) * 6), cSE = L.add<double>(size_t(cvG) * 6);
+  const size_t cKept = L.add<int>(size_t(cvD)), cSt = L.add<int>(size_t(cvD)), cBad = L.add<int>(size_t(cvD));
+  const size_t cNF = L.add<int>(size_t(cvG)), cNE = L.add<int>(size_t(cvG));
+  if (cvp) {
+    cvp->res_off = cRes;
+    cvp->res_bytes = L.bytes - cRes;
+    cvp->r_mape = 0;
+    cvp->r_thr = cThr - cRes;
+    cvp->r_rho = cRho - cRes;
+    cvp->r_sf = cSF - cRes;
+    cvp->r_se = cSE - cRes;
+    cvp->r_kept = cKept - cRes;
+    cvp->r_st = cSt - cRes;
+    cvp->r_bad = cBad - cRes;
+    cvp->r_nf = cNF - cRes;
+    cvp->r_ne = cNE - cRes;
+  }
   unsigned char* h = pinned_stage(e, up_bytes);
   auto H = [&](auto* type_tag, size_t off) { return reinterpret_cast<decltype(type_tag)>(h + off); };
   {
@@ -871,6 +1054,36 @@ int prepare_population(lann_engine* e, int n_jobs, const lann_job* jobs, int pre
     std::copy(t.h2.begin(), t.h2.end(), H((int*)nullptr, oH2));
     std::copy(t.param_offset.begin(), t.param_offset.end(), H((int64_t*)nullptr, oPO));
     std::copy(pop.toff.begin(), pop.toff.end(), H((int64_t*)nullptr, oTO));
+    if (cvp) {
+      double* cr = H((double*)nullptr, cRows);
+      double* ct = H((double*)nullptr, cTruth);
+      for (size_t q = 0; q < cv_set_tile.size(); ++q) {
+        const Tile& T = tiles[size_t(cv_set_tile[q])];
+        std::copy(T.test_rows.begin(), T.test_rows.end(), cr + cv_set_row[q] * 8);
+        std::copy(T.test_truth.begin(), T.test_truth.end(), ct + cv_set_row[q]);
+      }
+      int* ek = H((int*)nullptr, cK);
+      int64_t* er_ = H((int64_t*)nullptr, cER);
+      int* el = H((int*)nullptr, cEL);
+      int64_t* eo = H((int64_t*)nullptr, cEO);
+      std::copy(cvp->dev_members.begin(), cvp->dev_members.end(), H((int*)nullptr, cMem));
+      int64_t out = 0;
+      for (int en = 0, slot = 0; en < cvp->L.n_ens(); ++en) {
+        if (cvp->dev_of[size_t(en)] < 0) continue;
+        ek[slot] = cvp->L.group_folds[size_t(cvp->L.ens_group[size_t(en)])];
+        er_[slot] = cv_set_row[size_t(cv_ens_set[size_t(slot)])];
+        el[slot] = cvp->ens_test[size_t(en)];
+        eo[slot] = out;
+        out += el[slot];
+        ++slot;
+      }
+      std::copy(cv_fold_off.begin(), cv_fold_off.end(), H((int64_t*)nullptr, cFO));
+      std::copy(cv_fold_len.begin(), cv_fold_len.end(), H((int*)nullptr, cFL));
+      std::copy(cv_fold_items.begin(), cv_fold_items.end(), H((int*)nullptr, cFI));
+      std::copy(cv_ens_off.begin(), cv_ens_off.end(), H((int64_t*)nullptr, cGO));
+      std::copy(cv_ens_len.begin(), cv_ens_len.end(), H((int*)nullptr, cGL));
+      std::copy(cv_ens_items.begin(), cv_ens_items.end(), H((int*)nullptr, cGI));
+    }
     hlog("pack", h2);
   }
   if (Status st = validate_train(t)) return set_err(e, st);
@@ -911,6 +1124,34 @@ int prepare_population(lann_engine* e, int n_jobs, const lann_job* jobs, int pre
   pop.dB = V((int*)nullptr, oB, Mz);
   pop.dK = V((int*)nullptr, oK, Mz);
   pop.dS = V((int*)nullptr, oS, Mz);
+  if (cvp) {
+    auto P = [&](auto* type_tag, size_t off) { return reinterpret_cast<decltype(type_tag)>(d + off); };
+    FoldMeanArgs& f = cvp->fm;
+    f.n_ens = cvD;
+    f.kmax = cvK;
+    f.ens_k = P((const int*)nullptr, cK);
+    f.ens_models = P((const int*)nullptr, cMem);
+    f.ens_rows = P((const int64_t*)nullptr, cER);
+    f.ens_len = P((const int*)nullptr, cEL);
+    f.ens_out = P((const int64_t*)nullptr, cEO);
+    f.rows = P((const double*)nullptr, cRows);
+    f.truth = P((const double*)nullptr, cTruth);
+    f.model_bad = pop.dB.p;
+    f.model_status = pop.dS.p;
+    f.pred = P((double*)nullptr, cPred);
+    f.truth_out = P((double*)nullptr, cTOut);
+    f.ens_bad = P((int*)nullptr, cBad);
+    cvp->ev = EvalArgs{cvD, f.ens_out, f.ens_len, f.truth_out, f.pred, 0.3, P((double*)nullptr, cRes),
+                       P((double*)nullptr, cThr), P((int*)nullptr, cKept), P((double*)nullptr, cRho),
+                       P((int*)nullptr, cSt)};
+    double* scr = P((double*)nullptr, cScr);
+    cvp->sf = CvStatsArgs{cvG, P((const int64_t*)nullptr, cFO), P((const int*)nullptr, cFL),
+                          P((const int*)nullptr, cFI), pop.dMape.p, pop.dThr.p, pop.dRho.p, pop.dS.p, pop.dB.p,
+                          P((double*)nullptr, cSF), P((int*)nullptr, cNF), scr};
+    cvp->se = CvStatsArgs{cvG, P((const int64_t*)nullptr, cGO), P((const int*)nullptr, cGL),
+                          P((const int*)nullptr, cGI), cvp->ev.mape, cvp->ev.mape_thr, cvp->ev.rho, cvp->ev.status,
+                          f.ens_bad, P((double*)nullptr, cSE), P((int*)nullptr, cNE), scr};
+  }
   hlog("uploads", h3);
   const auto h4 = now();
   pop.plan = build_plan(e, t, precision, pop.dX.p, pop.dY.p, pop.rows);
@@ -938,6 +1179,16 @@ void run_device(Population& pop) {
               pop.dK.p, pop.dRho.p, pop.dS.p};
   launch_eval(ea, pop.max_eval, e->max_smem, pop.n_eval_rows, s);
   e->launches += eval_launch_count(pop.max_eval, e->max_smem);
+  if (pop.cv) {  // cross-validation summary: fold-mean test scores, then the group statistics
+    CvState& cv = *pop.cv;
+    const bool exact = pop.precision != LANN_FP32;
+    launch_fold_mean(pa, cv.fm, cv.max_test, exact, pop.M, pop.t.total_params, s);
+    launch_eval(cv.ev, cv.max_test, e->max_smem, cv.total_out, s);
+    launch_cv_stats(cv.sf, s);
+    launch_cv_stats(cv.se, s);
+    if (cv.n_dev > 0) e->launches += (exact ? 1 : 2) + eval_launch_count(cv.max_test, e->max_smem);
+    if (cv.L.n_groups() > 0) e->launches += 2;
+  }
   ck(cudaGetLastError(), "population launch");
 }
 
@@ -2004,6 +2255,90 @@ int lann_population_norm(const lann_population* p, double* norm_out) {
   for (int m = 0; m < pop.M; ++m)
     std::memcpy(norm_out + 18 * size_t(pop.model_job[m]), &norm[18 * size_t(m)], 18 * sizeof(double));
   return LANN_OK;
+}
+
+int lann_cv_layout(int32_t n_jobs, const lann_job* jobs, int32_t* n_groups, int32_t* n_ensembles) {
+  if (n_jobs < 0 || (n_jobs > 0 && !jobs)) return LANN_PARAM_ERROR;
+  const CvLayout L = cv_layout(n_jobs, jobs);
+  if (n_groups) *n_groups = L.n_groups();
+  if (n_ensembles) *n_ensembles = L.n_ens();
+  return LANN_OK;
+}
+
+int lann_population_cv_count(const lann_population* p, int32_t* n_groups, int32_t* n_ensembles) {
+  if (!p) return LANN_PARAM_ERROR;
+  const CvState* cv = p->pop.cv.get();
+  if (n_groups) *n_groups = cv ? cv->L.n_groups() : 0;
+  if (n_ensembles) *n_ensembles = cv ? cv->L.n_ens() : 0;
+  return LANN_OK;
+}
+
+int lann_population_cv(lann_population* p, lann_cv_group* groups, lann_cv_ensemble* ensembles) {
+  if (!p) return LANN_PARAM_ERROR;
+  Population& pop = p->pop;
+  const CvState* cv = pop.cv.get();
+  if (!cv) return LANN_OK;  // no k-fold jobs: nothing to summarise
+  try {
+    ck(cudaSetDevice(pop.e->device), "cudaSetDevice");
+    std::vector<unsigned char> hr(cv->res_bytes);
+    if (cv->res_bytes) {
+      ck(cudaMemcpyAsync(hr.data(), pop.blob.p + cv->res_off, cv->res_bytes, cudaMemcpyDeviceToHost, pop.e->stream),
+         "D2H");
+      t_d2h += int64_t(cv->res_bytes);
+    }
+    ck(cudaStreamSynchronize(pop.e->stream), "cv fetch");
+    auto D = [&](size_t off) { return reinterpret_cast<const double*>(hr.data() + off); };
+    auto I = [&](size_t off) { return reinterpret_cast<const int*>(hr.data() + off); };
+    const double *mape = D(cv->r_mape), *thr = D(cv->r_thr), *rho = D(cv->r_rho);
+    const double *sf = D(cv->r_sf), *se = D(cv->r_se);
+    const int *kept = I(cv->r_kept), *est = I(cv->r_st), *bad = I(cv->r_bad), *nf = I(cv->r_nf), *ne = I(cv->r_ne);
+    const int G = cv->L.n_groups(), E = cv->L.n_ens();
+    std::vector<int> group_test(size_t(G), 0);
+    for (int en = 0; en < E; ++en) {
+      const int slot = cv->dev_of[size_t(en)];
+      lann_cv_ensemble r{};
+      r.group = cv->L.ens_group[size_t(en)];
+      r.init_seed = cv->L.ens_seed[size_t(en)];
+      r.n_test = cv->ens_test[size_t(en)];
+      if (slot < 0) {
+        r.status = cv->host_status[size_t(en)];
+      } else if (bad[slot] >= 0) {  // a member diverged or had no held-out metrics
+        r.status = (bad[slot] & 1) ? LANN_DOMAIN_ERROR : LANN_TRAINING_ERROR;
+      } else {
+        r.status = est[slot] ? LANN_DOMAIN_ERROR : LANN_OK;
+        r.mape = mape[slot];
+        r.mape_thr = thr[slot];
+        r.rho = rho[slot];
+        r.n_kept = kept[slot];
+      }
+      if (slot >= 0) group_test[size_t(r.group)] = r.n_test;
+      if (ensembles) ensembles[en] = r;
+    }
+    if (groups)
+      for (int g = 0; g < G; ++g) {
+        lann_cv_group& o = groups[g];
+        o = lann_cv_group{};
+        o.first_job = cv->L.group_first[size_t(g)];
+        o.n_folds = cv->L.group_folds[size_t(g)];
+        o.n_models = cv->L.group_models[size_t(g)];
+        o.n_models_ok = nf[g];
+        o.n_ensembles = cv->L.group_ens[size_t(g)];
+        o.n_ensembles_ok = ne[g];
+        o.n_test = group_test[size_t(g)];
+        const double* a = sf + 6 * size_t(g);
+        const double* b = se + 6 * size_t(g);
+        o.fold_mape = {a[0], a[1]};
+        o.fold_mape_thr = {a[2], a[3]};
+        o.fold_rho = {a[4], a[5]};
+        o.test_mape = {b[0], b[1]};
+        o.test_mape_thr = {b[2], b[3]};
+        o.test_rho = {b[4], b[5]};
+      }
+    return LANN_OK;
+  } catch (const CudaFail& f) {
+    pop.e->err = f.what;
+    return LANN_CUDA_ERROR;
+  }
 }
 
 double lann_population_flop(const lann_population* p) { return p ? p->pop.train_flop : 0.0; }

@@ -92,6 +92,42 @@ struct EvalArgs {
   int* status;
 };
 
+// Cross-validation fold-mean models (lann_engine.h, "cross-validation summary"): every ensemble's
+// k fold models predict its test part, the predictions are averaged in fold order.
+struct FoldMeanArgs {
+  int n_ens;
+  int kmax;
+  const int* ens_k;          // folds of the ensemble
+  const int* ens_models;     // [n_ens][kmax] engine model index of fold f
+  const int64_t* ens_rows;   // first test row of the ensemble's test set (into rows / truth)
+  const int* ens_len;        // test rows
+  const int64_t* ens_out;    // first output slot
+  const double* rows;        // raw model inputs [n][8]
+  const double* truth;       // [n]
+  const int* model_bad;      // per model: non-finite epoch (>= 0: TrainingError)
+  const int* model_status;   // per model: held-out metrics status (0 ok)
+  double* pred;              // [total] fold-mean predictions
+  double* truth_out;         // [total] the ensemble's truth beside them (an eval set)
+  int* ens_bad;              // per ensemble: -1, or 2 f + (0: fold f diverged, 1: fold f had no metrics)
+};
+
+// Group statistics (mean in item order, median of the sorted values) of three metrics over the
+// OK items of each group: item i is OK when status[i] == 0 and bad[i] < 0.
+struct CvStatsArgs {
+  int n_groups;
+  const int64_t* item_off;
+  const int* item_len;
+  const int* items;          // item ids, per group in order
+  const double* m0;          // metric arrays indexed by item id
+  const double* m1;
+  const double* m2;
+  const int* status;
+  const int* bad;
+  double* out;               // [group][6]: mean, median of m0, m1, m2
+  int* n_ok;                 // [group]
+  double* scratch;           // [total items]: the compacted values of one metric
+};
+
 // shape = {I, H1, H2} when every model of the launch has that compiled shape, else null
 void launch_train_fp64(const TrainArgs& a, int max_p, int dyn_bytes, const int* shape, cudaStream_t s);
 bool fp64_shape_compiled(int in, int h1, int h2);
@@ -110,6 +146,11 @@ void launch_predict_fp64(const PredictArgs& a, cudaStream_t s);
 void launch_predict_fp32(const PredictArgs& a, int n_models, int64_t n_params, cudaStream_t s);
 void launch_eval(const EvalArgs& a, int max_len, int max_smem, int64_t total, cudaStream_t s);
 int eval_launch_count(int max_len, int max_smem);
+// fold-mean predictions of every ensemble (the population's PredictArgs give the models);
+// FP32 populations predict with the FP32 forward like launch_predict_fp32
+void launch_fold_mean(const PredictArgs& pa, const FoldMeanArgs& f, int max_len, bool exact, int n_models,
+                      int64_t n_params, cudaStream_t s);
+void launch_cv_stats(const CvStatsArgs& a, cudaStream_t s);
 
 }  // namespace lann
 

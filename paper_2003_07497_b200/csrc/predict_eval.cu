@@ -468,6 +468,151 @@ __global__ void __launch_bounds__(96) eval_sums_global(EvalArgs a, const double*
   }
 }
 
+// Fold-mean model of a cross-validation ensemble (lann_engine.h): grid (row blocks, ensemble),
+// one thread per test row; the k fold models predict the row one after another (a warp's rows
+// share every model, so weight loads are uniform) and the predictions are summed in fold order,
+// then divided by k. The ensemble's truth is written beside the predictions so the pair is an
+// ordinary eval set. Block (0, e) also records whether every member trained and evaluated OK.
+template <bool kExact>
+__global__ void __launch_bounds__(128) fold_mean_kernel(PredictArgs pa, FoldMeanArgs f, const double* rinv,
+                                                        const float* wf) {
+  const int e = blockIdx.y;
+  const int k = __ldg(f.ens_k + e);
+  const int* members = f.ens_models + (int64_t)e * f.kmax;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    int bad = -1;
+    for (int i = 0; i < k && bad < 0; ++i) {
+      const int m = __ldg(members + i);
+      if (__ldg(f.model_bad + m) >= 0) bad = 2 * i;                // TrainingError
+      else if (__ldg(f.model_status + m) != 0) bad = 2 * i + 1;  // no held-out metrics (DomainError)
+    }
+    f.ens_bad[e] = bad;
+  }
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  const int n = __ldg(f.ens_len + e);
+  if (r >= n) return;
+  const int64_t row = __ldg(f.ens_rows + e) + r;
+  double x[1][8];
+  const double2* xr = reinterpret_cast<const double2*>(f.rows + row * 8);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const double2 v = __ldg(xr + q);
+    x[0][2 * q] = v.x;
+    x[0][2 * q + 1] = v.y;
+  }
+  double sum = 0.0;
+  for (int i = 0; i < k; ++i) {
+    double o[1];
+    predict_rows<kExact, 1>(pa, rinv, wf, __ldg(members + i), x, o);
+    sum = i == 0 ? o[0] : __dadd_rn(sum, o[0]);
+  }
+  const int64_t out = __ldg(f.ens_out + e) + r;
+  f.pred[out] = __ddiv_rn(sum, (double)k);
+  f.truth_out[out] = __ldg(f.truth + row);
+}
+
+// Group statistics, one CTA per group: the OK items are compacted in order (block scan), then
+// per metric the mean is the sequential sum / count (one thread, item order) and the median the
+// value(s) at sorted positions (n-1)/2 and n/2, found by counting ranks (ties broken by order)
+// over tiles of the compacted values staged in shared memory.
+constexpr int kStatTile = 1024;
+
+__global__ void __launch_bounds__(256) cv_stats_kernel(CvStatsArgs a) {
+  __shared__ double tile[kStatTile];
+  __shared__ int warp_sum[8];
+  __shared__ int base;
+  __shared__ double mid[2];
+  const int g = blockIdx.x;
+  const int len = a.item_len[g];
+  const int64_t off = a.item_off[g];
+  const int* items = a.items + off;
+  double* vals = a.scratch + off;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) base = 0;
+  __syncthreads();
+  // ordered compaction: each thread keeps the (id, position) of its OK items of the first 8 chunks
+  // in registers; groups longer than 8 chunks are gathered sequentially by thread 0 instead
+  int my_id[8], my_pos[8], n_mine = 0;
+  int n_ok = 0;
+  for (int c0 = 0; c0 < len; c0 += blockDim.x) {
+    const int i = c0 + threadIdx.x;
+    int id = -1;
+    bool ok = false;
+    if (i < len) {
+      id = items[i];
+      ok = a.status[id] == 0 && a.bad[id] < 0;
+    }
+    const unsigned mask = __ballot_sync(0xffffffffu, ok);
+    if (lane == 0) warp_sum[warp] = __popc(mask);
+    __syncthreads();
+    int before = base;
+    for (int w = 0; w < warp; ++w) before += warp_sum[w];
+    before += __popc(mask & ((1u << lane) - 1u));
+    int total = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) total += warp_sum[w];
+    __syncthreads();
+    if (threadIdx.x == 0) base += total;
+    if (ok && n_mine < 8) {
+      my_id[n_mine] = id;
+      my_pos[n_mine] = before;
+      ++n_mine;
+    }
+    n_ok += total;
+  }
+  __syncthreads();
+  const int n = n_ok;
+  const double* ms[3] = {a.m0, a.m1, a.m2};
+  for (int q = 0; q < 3; ++q) {
+    // gather this metric's values in compacted order
+    for (int t = 0; t < n_mine; ++t) vals[my_pos[t]] = ms[q][my_id[t]];
+    if (len > 8 * (int)blockDim.x) {
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        int p = 0;
+        for (int i = 0; i < len; ++i) {
+          const int id = items[i];
+          if (a.status[id] == 0 && a.bad[id] < 0) vals[p++] = ms[q][id];
+        }
+      }
+    }
+    __syncthreads();
+    // ranks: each thread owns values i = threadIdx.x, + blockDim.x, ...
+    for (int i0 = 0; i0 < n; i0 += blockDim.x) {
+      const int i = i0 + threadIdx.x;
+      const double vi = i < n ? vals[i] : 0.0;
+      int rank = 0;
+      for (int j0 = 0; j0 < n; j0 += kStatTile) {
+        const int m = min(kStatTile, n - j0);
+        __syncthreads();
+        for (int j = threadIdx.x; j < m; j += blockDim.x) tile[j] = vals[j0 + j];
+        __syncthreads();
+        for (int j = 0; j < m; ++j) {
+          const double vj = tile[j];
+          rank += (vj < vi) || (vj == vi && j0 + j < i);
+        }
+      }
+      if (i < n) {
+        if (rank == (n - 1) / 2) mid[0] = vi;
+        if (rank == n / 2) mid[1] = vi;
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double mean = 0.0, median = 0.0;
+      if (n > 0) {
+        double acc = 0.0;
+        for (int i = 0; i < n; ++i) acc = __dadd_rn(acc, vals[i]);
+        mean = __ddiv_rn(acc, (double)n);
+        median = (n & 1) ? mid[1] : __ddiv_rn(__dadd_rn(mid[0], mid[1]), 2.0);
+      }
+      a.out[(int64_t)g * 6 + 2 * q] = mean;
+      a.out[(int64_t)g * 6 + 2 * q + 1] = median;
+      if (q == 0) a.n_ok[g] = n;
+    }
+    __syncthreads();
+  }
+}
+
 }  // namespace
 
 namespace {
@@ -531,6 +676,30 @@ void launch_eval(const EvalArgs& a, int max_len, int max_smem, int64_t total, cu
   eval_rank_global<<<grid, 256, 0, s>>>(a, rt, rp, pos);
   eval_sums_global<<<a.n_sets, 96, 0, s>>>(a, rt, rp, pos);
   cudaFreeAsync(scratch, s);
+}
+
+void launch_fold_mean(const PredictArgs& pa, const FoldMeanArgs& f, int max_len, bool exact, int n_models,
+                      int64_t n_params, cudaStream_t s) {
+  if (f.n_ens <= 0 || max_len <= 0) return;
+  const dim3 grid((unsigned)((max_len + 127) / 128), (unsigned)f.n_ens);
+  if (exact) {
+    fold_mean_kernel<true><<<grid, 128, 0, s>>>(pa, f, nullptr, nullptr);
+    return;
+  }
+  void* scratch = nullptr;
+  const size_t bytes = size_t(n_models) * 8 * sizeof(double) + size_t(n_params) * sizeof(float) + 16;
+  if (cudaMallocAsync(&scratch, bytes, s) != cudaSuccess) return;
+  double* rinv = static_cast<double*>(scratch);
+  float* wf = reinterpret_cast<float*>(rinv + size_t(n_models) * 8);
+  const int64_t n_prep = std::max<int64_t>(n_models, n_params);
+  predict_prep_kernel<<<(unsigned)((n_prep + 255) / 256), 256, 0, s>>>(pa, n_models, n_params, rinv, wf);
+  fold_mean_kernel<false><<<grid, 128, 0, s>>>(pa, f, rinv, wf);
+  cudaFreeAsync(scratch, s);
+}
+
+void launch_cv_stats(const CvStatsArgs& a, cudaStream_t s) {
+  if (a.n_groups <= 0) return;
+  cv_stats_kernel<<<a.n_groups, 256, 0, s>>>(a);
 }
 
 }  // namespace lann

@@ -16,7 +16,7 @@ import os
 import numpy as np
 
 from . import abi
-from .abi import ROW, Job, JobResult, MlpBatch, ModelSet, TrainBatch, World
+from .abi import ROW, CvEnsemble, CvGroup, Job, JobResult, MlpBatch, ModelSet, TrainBatch, World
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "lib", "libperfsage_b200.so")
@@ -116,6 +116,9 @@ def load_library(path: str = LIB_PATH):
     L.lann_population_destroy.argtypes = [vp]
     L.lann_population_norm.argtypes = [vp, vp]
     L.lann_transfer_bytes.argtypes = [vp, vp, C.c_int32]
+    L.lann_cv_layout.argtypes = [C.c_int32, C.POINTER(Job), vp, vp]
+    L.lann_population_cv_count.argtypes = [vp, vp, vp]
+    L.lann_population_cv.argtypes = [vp, C.POINTER(CvGroup), C.POINTER(CvEnsemble)]
     L.lann_train.argtypes = [vp, C.POINTER(TrainBatch)]
     L.lann_predict.argtypes = [vp, C.POINTER(ModelSet), C.c_int64, vp, vp, vp]
     L.lann_eval.argtypes = [vp, C.c_int32, vp, vp, vp, vp, C.c_double, vp, vp, vp, vp]
@@ -152,6 +155,18 @@ def load_library(path: str = LIB_PATH):
     L.lann_group_last_wall_ms.restype = C.c_double
     _lib = L
     return L
+
+
+def cv_layout(jobs):
+    """(groups, ensembles) a job list forms (lann_cv_layout; host only)."""
+    L = load_library()
+    n = len(jobs)
+    arr = (Job * max(1, n))(*jobs)
+    ng, ne = C.c_int32(), C.c_int32()
+    st = L.lann_cv_layout(n, arr, C.byref(ng), C.byref(ne))
+    if st:
+        raise ParamError("lann_cv_layout failed")
+    return ng.value, ne.value
 
 
 def _ptr(a):
@@ -488,6 +503,17 @@ class Population:
         out_p = [params[off[i]:off[i] + results[i].n_params].copy() for i in range(n)] if want_params else None
         out_t = [trace[toff[i]:toff[i] + self.jobs[i].epochs].copy() for i in range(n)] if trace is not None else None
         return st, results, out_p, out_t
+
+    def cv(self):
+        """The last pass's cross-validation summary (lann_population_cv): (groups, ensembles)."""
+        ng, ne = C.c_int32(), C.c_int32()
+        self.eng.L.lann_population_cv_count(self.h, C.byref(ng), C.byref(ne))
+        groups = (CvGroup * max(1, ng.value))()
+        ens = (CvEnsemble * max(1, ne.value))()
+        st = self.eng.L.lann_population_cv(self.h, groups, ens)
+        if st:
+            self.eng._raise(st)
+        return list(groups)[:ng.value], list(ens)[:ne.value]
 
     def close(self):
         if getattr(self, "h", None) and self.h.value:

@@ -145,6 +145,7 @@ class Oracle(_Lib):
         L.or_select_variants.argtypes = [C.POINTER(ModelSet), _i32p, C.c_int, C.c_int, C.c_uint64, C.c_int64, C.c_int64, _i32p, _dp]
         L.or_derive_seed.argtypes = [C.c_uint64, C.c_uint64]
         L.or_derive_seed.restype = C.c_uint64
+        L.or_fold_mean.argtypes = [C.c_int, C.POINTER(Job), C.POINTER(_dp), _dp, _dp, C.POINTER(C.c_int)]
 
     def run_job(self, job: Job, want_params=False, want_trace=False):
         r = JobResult()
@@ -180,6 +181,82 @@ class Oracle(_Lib):
         c = C.c_uint64(0)
         self.lib.or_candidate(kind, max_threads, seed, idx, base, C.byref(c))
         return base, c.value
+
+
+    def fold_mean(self, fold_jobs, params):
+        """or_fold_mean: the fold-mean model of one seed's k fold models on the split's test part
+        -> (pred, truth)."""
+        k = len(fold_jobs)
+        arr = (Job * k)(*fold_jobs)
+        keep = [np.ascontiguousarray(p, dtype=np.float64) for p in params]
+        pp = (_dp * k)(*[q.ctypes.data_as(_dp) for q in keep])
+        n = fold_jobs[0].count
+        pred, truth, nt = np.zeros(n), np.zeros(n), C.c_int(0)
+        st = self.lib.or_fold_mean(k, arr, pp, pred, truth, C.byref(nt))
+        assert st == 0, st
+        return pred[: nt.value], truth[: nt.value]
+
+    def cv_summary(self, jobs, results, params):
+        """The cross-validation summary (include/lann_engine.h) restated in Python over the
+        oracle's per-job results and weights: groups keyed by every job field except fold and
+        init_seed, ensembles by (group, init_seed); fold-mean test metrics through or_fold_mean and
+        the oracle's make_report; mean = sequential sum / n, median = sorted middle(s)."""
+        def gkey(j):
+            return (bytes(j.world), j.data_seed, j.count, j.train_fraction, j.n_folds, j.family, j.n_hidden,
+                    tuple(j.hidden), j.learning_rate, j.epochs, j.log_target, j.unconstrained)
+        groups, ens = {}, {}
+        for i, j in enumerate(jobs):
+            if j.n_folds < 2:
+                continue
+            g = groups.setdefault(gkey(j), {"first": i, "k": j.n_folds, "models": [], "ens": []})
+            g["models"].append(i)
+            key = (gkey(j), j.init_seed)
+            if key not in ens:
+                ens[key] = {"group": list(groups).index(gkey(j)), "seed": j.init_seed, "member": [-1] * j.n_folds}
+                g["ens"].append(key)
+            if 0 <= j.fold < j.n_folds and ens[key]["member"][j.fold] < 0:
+                ens[key]["member"][j.fold] = i
+        ok = lambda r: r.status == 0  # noqa: E731
+        out_ens = []
+        for key, e in ens.items():
+            rec = {"group": e["group"], "seed": e["seed"], "status": 0}
+            if any(m < 0 for m in e["member"]):
+                rec["status"] = 1  # LANN_PARAM_ERROR: a fold is missing
+            elif not all(ok(results[m]) for m in e["member"]):
+                rec["status"] = next(results[m].status for m in e["member"] if not ok(results[m]))
+            else:
+                pred, truth = self.fold_mean([jobs[m] for m in e["member"]], [params[m] for m in e["member"]])
+                st1, rec["mape"] = self.mape(truth, pred)
+                st2, rec["mape_thr"], rec["n_kept"] = self.mape_thresholded(truth, pred)
+                st3, rec["rho"] = self.spearman(truth, pred)
+                rec["status"] = st1 or st2 or st3
+                rec["n_test"] = len(truth)
+            out_ens.append(rec)
+
+        def stats(vals):
+            if not vals:
+                return (0.0, 0.0)
+            acc = 0.0
+            for v in vals:
+                acc += v
+            s_ = sorted(vals)
+            n = len(s_)
+            return (acc / n, s_[n // 2] if n % 2 else (s_[n // 2 - 1] + s_[n // 2]) / 2)
+        out_groups = []
+        ens_list = list(ens)
+        for gk, g in groups.items():
+            rows = [results[m] for m in g["models"] if ok(results[m])]
+            eo = [out_ens[ens_list.index(k)] for k in g["ens"]]
+            eo = [e for e in eo if e["status"] == 0]
+            out_groups.append({
+                "first_job": g["first"], "n_folds": g["k"], "n_models": len(g["models"]), "n_models_ok": len(rows),
+                "n_ensembles": len(g["ens"]), "n_ensembles_ok": len(eo),
+                "fold_mape": stats([r.mape for r in rows]), "fold_mape_thr": stats([r.mape_thr for r in rows]),
+                "fold_rho": stats([r.rho for r in rows]),
+                "test_mape": stats([e["mape"] for e in eo]), "test_mape_thr": stats([e["mape_thr"] for e in eo]),
+                "test_rho": stats([e["rho"] for e in eo]),
+            })
+        return out_groups, out_ens
 
 
 class Reference(_Lib):

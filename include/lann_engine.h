@@ -414,6 +414,11 @@ int lann_cv_layout(int32_t n_jobs, const lann_job* jobs, int32_t* n_groups, int3
 /* the last pass's summary; arrays sized by lann_cv_layout (or lann_population_cv_count) */
 int lann_population_cv_count(const lann_population* pop, int32_t* n_groups, int32_t* n_ensembles);
 int lann_population_cv(lann_population* pop, lann_cv_group* groups, lann_cv_ensemble* ensembles);
+/* the group statistics from per-job results and per-ensemble scores already on the host (merging
+ * shards that ran on several devices or processes), computed on the engine's device; ensembles in
+ * lann_cv_layout order, groups written (sized by lann_cv_layout) */
+int lann_cv_summarize(lann_engine* engine, int32_t n_jobs, const lann_job* jobs, const lann_job_result* results,
+                      const lann_cv_ensemble* ensembles, lann_cv_group* groups);
 
 /* The 48 kernel-variant-hardware combinations of BASELINE config 2 (worlds
  * only). Writes up to cap entries, returns the count. */
@@ -435,12 +440,21 @@ void lann_group_destroy(lann_group* group);
 const char* lann_group_last_error(const lann_group* group);
 int32_t lann_group_size(const lann_group* group);
 /* the shard cut for n_jobs jobs over n_shards devices (host only, no device needed):
- * bounds[0] = 0 <= bounds[1] <= ... <= bounds[n_shards] = n_jobs */
+ * bounds[0] = 0 <= bounds[1] <= ... <= bounds[n_shards] = n_jobs; cost-balanced, each cut then
+ * moved forward past adjacent jobs of the same cross-validation ensemble */
 int lann_shard_bounds(int32_t n_shards, int32_t n_jobs, const lann_job* jobs, int32_t* bounds);
 int lann_group_shard_bounds(const lann_group* group, int32_t n_jobs, const lann_job* jobs, int32_t* bounds);
 int lann_group_run_population(lann_group* group, int32_t n_jobs, const lann_job* jobs, int32_t precision,
                               lann_job_result* results, double* params_out, const int64_t* params_offset,
                               double* trace_out, const int64_t* trace_offset);
+/* lann_group_run_population with the cross-validation summary of the whole job list: the jobs
+ * of every ensemble are placed next to each other (ensembles in order of first appearance) and
+ * shard cuts never split an ensemble, each device scores its ensembles' fold-mean models, and the
+ * group statistics over all shards are computed on the first device (lann_cv_summarize). Results
+ * come back in job order; groups / ensembles sized by lann_cv_layout. FP64-exact summaries do not
+ * depend on the number of devices. */
+int lann_group_run_cv(lann_group* group, int32_t n_jobs, const lann_job* jobs, int32_t precision,
+                      lann_job_result* results, lann_cv_group* groups, lann_cv_ensemble* ensembles);
 /* device time of the last run: the maximum over the group's devices (their shards run
  * concurrently), and the wall time of the whole call */
 double lann_group_last_device_ms(const lann_group* group);

@@ -2410,6 +2410,11 @@ double job_cost(const lann_job& j) {
   return double(j.epochs) * double(std::max(0, n_train)) * p;
 }
 
+// adjacent jobs of one cross-validation ensemble (same group, same init seed) are never cut apart
+bool same_ensemble(const lann_job& a, const lann_job& b) {
+  return a.n_folds >= 2 && b.n_folds >= 2 && a.init_seed == b.init_seed && cv_group_key(a) == cv_group_key(b);
+}
+
 void shard_bounds(int n_jobs, const lann_job* jobs, int world, int32_t* b) {
   double total = 0.0;
   for (int i = 0; i < n_jobs; ++i) total += job_cost(jobs[i]);
@@ -2425,6 +2430,11 @@ void shard_bounds(int n_jobs, const lann_job* jobs, int world, int32_t* b) {
   }
   while (nb < world) b[nb++] = n_jobs;
   b[world] = n_jobs;
+  for (int w = 1; w < world; ++w) {  // snap each cut forward to the end of the ensemble it splits
+    int c = std::max(b[w], b[w - 1]);
+    while (c > 0 && c < n_jobs && same_ensemble(jobs[c - 1], jobs[c])) ++c;
+    b[w] = c;
+  }
 }
 }  // namespace
 
@@ -2515,3 +2525,252 @@ int lann_group_run_population(lann_group* g, int32_t n_jobs, const lann_job* job
     }
   return rc;
 }
+
+// ---- cross-validation statistics from host results (multi-device / multi-process merges) ------
+namespace {
+Status cv_group_stats(lann_engine* e, int n_jobs, const lann_job* jobs, const lann_job_result* results,
+                      const lann_cv_ensemble* ensembles, lann_cv_group* groups) {
+  const CvLayout L = cv_layout(n_jobs, jobs);
+  const int G = L.n_groups(), E = L.n_ens();
+  if (G == 0) return {};
+  // items: fold models (job order) and ensembles (ensemble order) of every group; their metrics
+  // and statuses packed beside them (bad = -1: the statuses carry every failure)
+  std::vector<int64_t> fo(static_cast<size_t>(G)), eo(static_cast<size_t>(G));
+  std::vector<int> fl(size_t(G), 0), el(size_t(G), 0), fi, ei;
+  std::vector<std::vector<int>> fg(static_cast<size_t>(G)), eg(static_cast<size_t>(G));
+  for (int j = 0; j < n_jobs; ++j)
+    if (L.job_group[size_t(j)] >= 0) fg[size_t(L.job_group[size_t(j)])].push_back(j);
+  for (int en = 0; en < E; ++en) eg[size_t(L.ens_group[size_t(en)])].push_back(en);
+  for (int g = 0; g < G; ++g) {
+    fo[size_t(g)] = int64_t(fi.size());
+    fl[size_t(g)] = int(fg[size_t(g)].size());
+    fi.insert(fi.end(), fg[size_t(g)].begin(), fg[size_t(g)].end());
+    eo[size_t(g)] = int64_t(ei.size());
+    el[size_t(g)] = int(eg[size_t(g)].size());
+    ei.insert(ei.end(), eg[size_t(g)].begin(), eg[size_t(g)].end());
+  }
+  const int N = std::max(n_jobs, E);
+  BlobLayout B;
+  const size_t oFO = B.add<int64_t>(size_t(G)), oFL = B.add<int>(size_t(G)), oFI = B.add<int>(fi.size());
+  const size_t oEO = B.add<int64_t>(size_t(G)), oEL = B.add<int>(size_t(G)), oEI = B.add<int>(ei.size());
+  const size_t oM = B.add<double>(size_t(N) * 6);      // job mape/thr/rho, then ensemble mape/thr/rho
+  const size_t oS = B.add<int>(size_t(N) * 2), oBad = B.add<int>(size_t(N));
+  const size_t up = B.bytes;
+  const size_t oOut = B.add<double>(size_t(G) * 12), oNok = B.add<int>(size_t(G) * 2);
+  const size_t oScr = B.add<double>(std::max(fi.size(), ei.size()));
+  std::vector<unsigned char> h(B.bytes, 0);
+  auto H = [&](auto* tag, size_t off) { return reinterpret_cast<decltype(tag)>(h.data() + off); };
+  std::copy(fo.begin(), fo.end(), H((int64_t*)nullptr, oFO));
+  std::copy(fl.begin(), fl.end(), H((int*)nullptr, oFL));
+  std::copy(fi.begin(), fi.end(), H((int*)nullptr, oFI));
+  std::copy(eo.begin(), eo.end(), H((int64_t*)nullptr, oEO));
+  std::copy(el.begin(), el.end(), H((int*)nullptr, oEL));
+  std::copy(ei.begin(), ei.end(), H((int*)nullptr, oEI));
+  double* m = H((double*)nullptr, oM);
+  int* st = H((int*)nullptr, oS);
+  for (int j = 0; j < n_jobs; ++j) {
+    m[size_t(j)] = results[j].mape;
+    m[size_t(N) + size_t(j)] = results[j].mape_thr;
+    m[2 * size_t(N) + size_t(j)] = results[j].rho;
+    st[j] = results[j].status;
+  }
+  for (int en = 0; en < E; ++en) {
+    m[3 * size_t(N) + size_t(en)] = ensembles[en].mape;
+    m[4 * size_t(N) + size_t(en)] = ensembles[en].mape_thr;
+    m[5 * size_t(N) + size_t(en)] = ensembles[en].rho;
+    st[size_t(N) + size_t(en)] = ensembles[en].status;
+  }
+  std::fill(H((int*)nullptr, oBad), H((int*)nullptr, oBad) + N, -1);
+  ck(cudaSetDevice(e->device), "cudaSetDevice");
+  DBuf<unsigned char> d(B.bytes, e->stream);
+  d.up(h.data(), up);
+  auto D = [&](auto* tag, size_t off) { return reinterpret_cast<decltype(tag)>(d.p + off); };
+  const double* dm = D((const double*)nullptr, oM);
+  const int* ds = D((const int*)nullptr, oS);
+  const int* dbad = D((const int*)nullptr, oBad);
+  double* out = D((double*)nullptr, oOut);
+  int* nok = D((int*)nullptr, oNok);
+  double* scr = D((double*)nullptr, oScr);
+  const size_t n = size_t(N);
+  launch_cv_stats(CvStatsArgs{G, D((const int64_t*)nullptr, oFO), D((const int*)nullptr, oFL),
+                              D((const int*)nullptr, oFI), dm, dm + n, dm + 2 * n, ds, dbad, out, nok, scr},
+                  e->stream);
+  launch_cv_stats(CvStatsArgs{G, D((const int64_t*)nullptr, oEO), D((const int*)nullptr, oEL),
+                              D((const int*)nullptr, oEI), dm + 3 * n, dm + 4 * n, dm + 5 * n, ds + n, dbad,
+                              out + size_t(G) * 6, nok + G, scr},
+                  e->stream);
+  ck(cudaGetLastError(), "cv stats launch");
+  ck(cudaMemcpyAsync(h.data() + oOut, d.p + oOut, B.bytes - oOut, cudaMemcpyDeviceToHost, e->stream), "D2H");
+  t_d2h += int64_t(B.bytes - oOut);
+  ck(cudaStreamSynchronize(e->stream), "cv stats");
+  const double* so = H((const double*)nullptr, oOut);
+  const int* no = H((const int*)nullptr, oNok);
+  for (int g = 0; g < G; ++g) {
+    lann_cv_group& o = groups[g];
+    o = lann_cv_group{};
+    o.first_job = L.group_first[size_t(g)];
+    o.n_folds = L.group_folds[size_t(g)];
+    o.n_models = L.group_models[size_t(g)];
+    o.n_models_ok = no[g];
+    o.n_ensembles = L.group_ens[size_t(g)];
+    o.n_ensembles_ok = no[G + g];
+    for (int en : eg[size_t(g)])
+      if (ensembles[en].n_test > 0) o.n_test = ensembles[en].n_test;
+    const double* a = so + 6 * size_t(g);
+    const double* b = so + 6 * size_t(G) + 6 * size_t(g);
+    o.fold_mape = {a[0], a[1]};
+    o.fold_mape_thr = {a[2], a[3]};
+    o.fold_rho = {a[4], a[5]};
+    o.test_mape = {b[0], b[1]};
+    o.test_mape_thr = {b[2], b[3]};
+    o.test_rho = {b[4], b[5]};
+  }
+  return {};
+}
+}  // namespace
+
+extern "C" {
+
+int lann_cv_summarize(lann_engine* e, int32_t n_jobs, const lann_job* jobs, const lann_job_result* results,
+                      const lann_cv_ensemble* ensembles, lann_cv_group* groups) {
+  if (!e) return LANN_NO_DEVICE;
+  if (n_jobs < 0 || (n_jobs > 0 && (!jobs || !results)) || !groups)
+    return set_err(e, {LANN_PARAM_ERROR, "null arguments"});
+  try {
+    return set_err(e, cv_group_stats(e, n_jobs, jobs, results, ensembles, groups));
+  } catch (const CudaFail& f) {
+    e->err = f.what;
+    return LANN_CUDA_ERROR;
+  }
+}
+
+int lann_group_run_cv(lann_group* g, int32_t n_jobs, const lann_job* jobs, int32_t precision,
+                      lann_job_result* results, lann_cv_group* groups, lann_cv_ensemble* ensembles) {
+  if (!g) return LANN_NO_DEVICE;
+  if (!results || !jobs || n_jobs < 1 || !groups || !ensembles) {
+    g->err = "empty population or null outputs";
+    return LANN_PARAM_ERROR;
+  }
+  const CvLayout L = cv_layout(n_jobs, jobs);
+  // every ensemble's jobs adjacent (ensembles in order of first appearance, members in job
+  // order), so the snapped shard cut keeps each ensemble on one device
+  std::vector<int> perm;
+  perm.reserve(static_cast<size_t>(n_jobs));
+  {
+    std::vector<std::vector<int>> members(static_cast<size_t>(L.n_ens()));
+    for (int j = 0; j < n_jobs; ++j)
+      if (L.job_ens[size_t(j)] >= 0) members[size_t(L.job_ens[size_t(j)])].push_back(j);
+    std::vector<char> done(static_cast<size_t>(L.n_ens()), 0);
+    for (int j = 0; j < n_jobs; ++j) {
+      const int en = L.job_ens[size_t(j)];
+      if (en < 0) {
+        perm.push_back(j);
+      } else if (!done[size_t(en)]) {
+        done[size_t(en)] = 1;
+        perm.insert(perm.end(), members[size_t(en)].begin(), members[size_t(en)].end());
+      }
+    }
+  }
+  std::vector<lann_job> pj(static_cast<size_t>(n_jobs));
+  for (int i = 0; i < n_jobs; ++i) pj[size_t(i)] = jobs[perm[size_t(i)]];
+  const int W = int(g->engines.size());
+  std::vector<int32_t> b(size_t(W) + 1);
+  shard_bounds(n_jobs, pj.data(), W, b.data());
+  std::vector<lann_job_result> pres(static_cast<size_t>(n_jobs));
+  std::vector<int> st(static_cast<size_t>(W), LANN_OK);
+  std::vector<double> dev_ms(static_cast<size_t>(W), 0.0);
+  std::vector<int64_t> h2d(static_cast<size_t>(W), 0), d2h(static_cast<size_t>(W), 0);
+  std::vector<std::vector<lann_cv_ensemble>> sh_ens(static_cast<size_t>(W));
+  std::vector<std::vector<int>> sh_first(static_cast<size_t>(W));  // first member (permuted index) of each local ensemble
+  const auto t0 = std::chrono::steady_clock::now();
+  auto work = [&](int w) {
+    const int lo = b[size_t(w)], n = b[size_t(w) + 1] - lo;
+    if (n <= 0) return;
+    lann_engine* e = g->engines[size_t(w)];
+    lann_transfer_bytes(nullptr, nullptr, 1);
+    lann_population* p = nullptr;
+    std::vector<lann_job_result> base;
+    int rc = population_create(e, n, pj.data() + lo, precision, 0, &p, false, &base);
+    if (!p) {
+      for (int j = 0; j < n; ++j) {
+        if (size_t(j) < base.size()) {
+          pres[size_t(lo + j)] = base[size_t(j)];
+        } else {
+          pres[size_t(lo + j)] = lann_job_result{};
+          pres[size_t(lo + j)].status = rc;
+          pres[size_t(lo + j)].nonfinite_epoch = -1;
+          pres[size_t(lo + j)].precision_run = -1;
+        }
+      }
+    } else {
+      rc = lann_population_run(p, 1);
+      if (rc == LANN_OK) rc = lann_population_fetch(p, pres.data() + lo, nullptr, nullptr, nullptr, nullptr);
+      const CvState* cv = p->pop.cv.get();
+      if (cv && (rc == LANN_OK || rc == LANN_TRAINING_ERROR || rc == LANN_DOMAIN_ERROR)) {
+        sh_ens[size_t(w)].resize(size_t(cv->L.n_ens()));
+        const int rc2 = lann_population_cv(p, nullptr, sh_ens[size_t(w)].data());
+        if (rc2 != LANN_OK) rc = rc2;
+        for (int en = 0; en < cv->L.n_ens(); ++en) {
+          int first = n;
+          for (int j : cv->L.ens_member[size_t(en)])
+            if (j >= 0) first = std::min(first, j);
+          sh_first[size_t(w)].push_back(lo + first);
+        }
+      }
+      lann_population_destroy(p);
+    }
+    st[size_t(w)] = rc;
+    dev_ms[size_t(w)] = lann_last_device_ms(e);
+    lann_transfer_bytes(&h2d[size_t(w)], &d2h[size_t(w)], 1);
+  };
+  std::vector<std::thread> threads;
+  for (int w = 1; w < W; ++w) threads.emplace_back(work, w);
+  work(0);
+  for (auto& t : threads) t.join();
+  g->last_device_ms = *std::max_element(dev_ms.begin(), dev_ms.end());
+  for (int w = 0; w < W; ++w) {
+    t_h2d += h2d[size_t(w)];
+    t_d2h += d2h[size_t(w)];
+  }
+  for (int i = 0; i < n_jobs; ++i) results[perm[size_t(i)]] = pres[size_t(i)];
+  // ensembles in the global layout's order; an ensemble not scored on any shard (every one of its
+  // jobs failed before a population formed) reports its missing / failed members from the results
+  for (int en = 0; en < L.n_ens(); ++en) {
+    lann_cv_ensemble& o = ensembles[en];
+    o = lann_cv_ensemble{};
+    o.group = L.ens_group[size_t(en)];
+    o.init_seed = L.ens_seed[size_t(en)];
+    o.status = LANN_PARAM_ERROR;
+    for (int j : L.ens_member[size_t(en)])
+      if (j >= 0 && results[j].status != LANN_OK) {
+        o.status = results[j].status;
+        break;
+      }
+  }
+  for (int w = 0; w < W; ++w)
+    for (size_t q = 0; q < sh_ens[size_t(w)].size(); ++q) {
+      const int global_job = perm[size_t(sh_first[size_t(w)][q])];
+      const int en = L.job_ens[size_t(global_job)];
+      lann_cv_ensemble r = sh_ens[size_t(w)][q];
+      r.group = L.ens_group[size_t(en)];
+      ensembles[en] = r;
+    }
+  g->err.clear();
+  int rc = LANN_OK;
+  for (int w = 0; w < W; ++w)
+    if (st[size_t(w)] != LANN_OK && rc == LANN_OK) {
+      rc = st[size_t(w)];
+      g->err = std::string("device ") + std::to_string(g->engines[size_t(w)]->device) + ": " +
+               lann_last_error(g->engines[size_t(w)]);
+    }
+  // the group statistics over every shard's models and ensembles, on the first device
+  const int rs = lann_cv_summarize(g->engines[0], n_jobs, jobs, results, ensembles, groups);
+  if (rs != LANN_OK && rc == LANN_OK) {
+    rc = rs;
+    g->err = lann_last_error(g->engines[0]);
+  }
+  g->last_wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  return rc;
+}
+
+}  // extern "C"

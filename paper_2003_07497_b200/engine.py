@@ -119,6 +119,10 @@ def load_library(path: str = LIB_PATH):
     L.lann_cv_layout.argtypes = [C.c_int32, C.POINTER(Job), vp, vp]
     L.lann_population_cv_count.argtypes = [vp, vp, vp]
     L.lann_population_cv.argtypes = [vp, C.POINTER(CvGroup), C.POINTER(CvEnsemble)]
+    L.lann_cv_summarize.argtypes = [vp, C.c_int32, C.POINTER(Job), C.POINTER(JobResult), C.POINTER(CvEnsemble),
+                                    C.POINTER(CvGroup)]
+    L.lann_group_run_cv.argtypes = [vp, C.c_int32, C.POINTER(Job), C.c_int32, C.POINTER(JobResult),
+                                    C.POINTER(CvGroup), C.POINTER(CvEnsemble)]
     L.lann_train.argtypes = [vp, C.POINTER(TrainBatch)]
     L.lann_predict.argtypes = [vp, C.POINTER(ModelSet), C.c_int64, vp, vp, vp]
     L.lann_eval.argtypes = [vp, C.c_int32, vp, vp, vp, vp, C.c_double, vp, vp, vp, vp]
@@ -434,6 +438,20 @@ class Engine:
         return idx, score, hist
 
     # ---- models::train_nn + predict_dataset + make_report over a population ----
+    def cv_summarize(self, jobs, results, ensembles):
+        """lann_cv_summarize: group statistics from host results and ensemble scores (merging
+        shards from several devices or processes) computed on this engine's device."""
+        n = len(jobs)
+        ng, ne = cv_layout(jobs)
+        arr = (Job * max(1, n))(*jobs)
+        res = (JobResult * max(1, n))(*results)
+        ens = (CvEnsemble * max(1, ne))(*ensembles)
+        groups = (CvGroup * max(1, ng))()
+        st = self.L.lann_cv_summarize(self.h, n, arr, res, ens, groups)
+        if st:
+            self._raise(st)
+        return list(groups)[:ng]
+
     def run_population(self, jobs, precision=abi.FP64_EXACT, want_params=False, want_trace=False):
         n = len(jobs)
         arr = (Job * n)(*jobs)
@@ -610,6 +628,17 @@ class Group:
         if want_params:
             plist = [params[off[k]: off[k] + res[k].n_params].copy() for k in range(n)]
         return st, list(res), plist
+
+    def run_cv(self, jobs, precision=abi.FP64_EXACT):
+        """lann_group_run_cv -> (status, results, cv groups, cv ensembles)."""
+        n = len(jobs)
+        arr = (Job * n)(*jobs)
+        res = (JobResult * n)()
+        ng, ne = cv_layout(jobs)
+        groups = (CvGroup * max(1, ng))()
+        ens = (CvEnsemble * max(1, ne))()
+        st = self.L.lann_group_run_cv(self.h, n, arr, precision, res, groups, ens)
+        return st, list(res), list(groups)[:ng], list(ens)[:ne]
 
 
 class Pinned:

@@ -24,8 +24,16 @@ def job_cost(j) -> float:
     return float(j.epochs) * n_train * p
 
 
+def _ensemble_key(j):
+    """A job's cross-validation ensemble (include/lann_engine.h): every field except fold."""
+    return (bytes(j.world), j.data_seed, j.count, j.train_fraction, j.n_folds, j.family, j.n_hidden,
+            j.hidden[0], j.hidden[1], j.learning_rate, j.epochs, j.log_target, j.unconstrained, j.init_seed)
+
+
 def shard_bounds(jobs: Sequence, world: int) -> List[int]:
-    """Contiguous split points [b0=0, b1, ..., bW=len] balancing cumulative cost."""
+    """Contiguous split points [b0=0, b1, ..., bW=len] balancing cumulative cost; each cut is then
+    moved forward past adjacent jobs of one cross-validation ensemble (k-fold jobs that differ only
+    in fold), so a shard scores its ensembles' fold-mean models itself (lann_shard_bounds)."""
     costs = [job_cost(j) for j in jobs]
     total = sum(costs)
     bounds, acc, r = [0], 0.0, 1
@@ -37,6 +45,12 @@ def shard_bounds(jobs: Sequence, world: int) -> List[int]:
     while len(bounds) < world:
         bounds.append(len(jobs))
     bounds.append(len(jobs))
+    for w in range(1, world):
+        c = max(bounds[w], bounds[w - 1])
+        while 0 < c < len(jobs) and jobs[c - 1].n_folds >= 2 and jobs[c].n_folds >= 2 and \
+                _ensemble_key(jobs[c - 1]) == _ensemble_key(jobs[c]):
+            c += 1
+        bounds[w] = c
     return bounds
 
 

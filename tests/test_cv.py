@@ -147,3 +147,29 @@ def test_cv_summary_fp32_population(engine, oracle):
         assert np.isfinite(a.test_mape.mean) and abs(a.test_mape_thr.mean - b.test_mape_thr.mean) < 5.0
     p32.close()
     p64.close()
+
+
+@pytest.mark.gpu
+def test_cv_group_equals_single_engine(engine):
+    """lann_group_run_cv over two shards (one B200 listed twice) == the single-engine summary, bit
+    for bit in FP64, also for a job list whose ensembles are interleaved (sorted by fold: the group
+    places each ensemble's jobs together before cutting); lann_cv_summarize over the single
+    engine's host results reproduces its on-device group statistics."""
+    base = small_sweep(n_seeds=3, epochs=80)
+    for jobs in (base, sorted(base, key=lambda j: j.fold)):
+        pop = E.Population(engine, jobs, abi.FP64_EXACT)
+        pop.run(1)
+        st, res, _, _ = pop.fetch()
+        groups, ens = pop.cv()
+        assert st == 0
+        again = engine.cv_summarize(jobs, res, ens)
+        assert [bytes(x) for x in again] == [bytes(x) for x in groups]
+        with E.Group([0, 0]) as g:
+            b = g.shard_bounds(jobs)
+            assert 0 < b[1] < len(jobs)
+            gst, gres, ggroups, gens = g.run_cv(jobs)
+        assert gst == 0, g.last_error
+        assert [bytes(x) for x in gres] == [bytes(x) for x in res]
+        assert [bytes(x) for x in gens] == [bytes(x) for x in ens]
+        assert [bytes(x) for x in ggroups] == [bytes(x) for x in groups]
+        pop.close()

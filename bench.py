@@ -446,6 +446,32 @@ def extras(E, eng, rank, world, barrier, max_over_ranks, args, flush, peaks):
             out["config5_lann_vs_ffnn"] = lann_vs_ffnn(eng)
         except Exception as ex:  # noqa: BLE001
             out["config5_lann_vs_ffnn"] = {"error": str(ex)}
+    def config3_cv_summary(eng, sweep, res, cv_ens, rank, world):
+        """Per-combination cross-validation statistics (lann_engine.h): on one GPU straight from the
+        device pass; with N ranks the shards' results and ensemble scores are gathered on the host
+        (gloo) and rank 0 computes the group statistics on its device (lann_cv_summarize)."""
+        if world > 1:
+            import torch.distributed as dist
+            parts = [None] * world
+            dist.all_gather_object(parts, ([bytes(r) for r in res], [bytes(e) for e in cv_ens]))
+            res = [abi.JobResult.from_buffer_copy(b) for p in parts for b in p[0]]
+            cv_ens = [abi.CvEnsemble.from_buffer_copy(b) for p in parts for b in p[1]]
+        if rank != 0:
+            return None
+        groups = eng.cv_summarize(sweep, res, cv_ens)
+        rows = [{"combo": i, "fold_mape_thr_median": g.fold_mape_thr.median,
+                 "test_mape_mean": g.test_mape.mean, "test_mape_thr_mean": g.test_mape_thr.mean,
+                 "test_mape_thr_median": g.test_mape_thr.median, "ensembles_ok": g.n_ensembles_ok}
+                for i, g in enumerate(groups)]
+        return {"groups": len(groups), "ensembles": len(cv_ens),
+                "ensembles_ok": int(sum(g.n_ensembles_ok for g in groups)),
+                "mean_over_combos_fold_mean_test_mape": float(np.mean([g.test_mape.mean for g in groups])),
+                "mean_over_combos_fold_mean_test_mape_thr": float(np.mean([g.test_mape_thr.mean for g in groups])),
+                "definition": "per combination: held-out fold metrics over 256 seeds x 5 folds and the test-part "
+                              "MAPE of each seed's fold-mean model ((p_0+...+p_4)/5), mean and median; computed "
+                              "on the device inside the timed pass (include/lann_engine.h)",
+                "per_combo": rows}
+
     try:
         n_seeds = int(os.environ.get("LANN_SWEEP_SEEDS", 256))
         sweep = popmod.config3_jobs(root_seed=1, n_seeds=n_seeds)
@@ -460,15 +486,18 @@ def extras(E, eng, rank, world, barrier, max_over_ranks, args, flush, peaks):
         tms = eng.last_train_ms
         tflops = ps.flop / (tms / 1e3) / 1e12
         st, res, _, _ = ps.fetch()
+        _, cv_ens = ps.cv()  # this shard's fold-mean test scores (shard cuts never split an ensemble)
         merged = sharding.gather_results(res, rank, world)
         me = popmod.model_epochs(sweep)
         thr = np.array([r[3] for r in merged]) if world > 1 else np.array([r.mape_thr for r in merged])
+        cv_summary = config3_cv_summary(eng, sweep, res, cv_ens, rank, world)
         out["config3_sweep_fp32"] = {"models": len(sweep), "model_epochs": me, "n_gpus": world, "scaling": "strong",
                                      "value": me / (ms / 1e3), "unit": "model-epochs/s", "ms": ms, "dtype": "f32",
                                      "rank0_models": len(mine), "rank0_train_tflops": tflops,
                                      "rank0_frac_of_fp32_peak": tflops / peaks["fp32_tflops"],
                                      "rank0_host_prepare_s": prep_s,
                                      "median_fold_thr_mape": float(np.median(thr)),
+                                     "cross_validation": cv_summary,
                                      "note": f"48 combos x {n_seeds} seeds x 5 folds; contiguous cost-balanced "
                                              "shards, one per rank, no data-path collective; max-over-ranks device time"}
         ps.close()

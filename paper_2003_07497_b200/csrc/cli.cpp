@@ -672,8 +672,17 @@ int cmd_sweep(const Args& a) {
   lann_group_shard_bounds(group, std::int32_t(jobs.size()), jobs.data(), bounds.data());
   const auto t0 = std::chrono::steady_clock::now();
   std::vector<lann_job_result> res(jobs.size());
-  const int st = lann_group_run_population(group, std::int32_t(jobs.size()), jobs.data(), precision, res.data(),
-                                           nullptr, nullptr, nullptr, nullptr);
+  // k-fold sweeps also return the cross-validation summary (fold-mean test scores per seed,
+  // per-combination fold and test statistics), computed on the devices
+  std::int32_t n_groups = 0, n_ens = 0;
+  lann_cv_layout(std::int32_t(jobs.size()), jobs.data(), &n_groups, &n_ens);
+  std::vector<lann_cv_group> cvg(std::size_t(std::max(1, n_groups)));
+  std::vector<lann_cv_ensemble> cve(std::size_t(std::max(1, n_ens)));
+  const int st = n_groups > 0
+                     ? lann_group_run_cv(group, std::int32_t(jobs.size()), jobs.data(), precision, res.data(),
+                                         cvg.data(), cve.data())
+                     : lann_group_run_population(group, std::int32_t(jobs.size()), jobs.data(), precision,
+                                                 res.data(), nullptr, nullptr, nullptr, nullptr);
   const auto t2 = std::chrono::steady_clock::now();
   const double dev_ms = lann_group_last_device_ms(group);
   double flop = 0.0;  // algorithmic FLOP of the trainers
@@ -707,10 +716,12 @@ int cmd_sweep(const Args& a) {
     if (r.status == LANN_OK) thr[{mt.family, mt.combo}].push_back(r.mape_thr);
   }
   os.close();
-  std::cout << std::left << std::setw(7) << "combo" << std::setw(8) << "kernel" << std::setw(22) << "variant"
-            << std::setw(7) << "model" << std::right << std::setw(10) << "models" << std::setw(14)
-            << "median MAPE30%" << "\n";
+  if (n_groups == 0)
+    std::cout << std::left << std::setw(7) << "combo" << std::setw(8) << "kernel" << std::setw(22) << "variant"
+              << std::setw(7) << "model" << std::right << std::setw(10) << "models" << std::setw(14)
+              << "median MAPE30%" << "\n";
   for (const auto& [key, v] : thr) {
+    if (n_groups > 0) break;
     auto s = v;
     std::sort(s.begin(), s.end());
     const double med = s.size() % 2 ? s[s.size() / 2] : 0.5 * (s[s.size() / 2 - 1] + s[s.size() / 2]);
@@ -732,7 +743,38 @@ int cmd_sweep(const Args& a) {
       std::cout << ' ' << devices[d] << ':' << bounds[d + 1] - bounds[d];
     std::cout << "\n";
   }
-  record_run(out, a, root, {}, {csv.string()});
+  std::vector<std::string> outputs{csv.string()};
+  if (n_groups > 0) {
+    // cv.csv: one row per combination x family: held-out fold statistics over its seeds x folds
+    // and the fold-mean model's test-part statistics over its seeds (mean, median)
+    const fs::path cvp = out / "cv.csv";
+    std::ofstream cs(cvp, std::ios::binary);
+    cs << "combo,kernel,variant,family,n_folds,n_models,n_models_ok,n_ensembles,n_ensembles_ok,n_test,"
+          "fold_mape_mean,fold_mape_median,fold_mape_thr_mean,fold_mape_thr_median,fold_rho_mean,fold_rho_median,"
+          "test_mape_mean,test_mape_median,test_mape_thr_mean,test_mape_thr_median,test_rho_mean,test_rho_median\n";
+    cs << std::setprecision(17);
+    std::cout << std::left << std::setw(7) << "combo" << std::setw(8) << "kernel" << std::setw(22) << "variant"
+              << std::setw(7) << "model" << std::right << std::setw(16) << "fold MAPE30% md" << std::setw(18)
+              << "fold-mean MAPE%" << std::setw(18) << "fold-mean MAPE30%" << "\n";
+    for (int gi = 0; gi < n_groups; ++gi) {
+      const lann_cv_group& g = cvg[std::size_t(gi)];
+      const auto& mt = meta[std::size_t(g.first_job)];
+      const std::string kname = kernels::to_string(kernels::KernelKind(worlds[std::size_t(mt.combo)].kind));
+      const std::string vname = datagen::combo_variant_id(mt.combo), fname = mt.family == LANN_NNC ? "nnc" : "nn";
+      cs << mt.combo << ',' << kname << ',' << vname << ',' << fname << ',' << g.n_folds << ',' << g.n_models << ','
+         << g.n_models_ok << ',' << g.n_ensembles << ',' << g.n_ensembles_ok << ',' << g.n_test;
+      for (const lann_cv_stat& v : {g.fold_mape, g.fold_mape_thr, g.fold_rho, g.test_mape, g.test_mape_thr, g.test_rho})
+        cs << ',' << v.mean << ',' << v.median;
+      cs << '\n';
+      std::cout << std::left << std::setw(7) << mt.combo << std::setw(8) << kname << std::setw(22) << vname
+                << std::setw(7) << fname << std::right << std::fixed << std::setprecision(2) << std::setw(16)
+                << g.fold_mape_thr.median << std::setw(18) << g.test_mape.mean << std::setw(18)
+                << g.test_mape_thr.mean << "\n";
+      std::cout.unsetf(std::ios::fixed);
+    }
+    outputs.push_back(cvp.string());
+  }
+  record_run(out, a, root, {}, outputs);
   return 0;
 }
 

@@ -75,7 +75,9 @@ EXPORTS = ["lann_engine_create", "lann_engine_destroy", "lann_last_error", "lann
            "lann_group_create", "lann_group_destroy", "lann_group_last_error", "lann_group_size",
            "lann_shard_bounds", "lann_group_shard_bounds", "lann_group_run_population",
            "lann_group_last_device_ms", "lann_group_last_wall_ms",
-           "lann_select_variants_compact", "lann_host_alloc", "lann_host_free"]
+           "lann_select_variants_compact", "lann_host_alloc", "lann_host_free",
+           "lann_cv_layout", "lann_population_cv_count", "lann_population_cv", "lann_cv_summarize",
+           "lann_group_run_cv"]
 
 
 def transfer_bytes(reset=False):

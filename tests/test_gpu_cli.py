@@ -140,6 +140,28 @@ def test_cli_sweep_matches_the_oracle(tmp_path, oracle):
         else:
             assert float(r["mape_thresholded"]) == ref.mape_thr
             assert float(r["rho"]) == ref.rho
+    # cv.csv: the per-combination cross-validation summary == the oracle's restatement
+    jobs = []
+    for combo in (0, 40):
+        w = worlds[combo]
+        ds = derive_seed(1, combo)
+        blur = w.kind == abi.BLUR
+        for s in range(2):
+            for fold in range(5):
+                jobs.append(abi.make_job(w, ds, n_folds=5, fold=fold, hidden=(5, 5) if blur else (8,), lr=1e-2,
+                                         epochs=int((20000 if blur else 8000) * 0.02), log_target=blur,
+                                         init_seed=derive_seed(ds, 1 + s)))
+    runs = [oracle.run_job(j, want_params=True) for j in jobs]
+    og, _ = oracle.cv_summary(jobs, [o for o, _, _ in runs], [p for _, p, _ in runs])
+    with open(tmp_path / "cv.csv") as f:
+        cv_rows = list(csv.DictReader(f))
+    assert [int(r["combo"]) for r in cv_rows] == [0, 40]
+    for r, o in zip(cv_rows, og):
+        blur = int(r["combo"]) == 40
+        assert int(r["n_ensembles_ok"]) == o["n_ensembles_ok"] == 2 and int(r["n_models_ok"]) == 10
+        for k in ("fold_mape", "fold_mape_thr", "fold_rho", "test_mape", "test_mape_thr", "test_rho"):
+            for a, b in ((float(r[k + "_mean"]), o[k][0]), (float(r[k + "_median"]), o[k][1])):
+                assert (a == pytest.approx(b, rel=1e-12)) if blur else a == b, (k, a, b)
 
 
 def test_cli_select_variants(tmp_path):

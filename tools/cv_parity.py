@@ -50,6 +50,7 @@ def main():
     d_test_thr = [a.test_mape_thr.mean - b.test_mape_thr.mean for a, b in zip(r32["groups"], r64["groups"])]
     d_fold_thr = [a.fold_mape_thr.median - b.fold_mape_thr.median for a, b in zip(r32["groups"], r64["groups"])]
     d_fold_mean = [a.fold_mape_thr.mean - b.fold_mape_thr.mean for a, b in zip(r32["groups"], r64["groups"])]
+    d_test_thr_med = [a.test_mape_thr.median - b.test_mape_thr.median for a, b in zip(r32["groups"], r64["groups"])]
     thr64 = np.array([x.mape_thr for x in r64["res"] if x.status == 0])
     thr32 = np.array([x.mape_thr for x in r32["res"] if x.status == 0])
     per_model = np.abs(np.array([a.mape_thr - b.mape_thr for a, b in zip(r32["res"], r64["res"])
@@ -61,6 +62,9 @@ def main():
         "fold_mean_test_mape_thr_per_combo": {"max_abs": float(np.max(np.abs(d_test_thr))),
                                               "median_abs": float(np.median(np.abs(d_test_thr))),
                                               "mean_signed": float(np.mean(d_test_thr))},
+        "fold_mean_test_mape_thr_median_over_seeds_per_combo": {
+            "max_abs": float(np.max(np.abs(d_test_thr_med))), "median_abs": float(np.median(np.abs(d_test_thr_med))),
+            "mean_signed": float(np.mean(d_test_thr_med))},
         "fold_thr_mape_median_per_combo": {"max_abs": float(np.max(np.abs(d_fold_thr))),
                                            "median_abs": float(np.median(np.abs(d_fold_thr)))},
         "fold_thr_mape_mean_per_combo": {"max_abs": float(np.max(np.abs(d_fold_mean))),
@@ -74,9 +78,13 @@ def main():
     }
     out["per_combo"] = [{"combo": i, "fp64_test_mape_mean": b.test_mape.mean, "fp32_test_mape_mean": a.test_mape.mean,
                          "fp64_test_mape_thr_mean": b.test_mape_thr.mean, "fp32_test_mape_thr_mean": a.test_mape_thr.mean,
+                         "fp64_test_mape_thr_median": b.test_mape_thr.median,
+                         "fp32_test_mape_thr_median": a.test_mape_thr.median,
                          "fp64_fold_thr_median": b.fold_mape_thr.median, "fp32_fold_thr_median": a.fold_mape_thr.median}
                         for i, (a, b) in enumerate(zip(r32["groups"], r64["groups"]))]
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+    out["note"] = ("means over seeds of the fold-mean test MAPE are heavy-tailed on the log-target blur "
+                   "combinations (40-47: a diverging seed's exp() extrapolation); medians are the robust statistic")
     with open(os.path.join(ROOT, "gpurun_out", "cv_parity.json"), "w") as f:
         json.dump(out, f, indent=1)
     print(json.dumps({k: v for k, v in out.items() if k != "per_combo"}, indent=1))

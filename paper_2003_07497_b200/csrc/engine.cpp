@@ -371,7 +371,7 @@ std::unique_ptr<TrainPlan> build_plan(lann_engine* e, const DevTrain& t, int pre
       b->gcount = DBuf<int>(gcount, s);
       b->sorted = DBuf<int>(ms, s);
       b->cost = cost;
-      if (std::getenv("LANN_PHASE_PROFILE")) b->prof = DBuf<long long>(4, s);
+      if (std::getenv("LANN_PHASE_PROFILE")) b->prof = DBuf<long long>(8, s);
       if (std::getenv("LANN_PLAN_VERBOSE"))
         std::fprintf(stderr, "fp32 bucket %d-%d-%d: %zu models, lanes %d, %d groups, rows <= %d\n", b->in, b->h1,
                      b->h2, ms.size(), b->lanes, b->n_groups, max_rows);
@@ -438,7 +438,7 @@ std::unique_ptr<TrainPlan> build_plan(lann_engine* e, const DevTrain& t, int pre
       if (!b->in_smem) b->scratch = DBuf<double>(size_t(scratch), s);
       b->soff = DBuf<int64_t>(soff, s);
       b->order = DBuf<int>(order, s);
-      if (std::getenv("LANN_PHASE_PROFILE")) b->prof = DBuf<long long>(4, s);
+      if (std::getenv("LANN_PHASE_PROFILE")) b->prof = DBuf<long long>(8, s);
       P.buckets64.push_back(std::move(b));
     }
     std::stable_sort(P.buckets64.begin(), P.buckets64.end(),
@@ -531,10 +531,11 @@ void execute_plan(lann_engine* e, const TrainPlan& P, double* dparams, double* d
                    b->h1, b->h2, c[0], c[1], c[2], c[3]);
     }
     for (const auto& b : P.buckets64) {
-      long long c[4] = {0, 0, 0, 0};
+      long long c[8] = {0, 0, 0, 0, 0, 0, 0, 0};
       ck(cudaMemcpy(c, b->prof.p, sizeof c, cudaMemcpyDeviceToHost), "profile D2H");
-      std::fprintf(stderr, "fp64 shape %d-%d-%d: cycles phaseA %lld chain %lld adam %lld wait %lld\n",
-                   b->shape[0], b->shape[1], b->shape[2], c[0], c[1], c[2], c[3]);
+      std::fprintf(stderr, "fp64 shape %d-%d-%d: cycles phaseA %lld chain %lld adam %lld wait %lld | producer "
+                   "weights %lld round0 %lld round1 %lld barrier %lld\n", b->shape[0], b->shape[1], b->shape[2],
+                   c[0], c[1], c[2], c[3], c[4], c[5], c[6], c[7]);
     }
   }
   if (n_launch > 1)

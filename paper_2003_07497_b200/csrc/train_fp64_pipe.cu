@@ -87,9 +87,11 @@ struct PipeShape {
 
   // One sample, forward + backward in the reference order; stores its record column:
   // weight terms (inv_n*delta)*a (mlp.cpp:113), bias terms inv_n*delta (mlp.cpp:117), err^2.
-  // w: this epoch's weights (the producer's registers); r: rec + s (row j at r[j * kLd]).
-  __device__ static void sample(const double (&w)[P], const double (&x)[I], double y,
-                                double* __restrict__ r, double inv_n) {
+  // w: this epoch's weights (the producer's registers, or the shared-memory copy read in place);
+  // r: rec + s (row j at r[j * kLd]).
+  template <class Wt>
+  __device__ static void sample(const Wt& w, const double (&x)[I], double y, double* __restrict__ r,
+                                double inv_n) {
     double a1[H1];
 #pragma unroll
     for (int o = 0; o < H1; ++o) {
@@ -179,7 +181,10 @@ __host__ __device__ constexpr int pipe_smem_doubles() {
   return S::ROWS * kLd + ((S::P + 1) & ~1) + 2 + 8;
 }
 
-template <int I, int H1, int H2, int NPW, bool kProf>
+// kWsmem: producers read the epoch's weights from shared memory where they are used (broadcast
+// loads) instead of holding all P in registers, which frees enough registers for more producer
+// warps (every block of an epoch in one round).
+template <int I, int H1, int H2, int NPW, bool kProf, bool kWsmem>
 __global__ void __launch_bounds__(32 * (kChainWarps + NPW), 1) train_fp64_pipe(TrainArgs a) {
   using S = PipeShape<I, H1, H2>;
   constexpr int R = (kMaxBlk + NPW - 1) / NPW;  // blocks per producer warp at most
@@ -341,26 +346,60 @@ __global__ void __launch_bounds__(32 * (kChainWarps + NPW), 1) train_fp64_pipe(T
       for (int i = 0; i < I; ++i) xr[q][i] = s < N ? X[(size_t)s * 8 + i] : 0.0;
       yr[q] = s < N ? Y[s] : 0.0;
     }
+    long long qc[4] = {0, 0, 0, 0};  // profiling: weights, round 0, round 1, epoch barrier
+    long long q0 = kProf ? clk() : 0;
     for (int e = 0; e < E; ++e) {
-      double wv[S::P];  // this epoch's weights: one broadcast read per epoch, not per sample
+      if constexpr (kWsmem) {
+        const double* wsm = ws;
 #pragma unroll
-      for (int j = 0; j < S::P; ++j) wv[j] = ws[j];
+        for (int q = 0; q < R; ++q) {
+          if (q * NPW < nb) {  // a round with at least one block
+            const int s = (w + q * NPW) * kBlk + k;
+            if (s < N) S::sample(wsm, xr[q], yr[q], rec + s, inv_n);
+            mbar_arrive(&bar[q]);  // every producer thread arrives on its round's barrier
+          }
+        }
+      } else {
+        double wv[S::P];  // this epoch's weights: one broadcast read per epoch, not per sample
 #pragma unroll
-      for (int q = 0; q < R; ++q) {
-        if (q * NPW < nb) {  // a round with at least one block
-          const int s = (w + q * NPW) * kBlk + k;
-          if (s < N) S::sample(wv, xr[q], yr[q], rec + s, inv_n);
-          mbar_arrive(&bar[q]);  // every producer thread arrives on its round's barrier
+        for (int j = 0; j < S::P; ++j) wv[j] = ws[j];
+        if (kProf) {
+          double dep = 0.0;  // wait for the weight loads before reading the clock
+#pragma unroll
+          for (int j = 0; j < S::P; ++j) dep += wv[j];
+          const long long t = clk();
+          qc[0] += (dep == 1.2345e300 ? 1 : 0) + t - q0;
+          q0 = t;
+        }
+#pragma unroll
+        for (int q = 0; q < R; ++q) {
+          if (q * NPW < nb) {  // a round with at least one block
+            const int s = (w + q * NPW) * kBlk + k;
+            if (s < N) S::sample(wv, xr[q], yr[q], rec + s, inv_n);
+            mbar_arrive(&bar[q]);  // every producer thread arrives on its round's barrier
+            if (kProf && q < 2) {
+              const long long t = clk();
+              qc[1 + q] += t - q0;
+              q0 = t;
+            }
+          }
         }
       }
       __syncthreads();
+      if (kProf) {
+        const long long t = clk();
+        qc[3] += t - q0;
+        q0 = t;
+      }
       last = Ls[e & 1];
       if (!isfinite(last)) break;
     }
+    if (kProf && tid == 32 * kChainWarps && blockIdx.x == 0)
+      for (int j = 0; j < 4; ++j) a.phase_cycles[4 + j] = qc[j];
   }
 }
 
-template <int I, int H1, int H2, int NPW>
+template <int I, int H1, int H2, int NPW, bool kWsmem = (NPW > 4)>
 void go_pipe(const TrainArgs& a, cudaStream_t s) {
   const int dyn = pipe_smem_doubles<I, H1, H2>() * 8;
   auto launch = [&](auto kern) {
@@ -370,10 +409,11 @@ void go_pipe(const TrainArgs& a, cudaStream_t s) {
   if (a.phase_cycles) {
     TrainArgs b = a;
     if (const char* f = std::getenv("LANN_PROF_FLAGS")) b.prof_flags = std::atoi(f);
-    cudaFuncSetAttribute(train_fp64_pipe<I, H1, H2, NPW, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
-    train_fp64_pipe<I, H1, H2, NPW, true><<<b.n_models, 32 * (kChainWarps + NPW), dyn, s>>>(b);
+    auto kern = train_fp64_pipe<I, H1, H2, NPW, true, kWsmem>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
+    kern<<<b.n_models, 32 * (kChainWarps + NPW), dyn, s>>>(b);
   }
-  else launch(train_fp64_pipe<I, H1, H2, NPW, false>);
+  else launch(train_fp64_pipe<I, H1, H2, NPW, false, kWsmem>);
 }
 
 template <int NPW>

@@ -346,7 +346,9 @@ __global__ void __launch_bounds__(32 * (kChainWarps + NPW), 1) train_fp64_pipe(T
       for (int i = 0; i < I; ++i) xr[q][i] = s < N ? X[(size_t)s * 8 + i] : 0.0;
       yr[q] = s < N ? Y[s] : 0.0;
     }
-    long long qc[4] = {0, 0, 0, 0};  // profiling: weights, round 0, round 1, epoch barrier
+    // profiling: (unused), round 0, round 1 (each from the previous mark: the epoch barrier's wait
+    // lands in the first memory access after it, BAR.SYNC.DEFER_BLOCKING), the barrier itself
+    long long qc[4] = {0, 0, 0, 0};
     long long q0 = kProf ? clk() : 0;
     for (int e = 0; e < E; ++e) {
       if constexpr (kWsmem) {
@@ -363,14 +365,6 @@ __global__ void __launch_bounds__(32 * (kChainWarps + NPW), 1) train_fp64_pipe(T
         double wv[S::P];  // this epoch's weights: one broadcast read per epoch, not per sample
 #pragma unroll
         for (int j = 0; j < S::P; ++j) wv[j] = ws[j];
-        if (kProf) {
-          double dep = 0.0;  // wait for the weight loads before reading the clock
-#pragma unroll
-          for (int j = 0; j < S::P; ++j) dep += wv[j];
-          const long long t = clk();
-          qc[0] += (dep == 1.2345e300 ? 1 : 0) + t - q0;
-          q0 = t;
-        }
 #pragma unroll
         for (int q = 0; q < R; ++q) {
           if (q * NPW < nb) {  // a round with at least one block

@@ -4,7 +4,7 @@
 mkdir -p gpurun_out
 TESTS=${TESTS:-tests}
 timeout 1500 python -m pytest $TESTS -m gpu -q -x 2>&1 | tail -40 > gpurun_out/pytest_gpu.txt
-timeout 300 python bench.py --steps 10 --warmup 3 > gpurun_out/bench.json 2> gpurun_out/bench.err
+timeout 600 python bench.py --steps 10 --warmup 3 > gpurun_out/bench.json 2> gpurun_out/bench.err
 if [ "${REF:-1}" = "1" ]; then
   timeout 300 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
 fi

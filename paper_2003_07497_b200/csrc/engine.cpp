@@ -1126,6 +1126,8 @@ int prepare_population(lann_engine* e, int n_jobs, const lann_job* jobs, int pre
   pop.dK = V((int*)nullptr, oK, Mz);
   pop.dS = V((int*)nullptr, oS, Mz);
   if (cvp) {
+    // the result block is fetched as one copy: zero it once so its alignment padding is defined
+    ck(cudaMemsetAsync(d + cvp->res_off, 0, cvp->res_bytes, s), "memset");
     auto P = [&](auto* type_tag, size_t off) { return reinterpret_cast<decltype(type_tag)>(d + off); };
     FoldMeanArgs& f = cvp->fm;
     f.n_ens = cvD;

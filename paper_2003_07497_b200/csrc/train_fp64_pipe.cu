@@ -71,6 +71,15 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned pari
       : "memory");
 }
 
+// The epoch barrier between the warp-specialised roles (chain warps and producer warps reach it
+// from different code): a named barrier over every thread of the CTA, each warp arriving as a
+// whole (bar.sync id, count: the warp-specialisation form; __syncthreads() is only defined when
+// all threads reach the same call site). Same memory ordering as __syncthreads().
+__device__ __forceinline__ void epoch_barrier() {
+  __syncwarp();  // the warp reconverges first (inline asm does not imply it)
+  asm volatile("barrier.sync 1, %0;" ::"r"(blockDim.x) : "memory");
+}
+
 // Parameter offsets of a compiled shape (H2 == 0: one hidden layer), flat layout of
 // mlp.cpp:124-131. Record row c (c < P) holds parameter c's per-sample term, row P the loss term.
 template <int I, int H1, int H2>
@@ -313,7 +322,7 @@ __global__ void __launch_bounds__(32 * (kChainWarps + NPW), 1) train_fp64_pipe(T
       }
       long long k3 = 0;
       if (kProf) k3 = clk();
-      __syncthreads();
+      epoch_barrier();
       if (kProf) {
         const long long k4 = clk();
         pc[0] += k1 - k0;  // epoch start -> producer block 0 stored
@@ -379,7 +388,7 @@ __global__ void __launch_bounds__(32 * (kChainWarps + NPW), 1) train_fp64_pipe(T
           }
         }
       }
-      __syncthreads();
+      epoch_barrier();
       if (kProf) {
         const long long t = clk();
         qc[3] += t - q0;

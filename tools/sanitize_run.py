@@ -34,4 +34,29 @@ thd = [1 if jobs[i].world.hw_class == abi.HW_CPU else 0 for i in idx]
 for prec in (abi.FP32, abi.FP64_EXACT):
     gi, gs = eng.select_variants(models, thd, abi.MM, 12, 7, 0, 5000, precision=prec)
     print("select", prec, int(gi.max()))
+# round 2: k-fold populations with the cross-validation summary (fold_mean_kernel, cv_stats_kernel),
+# the compact config-4 scorer, the batched predictor's 4-row path, the mlp.hpp batch operations
+cv_jobs = P.config3_jobs(root_seed=3, n_seeds=2, combos=E.default_combos()[::12])
+for j in cv_jobs:
+    j.epochs = 20
+for prec in (abi.FP32, abi.FP64_EXACT):
+    p = E.Population(eng, cv_jobs, prec)
+    p.run(1)
+    groups, ens = p.cv()
+    print("cv", prec, len(groups), sum(g.n_ensembles_ok for g in groups))
+    p.close()
+print("cv summarize", len(eng.cv_summarize(cv_jobs, eng.run_population(cv_jobs, abi.FP64_EXACT)[1],
+                                           [E.abi.CvEnsemble() for _ in range(E.cv_layout(cv_jobs)[1])])))
+ci, cs = np.zeros(5000, dtype=np.uint8), np.zeros(5000, dtype=np.float32)
+eng.select_variants_compact(models, thd, abi.MM, 12, 7, 0, 5000, idx=ci, score=cs)
+print("select compact", int(ci.max()))
+rows = np.random.default_rng(0).random((4096, abi.ROW))
+row_model = np.repeat(np.arange(len(models), dtype=np.int32), 4096 // len(models) + 1)[:4096]
+for prec in (abi.FP32, abi.FP64_EXACT):
+    out = eng.predict(models, rows, row_model, precision=prec)
+    print("predict", prec, float(out[0]))
+dims, w = [7, 8, 1], np.linspace(-0.5, 0.5, 73)
+Xs, ys = rows[:100, :7].copy(), rows[:100, 7].copy()
+fwd, loss, grad = eng.mlp_forward([(dims, w, Xs)]), eng.mse_loss([(dims, w, Xs, ys)]), eng.mse_gradient([(dims, w, Xs, ys)])
+print("mlp ops", np.ravel(fwd)[:1], np.ravel(loss)[:1], len(grad))
 print("done")

@@ -173,3 +173,32 @@ def test_cv_group_equals_single_engine(engine):
         assert [bytes(x) for x in gens] == [bytes(x) for x in ens]
         assert [bytes(x) for x in ggroups] == [bytes(x) for x in groups]
         pop.close()
+
+
+@pytest.mark.gpu
+def test_cv_summary_other_fold_counts_and_shapes(engine, oracle):
+    """Fold counts 2, 3 and 10 side by side in one population (different groups), ragged test
+    parts (count 301: 150 test rows) and an unconstrained 7-64-1 net (the generic predictor path of
+    fold_mean_kernel and the phased FP64 trainer): FP64 summary == the oracle's."""
+    w = P.combo_worlds()[0]
+    jobs = []
+    for k, count in ((2, 301), (3, 120), (10, 400)):
+        ds = P.derive_seed(11, k)
+        for s in range(2):
+            for f in range(k):
+                jobs.append(abi.make_job(w, ds, count=count, n_folds=k, fold=f, hidden=(8,), lr=1e-2, epochs=40,
+                                         init_seed=P.derive_seed(ds, 1 + s)))
+    ds = P.derive_seed(11, 99)
+    for f in range(3):
+        jobs.append(abi.make_job(w, ds, count=200, n_folds=3, fold=f, hidden=(64,), lr=1e-3, epochs=15,
+                                 init_seed=5, unconstrained=True))
+    pop = E.Population(engine, jobs, abi.FP64_EXACT)
+    pop.run(1)
+    st, res, _, _ = pop.fetch()
+    assert st == 0, engine.last_error
+    groups, ens = pop.cv()
+    runs = [oracle.run_job(j, want_params=True) for j in jobs]
+    og, oe = oracle.cv_summary(jobs, [o for o, _, _ in runs], [p for _, p, _ in runs])
+    assert [g.n_folds for g in groups] == [2, 3, 10, 3]
+    assert [g.n_test for g in groups] == [150, 60, 200, 100]
+    check_against_oracle(groups, ens, og, oe, jobs)

@@ -105,6 +105,50 @@ __global__ void chain(double* out, long long* cyc, int busy_warps) {
 #pragma unroll
         for (int u = 0; u < 32; ++u) g = __dadd_rn(g, p[u]);
       }
+    } else if (V == 8) {  // train_fp64_pipe's structure: 16-pair blocks, next block loaded before the links
+      double2 a[16], b[16];
+#pragma unroll
+      for (int u = 0; u < 16; ++u) a[u] = T[u];
+#pragma unroll
+      for (int blk = 0; blk < N / 32; ++blk) {
+        double2(&cur)[16] = (blk & 1) ? b : a;
+        double2(&nxt)[16] = (blk & 1) ? a : b;
+        const int nb = blk + 1 < N / 32 ? blk + 1 : blk;
+#pragma unroll
+        for (int u = 0; u < 16; ++u) nxt[u] = T[nb * 16 + u];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) { g = __dadd_rn(g, cur[u].x); g = __dadd_rn(g, cur[u].y); }
+      }
+    } else if (V == 9 || V == 10) {  // 8-pair units: loads of u + 2, a fixed-latency staging copy of u + 1
+      // (x * one or x + (-0), both exact), the DADD links of u over staged registers only
+      const double one = cyc[63] == 12345 ? 2.0 : 1.0, nz = cyc[63] == 12345 ? 1.0 : -0.0;
+      double2 la[8], lb[8];
+      double sa[16], sb[16];
+      auto stage = [&](double(&s_)[16], const double2(&l)[8]) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          s_[2 * u] = V == 9 ? __dmul_rn(l[u].x, one) : __dadd_rn(l[u].x, nz);
+          s_[2 * u + 1] = V == 9 ? __dmul_rn(l[u].y, one) : __dadd_rn(l[u].y, nz);
+        }
+      };
+#pragma unroll
+      for (int u = 0; u < 8; ++u) { la[u] = T[u]; lb[u] = T[8 + u]; }
+      stage(sa, la);
+      constexpr int NU = N / 16;
+#pragma unroll
+      for (int un = 0; un < NU; ++un) {
+        double2(&l2)[8] = (un & 1) ? lb : la;   // loads of un + 2 reuse the buffer of un
+        double2(&l1)[8] = (un & 1) ? la : lb;   // raw loads of un + 1
+        double(&sc)[16] = (un & 1) ? sb : sa;
+        double(&sn)[16] = (un & 1) ? sa : sb;
+        if (un + 2 < NU) {
+#pragma unroll
+          for (int u = 0; u < 8; ++u) l2[u] = T[(un + 2) * 8 + u];
+        }
+        if (un + 1 < NU) stage(sn, l1);
+#pragma unroll
+        for (int u = 0; u < 16; ++u) g = __dadd_rn(g, sc[u]);
+      }
     } else if (V == 2) {  // pure DADD chain over one row (phased kernel's product rows)
 #pragma unroll 8
       for (int j = 0; j < N / 2; ++j) {
@@ -125,7 +169,7 @@ __global__ void chain(double* out, long long* cyc, int busy_warps) {
 
 int main() {
   double* out; long long* cyc;
-  cudaMalloc(&out, 1024 * 8); cudaMallocManaged(&cyc, 64 * 8);
+  cudaMalloc(&out, 1024 * 8); cudaMallocManaged(&cyc, 64 * 8); cyc[63] = 0;
   const int smem = 40 * LD * 8;
   auto run = [&](auto k, const char* name, int busy) {
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -141,6 +185,9 @@ int main() {
     run(chain<7>, "V7 = V4, unpredicated load + select", busy);
     run(chain<6>, "V6 16-pair block: products then DADDs", busy);
     run(chain<2>, "V2 DADD over product row", busy);
+    run(chain<8>, "V8 pipe kernel's 16-pair blocks", busy);
+    run(chain<9>, "V9 8-pair units, staged by x*one", busy);
+    run(chain<10>, "V10 8-pair units, staged by x+(-0)", busy);
     run(chain<3>, "V3 register DADD chain", busy);
   }
   return 0;

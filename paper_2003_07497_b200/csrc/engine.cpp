@@ -576,7 +576,7 @@ unsigned char* pinned_stage(lann_engine* e, size_t bytes) {
 struct CvLayout {
   std::vector<int> job_group, job_ens;  // -1 for jobs outside k-fold groups
   std::vector<int> group_first, group_folds, group_models, group_ens;
-  std::vector<int> ens_group;
+  std::vector<int> ens_group, ens_first;  // ensemble's group, its first job
   std::vector<uint64_t> ens_seed;
   std::vector<std::vector<int>> ens_member;  // [ensemble][fold]: first job of that fold, -1 if absent
   int n_groups() const { return int(group_first.size()); }
@@ -626,6 +626,7 @@ CvLayout cv_layout(int n, const lann_job* jobs) {
     if (e == ens.end()) {
       e = ens.emplace(std::make_pair(gi, J.init_seed), L.n_ens()).first;
       L.ens_group.push_back(gi);
+      L.ens_first.push_back(j);
       L.ens_seed.push_back(J.init_seed);
       L.ens_member.emplace_back(size_t(J.n_folds), -1);
       ++L.group_ens[size_t(gi)];
@@ -2713,12 +2714,7 @@ int lann_group_run_cv(lann_group* g, int32_t n_jobs, const lann_job* jobs, int32
         sh_ens[size_t(w)].resize(size_t(cv->L.n_ens()));
         const int rc2 = lann_population_cv(p, nullptr, sh_ens[size_t(w)].data());
         if (rc2 != LANN_OK) rc = rc2;
-        for (int en = 0; en < cv->L.n_ens(); ++en) {
-          int first = n;
-          for (int j : cv->L.ens_member[size_t(en)])
-            if (j >= 0) first = std::min(first, j);
-          sh_first[size_t(w)].push_back(lo + first);
-        }
+        for (int en = 0; en < cv->L.n_ens(); ++en) sh_first[size_t(w)].push_back(lo + cv->L.ens_first[size_t(en)]);
       }
       lann_population_destroy(p);
     }

@@ -552,7 +552,7 @@ __global__ void __launch_bounds__(256) cv_stats_kernel(CvStatsArgs a) {
     for (int w = 0; w < (int)(blockDim.x >> 5); ++w) total += warp_sum[w];
     __syncthreads();
     if (threadIdx.x == 0) base += total;
-    if (ok && n_mine < 8) {
+    if (ok && len <= 8 * (int)blockDim.x) {
       my_id[n_mine] = id;
       my_pos[n_mine] = before;
       ++n_mine;

@@ -202,3 +202,34 @@ def test_cv_summary_other_fold_counts_and_shapes(engine, oracle):
     assert [g.n_folds for g in groups] == [2, 3, 10, 3]
     assert [g.n_test for g in groups] == [150, 60, 200, 100]
     check_against_oracle(groups, ens, og, oe, jobs)
+
+
+@pytest.mark.gpu
+def test_cv_summary_large_group_and_bad_folds(engine, oracle):
+    """A group of 2,100 fold models (more than one CTA's register-held compaction: the sequential
+    gather path of cv_stats_kernel) == the oracle; a job whose fold index is out of range
+    (ParamError) forms an ensemble with no valid member, through the single engine and the group."""
+    w = P.combo_worlds()[3]
+    ds = P.derive_seed(5, 3)
+    jobs = [abi.make_job(w, ds, n_folds=5, fold=f, hidden=(8,), lr=1e-2, epochs=3, init_seed=P.derive_seed(ds, 1 + s))
+            for s in range(420) for f in range(5)]
+    pop = E.Population(engine, jobs, abi.FP64_EXACT)
+    pop.run(1)
+    st, res, _, _ = pop.fetch()
+    groups, ens = pop.cv()
+    pop.close()
+    assert st == 0 and len(groups) == 1 and groups[0].n_models_ok == 2100 and groups[0].n_ensembles_ok == 420
+    runs = [oracle.run_job(j, want_params=True) for j in jobs]
+    og, oe = oracle.cv_summary(jobs, [o for o, _, _ in runs], [p for _, p, _ in runs])
+    check_against_oracle(groups, ens, og, oe, jobs)
+    bad = jobs[:10] + [abi.make_job(w, ds, n_folds=5, fold=7, hidden=(8,), lr=1e-2, epochs=3, init_seed=99)]
+    p2 = E.Population(engine, bad, abi.FP64_EXACT)
+    p2.run(1)
+    g1, e1 = p2.cv()
+    p2.close()
+    assert [e.status for e in e1] == [abi.OK, abi.OK, abi.PARAM_ERROR]
+    with E.Group([0, 0]) as g:
+        gst, gres, g2, e2 = g.run_cv(bad)
+    assert gres[-1].status == abi.PARAM_ERROR
+    assert [e.status for e in e2] == [abi.OK, abi.OK, abi.PARAM_ERROR]
+    assert [bytes(x) for x in g2] == [bytes(x) for x in g1]

@@ -164,14 +164,15 @@ def test_cv_group_equals_single_engine(engine):
         assert st == 0
         again = engine.cv_summarize(jobs, res, ens)
         assert [bytes(x) for x in again] == [bytes(x) for x in groups]
-        with E.Group([0, 0]) as g:
-            b = g.shard_bounds(jobs)
-            assert 0 < b[1] < len(jobs)
-            gst, gres, ggroups, gens = g.run_cv(jobs)
-        assert gst == 0, g.last_error
-        assert [bytes(x) for x in gres] == [bytes(x) for x in res]
-        assert [bytes(x) for x in gens] == [bytes(x) for x in ens]
-        assert [bytes(x) for x in ggroups] == [bytes(x) for x in groups]
+        for n_dev in (2, 4):  # identical outputs for any device count
+            with E.Group([0] * n_dev) as g:
+                b = g.shard_bounds(jobs)
+                assert 0 < b[1] < len(jobs)
+                gst, gres, ggroups, gens = g.run_cv(jobs)
+            assert gst == 0, g.last_error
+            assert [bytes(x) for x in gres] == [bytes(x) for x in res]
+            assert [bytes(x) for x in gens] == [bytes(x) for x in ens]
+            assert [bytes(x) for x in ggroups] == [bytes(x) for x in groups]
         pop.close()
 
 

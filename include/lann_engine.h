@@ -367,6 +367,8 @@ int lann_population_norm(const lann_population* pop, double* norm_out);
 /* host->device / device->host bytes moved by this thread's engine calls since the last reset */
 void lann_transfer_bytes(int64_t* h2d, int64_t* d2h, int32_t reset);
 int64_t lann_population_models(const lann_population* pop);
+/* frees the population; destroying its engine frees every population still alive (their handles
+ * are then invalid, and destroying one of them again is a no-op) */
 void lann_population_destroy(lann_population* pop);
 
 /* ---- cross-validation summary of a k-fold sweep (BASELINE config 3) -------------

@@ -50,6 +50,7 @@ struct lann_engine {
   size_t pin_cap = 0;
   float2* brcp = nullptr;        // FP32 Adam bias-correction reciprocal table (grows, kept)
   int brcp_n = 0;
+  std::vector<struct lann_population*> pops;  // live prepared populations (freed before the engine)
 };
 
 namespace lann {
@@ -1262,6 +1263,32 @@ struct lann_population {
   Population pop;
 };
 
+namespace {
+// Live prepared populations: lann_population_destroy on a handle that is no longer live (already
+// destroyed, or freed with its engine) is a no-op instead of a use-after-free.
+std::mutex g_pop_mu;
+std::vector<lann_population*> g_pops;
+void pop_register(lann_population* p) {
+  std::lock_guard<std::mutex> lk(g_pop_mu);
+  g_pops.push_back(p);
+  p->pop.e->pops.push_back(p);
+}
+bool pop_unregister(lann_population* p) {
+  std::lock_guard<std::mutex> lk(g_pop_mu);
+  auto it = std::find(g_pops.begin(), g_pops.end(), p);
+  if (it == g_pops.end()) return false;
+  g_pops.erase(it);
+  auto& v = p->pop.e->pops;
+  v.erase(std::remove(v.begin(), v.end(), p), v.end());
+  return true;
+}
+void pop_free(lann_population* p) {
+  cudaSetDevice(p->pop.e->device);
+  cudaStreamSynchronize(p->pop.e->stream);
+  delete p;  // device buffers are released on the engine's stream, which is still alive
+}
+}  // namespace
+
 extern "C" {
 
 int lann_engine_create(int device, lann_engine** out) {
@@ -1302,6 +1329,12 @@ int lann_engine_create(int device, lann_engine** out) {
 
 void lann_engine_destroy(lann_engine* e) {
   if (!e) return;
+  // populations still alive belong to this engine's stream and memory: free them first
+  while (!e->pops.empty()) {
+    lann_population* p = e->pops.back();
+    if (pop_unregister(p)) pop_free(p);
+    else e->pops.pop_back();
+  }
   cudaSetDevice(e->device);
   if (e->stream) cudaStreamSynchronize(e->stream);
   for (cudaEvent_t ev : {e->ev0, e->ev1, e->tr0, e->tr1, e->fork})
@@ -2200,6 +2233,7 @@ int population_create(lann_engine* e, int32_t n_jobs, const lann_job* jobs, int3
     e->err = f.what;
     return LANN_CUDA_ERROR;
   }
+  pop_register(p);
   *out = p;
   return LANN_OK;
 }
@@ -2349,10 +2383,8 @@ double lann_population_flop(const lann_population* p) { return p ? p->pop.train_
 int64_t lann_population_models(const lann_population* p) { return p ? p->pop.M : 0; }
 
 void lann_population_destroy(lann_population* p) {
-  if (!p) return;
-  cudaSetDevice(p->pop.e->device);
-  cudaStreamSynchronize(p->pop.e->stream);
-  delete p;
+  if (!p || !pop_unregister(p)) return;  // not live: destroyed already, or with its engine
+  pop_free(p);
 }
 
 // One-shot pipeline = create + one device pass + fetch, timed as a whole.

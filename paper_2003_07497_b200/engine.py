@@ -12,6 +12,7 @@ from __future__ import annotations
 
 import ctypes as C
 import os
+import weakref
 
 import numpy as np
 
@@ -237,6 +238,8 @@ class Engine:
 
     def close(self):
         if getattr(self, "h", None):
+            for p in list(getattr(self, "_pops", ())):  # prepared populations go first
+                p.close()
             self.L.lann_engine_destroy(self.h)
             self.h = None
 
@@ -483,11 +486,16 @@ class Population:
         n = len(self.jobs)
         self._arr = (Job * n)(*self.jobs)
         h = C.c_void_p()
+        if not eng.h:
+            raise Error("engine is closed")
         st = eng.L.lann_population_create(eng.h, n, self._arr, precision, int(record_trace), C.byref(h))
         if st and not h.value:
             eng._raise(st)
         self.h = h
         self.record_trace = record_trace
+        if not hasattr(eng, "_pops"):
+            eng._pops = weakref.WeakSet()
+        eng._pops.add(self)
 
     @property
     def flop(self) -> float:
@@ -498,16 +506,22 @@ class Population:
         return self.eng.L.lann_population_models(self.h)
 
     def run(self, n_steps=1):
+        if not self.h:
+            raise Error("population is closed (or its engine was)")
         st = self.eng.L.lann_population_run(self.h, n_steps)
         if st:
             self.eng._raise(st)
 
     def norms(self):
+        if not self.h:
+            raise Error("population is closed (or its engine was)")
         out = np.zeros((len(self.jobs), 18))
         self.eng.L.lann_population_norm(self.h, _ptr(out))
         return out
 
     def fetch(self, want_params=False, want_trace=False):
+        if not self.h:
+            raise Error("population is closed (or its engine was)")
         n = len(self.jobs)
         res = (JobResult * n)()
         params = off = trace = toff = None
@@ -526,6 +540,8 @@ class Population:
 
     def cv(self):
         """The last pass's cross-validation summary (lann_population_cv): (groups, ensembles)."""
+        if not self.h:
+            raise Error("population is closed (or its engine was)")
         ng, ne = C.c_int32(), C.c_int32()
         self.eng.L.lann_population_cv_count(self.h, C.byref(ng), C.byref(ne))
         groups = (CvGroup * max(1, ng.value))()

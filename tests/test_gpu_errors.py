@@ -1,6 +1,8 @@
 """GPU: the error contract of the C ABI mirrors the reference exceptions (errors.hpp):
 ParamError for configs ModelConfig::validate rejects (models.cpp:48-64), SchemaError for
 feature-length mismatches, DomainError for metric domains, TrainingError(epoch)."""
+import ctypes as C
+
 import numpy as np
 import pytest
 
@@ -109,3 +111,29 @@ def test_population_with_large_evaluation_set(engine, oracle):
     assert st == 0, engine.last_error
     ref, _, _ = oracle.run_job(j)
     assert (res[0].mape, res[0].mape_thr, res[0].rho) == (ref.mape, ref.mape_thr, ref.rho)
+
+
+@pytest.mark.gpu
+def test_population_outlives_its_engine():
+    """Closing an engine frees the populations prepared on it (C ABI: lann_engine_destroy frees
+    them; lann_population_destroy on such a handle, or twice, is a no-op) — no use-after-free."""
+    eng = E.Engine(0)
+    pops = [E.Population(eng, [job(epochs=5)], abi.FP64_EXACT) for _ in range(3)]
+    pops[0].run(1)
+    pops[1].close()
+    pops[1].close()
+    eng.close()
+    for p in pops:
+        with pytest.raises(E.Error):
+            p.run(1)
+        p.close()
+    # the C handles directly: the engine frees a population it still owns; destroying that handle
+    # afterwards (twice) is a no-op
+    eng2 = E.Engine(0)
+    arr = (abi.Job * 1)(job(epochs=5))
+    raw = C.c_void_p()
+    assert eng2.L.lann_population_create(eng2.h, 1, arr, abi.FP64_EXACT, 0, C.byref(raw)) == 0
+    assert eng2.L.lann_population_run(raw, 1) == 0
+    eng2.close()
+    eng2.L.lann_population_destroy(raw)
+    eng2.L.lann_population_destroy(raw)

@@ -265,8 +265,18 @@ def time_e2e(E, eng, jobs, precision, steps):
 def critical_path(jobs, train_launch_ms, clock_mhz, precision):
     max_epochs = max(j.epochs for j in jobs)
     us = 1e3 * train_launch_ms / max_epochs
+    cyc = us * clock_mhz
+    extra = {}
+    if precision == "fp64":
+        # the serial floor bit-exactness imposes: each parameter's gradient is an N-long dependent DADD
+        # chain in sample order (mlp.cpp:106-118), at the measured DADD latency (profiles/fp32_peak.json)
+        n = max(int(round(j.count * j.train_fraction)) for j in jobs if j.epochs == max_epochs)
+        lat = (load_json(os.path.join(ROOT, "profiles", "fp32_peak.json")) or {}).get("dadd_latency_cyc", 8.07)
+        extra = {"dadd_chain_floor_cycles": n * lat, "frac_of_chain_floor": n * lat / cyc,
+                 "chain_floor_note": f"{n} dependent DADD links x {lat} cycles (measured latency): the epoch's "
+                                     "irreducible serial part; producers' first round and Adam add to it"}
     return {"models_on_path": sum(1 for j in jobs if j.epochs == max_epochs), "epochs": max_epochs,
-            "us_per_epoch": us, "cycles_per_epoch": us * clock_mhz, "clock_mhz": clock_mhz,
+            "us_per_epoch": us, "cycles_per_epoch": cyc, "clock_mhz": clock_mhz, **extra,
             "sms_busy": f"{len(jobs)} of 148 (one CTA per model)",
             "note": ("per epoch (FP64 exact, train_fp64_pipe): producer warps run the samples' forward/backward "
                      "and store per-parameter terms; one lane per parameter extends its sample-order DADD chain "

@@ -177,7 +177,7 @@ struct Fp32Bucket {
 
 struct Fp64Bucket {
   int shape[3] = {0, 0, 0};  // compiled shape, or {0,0,0} = generic kernel
-  int n = 0, max_p = 0, dyn = 0, in_smem = 0, products = 0;
+  int n = 0, max_p = 0, dyn = 0, in_smem = 0, products = 0, chunk = 0;
   DBuf<int> order;
   DBuf<double> scratch;
   DBuf<int64_t> soff;
@@ -431,6 +431,20 @@ std::unique_ptr<TrainPlan> build_plan(lann_engine* e, const DevTrain& t, int pre
       }
       b->in_smem = max_bytes_smem <= size_t(e->max_smem);
       b->dyn = int(b->in_smem ? max_bytes_smem : max_state);
+      if (!b->in_smem && !std::getenv("LANN_FP64_GLOBAL_RECORDS")) {
+        // records too large for one CTA: keep them in shared memory a chunk of samples at a time
+        // (the largest even chunk that fits beside the model state; every bucket model's rows <= R)
+        int rows = 0;
+        for (int m : order) rows = std::max(rows, fp64_record_rows(t.h1[m], t.h2[m]));
+        const size_t room = size_t(e->max_smem) > max_state ? size_t(e->max_smem) - max_state : 0;
+        int ch = int(std::min<size_t>(room / (size_t(rows) * 8), 4096)) & ~1;
+        while (ch >= 32 && size_t(rows) * size_t(fp64_chunk_ld(ch)) * 8 > room) ch -= 2;
+        if (ch >= 32) {
+          b->in_smem = 1;
+          b->chunk = ch;
+          b->dyn = int(max_state + size_t(rows) * size_t(fp64_chunk_ld(ch)) * 8);
+        }
+      }
       // compiled shapes whose product rows fit too: phase B becomes pure DADD chains
       if (b->shape[0] > 0 && max_bytes_prod <= size_t(e->max_smem) && !std::getenv("LANN_FP64_NOPROD")) {
         b->products = 1;
@@ -516,6 +530,7 @@ void execute_plan(lann_engine* e, const TrainPlan& P, double* dparams, double* d
     a.scratch = b->scratch.p;
     a.scratch_offset = b->soff.p;
     a.smem_records = b->in_smem;
+    a.rec_chunk = b->chunk;
     a.rec_products = b->products;
     a.phase_cycles = b->prof.p;
     launch_train_fp64(a, b->max_p, b->dyn, b->shape[0] > 0 ? b->shape : nullptr, next_stream());

@@ -35,6 +35,8 @@ struct TrainArgs {
   const int64_t* scratch_offset;
   int smem_records;          // 1: per-sample records live in shared memory
   int rec_products;          // 1: phase A also stores every weight's per-sample product row
+  int rec_chunk = 0;         // > 0: shared-memory records hold this many samples at a time (chunks
+                             // of the sample range processed in order; the chains carry over)
   long long* phase_cycles;   // optional (LANN_PHASE_PROFILE): CTA 0's clock64 per phase
   int prof_flags = 0;        // profiling experiments (LANN_PROF_FLAGS), only read under phase_cycles
 };
@@ -138,6 +140,8 @@ bool launch_train_fp64_pipe(const TrainArgs& a, int I, int H1, int H2, int produ
 size_t fp64_record_bytes(int in, int h1, int h2, int n);
 size_t fp64_product_record_bytes(int in, int h1, int h2, int n);
 size_t fp64_state_bytes(int p);
+int fp64_record_rows(int h1, int h2);
+int fp64_chunk_ld(int ch);  // row stride (doubles) of chunked shared-memory records
 bool launch_train_fp32(const TrainF32Args& a, int in, int h1, int h2, int lanes, int tile_bytes,
                        cudaStream_t s);
 bool fp32_shape_supported(int in, int h1, int h2);

@@ -42,6 +42,9 @@ __host__ __device__ constexpr int rec_rows(int H1, int H2) {
   return 8 + 2 * (H1 + (H2 > 0 ? H2 : 0)) + 3;
 }
 __host__ __device__ constexpr int rec_ld(int N) { return (N + 1) & ~1; }  // even: 16-B aligned pairs
+// chunked records: a row stride = 2 (mod 16) doubles, so the 16-B loads of lanes reading different
+// rows at one sample column fall in distinct bank quads (conflict-free phase-B loads)
+__host__ __device__ constexpr int chunk_ld(int ch) { return ((ch + 15) & ~15) + 2; }
 // Product-row kernels (N <= 256) use one compile-time row stride: every phase-A record access
 // is then an immediate offset from the thread's sample column (no address arithmetic), and
 // 258 doubles = 516 words = 4 (mod 32) banks keeps a quarter-warp's 16-B loads of eight
@@ -130,6 +133,22 @@ struct Fixed {
 #pragma unroll
       for (int k = 0; k < 4; ++k)
         if (gi * 4 + k < H1) r[(A1 + gi * 4 + k) * ld] = z[k] > 0.0 ? z[k] : 0.0;
+    }
+    if constexpr (H2 == 0 && H1 > 16 && !kProd) {
+      // wide one-hidden-layer nets (the unconstrained I-64-1): the activations stay in the record
+      // rows just stored instead of a register array, same operation order (no spills)
+      double z = w[BO];
+      for (int i = 0; i < H1; ++i) z = __dadd_rn(z, __dmul_rn(w[WO + i], r[(A1 + i) * ld]));
+      const double err = __dsub_rn(z, y);
+      r[E2 * ld] = __dmul_rn(err, err);
+      const double dout = __dmul_rn(2.0, err);
+      r[TO * ld] = __dmul_rn(inv_n, dout);
+#pragma unroll 8
+      for (int i = 0; i < H1; ++i) {
+        const double acc = __dadd_rn(0.0, __dmul_rn(w[WO + i], dout));
+        r[(T1 + i) * ld] = __dmul_rn(inv_n, r[(A1 + i) * ld] > 0.0 ? acc : 0.0);
+      }
+      return;
     }
     double a1[H1];
 #pragma unroll
@@ -276,11 +295,10 @@ __device__ void sample_generic(const Shape& sh, const double* __restrict__ w, do
 // while the DADD chain of the current one runs.
 template <int U, bool kMul>
 __device__ __forceinline__ double chain_sum_impl(const double* __restrict__ tp,
-                                                 const double* __restrict__ ap, int N) {
+                                                 const double* __restrict__ ap, int N, double g = 0.0) {
   const double2* t2 = reinterpret_cast<const double2*>(tp);
   const double2* a2 = reinterpret_cast<const double2*>(ap);
   const int npairs = N / 2;
-  double g = 0.0;
   double2 ta[U], xa[U], tb[U], xb[U];
   auto load = [&](int j0, double2* t, double2* x) {
 #pragma unroll
@@ -325,7 +343,11 @@ __global__ void __launch_bounds__(256) train_fp64_exact(TrainArgs a) {
   const double lr = a.lr[m];
   const Shape sh = make_shape(a.tile_inputs[tile], a.h1[m], a.h2[m]);
   const int P = sh.P;
-  const int ld = PROD ? kProdLd : rec_ld(N);
+  // SMEM with a.rec_chunk: the records hold CH samples at a time; the sample range is processed
+  // in chunks, in order, and every chain carries its partial sum from one chunk to the next
+  const int CH = (SMEM && a.rec_chunk > 0 && a.rec_chunk < N) ? a.rec_chunk : N;
+  const bool chunked = CH < N;
+  const int ld = PROD ? kProdLd : chunked ? chunk_ld(CH) : rec_ld(CH);
   const int tid = threadIdx.x, nt = blockDim.x;
 
   double* w = smem;           // [P]
@@ -348,11 +370,15 @@ __global__ void __launch_bounds__(256) train_fp64_exact(TrainArgs a) {
   double wr = (KB == 1 && tid < P) ? gp[tid] : 0.0, mr = 0.0, vr = 0.0;
   const double* X = a.X + a.tile_offset[tile] * 8;
   const double* Y = a.y + a.tile_offset[tile];
-  for (int s = tid; s < N; s += nt) {
-    for (int i = 0; i < 7; ++i) rec[i * ld + s] = X[(size_t)s * 8 + i];
-    rec[7 * ld + s] = Y[s];        // inputs use rows 0..I-1 (I <= 7): row 7 holds the target
-    rec[sh.ones * ld + s] = 1.0;   // bias terms are t * 1.0 (exact)
-  }
+  // inputs use rows 0..I-1 (I <= 7), row 7 holds the target, bias terms are t * 1.0 (exact)
+  auto stage_inputs = [&](int c0, int nc) {
+    for (int s = tid; s < nc; s += nt) {
+      for (int i = 0; i < 7; ++i) rec[i * ld + s] = X[(size_t)(c0 + s) * 8 + i];
+      rec[7 * ld + s] = Y[c0 + s];
+      rec[sh.ones * ld + s] = 1.0;
+    }
+  };
+  if (!chunked) stage_inputs(0, N);
 
 
   // phase-B ownership: parameter p -> (record row of its delta, of its input or of 1.0)
@@ -395,34 +421,79 @@ __global__ void __launch_bounds__(256) train_fp64_exact(TrainArgs a) {
   for (int e = 0; e < E; ++e) {
     const long long clk0 = prof ? clock64() : 0;
     const double2 bc = a.bias_corr[e];  // issued early: its latency hides behind phase A
-    // ---- phase A: per-sample forward / backward (mlp.cpp:86-104) ----
-    for (int s = tid; s < N; s += nt) {
-      if constexpr (kFixed) F::template sample<PROD>(w, rec + s, ld, inv_n);
-      else sample_generic(sh, w, rec + s, ld, inv_n);
-    }
-    __syncthreads();
-    const long long clk1 = prof ? clock64() : 0;
-
-    // ---- phase B: sequential per-parameter sums + Adam (mlp.cpp:106-118, 142-154) ----
     double g[KB];
 #pragma unroll
     for (int k = 0; k < KB; ++k) g[k] = 0.0;
-    long long clk2 = 0;
-    if (tix[0] >= 0) {
-      if (PROD) {
-        g[0] = chain_sum_impl<4, false>(rec + tix[0] * ld, nullptr, N);
-        if (prof) clk2 = clock64();
-      } else if (KB == 1) {
-        g[0] = chain_sum_impl<4, true>(rec + tix[0] * ld, rec + aix[0] * ld, N);
-        if (prof) clk2 = clock64();
-      } else {
-        for (int s = 0; s < N; ++s) {
+    double Lacc = 0.0;
+    long long clk1 = 0, clk2 = 0, tA = 0, tB = 0;
+    for (int c0 = 0; c0 < N; c0 += CH) {
+      const int nc = N - c0 < CH ? N - c0 : CH;
+      if (chunked) {
+        if (c0 > 0) __syncthreads();  // the previous chunk's chains are done with the records
+        stage_inputs(c0, nc);
+        __syncthreads();
+      }
+      const long long ca = prof ? clock64() : 0;
+      // ---- phase A: per-sample forward / backward (mlp.cpp:86-104) ----
+      for (int s = tid; s < nc; s += nt) {
+        if constexpr (kFixed) F::template sample<PROD>(w, rec + s, ld, inv_n);
+        else sample_generic(sh, w, rec + s, ld, inv_n);
+      }
+      __syncthreads();
+      if (prof) {
+        clk1 = clock64();
+        tA += clk1 - ca;
+      }
+      // ---- phase B: sequential per-parameter sums, continued over this chunk (mlp.cpp:106-118) ----
+      if (tix[0] >= 0) {
+        if (PROD) {
+          g[0] = chain_sum_impl<4, false>(rec + tix[0] * ld, nullptr, nc, g[0]);
+        } else if (KB == 1) {
+          g[0] = chain_sum_impl<4, true>(rec + tix[0] * ld, rec + aix[0] * ld, nc, g[0]);
+        } else {
+          // the KB chains of a thread advance together (independent DADD chains interleave), two
+          // samples per 16-B load, the next pair's loads in flight while the current pair's links
+          // run; unowned slots read row 0 and are discarded
+          const double2* r2 = reinterpret_cast<const double2*>(rec);
+          int tr[KB], ar[KB];
 #pragma unroll
-          for (int k = 0; k < KB; ++k)
-            if (tix[k] >= 0)
-              g[k] = __dadd_rn(g[k], __dmul_rn(rec[tix[k] * ld + s], rec[aix[k] * ld + s]));
+          for (int k = 0; k < KB; ++k) {
+            tr[k] = (tix[k] >= 0 ? tix[k] : 0) * (ld / 2);
+            ar[k] = (tix[k] >= 0 ? aix[k] : 0) * (ld / 2);
+          }
+          const int npairs = nc / 2;
+          double2 ct[KB], ca[KB];
+#pragma unroll
+          for (int k = 0; k < KB; ++k) ct[k] = r2[tr[k]], ca[k] = r2[ar[k]];
+          for (int j = 0; j < npairs; ++j) {
+            const int jn = j + 1 < npairs ? j + 1 : j;
+            double p0[KB], p1[KB];
+#pragma unroll
+            for (int k = 0; k < KB; ++k) {
+              p0[k] = __dmul_rn(ct[k].x, ca[k].x);
+              p1[k] = __dmul_rn(ct[k].y, ca[k].y);
+              ct[k] = r2[tr[k] + jn];
+              ca[k] = r2[ar[k] + jn];
+            }
+#pragma unroll
+            for (int k = 0; k < KB; ++k)
+              if (tix[k] >= 0) g[k] = __dadd_rn(__dadd_rn(g[k], p0[k]), p1[k]);
+          }
+          if (nc & 1) {
+            const int sl = nc - 1;
+#pragma unroll
+            for (int k = 0; k < KB; ++k)
+              if (tix[k] >= 0) g[k] = __dadd_rn(g[k], __dmul_rn(rec[tix[k] * ld + sl], rec[aix[k] * ld + sl]));
+          }
         }
       }
+      if (tid == loss_tid) Lacc = chain_sum_impl<4, false>(rec + e2row * ld, nullptr, nc, Lacc);
+      if (prof) {
+        clk2 = clock64();
+        tB += clk2 - clk1;
+      }
+    }
+    if (tix[0] >= 0) {
       if (KB == 1) {
         const double mk = __dadd_rn(__dmul_rn(beta1, mr), __dmul_rn(c1, g[0]));
         const double vk = __dadd_rn(__dmul_rn(beta2, vr), __dmul_rn(__dmul_rn(c2, g[0]), g[0]));
@@ -448,8 +519,7 @@ __global__ void __launch_bounds__(256) train_fp64_exact(TrainArgs a) {
       }
     }
     if (tid == loss_tid) {
-      double L = chain_sum_impl<4, false>(rec + e2row * ld, nullptr, N);
-      L = __dmul_rn(L, inv_n);  // mlp.cpp:120
+      const double L = __dmul_rn(Lacc, inv_n);  // mlp.cpp:120
       Ls[0] = L;
       if (trace && (e % a.trace_stride) == 0) trace[e / a.trace_stride] = L;
     }
@@ -457,10 +527,10 @@ __global__ void __launch_bounds__(256) train_fp64_exact(TrainArgs a) {
     __syncthreads();
     if (prof) {
       const long long clk4 = clock64();
-      pc[0] += clk1 - clk0;  // phase A + barrier
-      pc[1] += clk2 - clk1;  // parameter-0 chain
+      pc[0] += tA;           // phase A + barrier (all chunks)
+      pc[1] += tB;           // parameter-0 chains (all chunks)
       pc[2] += clk3 - clk2;  // its Adam step
-      pc[3] += clk4 - clk3;  // waiting for the slowest chain / loss
+      pc[3] += clk4 - clk3 + (clk1 - clk0) - tA - tB;  // waits + chunk staging
     }
     last = Ls[0];
     if (!isfinite(last)) {  // mlp.cpp:166-169: TrainingError(epoch) before the update
@@ -492,10 +562,13 @@ size_t fp64_product_record_bytes(int in, int h1, int h2, int n) {
   return size_t(rec_rows(h1, h2) + nw) * size_t(kProdLd) * 8;
 }
 size_t fp64_state_bytes(int p) { return size_t((3 * p + 2 + 1) & ~1) * 8; }
+int fp64_record_rows(int h1, int h2) { return rec_rows(h1, h2); }
+int fp64_chunk_ld(int ch) { return chunk_ld(ch); }
 
 bool fp64_shape_compiled(int in, int h1, int h2) {
   if (h1 == 8 && h2 == 0) return in >= 1 && in <= 7;
   if (h1 == 5 && h2 == 5) return in >= 4 && in <= 6;
+  if (h1 == 64 && h2 == 0) return in >= 1 && in <= 7;  // the unconstrained prediction nets (x8 widths)
   return false;
 }
 
@@ -557,6 +630,17 @@ void launch_train_fp64(const TrainArgs& a, int max_p, int dyn_bytes, const int* 
         case 5: return go(train_fp64_exact<1, 5, 5, 5, true>);
         case 6: return go(train_fp64_exact<1, 6, 5, 5, true>);
       }
+    }
+  }
+  if (shape && shape[0] > 0 && shape[1] == 64 && shape[2] == 0 && kb <= 3 && a.smem_records) {
+    switch (shape[0]) {  // unconstrained I-64-1 nets: phase A unrolled, activations in registers
+      case 1: return go(train_fp64_exact<3, 1, 64, 0, true>);
+      case 2: return go(train_fp64_exact<3, 2, 64, 0, true>);
+      case 3: return go(train_fp64_exact<3, 3, 64, 0, true>);
+      case 4: return go(train_fp64_exact<3, 4, 64, 0, true>);
+      case 5: return go(train_fp64_exact<3, 5, 64, 0, true>);
+      case 6: return go(train_fp64_exact<3, 6, 64, 0, true>);
+      case 7: return go(train_fp64_exact<3, 7, 64, 0, true>);
     }
   }
   if (a.smem_records) {

@@ -124,9 +124,40 @@ def test_fp64_train_random_shapes(engine, oracle, seed):
         assert final[m] == t_exp[-1]
 
 
+@pytest.mark.parametrize("global_records", [False, True])
+def test_fp64_records_larger_than_shared_memory(engine, oracle, monkeypatch, global_records):
+    """Models whose per-sample records exceed one CTA's shared memory: processed in chunks of
+    samples held in shared memory, the chains carrying over between chunks (default), or in global
+    scratch (LANN_FP64_GLOBAL_RECORDS=1). Compiled wide net (7-64-1, criterion 6's unconstrained
+    shape), generic 1- and 2-hidden-layer shapes (6-40-40-1: eight chains per thread), a LANN
+    shape on N > 256 rows, odd and even N: weights and every epoch's loss == the oracle."""
+    if global_records:
+        monkeypatch.setenv("LANN_FP64_GLOBAL_RECORDS", "1")
+    rng = np.random.default_rng(21)
+    cases = [(7, [64], 2500, 4), (6, [40, 40], 1001, 3), (3, [20], 3001, 3), (7, [8], 1999, 6),
+             (4, [5, 5], 777, 6), (2, [9], 600, 5)]
+    tiles_X, tiles_y, models, expect = [], [], [], []
+    for k, (I, hidden, n, epochs) in enumerate(cases):
+        X, y = random_problem(rng, I, hidden, n)
+        dims = [I] + hidden + [1]
+        p0 = E.init_params(dims, 40 + k)
+        tiles_X.append(X)
+        tiles_y.append(y)
+        models.append({"tile": k, "h1": hidden[0], "h2": hidden[1] if len(hidden) > 1 else 0, "lr": 1e-3,
+                       "epochs": epochs, "params": p0})
+        Xp = np.zeros((n, 8))
+        Xp[:, :I] = X
+        expect.append(oracle.train_full_batch(dims, p0, Xp, y, 1e-3, epochs))
+    params, final, bad, traces = engine.train(tiles_X, tiles_y, models, abi.FP64_EXACT, trace=True)
+    for m, (st, p_exp, t_exp, b_exp) in enumerate(expect):
+        assert st == 0 and bad[m] == -1
+        assert np.array_equal(params[m], p_exp), cases[m]
+        assert np.array_equal(traces[m], t_exp), cases[m]
+
+
 def test_fp64_unconstrained_global_scratch(engine, oracle):
     """Unconstrained width (7->64->1, P=577) on N=2500 rows: per-sample records exceed shared
-    memory and live in global scratch (criterion 9 shape, acceptance_main.cpp:330-348)."""
+    memory (chunked shared-memory records; criterion 6 shape, acceptance_main.cpp:330-348)."""
     rng = np.random.default_rng(9)
     X, y = random_problem(rng, 7, [64], 2500)
     dims = [7, 64, 1]

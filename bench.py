@@ -535,9 +535,12 @@ def extras(E, eng, rank, world, barrier, max_over_ranks, args, flush, peaks):
             s64 = sweep(abi.FP64_EXACT, warm=False)
             me = popmod.model_epochs(s64["jobs"])
             med64 = float(np.median(s64["thr"]))
+            tf64 = s64["flop"] / (s64["tms"] / 1e3) / 1e12
             out["config3_sweep_fp64"] = {
                 "models": len(s64["jobs"]), "model_epochs": me, "n_gpus": world, "scaling": "strong",
                 "value": me / (s64["ms"] / 1e3), "unit": "model-epochs/s", "ms": s64["ms"], "dtype": "f64", "steps": 1,
+                "rank0_train_tflops": tf64, "rank0_frac_of_dfma_peak": tf64 / peaks["dfma_tflops"],
+                "rank0_frac_of_no_fma_peak": tf64 / peaks["dadd_tflops"],
                 "failed_models": s64["failed"], "median_fold_thr_mape": med64,
                 "fp32_gap_pp": abs(med64 - float(np.median(s32["thr"]))) if s32 is not None else None,
                 "parity": "bit-identical to the reference trainer (tests/test_gpu_full_length.py pins the 960-model "

@@ -583,7 +583,12 @@ void launch_train_fp64(const TrainArgs& a, int max_p, int dyn_bytes, const int* 
   // (train_fp64_pipe.cu) unless LANN_FP64_PHASED asks for this phased one
   if (shape && shape[0] > 0 && a.smem_records && a.rec_products && !std::getenv("LANN_FP64_PHASED") &&
       fp64_pipe_shape(shape[0], shape[1], shape[2])) {
-    int npw = 4;
+    // latency regime (fewer models than ~2 per SM: config 2): the product-record kernel, one CTA
+    // per SM; throughput regime (sweeps): factor records, two CTAs (models) per SM
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    int npw = a.n_models >= 2 * sms ? 41 : 4;
     if (const char* env = std::getenv("LANN_FP64_PRODUCERS")) npw = std::atoi(env);
     if (launch_train_fp64_pipe(a, shape[0], shape[1], shape[2], npw, s)) return;
   }

@@ -402,6 +402,325 @@ __global__ void __launch_bounds__(32 * (kChainWarps + NPW), 1) train_fp64_pipe(T
   }
 }
 
+// ---- throughput regime: factor records, two CTAs per SM --------------------------------------
+// For populations far larger than the GPU (config-3 sweeps) the latency kernel above leaves the SM
+// mostly idle: one 7-warp CTA per SM (its ~150 KB of product records and ~230 registers per thread
+// forbid a second), FP64 pipe ~27% and shared-memory pipe ~57% busy (profiles/r02_ncu_fp64_sweep.txt).
+// This variant stores per sample only the ~22 distinct FACTORS of the terms (mlp.cpp:106-118:
+// weight (o, i) adds (inv_n * delta_o) * a_i, a bias adds inv_n * delta_o): tout, the deltas t2[],
+// t1[] (inv_n folded in), the activations a2[], a1[], err^2; the inputs x[] and a row of ones are
+// static. A chain lane reads its two factor rows and forms each term with the same DMUL the
+// producer would have issued, so every term and every chain is bit-identical. Records drop to
+// ~60 KB, the producers read the epoch's weights from shared memory where they use them, and the
+// kernel is bounded to fit two CTAs (two models) per SM: one model's producers overlap the
+// other's chains.
+template <int I, int H1, int H2>
+struct FactorShape {
+  using S = PipeShape<I, H1, H2>;
+  static constexpr int R_TO = 0;              // tout = inv_n * 2 * err
+  static constexpr int R_A2 = 1;              // a2[H2]   (two hidden layers)
+  static constexpr int R_T2 = R_A2 + H2;      // t2[H2] = inv_n * delta2
+  static constexpr int R_A1 = R_T2 + H2;      // a1[H1]
+  static constexpr int R_T1 = R_A1 + H1;      // t1[H1] = inv_n * delta1
+  static constexpr int R_E2 = R_T1 + H1;      // err^2 (loss)
+  static constexpr int DYN = R_E2 + 1;
+  static constexpr int R_X = DYN;             // x[I] (static)
+  static constexpr int R_ONE = R_X + I;       // 1.0 (static)
+  static constexpr int ROWS = R_ONE + 1;
+  // the two factor rows of chain lane c (parameter c < P, the loss c == P, idle lanes beyond)
+  __device__ static void rows_of(int c, int& f1, int& f2) {
+    if (c < S::B1) {
+      f1 = R_T1 + c / I, f2 = R_X + c % I;
+    } else if (c < S::W2) {
+      f1 = R_T1 + (c - S::B1), f2 = R_ONE;
+    } else if (H2 > 0 && c < S::B2) {
+      f1 = R_T2 + (c - S::W2) / H1, f2 = R_A1 + (c - S::W2) % H1;
+    } else if (H2 > 0 && c < S::WO) {
+      f1 = R_T2 + (c - S::B2), f2 = R_ONE;
+    } else if (c < S::BO) {
+      f1 = R_TO, f2 = (H2 > 0 ? R_A2 : R_A1) + (c - S::WO);
+    } else if (c == S::BO) {
+      f1 = R_TO, f2 = R_ONE;
+    } else {
+      f1 = R_E2, f2 = R_ONE;  // the loss, and idle lanes (discarded)
+    }
+  }
+  // one sample, forward + backward in the reference order (as PipeShape::sample), storing factors
+  template <class Wt>
+  __device__ static void sample(const Wt& w, const double (&x)[I], double y, double* __restrict__ r,
+                                double inv_n) {
+    double a1[H1];
+#pragma unroll
+    for (int o = 0; o < H1; ++o) {
+      double z = w[S::B1 + o];
+#pragma unroll
+      for (int i = 0; i < I; ++i) z = __dadd_rn(z, __dmul_rn(w[S::W1 + o * I + i], x[i]));
+      a1[o] = z > 0.0 ? z : 0.0;
+    }
+    double z;
+    double a2[H2 > 0 ? H2 : 1];
+    if constexpr (H2 > 0) {
+#pragma unroll
+      for (int o = 0; o < H2; ++o) {
+        double q = w[S::B2 + o];
+#pragma unroll
+        for (int i = 0; i < H1; ++i) q = __dadd_rn(q, __dmul_rn(w[S::W2 + o * H1 + i], a1[i]));
+        a2[o] = q > 0.0 ? q : 0.0;
+      }
+      z = w[S::BO];
+#pragma unroll
+      for (int i = 0; i < H2; ++i) z = __dadd_rn(z, __dmul_rn(w[S::WO + i], a2[i]));
+    } else {
+      z = w[S::BO];
+#pragma unroll
+      for (int i = 0; i < H1; ++i) z = __dadd_rn(z, __dmul_rn(w[S::WO + i], a1[i]));
+    }
+    const double err = __dsub_rn(z, y);           // mlp.cpp:90
+    const double dout = __dmul_rn(2.0, err);      // mlp.cpp:92
+    r[R_TO * kLd] = __dmul_rn(inv_n, dout);       // left factor of mlp.cpp:113,117
+    r[R_E2 * kLd] = __dmul_rn(err, err);          // mlp.cpp:91
+    if constexpr (H2 > 0) {
+      double d2[H2];
+#pragma unroll
+      for (int i = 0; i < H2; ++i) {  // w*delta (mlp.cpp:97-100), ReLU gate; sums start at the first product
+        const double acc = __dmul_rn(w[S::WO + i], dout);
+        d2[i] = a2[i] > 0.0 ? acc : 0.0;
+        r[(R_A2 + i) * kLd] = a2[i];
+        r[(R_T2 + i) * kLd] = __dmul_rn(inv_n, d2[i]);
+      }
+#pragma unroll
+      for (int i = 0; i < H1; ++i) {
+        double acc = __dmul_rn(w[S::W2 + i], d2[0]);
+#pragma unroll
+        for (int o = 1; o < H2; ++o) acc = __dadd_rn(acc, __dmul_rn(w[S::W2 + o * H1 + i], d2[o]));
+        r[(R_A1 + i) * kLd] = a1[i];
+        r[(R_T1 + i) * kLd] = __dmul_rn(inv_n, a1[i] > 0.0 ? acc : 0.0);
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < H1; ++i) {
+        const double acc = __dmul_rn(w[S::WO + i], dout);
+        r[(R_A1 + i) * kLd] = a1[i];
+        r[(R_T1 + i) * kLd] = __dmul_rn(inv_n, a1[i] > 0.0 ? acc : 0.0);
+      }
+    }
+  }
+};
+
+template <int I, int H1, int H2>
+__host__ __device__ constexpr int factor_smem_doubles() {
+  using S = PipeShape<I, H1, H2>;
+  return FactorShape<I, H1, H2>::ROWS * kLd + ((S::P + 1) & ~1) + 2 + 8;
+}
+
+constexpr int kFactorCtasPerSm = 2;
+
+template <int I, int H1, int H2, int NPW, bool kProf>
+__global__ void __launch_bounds__(32 * (kChainWarps + NPW), kFactorCtasPerSm) train_fp64_factor(TrainArgs a) {
+  using S = PipeShape<I, H1, H2>;
+  using F = FactorShape<I, H1, H2>;
+  constexpr int R = (kMaxBlk + NPW - 1) / NPW;
+  extern __shared__ __align__(16) double smem[];
+  double* rec = smem;                                       // [F::ROWS][kLd]
+  double* ws = rec + F::ROWS * kLd;
+  double* Ls = ws + ((S::P + 1) & ~1);
+  unsigned long long* bar = reinterpret_cast<unsigned long long*>(Ls + 2);
+
+  const int m = a.order[blockIdx.x];
+  const int tile = a.model_tile[m];
+  const int N = a.tile_rows[tile];
+  const int nb = (N + kBlk - 1) / kBlk;
+  const int E = a.epochs[m];
+  const double lr = a.lr[m];
+  const int tid = threadIdx.x;
+  const double inv_n = 1.0 / (double)N;  // mlp.cpp:84
+  const double* gp = a.params + a.param_offset[m];
+  const double* X = a.X + a.tile_offset[tile] * 8;
+  const double* Y = a.y + a.tile_offset[tile];
+
+  for (int p = tid; p < S::P; p += blockDim.x) ws[p] = gp[p];
+  // dynamic rows start at zero (padding columns stay zero terms); static x rows hold the inputs
+  // (zero in padding columns), the ones row 1.0 everywhere
+  for (int s = tid; s < kLd; s += blockDim.x) {
+    for (int j = 0; j < F::DYN; ++j) rec[j * kLd + s] = 0.0;
+    for (int i = 0; i < I; ++i) rec[(F::R_X + i) * kLd + s] = s < N ? X[(size_t)s * 8 + i] : 0.0;
+    rec[F::R_ONE * kLd + s] = 1.0;
+  }
+  if (tid * NPW < nb) mbar_init(&bar[tid], 32 * NPW);
+  __syncthreads();
+
+  double* trace = a.loss_trace ? a.loss_trace + a.trace_offset[m] : nullptr;
+  int bad = -1;
+  double last = 0.0;
+
+  if (tid < 32 * kChainWarps) {
+    const int p = tid < S::P ? tid : tid == S::P ? -1 : -2;
+    int f1, f2;
+    F::rows_of(tid, f1, f2);
+    const double2* T1 = reinterpret_cast<const double2*>(rec + f1 * kLd);
+    const double2* T2 = reinterpret_cast<const double2*>(rec + f2 * kLd);
+    double wr = p >= 0 ? gp[p] : 0.0, mr = 0.0, vr = 0.0;
+    const double beta1 = 0.9, beta2 = 0.999, eps = 1e-8;
+    const double c1 = 1.0 - beta1, c2 = 1.0 - beta2;
+    long long pc[4] = {0, 0, 0, 0};
+    long long k0 = kProf ? clk() : 0;
+    int next_trace = 0;
+    constexpr int UP = 4;          // pairs (8 samples) per load unit
+    constexpr int kUpr = 4 * NPW;  // units per producer round (a block = 4 units)
+    double2 A1[UP], A2[UP], B1[UP], B2[UP];
+    const int nu = 4 * nb;
+    for (int e = 0; e < E; ++e) {
+      const unsigned ph = e & 1;
+      const double2 bc = a.bias_corr[e];
+      const double y1 = rcp_refined(bc.x), y2 = rcp_refined(bc.y);
+      long long k1 = 0, k2 = 0;
+      double g = 0.0;
+      auto load = [&](double2(&d1)[UP], double2(&d2)[UP], int u) {
+#pragma unroll
+        for (int j = 0; j < UP; ++j) {
+          d1[j] = T1[u * UP + j];
+          d2[j] = T2[u * UP + j];
+        }
+      };
+      // 8 links in sample order: each term is the product the producer would have formed
+      auto links = [&](const double2(&d1)[UP], const double2(&d2)[UP]) {
+#pragma unroll
+        for (int j = 0; j < UP; ++j) {
+          const double t0 = __dmul_rn(d1[j].x, d2[j].x), t1 = __dmul_rn(d1[j].y, d2[j].y);
+          g = __dadd_rn(g, t0);
+          g = __dadd_rn(g, t1);
+        }
+      };
+      mbar_wait(bar, ph);  // round 0's factor columns are stored
+      if (kProf) k1 = clk();
+      load(A1, A2, 0);
+#pragma unroll
+      for (int u = 0; u < 4 * kMaxBlk; ++u) {
+        if (u < nu) {
+          double2(&c1r)[UP] = (u & 1) ? B1 : A1;
+          double2(&c2r)[UP] = (u & 1) ? B2 : A2;
+          double2(&n1r)[UP] = (u & 1) ? A1 : B1;
+          double2(&n2r)[UP] = (u & 1) ? A2 : B2;
+          if ((u + 1) % kUpr != 0) {  // next unit in this (complete) round
+            load(n1r, n2r, u + 1 < nu ? u + 1 : u);
+            links(c1r, c2r);
+          } else {
+            links(c1r, c2r);
+            if (u + 1 < nu) {
+              mbar_wait(bar + (u + 1) / kUpr, ph);
+              load(n1r, n2r, u + 1);
+            }
+          }
+        }
+      }
+      if (kProf) k2 = clk();
+      if (p >= 0) {  // AdamState::update (mlp.cpp:142-154), as train_fp64_pipe
+        const double mk = __dadd_rn(__dmul_rn(beta1, mr), __dmul_rn(c1, g));
+        const double vk = __dadd_rn(__dmul_rn(beta2, vr), __dmul_rn(__dmul_rn(c2, g), g));
+        mr = mk;
+        vr = vk;
+        bool ok = true;
+        const double mhat = div_checked(mk, bc.x, y1, ok);
+        const double vhat = div_checked(vk, bc.y, y2, ok);
+        const double den = __dadd_rn(sqrt_checked(vhat, ok), eps);
+        const double num = __dmul_rn(lr, mhat);
+        const double step = div_checked(num, den, rcp_refined(den), ok);
+        if (fabs(mk) >= 0x1p-900) {
+          wr = __dsub_rn(wr, ok ? step : adam_step_ieee(mk, vk, bc, lr, eps));
+        } else if (mk == 0.0) {
+          wr = __dsub_rn(wr, copysign(0.0, mk));
+        } else if (fabs(wr) < 0x1p-820) {
+          wr = __dsub_rn(wr, adam_step_ieee(mk, vk, bc, lr, eps));
+        }
+        ws[p] = wr;
+      } else if (p == -1) {
+        const double L = __dmul_rn(g, inv_n);  // mlp.cpp:120
+        Ls[e & 1] = L;
+        if (trace && e == next_trace) {
+          trace[e / a.trace_stride] = L;
+          next_trace += a.trace_stride;
+        }
+      }
+      long long k3 = 0;
+      if (kProf) k3 = clk();
+      epoch_barrier();
+      if (kProf) {
+        const long long k4 = clk();
+        pc[0] += k1 - k0;
+        pc[1] += k2 - k1;
+        pc[2] += k3 - k2;
+        pc[3] += k4 - k3;
+        k0 = k4;
+      }
+      last = Ls[e & 1];
+      if (!isfinite(last)) {  // mlp.cpp:166-169: TrainingError(epoch)
+        bad = e;
+        break;
+      }
+    }
+    if (p >= 0) a.params[a.param_offset[m] + p] = wr;
+    if (p == -1) {
+      a.final_loss[m] = last;
+      a.nonfinite_epoch[m] = bad;
+    }
+    if (kProf && tid == 0 && blockIdx.x == 0)
+      for (int k = 0; k < 4; ++k) a.phase_cycles[k] = pc[k];
+  } else {
+    const int w = (tid >> 5) - kChainWarps, k = tid & 31;
+    double xr[R][I], yr[R];
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+      const int s = (w + q * NPW) * kBlk + k;
+#pragma unroll
+      for (int i = 0; i < I; ++i) xr[q][i] = s < N ? X[(size_t)s * 8 + i] : 0.0;
+      yr[q] = s < N ? Y[s] : 0.0;
+    }
+    const double* wsm = ws;  // the epoch's weights, read in shared memory where they are used
+    for (int e = 0; e < E; ++e) {
+#pragma unroll
+      for (int q = 0; q < R; ++q) {
+        if (q * NPW < nb) {
+          const int s = (w + q * NPW) * kBlk + k;
+          if (s < N) F::sample(wsm, xr[q], yr[q], rec + s, inv_n);
+          mbar_arrive(&bar[q]);
+        }
+      }
+      epoch_barrier();
+      last = Ls[e & 1];
+      if (!isfinite(last)) break;
+    }
+  }
+}
+
+template <int I, int H1, int H2, int NPW>
+void go_factor(const TrainArgs& a, cudaStream_t s) {
+  const int dyn = factor_smem_doubles<I, H1, H2>() * 8;
+  auto kern = a.phase_cycles ? train_fp64_factor<I, H1, H2, NPW, true> : train_fp64_factor<I, H1, H2, NPW, false>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
+  kern<<<a.n_models, 32 * (kChainWarps + NPW), dyn, s>>>(a);
+}
+
+bool dispatch_factor(const TrainArgs& a, int I, int H1, int H2, cudaStream_t s) {
+  if (H1 == 8 && H2 == 0) {
+    switch (I) {
+      case 1: return go_factor<1, 8, 0, 4>(a, s), true;
+      case 2: return go_factor<2, 8, 0, 4>(a, s), true;
+      case 3: return go_factor<3, 8, 0, 4>(a, s), true;
+      case 4: return go_factor<4, 8, 0, 4>(a, s), true;
+      case 5: return go_factor<5, 8, 0, 4>(a, s), true;
+      case 6: return go_factor<6, 8, 0, 4>(a, s), true;
+      case 7: return go_factor<7, 8, 0, 4>(a, s), true;
+    }
+  } else if (H1 == 5 && H2 == 5) {
+    switch (I) {
+      case 4: return go_factor<4, 5, 5, 4>(a, s), true;
+      case 5: return go_factor<5, 5, 5, 4>(a, s), true;
+      case 6: return go_factor<6, 5, 5, 4>(a, s), true;
+    }
+  }
+  return false;
+}
+
 template <int I, int H1, int H2, int NPW, bool kWsmem = (NPW > 4)>
 void go_pipe(const TrainArgs& a, cudaStream_t s) {
   const int dyn = pipe_smem_doubles<I, H1, H2>() * 8;
@@ -454,6 +773,7 @@ bool launch_train_fp64_pipe(const TrainArgs& a, int I, int H1, int H2, int produ
     case 2: return dispatch_pipe<2>(a, I, H1, H2, s);
     case 3: return dispatch_pipe<3>(a, I, H1, H2, s);
     case 8: return dispatch_pipe<8>(a, I, H1, H2, s);
+    case 41: return dispatch_factor(a, I, H1, H2, s);  // throughput regime: factor records, 2 CTAs/SM
     default: return dispatch_pipe<4>(a, I, H1, H2, s);
   }
 }

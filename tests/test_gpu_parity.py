@@ -363,3 +363,33 @@ def test_batched_predictor_compiled_and_generic_shapes(engine, oracle):
         m = models[rm[r]]
         if not m["log_target"]:
             assert abs(got32[r] - got[r]) <= 1e-5 * (m["norm"][17] - m["norm"][16]) + 1e-12
+
+
+@pytest.mark.parametrize("kernel", ["4", "41"])
+def test_fp64_pipeline_kernels_edge_sizes(engine, oracle, monkeypatch, kernel):
+    """Both FP64 kernels of the LANN shapes — the latency pipeline (product records, 4) and the
+    throughput pipeline (factor records, two CTAs per SM, 41) — on sample counts around the
+    32-sample blocks and producer rounds (2, 7, 31, 32, 33, 100, 129, 255, 256), one- and two-hidden
+    layer shapes: weights and every epoch's loss == the oracle."""
+    monkeypatch.setenv("LANN_FP64_PRODUCERS", kernel)
+    rng = np.random.default_rng(77)
+    tiles_X, tiles_y, models, expect, cases = [], [], [], [], []
+    for k, n in enumerate((2, 7, 31, 32, 33, 100, 129, 255, 256)):
+        for I, hidden in ((7, [8]), (4, [8]), (6, [5, 5])):
+            X, y = random_problem(rng, I, hidden, n)
+            dims = [I] + hidden + [1]
+            p0 = E.init_params(dims, 7 * k + I)
+            t = len(tiles_X)
+            tiles_X.append(X)
+            tiles_y.append(y)
+            models.append({"tile": t, "h1": hidden[0], "h2": hidden[1] if len(hidden) > 1 else 0, "lr": 1e-2,
+                           "epochs": 9, "params": p0})
+            Xp = np.zeros((n, 8))
+            Xp[:, :I] = X
+            expect.append(oracle.train_full_batch(dims, p0, Xp, y, 1e-2, 9))
+            cases.append((I, hidden, n))
+    params, final, bad, traces = engine.train(tiles_X, tiles_y, models, abi.FP64_EXACT, trace=True)
+    for m, (st, p_exp, t_exp, b_exp) in enumerate(expect):
+        assert st == 0 and bad[m] == -1
+        assert np.array_equal(params[m], p_exp), cases[m]
+        assert np.array_equal(traces[m], t_exp), cases[m]

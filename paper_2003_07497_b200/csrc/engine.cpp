@@ -2216,6 +2216,14 @@ namespace {
 int population_create(lann_engine* e, int32_t n_jobs, const lann_job* jobs, int32_t precision,
                       int32_t record_trace, lann_population** out, bool sync_uploads,
                       std::vector<lann_job_result>* base_out = nullptr);
+// a device pass that failed (CUDA error): every job reports the failure (jobs that failed host
+// preparation keep their own status)
+void fail_results(const Population& pop, int rc, lann_job_result* results) {
+  for (int j = 0; j < pop.n_jobs; ++j) {
+    results[j] = pop.base[size_t(j)];
+    if (results[j].status == LANN_OK) results[j].status = rc;
+  }
+}
 }
 
 int lann_population_create(lann_engine* e, int32_t n_jobs, const lann_job* jobs,
@@ -2427,6 +2435,7 @@ int lann_run_population(lann_engine* e, int32_t n_jobs, const lann_job* jobs, in
   }
   int rc = lann_population_run(p, 1);
   if (rc == LANN_OK) rc = lann_population_fetch(p, results, params_out, params_offset, trace_out, trace_offset);
+  else fail_results(p->pop, rc, results);
   lann_population_destroy(p);
   return rc;
 }
@@ -2756,6 +2765,7 @@ int lann_group_run_cv(lann_group* g, int32_t n_jobs, const lann_job* jobs, int32
     } else {
       rc = lann_population_run(p, 1);
       if (rc == LANN_OK) rc = lann_population_fetch(p, pres.data() + lo, nullptr, nullptr, nullptr, nullptr);
+      else fail_results(p->pop, rc, pres.data() + lo);
       const CvState* cv = p->pop.cv.get();
       if (cv && (rc == LANN_OK || rc == LANN_TRAINING_ERROR || rc == LANN_DOMAIN_ERROR)) {
         sh_ens[size_t(w)].resize(size_t(cv->L.n_ens()));

@@ -200,6 +200,9 @@ struct TrainPlan {
   const double* dY = nullptr;
   int trace_stride = 1;
   std::vector<int> model_precision;  // per model: the lann_precision its trainer runs in
+  // FP32 mode, shapes without a compiled FP32 kernel: the generic FP32 CTA kernel
+  DBuf<int> wide_order;
+  int wide_n = 0, wide_chunk = 0, wide_dyn = 0, wide_max_p = 0;
 };
 
 std::unique_ptr<TrainPlan> build_plan(lann_engine* e, const DevTrain& t, int precision,
@@ -220,7 +223,7 @@ std::unique_ptr<TrainPlan> build_plan(lann_engine* e, const DevTrain& t, int pre
   P.dY = dY;
   P.trace_stride = t.trace_stride;
 
-  std::vector<int> fp64_models;
+  std::vector<int> fp64_models, wide_models;
   P.model_precision.assign(size_t(t.n_models), LANN_FP64_EXACT);
   if (precision == LANN_FP32) {
     P.rows_f = DBuf<float>(size_t(total_rows) * 8, s);
@@ -233,8 +236,12 @@ std::unique_ptr<TrainPlan> build_plan(lann_engine* e, const DevTrain& t, int pre
       if (fp32_shape_supported(I, t.h1[m], t.h2[m]) && t.tile_rows[tile] * 32 <= 96 * 1024) {
         by_shape[{I, t.h1[m], t.h2[m]}].push_back(m);
         P.model_precision[size_t(m)] = LANN_FP32;
-      } else
+      } else if (fp32_wide_supported(I, t.h1[m], t.h2[m]) && !std::getenv("LANN_FP32_NO_WIDE")) {
+        wide_models.push_back(m);
+        P.model_precision[size_t(m)] = LANN_FP32;
+      } else {
         fp64_models.push_back(m);
+      }
     }
     int env_lanes = 0;
     if (const char* env = std::getenv("LANN_FP32_LANES")) env_lanes = std::atoi(env);
@@ -242,7 +249,7 @@ std::unique_ptr<TrainPlan> build_plan(lann_engine* e, const DevTrain& t, int pre
         env_lanes != 64 && env_lanes != 128 && env_lanes != 256)
       env_lanes = 0;
     // populations too small to fill the GPU with warps get a whole CTA (4 warps) per model
-    const int total_fp32 = t.n_models - int(fp64_models.size());
+    const int total_fp32 = t.n_models - int(fp64_models.size()) - int(wide_models.size());
     const bool small = total_fp32 <= 4 * e->sms;
     // Large populations: all warp-kernel buckets run concurrently (one stream each), so the GPU
     // stays full whatever a single bucket's wave count is; then the cheapest mapping is 2 lanes
@@ -252,6 +259,7 @@ std::unique_ptr<TrainPlan> build_plan(lann_engine* e, const DevTrain& t, int pre
     int max_epochs_all = 0;
     for (auto& [shape, ms] : by_shape)
       for (int m : ms) max_epochs_all = std::max(max_epochs_all, t.epochs[m]);
+    for (int m : wide_models) max_epochs_all = std::max(max_epochs_all, t.epochs[m]);
     // the CTA kernel reads its bias corrections per epoch instead of computing them; the table
     // is engine-resident (grown on demand), not re-uploaded per population
     if (e->brcp_n < max_epochs_all) {
@@ -381,6 +389,34 @@ std::unique_ptr<TrainPlan> build_plan(lann_engine* e, const DevTrain& t, int pre
     // longest bucket first so it starts first on its stream
     std::stable_sort(P.buckets.begin(), P.buckets.end(),
                      [](const auto& a, const auto& b) { return a->cost > b->cost; });
+    if (!wide_models.empty()) {
+      // one CTA per model, longest first; records a chunk of samples at a time (the largest
+      // multiple of 32 that fits beside the largest model's state)
+      std::stable_sort(wide_models.begin(), wide_models.end(), [&](int a, int b) {
+        return double(t.epochs[a]) * t.tile_rows[t.model_tile[a]] > double(t.epochs[b]) * t.tile_rows[t.model_tile[b]];
+      });
+      int rows = 0, max_n = 1;
+      for (int m : wide_models) {
+        const int tile = t.model_tile[m];
+        rows = std::max(rows, fp32_wide_rows(t.h1[m], t.h2[m]));
+        P.wide_max_p = std::max(P.wide_max_p, param_count(t.tile_inputs[tile], t.h1[m], t.h2[m]));
+        max_n = std::max(max_n, t.tile_rows[tile]);
+      }
+      int ch = int(std::min<int64_t>(((max_n + 31) / 32) * 32, 4096));
+      while (ch > 32 && fp32_wide_smem_bytes(P.wide_max_p, rows, ch) > size_t(e->max_smem)) ch -= 32;
+      if (ch > 256) ch &= ~255;  // whole passes of the 256 phase-A threads
+      if (fp32_wide_smem_bytes(P.wide_max_p, rows, ch) <= size_t(e->max_smem)) {
+        P.wide_chunk = ch;
+        P.wide_dyn = int(fp32_wide_smem_bytes(P.wide_max_p, rows, ch));
+        P.wide_n = int(wide_models.size());
+        P.wide_order = DBuf<int>(wide_models, s);
+      } else {  // no room for a 32-sample chunk: the FP64 exact kernel takes them (and says so)
+        for (int m : wide_models) {
+          P.model_precision[size_t(m)] = LANN_FP64_EXACT;
+          fp64_models.push_back(m);
+        }
+      }
+    }
   } else {
     fp64_models.resize(t.n_models);
     std::iota(fp64_models.begin(), fp64_models.end(), 0);
@@ -467,7 +503,7 @@ std::unique_ptr<TrainPlan> build_plan(lann_engine* e, const DevTrain& t, int pre
 void execute_plan(lann_engine* e, const TrainPlan& P, double* dparams, double* dfinal, int* dbad,
                   double* dtrace, const int64_t* dtrace_off) {
   cudaStream_t s = e->stream;
-  const int n_launch = int(P.buckets.size()) + int(P.buckets64.size());
+  const int n_launch = int(P.buckets.size()) + int(P.buckets64.size()) + (P.wide_n > 0 ? 1 : 0);
   ck(cudaEventRecord(e->tr0, s), "event");
   ck(cudaEventRecord(e->fork, s), "event");
   int k = 0;
@@ -503,6 +539,33 @@ void execute_plan(lann_engine* e, const TrainPlan& P, double* dparams, double* d
     if (!launch_train_fp32(a, b->in, b->h1, b->h2, b->lanes, b->tile_bytes, next_stream()))
       throw CudaFail{"no FP32 kernel for this shape"};
     ck(cudaGetLastError(), "train_fp32 launch");
+    e->launches += 1;
+  }
+  if (P.wide_n > 0) {
+    TrainWideArgs a{};
+    a.n_models = P.wide_n;
+    a.order = P.wide_order.p;
+    a.rows = P.rows_f.p;
+    a.tile_rows = P.tile_rows.p;
+    a.tile_inputs = P.tile_inputs.p;
+    a.tile_offset = P.tile_off.p;
+    a.model_tile = P.model_tile.p;
+    a.h1 = P.h1.p;
+    a.h2 = P.h2.p;
+    a.lr = P.lr.p;
+    a.epochs = P.epochs.p;
+    a.param_offset = P.poff.p;
+    a.params = dparams;
+    a.final_loss = dfinal;
+    a.nonfinite_epoch = dbad;
+    a.loss_trace = dtrace;
+    a.trace_offset = dtrace_off;
+    a.trace_stride = P.trace_stride;
+    a.bias_rcp = P.brcp;
+    a.chunk = P.wide_chunk;
+    a.max_p = P.wide_max_p;
+    launch_train_fp32_wide(a, P.wide_dyn, next_stream());
+    ck(cudaGetLastError(), "train_fp32_wide launch");
     e->launches += 1;
   }
   for (const auto& b : P.buckets64) {

@@ -64,6 +64,37 @@ struct TrainF32Args {
   const float2* bias_rcp;    // [max_epochs] {1/(1-0.9^t), 1/(1-0.999^t)} from the host (CTA kernel)
 };
 
+// FP32 trainer for the shapes without a compiled FP32 kernel (unconstrained widths, any 1-2 hidden
+// layers up to 64 units, I <= 7): one model per CTA, records in shared memory a chunk of samples
+// at a time (train_fp32.cu, train_fp32_wide_kernel).
+struct TrainWideArgs {
+  int n_models;
+  const int* order;          // engine model indices of the launch
+  const float* rows;         // packed FP32 rows [rows][8]: x0..x6, y at column 7
+  const int* tile_rows;
+  const int* tile_inputs;
+  const int64_t* tile_offset;
+  const int* model_tile;
+  const int* h1;
+  const int* h2;
+  const double* lr;
+  const int* epochs;
+  const int64_t* param_offset;
+  double* params;            // in/out (fp64 in the ABI, fp32 inside)
+  double* final_loss;
+  int* nonfinite_epoch;
+  double* loss_trace;
+  const int64_t* trace_offset;
+  int trace_stride;
+  const float2* bias_rcp;    // [max_epochs] {1/(1-0.9^t), 1/(1-0.999^t)}
+  int chunk;                 // samples per shared-memory record chunk
+  int max_p;                 // largest parameter count of the launch
+};
+bool fp32_wide_supported(int in, int h1, int h2);
+int fp32_wide_rows(int h1, int h2);
+size_t fp32_wide_smem_bytes(int max_p, int rows, int chunk);
+void launch_train_fp32_wide(const TrainWideArgs& a, int dyn_bytes, cudaStream_t s);
+
 // Prediction over rows (models.cpp:346-363).
 struct PredictArgs {
   int64_t n_rows;

@@ -1082,6 +1082,212 @@ __global__ void pack_rows_kernel(const double* X, const double* y, int64_t n, fl
   out[i] = c == 7 ? (float)y[r] : (float)X[i];
 }
 
+
+// ---------------------------------------------------------------------------------
+// FP32 for every other shape (unconstrained widths: 7-64-1, 6-40-40-1, ...; any I <= 7 and 1-2
+// hidden layers of <= 64 units): one model per CTA of 256 threads. Weights and Adam moments in
+// shared memory; per epoch the samples go through in chunks whose records (inputs, activations,
+// deltas, one row per quantity, samples contiguous) fit shared memory: phase A threads own
+// samples (forward and backward with FMA, the 2/N scale folded into the output delta), phase B
+// threads own parameters and accumulate their sums over the chunk (carried across chunks); the
+// loss is a block reduction of the per-thread err^2 sums; Adam as the other FP32 kernels
+// (host bias-correction reciprocals).
+constexpr int kWideT = 256;
+constexpr int kWideKB = 20;  // parameters per thread: P <= 5120
+
+__host__ __device__ constexpr int wide_rows(int h1, int h2) { return 8 + 2 * (h1 + h2) + 1; }
+
+__global__ void __launch_bounds__(kWideT) train_fp32_wide_kernel(TrainWideArgs a) {
+  extern __shared__ __align__(16) float wsm[];
+  const int m = a.order[blockIdx.x];
+  const int tile = a.model_tile[m];
+  const int N = a.tile_rows[tile];
+  const int I = a.tile_inputs[tile], H1 = a.h1[m], H2 = a.h2[m];
+  const int E = a.epochs[m];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nl = H2 > 0 ? 3 : 2;
+  int dims[4] = {I, H1, H2 > 0 ? H2 : 1, 1};
+  int woff[3], boff[3], P = 0;
+  for (int l = 0; l < nl; ++l) {
+    woff[l] = P;
+    P += dims[l] * dims[l + 1];
+    boff[l] = P;
+    P += dims[l + 1];
+  }
+  // record rows: x 0..6 | y 7 | a1 | a2 | t1 | t2 | tout (one row per quantity, samples contiguous)
+  const int hid = H1 + (H2 > 0 ? H2 : 0);
+  const int inoff[3] = {0, 8, 8 + H1};
+  const int toff[3] = {8 + hid, 8 + hid + H1, 8 + hid + H1 + (H2 > 0 ? H2 : 0)};
+  const int PP = (a.max_p + 3) & ~3;
+  float* w = wsm;
+  float* mo = w + PP;
+  float* ve = mo + PP;
+  float* red = ve + PP;  // [32] block reduction
+  float* rec = red + 32;
+  const int CH = a.chunk, ld = CH + 4;  // ld = 4 mod 32: a quarter-warp's float4 rows hit distinct banks
+  const float* rows = a.rows + a.tile_offset[tile] * 8;
+  const double* gp = a.params + a.param_offset[m];
+  for (int p = tid; p < P; p += kWideT) {
+    w[p] = (float)gp[p];
+    mo[p] = 0.f;
+    ve[p] = 0.f;
+  }
+  // phase-B ownership: parameter p -> record row of its delta and of its input (-1: a bias)
+  // packed (delta row << 16) | (input row + 1); -1: no parameter
+  int pix[kWideKB];
+#pragma unroll
+  for (int k = 0; k < kWideKB; ++k) {
+    const int p = tid + k * kWideT;
+    pix[k] = -1;
+    for (int l = 0; l < nl && p < P; ++l) {
+      const int in = dims[l], out = dims[l + 1];
+      if (p >= woff[l] && p < boff[l])
+        pix[k] = ((toff[l] + (p - woff[l]) / in) << 16) | (inoff[l] + (p - woff[l]) % in + 1);
+      else if (p >= boff[l] && p < boff[l] + out)
+        pix[k] = (toff[l] + (p - boff[l])) << 16;
+    }
+  }
+  const float lr = (float)a.lr[m];
+  const float scale = 2.0f / (float)N, inv_n = 1.0f / (float)N;
+  double* trace = a.loss_trace ? a.loss_trace + a.trace_offset[m] : nullptr;
+  int bad = -1;
+  float last = 0.f;
+  __syncthreads();
+  for (int e = 0; e < E; ++e) {
+    const float2 br = a.bias_rcp[e];
+    const float step = lr * br.x, rb2 = br.y;
+    float g[kWideKB];
+#pragma unroll
+    for (int k = 0; k < kWideKB; ++k) g[k] = 0.f;
+    float lsum = 0.f;
+    for (int c0 = 0; c0 < N; c0 += CH) {
+      const int nc = N - c0 < CH ? N - c0 : CH;
+      for (int sl = tid; sl < nc; sl += kWideT) {  // this chunk's inputs and targets
+        const float* rw = rows + (size_t)(c0 + sl) * 8;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) rec[i * ld + sl] = rw[i];
+      }
+      __syncthreads();
+      // ---- phase A: forward / backward per sample (mlp.cpp:86-104) ----
+      for (int sl = tid; sl < nc; sl += kWideT) {
+        float* r = rec + sl;
+        for (int l = 0; l < nl; ++l) {
+          const int in = dims[l], out = dims[l + 1];
+          const float* wl = w + woff[l];
+          const float* bl = w + boff[l];
+          const float* ain = r + inoff[l] * ld;
+          if (l + 1 < nl) {
+            float* aout = r + inoff[l + 1] * ld;
+            for (int o = 0; o < out; o += 4) {  // four independent FMA chains in flight
+              float z[4];
+#pragma unroll
+              for (int q = 0; q < 4; ++q) z[q] = o + q < out ? bl[o + q] : 0.f;
+              for (int i = 0; i < in; ++i) {
+                const float ai = ain[i * ld];
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                  if (o + q < out) z[q] = fmaf(wl[(o + q) * in + i], ai, z[q]);
+              }
+#pragma unroll
+              for (int q = 0; q < 4; ++q)
+                if (o + q < out) aout[(o + q) * ld] = fmaxf(z[q], 0.f);
+            }
+          } else {
+            float z = bl[0];
+            for (int i = 0; i < in; ++i) z = fmaf(wl[i], ain[i * ld], z);
+            const float err = z - r[7 * ld];
+            lsum = fmaf(err, err, lsum);
+            r[toff[l] * ld] = err * scale;  // d loss / d out, with the 1/N of the mean
+          }
+        }
+        for (int l = nl - 2; l >= 0; --l) {  // hidden deltas from the next layer's
+          const int nin = dims[l + 1], nout = dims[l + 2];
+          const float* wn = w + woff[l + 1];
+          const float* dn = r + toff[l + 1] * ld;
+          const float* act = r + inoff[l + 1] * ld;
+          float* d = r + toff[l] * ld;
+          for (int i = 0; i < nin; i += 4) {
+            float acc[4] = {0.f, 0.f, 0.f, 0.f};
+            for (int o = 0; o < nout; ++o) {
+              const float dno = dn[o * ld];
+#pragma unroll
+              for (int q = 0; q < 4; ++q)
+                if (i + q < nin) acc[q] = fmaf(wn[o * nin + i + q], dno, acc[q]);
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              if (i + q < nin) d[(i + q) * ld] = act[(i + q) * ld] > 0.f ? acc[q] : 0.f;
+          }
+        }
+      }
+      __syncthreads();
+      // ---- phase B: gradient sums over this chunk, carried across chunks ----
+#pragma unroll
+      for (int k = 0; k < kWideKB; ++k) {
+        if (pix[k] >= 0) {  // float4 record reads, eight partial sums: eight FMA chains in flight
+          const float* tr = rec + (pix[k] >> 16) * ld;
+          const int ai = (pix[k] & 0xffff) - 1;
+          if (ai >= 0) {
+            const float* ar = rec + ai * ld;
+            float4 u = make_float4(g[k], 0.f, 0.f, 0.f), v = make_float4(0.f, 0.f, 0.f, 0.f);
+            int sl = 0;
+            for (; sl + 8 <= nc; sl += 8) {
+              const float4 t0 = *reinterpret_cast<const float4*>(tr + sl);
+              const float4 a0 = *reinterpret_cast<const float4*>(ar + sl);
+              const float4 t1 = *reinterpret_cast<const float4*>(tr + sl + 4);
+              const float4 a1 = *reinterpret_cast<const float4*>(ar + sl + 4);
+              u.x = fmaf(t0.x, a0.x, u.x); u.y = fmaf(t0.y, a0.y, u.y);
+              u.z = fmaf(t0.z, a0.z, u.z); u.w = fmaf(t0.w, a0.w, u.w);
+              v.x = fmaf(t1.x, a1.x, v.x); v.y = fmaf(t1.y, a1.y, v.y);
+              v.z = fmaf(t1.z, a1.z, v.z); v.w = fmaf(t1.w, a1.w, v.w);
+            }
+            for (; sl < nc; ++sl) u.x = fmaf(tr[sl], ar[sl], u.x);
+            g[k] = ((u.x + u.y) + (u.z + u.w)) + ((v.x + v.y) + (v.z + v.w));
+          } else {
+            float4 u = make_float4(g[k], 0.f, 0.f, 0.f), v = make_float4(0.f, 0.f, 0.f, 0.f);
+            int sl = 0;
+            for (; sl + 8 <= nc; sl += 8) {
+              const float4 t0 = *reinterpret_cast<const float4*>(tr + sl);
+              const float4 t1 = *reinterpret_cast<const float4*>(tr + sl + 4);
+              u.x += t0.x; u.y += t0.y; u.z += t0.z; u.w += t0.w;
+              v.x += t1.x; v.y += t1.y; v.z += t1.z; v.w += t1.w;
+            }
+            for (; sl < nc; ++sl) u.x += tr[sl];
+            g[k] = ((u.x + u.y) + (u.z + u.w)) + ((v.x + v.y) + (v.z + v.w));
+          }
+        }
+      }
+      __syncthreads();  // the next chunk overwrites the records
+    }
+    // the pre-update loss (mlp.cpp:165-172): block reduction of the per-thread err^2 sums
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) lsum += __shfl_xor_sync(0xffffffffu, lsum, off);
+    if (lane == 0) red[warp] = lsum;
+    __syncthreads();
+    float L = 0.f;
+#pragma unroll
+    for (int q = 0; q < kWideT / 32; ++q) L += red[q];
+    L *= inv_n;
+    last = L;
+    if (trace && tid == 0 && (e % a.trace_stride) == 0) trace[e / a.trace_stride] = (double)L;
+    if (!isfinite(L)) {
+      bad = e;
+      break;  // uniform: every thread read the same sums
+    }
+#pragma unroll
+    for (int k = 0; k < kWideKB; ++k) {
+      const int p = tid + k * kWideT;
+      if (pix[k] >= 0) w[p] -= adam_step(mo[p], ve[p], g[k], step, rb2);
+    }
+    __syncthreads();
+  }
+  double* outp = a.params + a.param_offset[m];
+  for (int p = tid; p < P; p += kWideT) outp[p] = (double)w[p];
+  if (tid == 0) {
+    a.final_loss[m] = (double)last;
+    a.nonfinite_epoch[m] = bad;
+  }
+}
 }  // namespace
 
 // Resident one-warp CTAs per SM of the warp kernel for (shape, lanes): the wave size the
@@ -1166,6 +1372,20 @@ bool launch_train_fp32(const TrainF32Args& a, int in, int h1, int h2, int lanes,
 void launch_pack_rows(const double* X, const double* y, int64_t n, float* out, cudaStream_t s) {
   if (n <= 0) return;
   pack_rows_kernel<<<(unsigned)((n * 8 + 255) / 256), 256, 0, s>>>(X, y, n, out);
+}
+
+bool fp32_wide_supported(int in, int h1, int h2) {
+  return in >= 1 && in <= 7 && h1 >= 1 && h1 <= 64 && h2 >= 0 && h2 <= 64 &&
+         (in + 1) * h1 + (h2 > 0 ? (h1 + 1) * h2 + h2 + 1 : h1 + 1) <= kWideT * kWideKB;
+}
+int fp32_wide_rows(int h1, int h2) { return wide_rows(h1, h2); }
+size_t fp32_wide_smem_bytes(int max_p, int rows, int chunk) {
+  return (3 * size_t((max_p + 3) & ~3) + 32 + size_t(rows) * size_t(chunk + 4)) * sizeof(float);
+}
+void launch_train_fp32_wide(const TrainWideArgs& a, int dyn_bytes, cudaStream_t s) {
+  if (a.n_models <= 0) return;
+  cudaFuncSetAttribute(train_fp32_wide_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_bytes);
+  train_fp32_wide_kernel<<<a.n_models, kWideT, dyn_bytes, s>>>(a);
 }
 
 }  // namespace lann

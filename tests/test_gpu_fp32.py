@@ -209,16 +209,61 @@ def test_fp32_training_error_and_trace_tail(engine, monkeypatch, lanes, I, hidde
     assert ei.value.epoch == 0
 
 
-def test_fp32_requests_report_the_precision_that_ran(engine):
-    """Shapes with an FP32 kernel (H=8, 5-5) run in FP32; an unconstrained 7-64-1 net has none and
-    runs in the FP64 exact mode, which lann_job_result.precision_run says."""
+def test_fp32_requests_report_the_precision_that_ran(engine, monkeypatch):
+    """Every shape runs in FP32 under an FP32 request: the LANN shapes on their packed kernels, the
+    unconstrained 7-64-1 net on the generic FP32 CTA kernel; lann_job_result.precision_run says
+    which precision ran (with LANN_FP32_NO_WIDE the generic shapes fall back to FP64 exact and
+    report it)."""
     w = abi.acceptance_world()
     jobs = [abi.make_job(w, 1, count=120, epochs=30), abi.make_job(w, 2, count=120, epochs=30, hidden=(64,),
                                                                    unconstrained=True)]
     st, res, _, _ = engine.run_population(jobs, abi.FP32)
     assert st == 0
+    assert [r.precision_run for r in res] == [abi.FP32, abi.FP32]
+    monkeypatch.setenv("LANN_FP32_NO_WIDE", "1")
+    st, res, _, _ = engine.run_population(jobs, abi.FP32)
     assert [r.precision_run for r in res] == [abi.FP32, abi.FP64_EXACT]
+    monkeypatch.delenv("LANN_FP32_NO_WIDE")
     st, res, _, _ = engine.run_population(jobs, abi.FP64_EXACT)
     assert [r.precision_run for r in res] == [abi.FP64_EXACT, abi.FP64_EXACT]
     st, res, _, _ = engine.run_population([abi.make_job(w, 1, count=120, epochs=30, lr=0.5)], abi.FP32)
     assert res[0].precision_run == -1
+
+
+@pytest.mark.parametrize("hidden,n", [((64,), 2500), ((40, 40), 1000), ((20,), 300), ((13, 7), 777)])
+def test_fp32_generic_shapes_track_fp64(engine, hidden, n):
+    """The generic FP32 CTA kernel (shapes without a packed FP32 kernel; records in shared-memory
+    chunks for large N) against the FP64 exact trainer from identical weights: the loss trace's
+    pre-divergence prefix within 1e-4 relative (north_star's per-epoch bar) and the trained
+    weights still close after 40 epochs."""
+    rng = np.random.default_rng(31)
+    I = 6 if len(hidden) == 2 else 7
+    X = rng.uniform(0, 1, (n, I))
+    y = rng.uniform(0, 1, n)
+    dims = [I] + list(hidden) + [1]
+    p0 = E.init_params(dims, 9)
+    model = {"tile": 0, "h1": hidden[0], "h2": hidden[1] if len(hidden) > 1 else 0, "lr": 1e-3, "epochs": 40,
+             "params": p0}
+    p64, f64, b64, t64 = engine.train([X], [y], [model], abi.FP64_EXACT, trace=True)
+    p32, f32, b32, t32 = engine.train([X], [y], [model], abi.FP32, trace=True)
+    assert b32[0] == -1 and b64[0] == -1
+    rel = np.abs(t32[0] - t64[0]) / np.abs(t64[0])
+    assert rel.max() <= 1e-4, rel.max()
+    assert np.max(np.abs(p32[0] - p64[0])) <= 1e-3
+
+
+def test_fp32_unconstrained_criterion6(engine):
+    """Acceptance criterion 6's unconstrained nets (7-64-1, 2500 training rows, 3000 epochs, five
+    seeds) in FP32: every model trains, and the median thresholded MAPE stays within 1 pp of the
+    FP64 exact run's (the reference's)."""
+    w = abi.acceptance_world()
+    jobs = [abi.make_job(w, P.derive_seed(90, s), count=5000, hidden=(64,), lr=1e-2, epochs=3000, init_seed=s,
+                         unconstrained=True) for s in range(1, 6)]
+    st32, r32, _, _ = engine.run_population(jobs, abi.FP32)
+    st64, r64, _, _ = engine.run_population(jobs, abi.FP64_EXACT)
+    assert st32 == 0 and st64 == 0
+    assert all(r.precision_run == abi.FP32 for r in r32)
+    m32 = float(np.median([r.mape_thr for r in r32]))
+    m64 = float(np.median([r.mape_thr for r in r64]))
+    print(f"criterion 6: FP32 median thr-MAPE {m32:.3f}% vs FP64 exact {m64:.3f}%")
+    assert abs(m32 - m64) <= 1.0

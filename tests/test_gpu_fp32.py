@@ -267,3 +267,47 @@ def test_fp32_unconstrained_criterion6(engine):
     m64 = float(np.median([r.mape_thr for r in r64]))
     print(f"criterion 6: FP32 median thr-MAPE {m32:.3f}% vs FP64 exact {m64:.3f}%")
     assert abs(m32 - m64) <= 1.0
+
+
+@pytest.mark.parametrize("I,hidden,n", [(7, (64,), 2501), (6, (40, 40), 300), (7, (13,), 7)])
+def test_fp32_generic_kernel_training_error_and_trace_tail(engine, I, hidden, n):
+    """The generic FP32 CTA kernel (unconstrained shapes): ragged sample counts (a chunk tail that
+    is not a multiple of the float4 step, fewer samples than one chunk), every pre-update loss
+    recorded with the last one as the final loss, and a non-finite target -> TrainingError(epoch 0)
+    (mlp.cpp:166-169); the run is the FP32 kernel's, not an FP64 fallback."""
+    rng = np.random.default_rng(5)
+    X = rng.uniform(0, 1, (n, I))
+    y = rng.uniform(0, 1, n)
+    dims = [I, *hidden, 1]
+    m = {"tile": 0, "h1": hidden[0], "h2": hidden[1] if len(hidden) > 1 else 0, "lr": 1e-2, "epochs": 23,
+         "params": E.init_params(dims, 4)}
+    params, final, bad, traces = engine.train([X], [y], [m], abi.FP32, trace=True)
+    assert bad[0] == -1
+    assert len(traces[0]) == 23 and np.all(np.isfinite(traces[0]))
+    assert final[0] == traces[0][-1]
+    _, _, _, t64 = engine.train([X], [y], [m], abi.FP64_EXACT, trace=True)
+    assert np.max(np.abs(traces[0][:5] - t64[0][:5]) / np.abs(t64[0][:5])) <= 1e-4
+    y_bad = y.copy()
+    y_bad[n // 2] = np.nan
+    with pytest.raises(E.TrainingError) as ei:
+        engine.train([X], [y_bad], [m], abi.FP32)
+    assert ei.value.epoch == 0
+
+
+def test_fp32_generic_kernel_mixed_launch(engine):
+    """Several unconstrained shapes and sample counts in ONE population launch (the chunk is sized
+    for the largest model): each model's trace prefix tracks its own FP64 exact run."""
+    rng = np.random.default_rng(8)
+    shapes = [(7, (64,), 900), (6, (40, 40), 257), (5, (20,), 31), (7, (9, 33), 1200)]
+    Xs, ys, models = [], [], []
+    for t, (I, hidden, n) in enumerate(shapes):
+        Xs.append(rng.uniform(0, 1, (n, I)))
+        ys.append(rng.uniform(0, 1, n))
+        models.append({"tile": t, "h1": hidden[0], "h2": hidden[1] if len(hidden) > 1 else 0, "lr": 1e-3,
+                       "epochs": 20, "params": E.init_params([I, *hidden, 1], 11 + t)})
+    _, _, b32, t32 = engine.train(Xs, ys, models, abi.FP32, trace=True)
+    _, _, b64, t64 = engine.train(Xs, ys, models, abi.FP64_EXACT, trace=True)
+    for k in range(len(shapes)):
+        assert b32[k] == -1 and b64[k] == -1
+        rel = np.abs(t32[k] - t64[k]) / np.abs(t64[k])
+        assert rel.max() <= 1e-4, (k, rel.max())

@@ -19,13 +19,16 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 CLI = os.path.join(ROOT, "paper_2003_07497_b200", "bin", "perfsage")
 
 
-def test_group_of_two_shards_equals_one_engine(engine):
+@pytest.mark.parametrize("n_dev", [2, 4, 8])
+def test_group_of_shards_equals_one_engine(engine, n_dev):
+    """SURVEY 8(e)'s determinism invariant: identical outputs for G = 1, 2, 4, 8 shards."""
     jobs = P.config2_jobs(root_seed=3, epochs_scale=0.05)
     st1, res1, par1, _ = engine.run_population(jobs, abi.FP64_EXACT, want_params=True)
     assert st1 == 0
-    with E.Group([0, 0]) as g:
+    with E.Group([0] * n_dev) as g:
         b = g.shard_bounds(jobs)
-        assert b[0] == 0 < b[1] < b[2] == len(jobs)
+        assert len(b) == n_dev + 1 and b[0] == 0 and b[-1] == len(jobs)
+        assert all(b[k] < b[k + 1] for k in range(n_dev))
         st2, res2, par2 = g.run_population(jobs, abi.FP64_EXACT, want_params=True)
         assert st2 == 0, g.last_error
         assert g.last_device_ms > 0 and g.last_wall_ms > 0

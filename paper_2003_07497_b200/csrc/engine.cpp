@@ -1205,6 +1205,9 @@ int prepare_population(lann_engine* e, int n_jobs, const lann_job* jobs, int pre
   pop.dB = V((int*)nullptr, oB, Mz);
   pop.dK = V((int*)nullptr, oK, Mz);
   pop.dS = V((int*)nullptr, oS, Mz);
+  // the per-model result block is fetched as one copy: zero it once so the alignment padding
+  // between its arrays (M not a multiple of 4) is defined (compute-sanitizer initcheck)
+  if (pop.res_bytes) ck(cudaMemsetAsync(d + pop.res_off, 0, pop.res_bytes, s), "memset");
   if (cvp) {
     // the result block is fetched as one copy: zero it once so its alignment padding is defined
     ck(cudaMemsetAsync(d + cvp->res_off, 0, cvp->res_bytes, s), "memset");

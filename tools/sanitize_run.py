@@ -60,3 +60,15 @@ Xs, ys = rows[:100, :7].copy(), rows[:100, 7].copy()
 fwd, loss, grad = eng.mlp_forward([(dims, w, Xs)]), eng.mse_loss([(dims, w, Xs, ys)]), eng.mse_gradient([(dims, w, Xs, ys)])
 print("mlp ops", np.ravel(fwd)[:1], np.ravel(loss)[:1], len(grad))
 print("done")
+# late round 2: unconstrained shapes (FP64 exact with chunked shared-memory records, the generic
+# FP32 kernel) and the throughput-regime FP64 factor kernel (>= 2 models per SM)
+wide = [abi.make_job(abi.acceptance_world(), P.derive_seed(90, s), count=5000, hidden=h, lr=1e-2, epochs=3,
+                     init_seed=s, unconstrained=True) for s, h in ((1, (64,)), (2, (40, 40)))]
+for prec in (abi.FP32, abi.FP64_EXACT):
+    st, res, _, _ = eng.run_population(wide, prec)
+    print("unconstrained", prec, st, [r.precision_run for r in res])
+big = P.config3_jobs(root_seed=5, n_seeds=8)  # >= 2 models per SM per shape bucket
+for j in big:
+    j.epochs = 3
+print("fp64 sweep (factor kernel)", eng.run_population(big, abi.FP64_EXACT)[0])
+print("done (late round 2)")

@@ -113,8 +113,10 @@ typedef struct lann_job_result {
   double final_loss;       /* loss_trace.back() */
   double mape, mape_thr, rho; /* on the evaluation part */
   int32_t n_kept;
-  int32_t precision_run;   /* lann_precision the trainer actually ran (-1: not trained): LANN_FP32 requests for
-                              shapes without an FP32 kernel (or tiles over 96 KB) run in
+  int32_t precision_run;   /* lann_precision the trainer actually ran (-1: not trained): LANN_FP32 requests
+                              run in FP32 for every shape with hidden layers of <= 64 units and <= 5120
+                              parameters (packed kernels for the LANN shapes, a generic CTA kernel for
+                              the rest); wider nets, and LANN shapes whose tile exceeds 96 KB, run in
                               LANN_FP64_EXACT and say so here */
 } lann_job_result;
 

@@ -79,4 +79,14 @@ __device__ __forceinline__ double sqrt_checked(double v, bool& ok) {
   return s;
 }
 
+// The ReLU and its gate (mlp.cpp:49,102): v where c > 0, else +0.0 (a NaN c gives +0.0, as the
+// reference's comparison does). Two 32-bit selects on one predicate: the plain ternary compiles
+// to a NaN-aware max sequence (~6 instructions) on the layer-to-layer dependency path
+// (train_fp64_pipe's producers: 436 -> 384 instructions per sample, config 2 FP64 53.5 -> 51.2 ms).
+__device__ __forceinline__ double gate(double c, double v) {
+  const bool on = c > 0.0;
+  const int hi = on ? __double2hiint(v) : 0, lo = on ? __double2loint(v) : 0;
+  return __hiloint2double(hi, lo);
+}
+
 }  // namespace lann

@@ -17,6 +17,7 @@
 #include <cmath>
 #include <type_traits>
 
+#include "exact_fp64.cuh"
 #include "kernels.cuh"
 
 namespace lann {
@@ -42,7 +43,7 @@ __device__ __noinline__ double forward_generic(const Row8 xr, const double* nrm,
     for (int o = 0; o < H1; ++o) {
       double z = w[I * H1 + o];
       for (int i = 0; i < I; ++i) z = __dadd_rn(z, __dmul_rn(w[o * I + i], a0[i]));
-      a1[o] = z > 0.0 ? z : 0.0;
+      a1[o] = gate(z, z);
     }
     int off = (I + 1) * H1;
     const double* last_in = a1;
@@ -51,7 +52,7 @@ __device__ __noinline__ double forward_generic(const Row8 xr, const double* nrm,
       for (int o = 0; o < H2; ++o) {
         double z = w[off + H1 * H2 + o];
         for (int i = 0; i < H1; ++i) z = __dadd_rn(z, __dmul_rn(w[off + o * H1 + i], a1[i]));
-        a2[o] = z > 0.0 ? z : 0.0;
+        a2[o] = gate(z, z);
       }
       off += (H1 + 1) * H2;
       last_in = a2;
@@ -114,7 +115,7 @@ __device__ __forceinline__ void forward_shape(const double (&x)[R][8], const dou
     else return fmaf(ww, a, z);
   };
   auto relu = [](T z) -> T {
-    if constexpr (kExact) return z > 0.0 ? z : 0.0;
+    if constexpr (kExact) return gate(z, z);
     else return fmaxf(z, 0.f);
   };
 #pragma unroll

@@ -29,6 +29,7 @@
 #include <cmath>
 #include <cstdlib>
 
+#include "exact_fp64.cuh"
 #include "kernels.cuh"
 
 namespace lann {
@@ -132,7 +133,7 @@ struct Fixed {
           if (gi * 4 + k < H1) z[k] = __dadd_rn(z[k], __dmul_rn(w[W1 + (gi * 4 + k) * I + i], x[i]));
 #pragma unroll
       for (int k = 0; k < 4; ++k)
-        if (gi * 4 + k < H1) r[(A1 + gi * 4 + k) * ld] = z[k] > 0.0 ? z[k] : 0.0;
+        if (gi * 4 + k < H1) r[(A1 + gi * 4 + k) * ld] = gate(z[k], z[k]);
     }
     if constexpr (H2 == 0 && H1 > 16 && !kProd) {
       // wide one-hidden-layer nets (the unconstrained I-64-1): the activations stay in the record
@@ -146,7 +147,7 @@ struct Fixed {
 #pragma unroll 8
       for (int i = 0; i < H1; ++i) {
         const double acc = __dadd_rn(0.0, __dmul_rn(w[WO + i], dout));
-        r[(T1 + i) * ld] = __dmul_rn(inv_n, r[(A1 + i) * ld] > 0.0 ? acc : 0.0);
+        r[(T1 + i) * ld] = __dmul_rn(inv_n, gate(r[(A1 + i) * ld], acc));
       }
       return;
     }
@@ -164,7 +165,7 @@ struct Fixed {
         for (int o = 0; o < H2; ++o) a2[o] = __dadd_rn(a2[o], __dmul_rn(w[W2 + o * H1 + i], a1[i]));
 #pragma unroll
       for (int o = 0; o < H2; ++o) {
-        a2[o] = a2[o] > 0.0 ? a2[o] : 0.0;
+        a2[o] = gate(a2[o], a2[o]);
         if constexpr (!kProd) r[(A2 + o) * ld] = a2[o];  // kProd: only phase A reads a2
       }
       z = w[BO];
@@ -186,7 +187,7 @@ struct Fixed {
 #pragma unroll
       for (int i = 0; i < H2; ++i) {
         const double acc = __dadd_rn(0.0, __dmul_rn(w[WO + i], dout));
-        d2[i] = a2[i] > 0.0 ? acc : 0.0;
+        d2[i] = gate(a2[i], acc);
         t2[i] = __dmul_rn(inv_n, d2[i]);
         r[(T2 + i) * ld] = t2[i];
       }
@@ -199,7 +200,7 @@ struct Fixed {
         for (int i = 0; i < H1; ++i) acc[i] = __dadd_rn(acc[i], __dmul_rn(w[W2 + o * H1 + i], d2[o]));
 #pragma unroll
       for (int i = 0; i < H1; ++i) {
-        t1[i] = __dmul_rn(inv_n, a1[i] > 0.0 ? acc[i] : 0.0);
+        t1[i] = __dmul_rn(inv_n, gate(a1[i], acc[i]));
         r[(T1 + i) * ld] = t1[i];
       }
       if constexpr (kProd) {  // the terms t * a of mlp.cpp:113 (same product, formed once here)
@@ -214,7 +215,7 @@ struct Fixed {
 #pragma unroll
       for (int i = 0; i < H1; ++i) {
         const double acc = __dadd_rn(0.0, __dmul_rn(w[WO + i], dout));
-        t1[i] = __dmul_rn(inv_n, a1[i] > 0.0 ? acc : 0.0);
+        t1[i] = __dmul_rn(inv_n, gate(a1[i], acc));
         r[(T1 + i) * ld] = t1[i];
       }
       if constexpr (kProd) {
@@ -255,7 +256,7 @@ __device__ void sample_generic(const Shape& sh, const double* __restrict__ w, do
         }
 #pragma unroll
         for (int k = 0; k < 4; ++k)
-          if (k < n4) aout[(o + k) * ld] = z[k] > 0.0 ? z[k] : 0.0;
+          if (k < n4) aout[(o + k) * ld] = gate(z[k], z[k]);
       }
     } else {
       double z = bl[0];
@@ -282,7 +283,7 @@ __device__ void sample_generic(const Shape& sh, const double* __restrict__ w, do
       }
 #pragma unroll
       for (int k = 0; k < 4; ++k)
-        if (k < n4) d[(i + k) * ld] = act[(i + k) * ld] > 0.0 ? acc[k] : 0.0;
+        if (k < n4) d[(i + k) * ld] = gate(act[(i + k) * ld], acc[k]);
     }
   }
   // scale in place: t = inv_n * delta (the left factor of mlp.cpp:113,117)

@@ -107,7 +107,7 @@ struct PipeShape {
       double z = w[B1 + o];
 #pragma unroll
       for (int i = 0; i < I; ++i) z = __dadd_rn(z, __dmul_rn(w[W1 + o * I + i], x[i]));
-      a1[o] = z > 0.0 ? z : 0.0;
+      a1[o] = gate(z, z);
     }
     double z;
     double a2[H2 > 0 ? H2 : 1];
@@ -117,7 +117,7 @@ struct PipeShape {
         double q = w[B2 + o];
 #pragma unroll
         for (int i = 0; i < H1; ++i) q = __dadd_rn(q, __dmul_rn(w[W2 + o * H1 + i], a1[i]));
-        a2[o] = q > 0.0 ? q : 0.0;
+        a2[o] = gate(q, q);
       }
       z = w[BO];
 #pragma unroll
@@ -143,7 +143,7 @@ struct PipeShape {
 #pragma unroll
       for (int i = 0; i < H2; ++i) {  // w*delta (mlp.cpp:97-100), ReLU gate
         const double acc = __dmul_rn(w[WO + i], dout);
-        d2[i] = a2[i] > 0.0 ? acc : 0.0;
+        d2[i] = gate(a2[i], acc);
         r[(WO + i) * kLd] = __dmul_rn(tout, a2[i]);
       }
 #pragma unroll
@@ -158,13 +158,13 @@ struct PipeShape {
         double acc = __dmul_rn(w[W2 + i], d2[0]);
 #pragma unroll
         for (int o = 1; o < H2; ++o) acc = __dadd_rn(acc, __dmul_rn(w[W2 + o * H1 + i], d2[o]));
-        t1[i] = __dmul_rn(inv_n, a1[i] > 0.0 ? acc : 0.0);
+        t1[i] = __dmul_rn(inv_n, gate(a1[i], acc));
       }
     } else {
 #pragma unroll
       for (int i = 0; i < H1; ++i) {
         const double acc = __dmul_rn(w[WO + i], dout);
-        t1[i] = __dmul_rn(inv_n, a1[i] > 0.0 ? acc : 0.0);
+        t1[i] = __dmul_rn(inv_n, gate(a1[i], acc));
         r[(WO + i) * kLd] = __dmul_rn(tout, a1[i]);
       }
     }
@@ -455,7 +455,7 @@ struct FactorShape {
       double z = w[S::B1 + o];
 #pragma unroll
       for (int i = 0; i < I; ++i) z = __dadd_rn(z, __dmul_rn(w[S::W1 + o * I + i], x[i]));
-      a1[o] = z > 0.0 ? z : 0.0;
+      a1[o] = gate(z, z);
     }
     double z;
     double a2[H2 > 0 ? H2 : 1];
@@ -465,7 +465,7 @@ struct FactorShape {
         double q = w[S::B2 + o];
 #pragma unroll
         for (int i = 0; i < H1; ++i) q = __dadd_rn(q, __dmul_rn(w[S::W2 + o * H1 + i], a1[i]));
-        a2[o] = q > 0.0 ? q : 0.0;
+        a2[o] = gate(q, q);
       }
       z = w[S::BO];
 #pragma unroll
@@ -484,7 +484,7 @@ struct FactorShape {
 #pragma unroll
       for (int i = 0; i < H2; ++i) {  // w*delta (mlp.cpp:97-100), ReLU gate; sums start at the first product
         const double acc = __dmul_rn(w[S::WO + i], dout);
-        d2[i] = a2[i] > 0.0 ? acc : 0.0;
+        d2[i] = gate(a2[i], acc);
         r[(R_A2 + i) * kLd] = a2[i];
         r[(R_T2 + i) * kLd] = __dmul_rn(inv_n, d2[i]);
       }
@@ -494,14 +494,14 @@ struct FactorShape {
 #pragma unroll
         for (int o = 1; o < H2; ++o) acc = __dadd_rn(acc, __dmul_rn(w[S::W2 + o * H1 + i], d2[o]));
         r[(R_A1 + i) * kLd] = a1[i];
-        r[(R_T1 + i) * kLd] = __dmul_rn(inv_n, a1[i] > 0.0 ? acc : 0.0);
+        r[(R_T1 + i) * kLd] = __dmul_rn(inv_n, gate(a1[i], acc));
       }
     } else {
 #pragma unroll
       for (int i = 0; i < H1; ++i) {
         const double acc = __dmul_rn(w[S::WO + i], dout);
         r[(R_A1 + i) * kLd] = a1[i];
-        r[(R_T1 + i) * kLd] = __dmul_rn(inv_n, a1[i] > 0.0 ? acc : 0.0);
+        r[(R_T1 + i) * kLd] = __dmul_rn(inv_n, gate(a1[i], acc));
       }
     }
   }

@@ -402,6 +402,308 @@ __global__ void __launch_bounds__(32 * (kChainWarps + NPW), 1) train_fp64_pipe(T
   }
 }
 
+// ---- latency regime, pair-row records (LANN_FP64_PRODUCERS=42) ------------------------------
+// The same epoch as train_fp64_pipe, with the record rows stored in PAIRS: slot k of the
+// producer's emission order (PairShape::slot_row) goes to pair k/2, and pair q holds, per sample
+// s, the two slots' terms side by side (pair q at rec + q * kLdP, sample s at + 2 s). A producer
+// lane then stores two terms with one STS.128 (half the store instructions, and half the
+// write-after-read waits of a term DMUL on an earlier store's source register,
+// profiles/r02_fp64pipe_stalls.txt), and a chain lane owns a pair: two independent DADD chains per
+// thread, fed by one LDS.128 per sample. Two chain warps. Bit-identical: every chain still sums
+// its row's terms over samples 0..N-1 in order.
+constexpr int kLdP = 514;  // pair stride (doubles): 2 x 256 samples + 2, so 8 lanes' 16-B loads cover the 32 banks
+constexpr int kPairWarps = 2;
+constexpr int kHalf = 16;  // samples per chain load batch
+
+template <int I, int H1, int H2>
+struct PairShape {
+  using S = PipeShape<I, H1, H2>;
+  static constexpr int SLOTS = (S::ROWS + 1) & ~1;
+  static constexpr int NPAIR = SLOTS / 2;
+  static_assert(NPAIR <= 32 * kPairWarps, "one chain lane per row pair");
+  // record row of emission slot k (the order of PairOut::put calls in sample() below); -2: padding
+  __host__ __device__ static int slot_row(int k) {
+    if (k == 0) return S::P;
+    if (k == 1) return S::BO;
+    k -= 2;
+    if constexpr (H2 > 0) {
+      if (k < H2) return S::WO + k;
+      k -= H2;
+      if (k < H2 * (H1 + 1)) {
+        const int o = k / (H1 + 1), i = k % (H1 + 1);
+        return i < H1 ? S::W2 + o * H1 + i : S::B2 + o;
+      }
+      k -= H2 * (H1 + 1);
+    } else {
+      if (k < H1) return S::WO + k;
+      k -= H1;
+    }
+    if (k < H1 * (I + 1)) {
+      const int o = k / (I + 1), i = k % (I + 1);
+      return i < I ? S::W1 + o * I + i : S::B1 + o;
+    }
+    return -2;
+  }
+  // the producer's store stream: slots in emission order, two per STS.128 (the slot counter is a
+  // compile-time constant after unrolling)
+  struct PairOut {
+    double* base;  // rec + 2 * sample
+    double pend;
+    int slot;
+    __device__ __forceinline__ void put(double v) {
+      if (slot & 1)
+        *reinterpret_cast<double2*>(base + (slot >> 1) * kLdP) = make_double2(pend, v);
+      else
+        pend = v;
+      ++slot;
+    }
+    __device__ __forceinline__ void finish() {
+      if (slot & 1) put(0.0);  // padding slot: a zero term
+    }
+  };
+  // PipeShape::sample with the stores through PairOut (same operations, same order)
+  template <class Wt>
+  __device__ static void sample(const Wt& w, const double (&x)[I], double y, double* __restrict__ base,
+                                double inv_n) {
+    PairOut out{base, 0.0, 0};
+    double a1[H1];
+#pragma unroll
+    for (int o = 0; o < H1; ++o) {
+      double z = w[S::B1 + o];
+#pragma unroll
+      for (int i = 0; i < I; ++i) z = __dadd_rn(z, __dmul_rn(w[S::W1 + o * I + i], x[i]));
+      a1[o] = gate(z, z);
+    }
+    double z;
+    double a2[H2 > 0 ? H2 : 1];
+    if constexpr (H2 > 0) {
+#pragma unroll
+      for (int o = 0; o < H2; ++o) {
+        double q = w[S::B2 + o];
+#pragma unroll
+        for (int i = 0; i < H1; ++i) q = __dadd_rn(q, __dmul_rn(w[S::W2 + o * H1 + i], a1[i]));
+        a2[o] = gate(q, q);
+      }
+      z = w[S::BO];
+#pragma unroll
+      for (int i = 0; i < H2; ++i) z = __dadd_rn(z, __dmul_rn(w[S::WO + i], a2[i]));
+    } else {
+      z = w[S::BO];
+#pragma unroll
+      for (int i = 0; i < H1; ++i) z = __dadd_rn(z, __dmul_rn(w[S::WO + i], a1[i]));
+    }
+    const double err = __dsub_rn(z, y);          // mlp.cpp:90
+    const double dout = __dmul_rn(2.0, err);     // mlp.cpp:92
+    const double tout = __dmul_rn(inv_n, dout);  // left factor of mlp.cpp:113,117
+    out.put(__dmul_rn(err, err));                // slot 0: the loss term (mlp.cpp:91)
+    out.put(tout);                               // slot 1: BO
+    double t1[H1];
+    if constexpr (H2 > 0) {
+      double d2[H2];
+#pragma unroll
+      for (int i = 0; i < H2; ++i) {
+        const double acc = __dmul_rn(w[S::WO + i], dout);
+        d2[i] = gate(a2[i], acc);
+        out.put(__dmul_rn(tout, a2[i]));  // WO + i
+      }
+#pragma unroll
+      for (int o = 0; o < H2; ++o) {
+        const double t2 = __dmul_rn(inv_n, d2[o]);
+#pragma unroll
+        for (int i = 0; i < H1; ++i) out.put(__dmul_rn(t2, a1[i]));  // W2 + o * H1 + i
+        out.put(t2);                                                  // B2 + o
+      }
+#pragma unroll
+      for (int i = 0; i < H1; ++i) {
+        double acc = __dmul_rn(w[S::W2 + i], d2[0]);
+#pragma unroll
+        for (int o = 1; o < H2; ++o) acc = __dadd_rn(acc, __dmul_rn(w[S::W2 + o * H1 + i], d2[o]));
+        t1[i] = __dmul_rn(inv_n, gate(a1[i], acc));
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < H1; ++i) {
+        const double acc = __dmul_rn(w[S::WO + i], dout);
+        t1[i] = __dmul_rn(inv_n, gate(a1[i], acc));
+        out.put(__dmul_rn(tout, a1[i]));  // WO + i
+      }
+    }
+#pragma unroll
+    for (int o = 0; o < H1; ++o) {
+#pragma unroll
+      for (int i = 0; i < I; ++i) out.put(__dmul_rn(t1[o], x[i]));  // W1 + o * I + i
+      out.put(t1[o]);                                                // B1 + o
+    }
+    out.finish();
+  }
+};
+
+template <int I, int H1, int H2>
+__host__ __device__ constexpr int pair_smem_doubles() {
+  using Q = PairShape<I, H1, H2>;
+  using S = PipeShape<I, H1, H2>;
+  // record pairs | weights (even) | loss (2) | mbarriers (<= 8 x u64)
+  return Q::NPAIR * kLdP + ((S::P + 1) & ~1) + 2 + 8;
+}
+
+template <int I, int H1, int H2, int NPW>
+__global__ void __launch_bounds__(32 * (kPairWarps + NPW), 1) train_fp64_pair(TrainArgs a) {
+  using S = PipeShape<I, H1, H2>;
+  using Q = PairShape<I, H1, H2>;
+  constexpr int R = (kMaxBlk + NPW - 1) / NPW;
+  extern __shared__ __align__(16) double smem[];
+  double* rec = smem;                                       // [NPAIR][kLdP]
+  double* ws = rec + Q::NPAIR * kLdP;                       // [P] weights
+  double* Ls = ws + ((S::P + 1) & ~1);                      // [2] epoch loss
+  unsigned long long* bar = reinterpret_cast<unsigned long long*>(Ls + 2);
+
+  const int m = a.order[blockIdx.x];
+  const int tile = a.model_tile[m];
+  const int N = a.tile_rows[tile];
+  const int nb = (N + kBlk - 1) / kBlk;
+  const int nh = 2 * nb;  // chain load batches of kHalf samples
+  const int E = a.epochs[m];
+  const double lr = a.lr[m];
+  const int tid = threadIdx.x;
+  const double inv_n = 1.0 / (double)N;  // mlp.cpp:84
+  const double* gp = a.params + a.param_offset[m];
+  const double* X = a.X + a.tile_offset[tile] * 8;
+  const double* Y = a.y + a.tile_offset[tile];
+
+  for (int p = tid; p < S::P; p += blockDim.x) ws[p] = gp[p];
+  // padding columns (samples N.. up to the block end) hold zero terms (see train_fp64_pipe)
+  for (int q = tid; q < Q::NPAIR * kLdP; q += blockDim.x) rec[q] = 0.0;
+  if (tid * NPW < nb) mbar_init(&bar[tid], 32 * NPW);
+  __syncthreads();
+
+  double* trace = a.loss_trace ? a.loss_trace + a.trace_offset[m] : nullptr;
+  int bad = -1;
+  double last = 0.0;
+
+  if (tid < 32 * kPairWarps) {
+    // ---- chain lanes: lane c sums the two rows of pair c over the samples in order, then Adam ----
+    const int c = tid < Q::NPAIR ? tid : 0;  // idle lanes shadow lane 0 (broadcast loads)
+    const int r0 = tid < Q::NPAIR ? Q::slot_row(2 * c) : -2, r1 = tid < Q::NPAIR ? Q::slot_row(2 * c + 1) : -2;
+    const int p0 = r0 >= 0 && r0 < S::P ? r0 : r0 == S::P ? -1 : -2;  // parameter, -1 the loss, -2 none
+    const int p1 = r1 >= 0 && r1 < S::P ? r1 : r1 == S::P ? -1 : -2;
+    const double2* Tr = reinterpret_cast<const double2*>(rec + c * kLdP);
+    double w0 = p0 >= 0 ? gp[p0] : 0.0, m0 = 0.0, v0 = 0.0;
+    double w1 = p1 >= 0 ? gp[p1] : 0.0, m1 = 0.0, v1 = 0.0;
+    const double beta1 = 0.9, beta2 = 0.999, eps = 1e-8;
+    const double c1 = 1.0 - beta1, c2 = 1.0 - beta2;
+    int next_trace = 0;
+    double2 A[kHalf], B[kHalf];
+    for (int e = 0; e < E; ++e) {
+      const unsigned ph = e & 1;
+      const double2 bc = a.bias_corr[e];
+      const double y1 = rcp_refined(bc.x), y2 = rcp_refined(bc.y);
+      double g0 = 0.0, g1 = 0.0;
+      auto load = [&](double2(&dst)[kHalf], int h) {
+#pragma unroll
+        for (int j = 0; j < kHalf; ++j) dst[j] = Tr[h * kHalf + j];
+      };
+      auto links = [&](const double2(&cur)[kHalf]) {  // 16 samples, two chains (mlp.cpp:106-118)
+#pragma unroll
+        for (int j = 0; j < kHalf; ++j) {
+          g0 = __dadd_rn(g0, cur[j].x);
+          g1 = __dadd_rn(g1, cur[j].y);
+        }
+      };
+      mbar_wait(bar, ph);  // round 0's columns are stored
+      load(A, 0);
+#pragma unroll
+      for (int h = 0; h < 2 * kMaxBlk; ++h) {
+        if (h < nh) {
+          double2(&cur)[kHalf] = (h & 1) ? B : A;
+          double2(&nxt)[kHalf] = (h & 1) ? A : B;
+          const int b = h >> 1;
+          if (!((h & 1) && (b + 1) % NPW == 0)) {  // the next batch is in this (complete) round
+            load(nxt, h + 1 < nh ? h + 1 : h);
+            links(cur);
+          } else {
+            links(cur);
+            if (h + 1 < nh) {
+              mbar_wait(bar + (b + 1) / NPW, ph);
+              load(nxt, h + 1);
+            }
+          }
+        }
+      }
+      // AdamState::update (mlp.cpp:142-154) for both parameters of the pair, as train_fp64_pipe
+      auto adam = [&](double g, double& wr, double& mr, double& vr) {
+        const double mk = __dadd_rn(__dmul_rn(beta1, mr), __dmul_rn(c1, g));
+        const double vk = __dadd_rn(__dmul_rn(beta2, vr), __dmul_rn(__dmul_rn(c2, g), g));
+        mr = mk;
+        vr = vk;
+        bool ok = true;
+        const double mhat = div_checked(mk, bc.x, y1, ok);
+        const double vhat = div_checked(vk, bc.y, y2, ok);
+        const double den = __dadd_rn(sqrt_checked(vhat, ok), eps);
+        const double num = __dmul_rn(lr, mhat);
+        const double step = div_checked(num, den, rcp_refined(den), ok);
+        if (fabs(mk) >= 0x1p-900) {
+          wr = __dsub_rn(wr, ok ? step : adam_step_ieee(mk, vk, bc, lr, eps));
+        } else if (mk == 0.0) {
+          wr = __dsub_rn(wr, copysign(0.0, mk));
+        } else if (fabs(wr) < 0x1p-820) {
+          wr = __dsub_rn(wr, adam_step_ieee(mk, vk, bc, lr, eps));
+        }
+      };
+      if (p0 >= 0) adam(g0, w0, m0, v0);
+      if (p1 >= 0) adam(g1, w1, m1, v1);
+      if (p0 >= 0) ws[p0] = w0;
+      if (p1 >= 0) ws[p1] = w1;
+      if (p0 == -1 || p1 == -1) {
+        const double L = __dmul_rn(p0 == -1 ? g0 : g1, inv_n);  // mlp.cpp:120
+        Ls[e & 1] = L;
+        if (trace && e == next_trace) {
+          trace[e / a.trace_stride] = L;
+          next_trace += a.trace_stride;
+        }
+      }
+      epoch_barrier();
+      last = Ls[e & 1];
+      if (!isfinite(last)) {  // mlp.cpp:166-169: TrainingError(epoch)
+        bad = e;
+        break;
+      }
+    }
+    if (p0 >= 0) a.params[a.param_offset[m] + p0] = w0;
+    if (p1 >= 0) a.params[a.param_offset[m] + p1] = w1;
+    if (p0 == -1 || p1 == -1) {
+      a.final_loss[m] = last;
+      a.nonfinite_epoch[m] = bad;
+    }
+  } else {
+    // ---- producer warps: blocks w, w + NPW, ... ; inputs kept in registers ----
+    const int w = (tid >> 5) - kPairWarps, k = tid & 31;
+    double xr[R][I], yr[R];
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+      const int s = (w + q * NPW) * kBlk + k;
+#pragma unroll
+      for (int i = 0; i < I; ++i) xr[q][i] = s < N ? X[(size_t)s * 8 + i] : 0.0;
+      yr[q] = s < N ? Y[s] : 0.0;
+    }
+    for (int e = 0; e < E; ++e) {
+      double wv[S::P];
+#pragma unroll
+      for (int j = 0; j < S::P; ++j) wv[j] = ws[j];
+#pragma unroll
+      for (int q = 0; q < R; ++q) {
+        if (q * NPW < nb) {
+          const int s = (w + q * NPW) * kBlk + k;
+          if (s < N) Q::sample(wv, xr[q], yr[q], rec + 2 * s, inv_n);
+          mbar_arrive(&bar[q]);
+        }
+      }
+      epoch_barrier();
+      last = Ls[e & 1];
+      if (!isfinite(last)) break;
+    }
+  }
+}
+
 // ---- throughput regime: factor records, two CTAs per SM --------------------------------------
 // For populations far larger than the GPU (config-3 sweeps) the latency kernel above leaves the SM
 // mostly idle: one 7-warp CTA per SM (its ~150 KB of product records and ~230 registers per thread
@@ -738,6 +1040,36 @@ void go_pipe(const TrainArgs& a, cudaStream_t s) {
   else launch(train_fp64_pipe<I, H1, H2, NPW, false, kWsmem>);
 }
 
+template <int I, int H1, int H2>
+void go_pair(const TrainArgs& a, cudaStream_t s) {
+  constexpr int NPW = 4;
+  const int dyn = pair_smem_doubles<I, H1, H2>() * 8;
+  auto kern = train_fp64_pair<I, H1, H2, NPW>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
+  kern<<<a.n_models, 32 * (kPairWarps + NPW), dyn, s>>>(a);
+}
+
+bool dispatch_pair(const TrainArgs& a, int I, int H1, int H2, cudaStream_t s) {
+  if (H1 == 8 && H2 == 0) {
+    switch (I) {
+      case 1: return go_pair<1, 8, 0>(a, s), true;
+      case 2: return go_pair<2, 8, 0>(a, s), true;
+      case 3: return go_pair<3, 8, 0>(a, s), true;
+      case 4: return go_pair<4, 8, 0>(a, s), true;
+      case 5: return go_pair<5, 8, 0>(a, s), true;
+      case 6: return go_pair<6, 8, 0>(a, s), true;
+      case 7: return go_pair<7, 8, 0>(a, s), true;
+    }
+  } else if (H1 == 5 && H2 == 5) {
+    switch (I) {
+      case 4: return go_pair<4, 5, 5>(a, s), true;
+      case 5: return go_pair<5, 5, 5>(a, s), true;
+      case 6: return go_pair<6, 5, 5>(a, s), true;
+    }
+  }
+  return false;
+}
+
 template <int NPW>
 bool dispatch_pipe(const TrainArgs& a, int I, int H1, int H2, cudaStream_t s) {
   if (H1 == 8 && H2 == 0) {
@@ -774,6 +1106,7 @@ bool launch_train_fp64_pipe(const TrainArgs& a, int I, int H1, int H2, int produ
     case 3: return dispatch_pipe<3>(a, I, H1, H2, s);
     case 8: return dispatch_pipe<8>(a, I, H1, H2, s);
     case 41: return dispatch_factor(a, I, H1, H2, s);  // throughput regime: factor records, 2 CTAs/SM
+    case 42: return dispatch_pair(a, I, H1, H2, s);    // latency regime, pair-row records
     default: return dispatch_pipe<4>(a, I, H1, H2, s);
   }
 }

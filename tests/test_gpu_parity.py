@@ -365,17 +365,18 @@ def test_batched_predictor_compiled_and_generic_shapes(engine, oracle):
             assert abs(got32[r] - got[r]) <= 1e-5 * (m["norm"][17] - m["norm"][16]) + 1e-12
 
 
-@pytest.mark.parametrize("kernel", ["4", "41"])
+@pytest.mark.parametrize("kernel", ["4", "41", "42"])
 def test_fp64_pipeline_kernels_edge_sizes(engine, oracle, monkeypatch, kernel):
-    """Both FP64 kernels of the LANN shapes — the latency pipeline (product records, 4) and the
-    throughput pipeline (factor records, two CTAs per SM, 41) — on sample counts around the
+    """The FP64 kernels of the LANN shapes — the latency pipeline (product records, 4), the
+    throughput pipeline (factor records, two CTAs per SM, 41) and the pair-row latency variant
+    (two rows per chain lane, a padding slot for odd row counts: 5-5-5, 42) — on sample counts around the
     32-sample blocks and producer rounds (2, 7, 31, 32, 33, 100, 129, 255, 256), one- and two-hidden
     layer shapes: weights and every epoch's loss == the oracle."""
     monkeypatch.setenv("LANN_FP64_PRODUCERS", kernel)
     rng = np.random.default_rng(77)
     tiles_X, tiles_y, models, expect, cases = [], [], [], [], []
     for k, n in enumerate((2, 7, 31, 32, 33, 100, 129, 255, 256)):
-        for I, hidden in ((7, [8]), (4, [8]), (6, [5, 5])):
+        for I, hidden in ((7, [8]), (4, [8]), (6, [5, 5]), (5, [5, 5])):
             X, y = random_problem(rng, I, hidden, n)
             dims = [I] + hidden + [1]
             p0 = E.init_params(dims, 7 * k + I)

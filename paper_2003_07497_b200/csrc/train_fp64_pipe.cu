@@ -704,6 +704,153 @@ __global__ void __launch_bounds__(32 * (kPairWarps + NPW), 1) train_fp64_pair(Tr
   }
 }
 
+// Pair-row producers with one row per chain lane (LANN_FP64_PRODUCERS=43): the producers of
+// train_fp64_pair (two terms per STS.128), the chains and Adam of train_fp64_pipe (three chain
+// warps, one slot per lane), each chain lane reading its half of a pair with one 8-byte load per
+// sample (a warp's 32 loads: 256 contiguous-in-pairs bytes at the kLdP stride, two wavefronts).
+template <int I, int H1, int H2, int NPW>
+__global__ void __launch_bounds__(32 * (kChainWarps + NPW), 1) train_fp64_pair1(TrainArgs a) {
+  using S = PipeShape<I, H1, H2>;
+  using Q = PairShape<I, H1, H2>;
+  static_assert(Q::SLOTS <= 32 * kChainWarps, "one chain lane per slot");
+  constexpr int R = (kMaxBlk + NPW - 1) / NPW;
+  extern __shared__ __align__(16) double smem[];
+  double* rec = smem;                                       // [NPAIR][kLdP]
+  double* ws = rec + Q::NPAIR * kLdP;                       // [P] weights
+  double* Ls = ws + ((S::P + 1) & ~1);                      // [2] epoch loss
+  unsigned long long* bar = reinterpret_cast<unsigned long long*>(Ls + 2);
+
+  const int m = a.order[blockIdx.x];
+  const int tile = a.model_tile[m];
+  const int N = a.tile_rows[tile];
+  const int nb = (N + kBlk - 1) / kBlk;
+  const int E = a.epochs[m];
+  const double lr = a.lr[m];
+  const int tid = threadIdx.x;
+  const double inv_n = 1.0 / (double)N;  // mlp.cpp:84
+  const double* gp = a.params + a.param_offset[m];
+  const double* X = a.X + a.tile_offset[tile] * 8;
+  const double* Y = a.y + a.tile_offset[tile];
+
+  for (int p = tid; p < S::P; p += blockDim.x) ws[p] = gp[p];
+  for (int q = tid; q < Q::NPAIR * kLdP; q += blockDim.x) rec[q] = 0.0;
+  if (tid * NPW < nb) mbar_init(&bar[tid], 32 * NPW);
+  __syncthreads();
+
+  double* trace = a.loss_trace ? a.loss_trace + a.trace_offset[m] : nullptr;
+  int bad = -1;
+  double last = 0.0;
+
+  if (tid < 32 * kChainWarps) {
+    const int c = tid < Q::SLOTS ? tid : 0;  // idle lanes shadow slot 0 (broadcast loads)
+    const int r = tid < Q::SLOTS ? Q::slot_row(c) : -2;
+    const int p = r >= 0 && r < S::P ? r : r == S::P ? -1 : -2;
+    const double* Tr = rec + (c >> 1) * kLdP + (c & 1);  // sample s at Tr[2 s]
+    double wr = p >= 0 ? gp[p] : 0.0, mr = 0.0, vr = 0.0;
+    const double beta1 = 0.9, beta2 = 0.999, eps = 1e-8;
+    const double c1 = 1.0 - beta1, c2 = 1.0 - beta2;
+    int next_trace = 0;
+    double A[kBlk], B[kBlk];
+    for (int e = 0; e < E; ++e) {
+      const unsigned ph = e & 1;
+      const double2 bc = a.bias_corr[e];
+      const double y1 = rcp_refined(bc.x), y2 = rcp_refined(bc.y);
+      double g = 0.0;
+      auto load = [&](double(&dst)[kBlk], int b) {
+#pragma unroll
+        for (int j = 0; j < kBlk; ++j) dst[j] = Tr[2 * (b * kBlk + j)];
+      };
+      auto links = [&](const double(&cur)[kBlk]) {  // 32 links in sample order (mlp.cpp:106-118)
+#pragma unroll
+        for (int j = 0; j < kBlk; ++j) g = __dadd_rn(g, cur[j]);
+      };
+      mbar_wait(bar, ph);
+      load(A, 0);
+#pragma unroll
+      for (int b = 0; b < kMaxBlk; ++b) {
+        if (b < nb) {
+          double(&cur)[kBlk] = (b & 1) ? B : A;
+          double(&nxt)[kBlk] = (b & 1) ? A : B;
+          if ((b + 1) % NPW != 0) {
+            load(nxt, b + 1 < nb ? b + 1 : b);
+            links(cur);
+          } else {
+            links(cur);
+            if (b + 1 < nb) {
+              mbar_wait(bar + (b + 1) / NPW, ph);
+              load(nxt, b + 1);
+            }
+          }
+        }
+      }
+      if (p >= 0) {  // AdamState::update (mlp.cpp:142-154), as train_fp64_pipe
+        const double mk = __dadd_rn(__dmul_rn(beta1, mr), __dmul_rn(c1, g));
+        const double vk = __dadd_rn(__dmul_rn(beta2, vr), __dmul_rn(__dmul_rn(c2, g), g));
+        mr = mk;
+        vr = vk;
+        bool ok = true;
+        const double mhat = div_checked(mk, bc.x, y1, ok);
+        const double vhat = div_checked(vk, bc.y, y2, ok);
+        const double den = __dadd_rn(sqrt_checked(vhat, ok), eps);
+        const double num = __dmul_rn(lr, mhat);
+        const double step = div_checked(num, den, rcp_refined(den), ok);
+        if (fabs(mk) >= 0x1p-900) {
+          wr = __dsub_rn(wr, ok ? step : adam_step_ieee(mk, vk, bc, lr, eps));
+        } else if (mk == 0.0) {
+          wr = __dsub_rn(wr, copysign(0.0, mk));
+        } else if (fabs(wr) < 0x1p-820) {
+          wr = __dsub_rn(wr, adam_step_ieee(mk, vk, bc, lr, eps));
+        }
+        ws[p] = wr;
+      } else if (p == -1) {
+        const double L = __dmul_rn(g, inv_n);  // mlp.cpp:120
+        Ls[e & 1] = L;
+        if (trace && e == next_trace) {
+          trace[e / a.trace_stride] = L;
+          next_trace += a.trace_stride;
+        }
+      }
+      epoch_barrier();
+      last = Ls[e & 1];
+      if (!isfinite(last)) {  // mlp.cpp:166-169: TrainingError(epoch)
+        bad = e;
+        break;
+      }
+    }
+    if (p >= 0) a.params[a.param_offset[m] + p] = wr;
+    if (p == -1) {
+      a.final_loss[m] = last;
+      a.nonfinite_epoch[m] = bad;
+    }
+  } else {
+    const int w = (tid >> 5) - kChainWarps, k = tid & 31;
+    double xr[R][I], yr[R];
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+      const int s = (w + q * NPW) * kBlk + k;
+#pragma unroll
+      for (int i = 0; i < I; ++i) xr[q][i] = s < N ? X[(size_t)s * 8 + i] : 0.0;
+      yr[q] = s < N ? Y[s] : 0.0;
+    }
+    for (int e = 0; e < E; ++e) {
+      double wv[S::P];
+#pragma unroll
+      for (int j = 0; j < S::P; ++j) wv[j] = ws[j];
+#pragma unroll
+      for (int q = 0; q < R; ++q) {
+        if (q * NPW < nb) {
+          const int s = (w + q * NPW) * kBlk + k;
+          if (s < N) Q::sample(wv, xr[q], yr[q], rec + 2 * s, inv_n);
+          mbar_arrive(&bar[q]);
+        }
+      }
+      epoch_barrier();
+      last = Ls[e & 1];
+      if (!isfinite(last)) break;
+    }
+  }
+}
+
 // ---- throughput regime: factor records, two CTAs per SM --------------------------------------
 // For populations far larger than the GPU (config-3 sweeps) the latency kernel above leaves the SM
 // mostly idle: one 7-warp CTA per SM (its ~150 KB of product records and ~230 registers per thread
@@ -1040,31 +1187,38 @@ void go_pipe(const TrainArgs& a, cudaStream_t s) {
   else launch(train_fp64_pipe<I, H1, H2, NPW, false, kWsmem>);
 }
 
-template <int I, int H1, int H2>
+template <int I, int H1, int H2, bool kOne>
 void go_pair(const TrainArgs& a, cudaStream_t s) {
   constexpr int NPW = 4;
   const int dyn = pair_smem_doubles<I, H1, H2>() * 8;
-  auto kern = train_fp64_pair<I, H1, H2, NPW>;
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
-  kern<<<a.n_models, 32 * (kPairWarps + NPW), dyn, s>>>(a);
+  if constexpr (kOne) {
+    auto kern = train_fp64_pair1<I, H1, H2, NPW>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
+    kern<<<a.n_models, 32 * (kChainWarps + NPW), dyn, s>>>(a);
+  } else {
+    auto kern = train_fp64_pair<I, H1, H2, NPW>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
+    kern<<<a.n_models, 32 * (kPairWarps + NPW), dyn, s>>>(a);
+  }
 }
 
+template <bool kOne>
 bool dispatch_pair(const TrainArgs& a, int I, int H1, int H2, cudaStream_t s) {
   if (H1 == 8 && H2 == 0) {
     switch (I) {
-      case 1: return go_pair<1, 8, 0>(a, s), true;
-      case 2: return go_pair<2, 8, 0>(a, s), true;
-      case 3: return go_pair<3, 8, 0>(a, s), true;
-      case 4: return go_pair<4, 8, 0>(a, s), true;
-      case 5: return go_pair<5, 8, 0>(a, s), true;
-      case 6: return go_pair<6, 8, 0>(a, s), true;
-      case 7: return go_pair<7, 8, 0>(a, s), true;
+      case 1: return go_pair<1, 8, 0, kOne>(a, s), true;
+      case 2: return go_pair<2, 8, 0, kOne>(a, s), true;
+      case 3: return go_pair<3, 8, 0, kOne>(a, s), true;
+      case 4: return go_pair<4, 8, 0, kOne>(a, s), true;
+      case 5: return go_pair<5, 8, 0, kOne>(a, s), true;
+      case 6: return go_pair<6, 8, 0, kOne>(a, s), true;
+      case 7: return go_pair<7, 8, 0, kOne>(a, s), true;
     }
   } else if (H1 == 5 && H2 == 5) {
     switch (I) {
-      case 4: return go_pair<4, 5, 5>(a, s), true;
-      case 5: return go_pair<5, 5, 5>(a, s), true;
-      case 6: return go_pair<6, 5, 5>(a, s), true;
+      case 4: return go_pair<4, 5, 5, kOne>(a, s), true;
+      case 5: return go_pair<5, 5, 5, kOne>(a, s), true;
+      case 6: return go_pair<6, 5, 5, kOne>(a, s), true;
     }
   }
   return false;
@@ -1106,7 +1260,8 @@ bool launch_train_fp64_pipe(const TrainArgs& a, int I, int H1, int H2, int produ
     case 3: return dispatch_pipe<3>(a, I, H1, H2, s);
     case 8: return dispatch_pipe<8>(a, I, H1, H2, s);
     case 41: return dispatch_factor(a, I, H1, H2, s);  // throughput regime: factor records, 2 CTAs/SM
-    case 42: return dispatch_pair(a, I, H1, H2, s);    // latency regime, pair-row records
+    case 42: return dispatch_pair<false>(a, I, H1, H2, s);  // latency regime, pair-row records
+    case 43: return dispatch_pair<true>(a, I, H1, H2, s);   // pair-row producers, one row per chain lane
     default: return dispatch_pipe<4>(a, I, H1, H2, s);
   }
 }

@@ -365,7 +365,7 @@ def test_batched_predictor_compiled_and_generic_shapes(engine, oracle):
             assert abs(got32[r] - got[r]) <= 1e-5 * (m["norm"][17] - m["norm"][16]) + 1e-12
 
 
-@pytest.mark.parametrize("kernel", ["4", "41", "42"])
+@pytest.mark.parametrize("kernel", ["4", "41", "42", "43"])
 def test_fp64_pipeline_kernels_edge_sizes(engine, oracle, monkeypatch, kernel):
     """The FP64 kernels of the LANN shapes — the latency pipeline (product records, 4), the
     throughput pipeline (factor records, two CTAs per SM, 41) and the pair-row latency variant
